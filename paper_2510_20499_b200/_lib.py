@@ -1,0 +1,130 @@
+"""ctypes binding of the engine's C-ABI (include/bp.h) — the only way Python reaches the GPU.
+
+The shared library is built in-tree (``paper_2510_20499_b200/libbp.so``) by ``__graft_entry__.build``
+or ``make -C paper_2510_20499_b200/csrc``.  There is no CPU fallback: importing works without a
+GPU, but every compute call fails loudly (``BPError``) when the library or a device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libbp.so"
+
+BP_OK, BP_ERR_INVALID_ARGUMENT, BP_ERR_OUT_OF_RANGE, BP_ERR_RUNTIME, BP_ERR_CUDA = 0, 1, 2, 3, 4
+TIGHTENED, INFEASIBLE, UNCHANGED = 0, 1, 2
+
+
+class BPError(RuntimeError):
+    """Engine failure; ``code`` is the C-ABI error code."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"[bp error {code}] {msg}")
+        self.code = code
+
+
+class bp_problem_desc(C.Structure):
+    _fields_ = [
+        ("n_vars", C.c_int32), ("n_cons", C.c_int32),
+        ("row_start", C.c_void_p), ("row_col", C.c_void_p), ("row_val", C.c_void_p),
+        ("col_start", C.c_void_p), ("col_row", C.c_void_p), ("col_val", C.c_void_p),
+        ("var_lower", C.c_void_p), ("var_upper", C.c_void_p), ("is_integer", C.c_void_p),
+        ("cons_lower", C.c_void_p), ("cons_upper", C.c_void_p),
+    ]
+
+
+class bp_limits(C.Structure):
+    _fields_ = [("max_rounds", C.c_int32), ("time_limit", C.c_double),
+                ("abs_threshold", C.c_double), ("rel_threshold", C.c_double),
+                ("incremental", C.c_int32)]
+
+
+class bp_result(C.Structure):
+    _fields_ = [("status", C.c_int32), ("rounds", C.c_int32), ("crossed_vars", C.c_int32)]
+
+
+_lib = None
+
+# (name, restype, argtypes) — every symbol include/bp.h declares.
+_SIGS = [
+    ("bp_last_error", C.c_char_p, []),
+    ("bp_limits_default", None, [C.POINTER(bp_limits)]),
+    ("bp_device_count", C.c_int, [C.POINTER(C.c_int32)]),
+    ("bp_problem_create", C.c_int, [C.POINTER(bp_problem_desc), C.c_int32, C.POINTER(C.c_void_p)]),
+    ("bp_problem_destroy", C.c_int, [C.c_void_p]),
+    ("bp_problem_info", C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int64)]),
+    ("bp_compute_activities", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]),
+    ("bp_tighten_bounds", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                    C.POINTER(bp_limits), C.c_void_p, C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_int32)]),
+    ("bp_propagate", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.POINTER(bp_limits),
+                               C.POINTER(bp_result)]),
+    ("bp_propagate_device", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32),
+                                      C.POINTER(bp_limits), C.POINTER(bp_result), C.c_void_p]),
+    ("bp_kernel_launches", C.c_int64, []),
+]
+
+
+def exported_symbols():
+    return [s[0] for s in _SIGS]
+
+
+def lib():
+    """Load libbp.so (raises BPError if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise BPError(BP_ERR_RUNTIME, f"engine library not built: {LIB_PATH} "
+                                          "(run __graft_entry__.build())")
+        L = C.CDLL(str(LIB_PATH))
+        for name, res, args in _SIGS:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc != BP_OK:
+        msg = lib().bp_last_error().decode(errors="replace")
+        if rc == BP_ERR_INVALID_ARGUMENT:
+            raise ValueError(msg)
+        if rc == BP_ERR_OUT_OF_RANGE:
+            raise IndexError(msg)
+        raise BPError(rc, msg)
+
+
+def ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def limits_struct(lim=None) -> bp_limits:
+    s = bp_limits()
+    lib().bp_limits_default(C.byref(s))
+    if lim is not None:
+        s.max_rounds = int(lim.max_rounds)
+        s.time_limit = float(lim.time_limit)
+        s.abs_threshold = float(lim.abs_threshold)
+        s.rel_threshold = float(lim.rel_threshold)
+        s.incremental = 1 if lim.incremental else 0
+    return s
+
+
+def kernel_launches() -> int:
+    return int(lib().bp_kernel_launches())
+
+
+def device_count() -> int:
+    c = C.c_int32(0)
+    if os.environ.get("CUDA_VISIBLE_DEVICES", None) == "":
+        return 0
+    rc = lib().bp_device_count(C.byref(c))
+    return int(c.value) if rc == BP_OK else 0

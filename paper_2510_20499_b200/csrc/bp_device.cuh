@@ -1,0 +1,235 @@
+// Device-side data model and arithmetic helpers of the bound-propagation engine.
+//
+// Bit-exactness contract: every floating-point expression below reproduces the
+// reference's operation order with separately rounded IEEE operations (the library is compiled
+// with --fmad=false, so no multiply-add is ever contracted), `std::min/max` are restated as
+// "keep the first operand on ties" (never fmin/fmax: they differ on signed zeros), and
+// activities are sequential sums within fixed 16384-entry segments (problem.hpp:274).
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+namespace bp {
+
+enum { BP_STATUS_UNSET = -1, BP_STATUS_TIGHTENED = 0, BP_STATUS_INFEASIBLE = 1, BP_STATUS_UNCHANGED = 2 };
+
+constexpr int kSumSegment = 16384;   // problem.hpp:274
+constexpr int kShortNnz   = 32;      // rows/cols at or below: one lane each
+constexpr int kSegNnz     = 2048;    // rows above: producer/consumer warp pair per 16384-segment
+constexpr double kIntEps  = 1e-6;    // common.hpp:24
+
+// Row record gathered by the tightening sweep: one 32-byte sector, one LDG.256.
+//   min/max = finite parts of the min/max activity when no infinite contributor exists;
+//             otherwise a NaN box carrying the infinite-contributor count, with the finite part
+//             in RowAux (read only in the rare "single infinite contributor" case,
+//             propagation.hpp:311-313).
+//   g/h     = cons_upper / cons_lower (static), co-located so a gather fetches everything.
+struct alignas(32) RowRec {
+  double min, max, g, h;
+};
+
+constexpr unsigned long long kBoxMask = 0xFFFFFFFF00000000ull;
+constexpr unsigned long long kBoxBase = 0x7FF4B0B000000000ull;  // payload arithmetic never makes
+
+__host__ __device__ __forceinline__ double box_count(int c)
+{
+  unsigned long long u = kBoxBase | (unsigned long long)(unsigned)c;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)u);
+#else
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+#endif
+}
+__device__ __forceinline__ bool is_box(double x)
+{
+  return ((unsigned long long)__double_as_longlong(x) & kBoxMask) == kBoxBase;
+}
+__device__ __forceinline__ int box_value(double x)
+{
+  return (int)(unsigned)((unsigned long long)__double_as_longlong(x) & 0xFFFFFFFFull);
+}
+
+// std::min / std::max semantics (first operand kept on ties).
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+__device__ __forceinline__ RowRec ld_rec(const RowRec* p)
+{
+  RowRec r;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r.min), "=d"(r.max), "=d"(r.g), "=d"(r.h)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_rec(RowRec* p, const RowRec& r)
+{
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.min), "d"(r.max), "d"(r.g),
+               "d"(r.h)
+               : "memory");
+}
+
+// Activity contribution of one entry (propagation.hpp:159-170). Infinite contributors return a
+// 0.0 contribution plus a count: adding +0.0 to a running sum that starts at +0.0 never changes
+// it (the running sum can never be -0.0 under round-to-nearest), so this equals "skip".
+__device__ __forceinline__ void contrib(double a, double lo, double up, double& cmin, double& cmax,
+                                        int& imin, int& imax)
+{
+  if (a > 0.0) {
+    imin = (lo == -INFINITY);
+    imax = (up == INFINITY);
+    cmin = imin ? 0.0 : __dmul_rn(a, lo);
+    cmax = imax ? 0.0 : __dmul_rn(a, up);
+  } else {
+    imin = (up == INFINITY);
+    imax = (lo == -INFINITY);
+    cmin = imin ? 0.0 : __dmul_rn(a, up);
+    cmax = imax ? 0.0 : __dmul_rn(a, lo);
+  }
+}
+
+struct Limits {
+  int max_rounds;
+  double time_limit;
+  double abs_threshold;
+  double rel_threshold;
+  int incremental;
+};
+
+// propagation.hpp:273-282
+__device__ __forceinline__ bool counts_as_change(double imp, bool integer, double width,
+                                                 const Limits& lim)
+{
+  if (imp <= 0.0) return false;
+  if (imp == INFINITY) return true;
+  if (integer) return imp >= 1.0 - 1e-9;
+  double thr = lim.abs_threshold;
+  if (isfinite(width)) thr = smax(thr, __dmul_rn(lim.rel_threshold, width));
+  return imp > thr;
+}
+
+// Candidate fold state of one variable: new bound value + CSC position of the element that
+// set it (-1 = the current bound). The sequential std::min fold of the reference keeps the
+// FIRST minimal element, i.e. the lexicographic minimum of (value, position) under numeric
+// equality -- which is associative, so long columns may be reduced in parallel.
+struct Fold {
+  double lo;
+  int lo_pos;
+  double up;
+  int up_pos;
+};
+
+// One CSC entry's contribution to the fold (propagation.hpp:297-352).
+__device__ __forceinline__ void fold_entry(Fold& f, double lo, double up, bool integer, double a,
+                                           const RowRec& r, const double2* aux, int k, int pos)
+{
+  if (isfinite(r.g)) {
+    double rest;
+    bool usable;
+    if (!is_box(r.min)) {
+      rest   = __dsub_rn(r.min, (a > 0.0) ? __dmul_rn(a, lo) : __dmul_rn(a, up));
+      usable = true;
+    } else {
+      const bool my_inf = (a > 0.0) ? (lo == -INFINITY) : (up == INFINITY);
+      usable            = (box_value(r.min) == 1) && my_inf;
+      rest              = usable ? aux[k].x : 0.0;
+    }
+    if (usable) {
+      const double cand = __ddiv_rn(__dsub_rn(r.g, rest), a);
+      if (a > 0.0) {
+        const double c = integer ? floor(__dadd_rn(cand, kIntEps)) : cand;
+        if (c < f.up) { f.up = c; f.up_pos = pos; }
+      } else {
+        const double c = integer ? ceil(__dsub_rn(cand, kIntEps)) : cand;
+        if (f.lo < c) { f.lo = c; f.lo_pos = pos; }
+      }
+    }
+  }
+  if (isfinite(r.h)) {
+    double rest;
+    bool usable;
+    if (!is_box(r.max)) {
+      rest   = __dsub_rn(r.max, (a > 0.0) ? __dmul_rn(a, up) : __dmul_rn(a, lo));
+      usable = true;
+    } else {
+      const bool my_inf = (a > 0.0) ? (up == INFINITY) : (lo == -INFINITY);
+      usable            = (box_value(r.max) == 1) && my_inf;
+      rest              = usable ? aux[k].y : 0.0;
+    }
+    if (usable) {
+      const double cand = __ddiv_rn(__dsub_rn(r.h, rest), a);
+      if (a > 0.0) {
+        const double c = integer ? ceil(__dsub_rn(cand, kIntEps)) : cand;
+        if (f.lo < c) { f.lo = c; f.lo_pos = pos; }
+      } else {
+        const double c = integer ? floor(__dadd_rn(cand, kIntEps)) : cand;
+        if (c < f.up) { f.up = c; f.up_pos = pos; }
+      }
+    }
+  }
+}
+
+// Combine two partial folds of disjoint position sets (lexicographic (value, position)).
+__device__ __forceinline__ void fold_combine(Fold& f, double olo, int olo_pos, double oup,
+                                             int oup_pos)
+{
+  if (f.lo < olo || (olo == f.lo && olo_pos < f.lo_pos)) { f.lo = olo; f.lo_pos = olo_pos; }
+  if (oup < f.up || (oup == f.up && oup_pos < f.up_pos)) { f.up = oup; f.up_pos = oup_pos; }
+}
+
+// propagation.hpp:354-369. Returns 1 changed, 0 unchanged, -1 crossing; writes *b on change.
+__device__ __forceinline__ int finish_var(double2* b, double lo, double up, double new_lo,
+                                          double new_up, bool integer, const Limits& lim)
+{
+  if (new_lo > __dadd_rn(new_up, 1e-9)) return -1;
+  if (new_lo > new_up) new_lo = new_up;
+  const double width = __dsub_rn(up, lo);
+  bool changed       = false;
+  double wlo = lo, wup = up;
+  const double lo_imp = (lo == -INFINITY && new_lo > -INFINITY) ? INFINITY : __dsub_rn(new_lo, lo);
+  if (counts_as_change(lo_imp, integer, width, lim)) { wlo = new_lo; changed = true; }
+  const double up_imp = (up == INFINITY && new_up < INFINITY) ? INFINITY : __dsub_rn(up, new_up);
+  if (counts_as_change(up_imp, integer, width, lim)) { wup = new_up; changed = true; }
+  if (changed) *b = make_double2(wlo, wup);
+  return changed ? 1 : 0;
+}
+
+// Immutable device problem: the matrix twice (CSR + CSC) plus work-partition tables built once
+// at upload (SURVEY §8a A4's LRB bins, re-designed for warps: see DESIGN.md §3).
+struct DevProblem {
+  int n, m;
+  long long nnz;
+  const int* row_start;
+  const int* row_col;
+  const double* row_val;
+  const int* col_start;
+  const int* col_row;
+  const double* col_val;
+  const double2* cons;      // (lower, upper) per row
+  const uint8_t* is_int;
+  // rows with nnz <= kShortNnz, natural order (lane per row)
+  int n_srow;
+  const int* srow;
+  // rows with kShortNnz < nnz <= kSegNnz, nnz descending (warp per row)
+  int n_mrow;
+  const int* mrow;
+  // segment tasks of rows with nnz > kSegNnz: (row, segment), longest rows first
+  int n_seg;
+  const int2* seg_task;
+  const int* seg_base;      // per row (m entries; -1 if not segmented): first partial slot
+  // columns: nnz <= kShortNnz natural order (lane per var) / longer, nnz descending (warp per var)
+  int n_scol;
+  const int* scol;
+  int n_mcol;
+  const int* mcol;
+};
+
+struct SegPart {
+  double min, max;
+  int nmin, nmax;
+  int pad0, pad1;
+};
+
+}  // namespace bp

@@ -1,0 +1,149 @@
+// Host-side engine objects shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "bp_device.cuh"
+
+namespace bp {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define BP_CUDA(x)                                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::bp::cuda_error(std::string(#x) + ": " + cudaGetErrorString(e_) + " (" +       \
+                             __FILE__ + ":" + std::to_string(__LINE__) + ")");              \
+  } while (0)
+
+// Owning device allocation.
+template <class T>
+struct DBuf {
+  T* p       = nullptr;
+  size_t n   = 0;
+  DBuf()     = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset()
+  {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count)
+  {
+    reset();
+    n = count;
+    if (count) BP_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  }
+  void upload(const T* src, size_t count)
+  {
+    alloc(count);
+    if (count) BP_CUDA(cudaMemcpy(p, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  }
+  void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
+};
+
+// Per-round frontier/counter block (double-buffered by round parity).
+struct ParCtl {
+  int n_drow_all, n_drow_s, n_drow_m, n_dseg;  // staged together (stage_rows)
+  int n_dvar_s, n_dvar_m;                      // staged together (stage_vars)
+  int n_changed, n_crossed;
+  int any_rows, cur_seg, cur_m, cur_s;
+  int cur_vm, cur_vs, cur_x1, cur_x2;
+  int n_xtask, stop;
+  unsigned long long colnnz, roww;
+  int pad[4];
+};
+
+struct Ctl {
+  ParCtl par[2];
+  int status, rounds, crossed, any_change;
+  int pad[12];
+};
+
+// Mutable per-problem workspace (one propagate at a time per problem; calls serialized).
+struct DevState {
+  double2* bounds;
+  RowRec* rec;
+  double2* aux;
+  SegPart* seg_part;
+  int* seg_done;
+  unsigned* row_stamp;
+  unsigned* var_stamp;
+  int* drow_all[2];
+  int* drow_s[2];
+  int* drow_m[2];
+  int2* dseg[2];
+  int2* xtask[2];  // (row, 256-entry chunk) tasks for var expansion
+  int* dvar_s[2];
+  int* dvar_m[2];
+  int* changed;
+  Ctl* ctl;
+};
+
+enum Mode { MODE_PROPAGATE = 0, MODE_ACTIVITY = 1, MODE_TIGHTEN = 2 };
+
+struct Problem {
+  int device = 0;
+  int n = 0, m = 0;
+  long long nnz = 0;
+  // host copies kept for classification of caller-supplied lists
+  std::vector<int> h_row_start, h_col_start;
+  std::vector<int> h_seg_base;
+  // device arrays
+  DBuf<int> row_start, row_col, col_start, col_row;
+  DBuf<double> row_val, col_val;
+  DBuf<double2> cons;
+  DBuf<uint8_t> is_int;
+  DBuf<int> srow, mrow, scol, mcol, seg_base;
+  DBuf<int2> seg_task;
+  int n_srow = 0, n_mrow = 0, n_scol = 0, n_mcol = 0, n_seg = 0;
+  // workspace
+  DBuf<double2> bounds;
+  DBuf<RowRec> rec;
+  DBuf<double2> aux;
+  DBuf<SegPart> seg_part;
+  DBuf<int> seg_done;
+  DBuf<unsigned> row_stamp, var_stamp;
+  DBuf<int> lists_i;  // backing store for int lists
+  DBuf<int2> lists_i2;
+  DBuf<Ctl> ctl;
+  DevState st{};
+  unsigned stamp_base = 1;
+  int grid_blocks = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+
+  DevProblem dev() const;
+};
+
+void problem_build(Problem& P, int n, int m, const int* row_start, const int* row_col,
+                   const double* row_val, const int* col_start, const int* col_row,
+                   const double* col_val, const double* var_lower, const double* var_upper,
+                   const uint8_t* is_integer, const double* cons_lower, const double* cons_upper);
+
+struct RunResult {
+  int status, rounds, crossed;
+};
+
+// Runs the persistent kernel on the device-resident working bounds P.st.bounds.
+// For MODE_ACTIVITY / MODE_TIGHTEN with lists, the frontier lists of parity 1 must be staged.
+RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s);
+
+// Stage caller row/var lists into the parity-1 frontier buffers (host-classified).
+void stage_rows(Problem& P, const int* rows, int nrows, cudaStream_t s);
+void stage_vars(Problem& P, const int* vars, int nvars, cudaStream_t s);
+
+extern long long g_kernel_launches;
+
+}  // namespace bp
