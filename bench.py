@@ -1,0 +1,355 @@
+"""Benchmark: BP nnz/s and HBM GB/s vs peak on BASELINE.json configs[1] (C2: synthetic 1M x 1M MILP,
+power-law rows median 7 / max ~100k) — one full `propagate` to fixpoint from the original bounds per
+step, on the persistent sm_100a engine.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2|C1]
+
+One JSON line on rank 0. `value` = BP nnz visits/s (the reference trajectory's work, counted by
+the engine's exact-frontier stats pass) over all ranks, device-timed with CUDA events, max over
+ranks; inputs resident in HBM. `e2e` = the same metric through the C-ABI with host (pinned)
+bounds copied in and out every step. `roofline` = algorithmic bytes of the engine kernel per
+launch / its CUDA-event duration vs MEASURED_PEAKS.json hbm_gbs. `cpu_baseline` = the reference
+(oracle/_ref, compiled from /root/reference) propagate on the host cores. N > 1: independent
+replicas (a single propagation does not shard), weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return HBM_FALLBACK, "fallback"
+
+
+def make_workload(name):
+    from paper_2510_20499_b200 import synth
+    if name == "C2":
+        return synth.c2(), "C2: synthetic MILP 1M x 1M, Pareto rows (median 7, max ~100k), skewed cols"
+    if name == "C1":
+        return synth.c1(), "C1: synthetic MILP 10k x 10k, ~8 nnz/row, mixed types"
+    raise SystemExit(f"unknown workload {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clock/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self, t0, t1):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.t.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons, n_in = [], [], set(), 0
+        for ts, line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            inside = t0 - 0.06 <= ts <= t1 + 0.06
+            try:
+                smax.append(float(f[2]))
+                if inside:
+                    sm.append(float(f[1]))
+                    n_in += 1
+                    for nm, v in zip(names, f[5:9]):
+                        if v.lower().startswith("active"):
+                            reasons.add(nm)
+            except ValueError:
+                continue
+        if not sm:  # region shorter than one sample: nearest samples
+            near = sorted(self.lines, key=lambda x: min(abs(x[0] - t0), abs(x[0] - t1)))[:2]
+            for ts, line in near:
+                f = [x.strip() for x in line.split(",")]
+                try:
+                    sm.append(float(f[1]))
+                except (ValueError, IndexError):
+                    pass
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples_in_region": n_in}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference_propagate(p, reps=1):
+    """The reference's own propagate (oracle/_ref/libpulse_ref.so) on all host threads."""
+    from oracle.bind import Ref, RefProblem, ref_propagate
+    if not Ref.available():
+        return None
+    rp = RefProblem.from_def(p)
+    root = p.root_bounds()
+    times = []
+    out = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = ref_propagate(rp, root)
+        times.append(time.perf_counter() - t0)
+    return times, out, int(Ref.lib().ref_max_threads())
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference CPU implementation on this box's host cores."""
+    if rank != 0:
+        return
+    p, desc = make_workload(args.workload)
+    visits = None
+    res = cpu_reference_propagate(p, reps=1)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpulse_ref.so not built"}))
+        return
+    # the visit count of the reference trajectory (identical to ours; from the port's replay)
+    visits = reference_visits(p)
+    for _ in range(args.warmup):
+        cpu_reference_propagate(p, reps=1)
+    t0 = time.perf_counter()
+    times, out, cores = cpu_reference_propagate(p, reps=args.steps)
+    el = time.perf_counter() - t0
+    v = visits * args.steps / el
+    line = {"metric": "BP nnz/s", "value": v, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": desc, "rounds": out[3], "nnz_visits_per_step": visits},
+            "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": cores, "kind": "reference",
+                             "sample": f"{args.steps} full propagate calls of {args.workload}"},
+            "e2e": {"value": v, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def reference_visits(p):
+    """Σ_r (row nnz of R_r + col nnz of V_r) of the reference trajectory, replayed round by round
+    with the C port (CPU-side accounting for the reference arm; identical to the engine stats)."""
+    from oracle.bind import PortProblem
+    pp = PortProblem(p)
+    b = p.root_bounds()
+    n, m = p.n_vars, p.n_cons
+    rnnz = np.diff(p.row_start).astype(np.int64)
+    cnnz = np.diff(p.col_start).astype(np.int64)
+    visits = int(rnnz.sum() + cnnz.sum())
+    act, nmin, nmax = pp.compute_activities(b)
+    b, inf, changed, _ = pp.tighten_bounds(b, False, act, nmin, nmax)
+    rounds = 1
+    while changed and not inf and rounds < 64:
+        ch = np.array(changed, dtype=np.int64)
+        rows = np.unique(np.concatenate([p.col_row[p.col_start[i]:p.col_start[i + 1]] for i in ch]))
+        if rows.size == 0:
+            break
+        vars_ = np.unique(np.concatenate([p.row_col[p.row_start[k]:p.row_start[k + 1]] for k in rows]))
+        visits += int(rnnz[rows].sum() + cnnz[vars_].sum())
+        act, nmin, nmax = pp.compute_activities(b, rows=rows, act=act, nmin=nmin, nmax=nmax)
+        b, inf, changed, _ = pp.tighten_bounds(b, False, act, nmin, nmax, vars_=vars_)
+        rounds += 1
+    return visits
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=["C2", "C1"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_20499_b200 import BoundsState, metrics, propagate
+    from paper_2510_20499_b200 import _lib
+    from paper_2510_20499_b200.propagation import FORCE_FRONTIER, device_problem, propagate_device
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p, desc = make_workload(args.workload)
+    dp = device_problem(p, device=local)
+    n, m, N = p.n_vars, p.n_cons, p.nnz()
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    d_root = torch.from_numpy(p.root_bounds()).cuda()
+    d_work = torch.empty_like(d_root)
+
+    # 1) exact-frontier stats pass: the reference trajectory's dirty sets, for the work counts
+    d_stats = torch.zeros(64 * metrics.STAT_COLS, dtype=torch.int64, device="cuda")
+    d_work.copy_(d_root)
+    r_stats, _ = propagate_device(p, d_work.data_ptr(), False, None, sptr, FORCE_FRONTIER,
+                                  d_stats.data_ptr())
+    stats = metrics.trim(d_stats.cpu().numpy(), r_stats.rounds)
+    ref_bits = d_work.cpu().numpy().view(np.uint64).copy()
+    visits = metrics.nnz_visits(stats)
+    alg_bytes = metrics.algorithmic_bytes(stats, n, m)
+
+    def step():
+        d_work.copy_(d_root)
+        return propagate_device(p, d_work.data_ptr(), False, None, sptr)
+
+    for _ in range(args.warmup):
+        r, _ = step()
+    torch.cuda.synchronize()
+    # the fast path (full-round substitution) must reproduce the exact-frontier result bit for bit
+    assert (r.status, r.rounds, r.crossed_vars) == (r_stats.status, r_stats.rounds, r_stats.crossed_vars)
+    assert np.array_equal(d_work.cpu().numpy().view(np.uint64), ref_bits), "fast path != exact frontier"
+
+    L = _lib.lib()
+    import ctypes as C
+    tot0, nl0 = C.c_double(), C.c_int64()
+    L.bp_kernel_time(dp.h, None, C.byref(tot0), C.byref(nl0))
+    launches0 = _lib.kernel_launches()
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = _lib.kernel_launches() - launches0
+    tot1, nl1 = C.c_double(), C.c_int64()
+    L.bp_kernel_time(dp.h, None, C.byref(tot1), C.byref(nl1))
+    kern_ms = (tot1.value - tot0.value) / max(1, nl1.value - nl0.value)
+    clocks = sampler.stop(t_wall0, t_wall1) if rank == 0 else None
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        kt = torch.tensor([kern_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+        kern_ms = float(kt.item())
+
+    # 2) e2e: host (pinned) bounds through the C-ABI call bp_propagate, H2D + D2H every step
+    host_root = p.root_bounds()
+    pinned = torch.empty(host_root.size, dtype=torch.float64).pin_memory()
+    hb = pinned.numpy()
+    e2e_times = []
+    for i in range(args.e2e_steps + 2):
+        hb[:] = host_root
+        b = BoundsState(raw=hb)
+        b.b = hb  # operate on the pinned buffer in place
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rr = propagate(p, b)
+        t1 = time.perf_counter()
+        if i >= 2:
+            e2e_times.append(t1 - t0)
+    e2e_s = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+        prof = ROOT / "profiles" / "ncu_k_engine_summary.json"
+        traffic = None
+        if prof.exists():
+            try:
+                traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch", {}).get(args.workload)
+            except Exception:
+                traffic = None
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            res = cpu_reference_propagate(p, reps=1)
+            if res is not None:
+                times, out, cores = res
+                cpu = {"value": visits / times[0], "unit": "nnz/s", "cores": cores,
+                       "kind": "reference",
+                       "sample": f"1 full propagate of {args.workload} ({out[3]} rounds, "
+                                 f"{times[0]:.2f} s), reference compiled from /root/reference"}
+                assert out[3] == r.rounds and out[2] == int(r.status), "reference trajectory differs"
+        value = world * visits * args.steps / (ms * 1e-3)
+        line = {
+            "metric": "BP nnz/s", "value": value, "unit": "nnz/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": desc, "n_vars": n, "n_cons": m, "nnz": N,
+                       "rounds": r.rounds, "status": int(r.status),
+                       "nnz_visits_per_step": visits, "algorithmic_bytes_per_step": alg_bytes,
+                       "full_rounds_in_reference_trajectory": int(stats[:, 0].sum()),
+                       "l2": "no flush: CSR+CSC inputs (%.0f MB) exceed the 126 MB L2" % (N * 24 / 1e6),
+                       "parallelism": f"replicas x{world}"},
+            "e2e": {"value": world * visits / e2e_s, "unit": "nnz/s",
+                    "h2d_bytes_per_step": int(host_root.nbytes), "d2h_bytes_per_step": int(host_root.nbytes),
+                    "ms_per_step": e2e_s * 1e3, "api": "bp_propagate (C-ABI, host pinned bounds)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k_engine", "kernel_ms": kern_ms},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

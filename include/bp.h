@@ -103,8 +103,21 @@ int bp_propagate(bp_problem* p, double* bounds2n, int32_t* infeasible, const bp_
 int bp_propagate_device(bp_problem* p, double* d_bounds2n, int32_t* infeasible,
                         const bp_limits* lim, bp_result* res, void* stream);
 
-/* Nsight-visible counter: number of engine kernels launched by this process. */
+/* Device-resident propagate with options. flags: BP_FORCE_FRONTIER (bit 0) disables the engine's
+ * full-round substitution for large frontiers, i.e. runs the reference's exact dirty-set
+ * trajectory (results are bit-identical either way). d_stats, if non-NULL, is a DEVICE array of
+ * 6 * max_rounds int64 receiving per round {full, |dirty rows|, row nnz visited, |dirty vars|,
+ * col nnz visited, |changed vars|} — the reference's algorithmic work. */
+#define BP_FORCE_FRONTIER 1
+int bp_propagate_ex(bp_problem* p, double* d_bounds2n, int32_t* infeasible, const bp_limits* lim,
+                    bp_result* res, void* stream, int32_t flags, int64_t* d_stats);
+
+/* Number of engine kernels launched by this process. */
 int64_t bp_kernel_launches(void);
+
+/* Device time of engine launches on this problem, measured with CUDA events recorded on the
+ * launching stream around each launch: the last one, the running total, and the launch count. */
+int bp_kernel_time(const bp_problem* p, double* last_ms, double* total_ms, int64_t* launches);
 
 #ifdef __cplusplus
 }

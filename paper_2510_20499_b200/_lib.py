@@ -68,7 +68,12 @@ _SIGS = [
                                C.POINTER(bp_result)]),
     ("bp_propagate_device", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32),
                                       C.POINTER(bp_limits), C.POINTER(bp_result), C.c_void_p]),
+    ("bp_propagate_ex", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32),
+                                  C.POINTER(bp_limits), C.POINTER(bp_result), C.c_void_p, C.c_int32,
+                                  C.c_void_p]),
     ("bp_kernel_launches", C.c_int64, []),
+    ("bp_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_int64)]),
 ]
 
 

@@ -146,6 +146,16 @@ void bp_limits_default(bp_limits* lim)
 
 int64_t bp_kernel_launches(void) { return bp::g_kernel_launches; }
 
+int bp_kernel_time(const bp_problem* p, double* last_ms, double* total_ms, int64_t* launches)
+{
+  return guard([&] {
+    need(p, "null problem");
+    if (last_ms) *last_ms = p->impl.last_kernel_ms;
+    if (total_ms) *total_ms = p->impl.total_kernel_ms;
+    if (launches) *launches = p->impl.n_launch;
+  });
+}
+
 int bp_device_count(int32_t* count)
 {
   return guard([&] {
@@ -198,6 +208,8 @@ int bp_problem_destroy(bp_problem* p)
     if (!p) return;
     cudaSetDevice(p->impl.device);
     if (p->impl.stream) cudaStreamDestroy(p->impl.stream);
+    if (p->impl.ev0) cudaEventDestroy(p->impl.ev0);
+    if (p->impl.ev1) cudaEventDestroy(p->impl.ev1);
     delete p;
   });
 }
@@ -280,6 +292,12 @@ int bp_tighten_bounds(bp_problem* p, double* bounds2n, int32_t* infeasible, cons
 int bp_propagate_device(bp_problem* p, double* d_bounds2n, int32_t* infeasible,
                         const bp_limits* lim, bp_result* res, void* stream)
 {
+  return bp_propagate_ex(p, d_bounds2n, infeasible, lim, res, stream, 0, nullptr);
+}
+
+int bp_propagate_ex(bp_problem* p, double* d_bounds2n, int32_t* infeasible, const bp_limits* lim,
+                    bp_result* res, void* stream, int32_t flags, int64_t* d_stats)
+{
   return guard([&] {
     need(p && d_bounds2n && infeasible && res, "null argument");
     bp::Problem& P = p->impl;
@@ -299,7 +317,9 @@ int bp_propagate_device(bp_problem* p, double* d_bounds2n, int32_t* infeasible,
       BP_CUDA(cudaMemcpyAsync(P.st.bounds, d_bounds2n, sizeof(double) * 2 * P.n,
                               cudaMemcpyDeviceToDevice, s));
     reset_ctl(P, s);
-    const bp::RunResult r = bp::run_engine(P, bp::MODE_PROPAGATE, true, l, s);
+    const bp::RunResult r = bp::run_engine(P, bp::MODE_PROPAGATE, true, l, s,
+                                           (flags & BP_FORCE_FRONTIER) ? bp::ENGINE_FORCE_FRONTIER : 0,
+                                           reinterpret_cast<long long*>(d_stats));
     if (P.n)
       BP_CUDA(cudaMemcpyAsync(d_bounds2n, P.st.bounds, sizeof(double) * 2 * P.n,
                               cudaMemcpyDeviceToDevice, s));

@@ -61,8 +61,8 @@ struct ParCtl {
   int any_rows, cur_seg, cur_m, cur_s;
   int cur_vm, cur_vs, cur_x1, cur_x2;
   int n_xtask, stop;
-  unsigned long long colnnz, roww;
-  int pad[4];
+  unsigned long long colnnz, roww, colw;
+  int pad[2];
 };
 
 struct Ctl {
@@ -122,6 +122,10 @@ struct Problem {
   unsigned stamp_base = 1;
   int grid_blocks = 0;
   cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket every engine launch on its stream
+  double last_kernel_ms = 0.0;
+  double total_kernel_ms = 0.0;
+  long long n_launch = 0;
   std::mutex mu;
 
   DevProblem dev() const;
@@ -138,7 +142,13 @@ struct RunResult {
 
 // Runs the persistent kernel on the device-resident working bounds P.st.bounds.
 // For MODE_ACTIVITY / MODE_TIGHTEN with lists, the frontier lists of parity 1 must be staged.
-RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s);
+// flags: ENGINE_FORCE_FRONTIER never substitutes a full round for a large frontier (the exact
+// reference trajectory of dirty sets, used to count its work); stats (device, kStatCols per round)
+// receives per-round work counts when non-null.
+enum { ENGINE_FORCE_FRONTIER = 1 };
+constexpr int kStatCols = 6;  // full, |R|, row nnz visits, |V|, col nnz visits, |changed|
+RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s,
+                     int flags = 0, long long* d_stats = nullptr);
 
 // Stage caller row/var lists into the parity-1 frontier buffers (host-classified).
 void stage_rows(Problem& P, const int* rows, int nrows, cudaStream_t s);

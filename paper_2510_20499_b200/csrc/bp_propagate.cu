@@ -522,6 +522,7 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
   const DevState& S   = c.S;
   const int ntask     = ld_volatile(&qc->n_xtask);
   const unsigned lt   = lanemask_lt();
+  unsigned long long colw = 0;
   for (int t = warp_fetch(c, &pc->cur_x2, 1); t < ntask; t = warp_fetch(c, &pc->cur_x2, 1)) {
     const int2 tk = S.xtask[qpar][t];
     const int rs  = __ldg(P.row_start + tk.x), re = __ldg(P.row_start + tk.x + 1);
@@ -540,12 +541,16 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
       const int L     = nw[h] ? __ldg(P.col_start + vj[h] + 1) - __ldg(P.col_start + vj[h]) : 0;
       const bool is_s = nw[h] && L <= kShortNnz;
       const bool is_m = nw[h] && L > kShortNnz;
+      colw += (unsigned long long)L;
       int pos         = warp_append(&qc->n_dvar_s, is_s, lt);
       if (is_s) S.dvar_s[qpar][pos] = vj[h];
       pos = warp_append(&qc->n_dvar_m, is_m, lt);
       if (is_m) S.dvar_m[qpar][pos] = vj[h];
     }
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) colw += __shfl_xor_sync(FULL, colw, o);
+  if (c.lane == 0 && colw) atomicAdd(&qc->colw, colw);
 }
 
 __device__ void zero_par(ParCtl* q)
@@ -556,7 +561,7 @@ __device__ void zero_par(ParCtl* q)
 
 __global__ void __launch_bounds__(kThreads, 2)
     k_engine(DevProblem P, DevState S, Limits lim, int mode, int full_first, unsigned stamp_base,
-             unsigned long long dense_thr)
+             unsigned long long dense_thr, long long* stats)
 {
   __shared__ Smem sm;
   cg::grid_group grid = cg::this_grid();
@@ -599,6 +604,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     grid.sync();
     const int cr = ld_volatile(&pc->n_crossed);
     const int nc = ld_volatile(&pc->n_changed);
+    if (stats && blockIdx.x == 0 && threadIdx.x == 0) {
+      const bool fr = full || !lim.incremental;
+      long long* st = stats + (long long)(rounds - 1) * kStatCols;
+      st[0] = fr ? 1 : 0;
+      st[1] = fr ? P.m : ld_volatile(&pc->n_drow_all);
+      st[2] = fr ? P.nnz : (long long)ld_volatile(&pc->roww);
+      st[3] = fr ? P.n : ld_volatile(&pc->n_dvar_s) + ld_volatile(&pc->n_dvar_m);
+      st[4] = fr ? P.nnz : (long long)ld_volatile(&pc->colw);
+      st[5] = nc;
+    }
     if (cr > 0) {
       status      = BP_STATUS_INFEASIBLE;
       crossed_out = cr;
@@ -804,9 +819,12 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   if (per_sm < 1) throw cuda_error("engine kernel cannot be resident (occupancy 0)");
   P.grid_blocks = dev_sms * std::min(per_sm, 2);
   BP_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+  BP_CUDA(cudaEventCreate(&P.ev0));
+  BP_CUDA(cudaEventCreate(&P.ev1));
 }
 
-RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s)
+RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s, int flags,
+                     long long* d_stats)
 {
   DevProblem d                 = P.dev();
   DevState st                  = P.st;
@@ -821,9 +839,13 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   }
   unsigned sb                  = P.stamp_base;
   P.stamp_base += (unsigned)std::max(lim.max_rounds, 1) + 1;
-  unsigned long long dense_thr = (unsigned long long)(P.nnz / 4);
-  void* args[] = {&d, &st, &l, &md, &ff, &sb, &dense_thr};
+  unsigned long long dense_thr = (flags & ENGINE_FORCE_FRONTIER) ? ~0ull
+                                                                 : (unsigned long long)(P.nnz / 4);
+  long long* stp = d_stats;
+  void* args[] = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp};
+  BP_CUDA(cudaEventRecord(P.ev0, s));
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, 0, s));
+  BP_CUDA(cudaEventRecord(P.ev1, s));
   ++g_kernel_launches;
   RunResult r{0, 0, 0};
   if (mode == MODE_PROPAGATE) {
@@ -836,6 +858,11 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   } else {
     BP_CUDA(cudaStreamSynchronize(s));
   }
+  float ms = 0.f;
+  BP_CUDA(cudaEventElapsedTime(&ms, P.ev0, P.ev1));
+  P.last_kernel_ms = ms;
+  P.total_kernel_ms += ms;
+  P.n_launch++;
   return r;
 }
 

@@ -87,8 +87,9 @@ class ProblemDef:
 def csc_from_csr(n_vars: int, row_start, row_col, row_val):
     """Stable transpose (problem.hpp:211-225): entries of column i list their rows ascending."""
     n_cons = len(row_start) - 1
-    rows = np.repeat(np.arange(n_cons, dtype=np.int32), np.diff(row_start))
-    order = np.argsort(row_col, kind="stable")
+    rows = np.repeat(np.arange(n_cons, dtype=np.int64), np.diff(row_start))
+    # (col, row) keys are unique, so any sort is the stable transpose
+    order = np.argsort(np.asarray(row_col, dtype=np.int64) * max(n_cons, 1) + rows)
     counts = np.bincount(row_col, minlength=n_vars)
     col_start = np.zeros(n_vars + 1, dtype=np.int32)
     np.cumsum(counts, out=col_start[1:])

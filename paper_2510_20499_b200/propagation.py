@@ -263,16 +263,22 @@ def propagate(p: ProblemDef, b: BoundsState, lim: PropagationLimits | None = Non
     return PropagationResult(PropagationStatus(res.status), int(res.rounds), int(res.crossed_vars))
 
 
+FORCE_FRONTIER = 1
+
+
 def propagate_device(p: ProblemDef, d_bounds_ptr: int, infeasible: bool = False,
-                     lim: PropagationLimits | None = None, stream_ptr: int = 0):
+                     lim: PropagationLimits | None = None, stream_ptr: int = 0, flags: int = 0,
+                     d_stats_ptr: int = 0):
     """Device-resident variant: ``d_bounds_ptr`` is a device pointer to 2n doubles (e.g. a torch
-    tensor's ``data_ptr()``). Returns (PropagationResult, infeasible)."""
+    tensor's ``data_ptr()``). ``flags``/``d_stats_ptr`` as bp_propagate_ex.
+    Returns (PropagationResult, infeasible)."""
     dp = device_problem(p)
     inf = C.c_int32(1 if infeasible else 0)
     res = _lib.bp_result()
     ls = _lib.limits_struct(lim)
-    _lib.check(_lib.lib().bp_propagate_device(dp.h, C.c_void_p(d_bounds_ptr), C.byref(inf),
-                                              C.byref(ls), C.byref(res),
-                                              C.c_void_p(stream_ptr) if stream_ptr else None))
+    _lib.check(_lib.lib().bp_propagate_ex(dp.h, C.c_void_p(d_bounds_ptr), C.byref(inf),
+                                          C.byref(ls), C.byref(res),
+                                          C.c_void_p(stream_ptr) if stream_ptr else None,
+                                          int(flags), C.c_void_p(d_stats_ptr) if d_stats_ptr else None))
     return PropagationResult(PropagationStatus(res.status), int(res.rounds),
                              int(res.crossed_vars)), bool(inf.value)

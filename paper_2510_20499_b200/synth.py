@@ -25,7 +25,13 @@ def _distinct_cols(rng, lengths, n, col_sampler):
     m = lengths.size
     rows = np.repeat(np.arange(m, dtype=np.int64), lengths)
     cols = col_sampler(rows.size).astype(np.int64)
-    key = np.unique(rows * n + cols)  # sorted by (row, col), distinct
+    key = rows * n + cols
+    key.sort()
+    if key.size:
+        keep = np.empty(key.size, dtype=bool)
+        keep[0] = True
+        np.not_equal(key[1:], key[:-1], out=keep[1:])
+        key = key[keep]  # sorted by (row, col), distinct
     r = (key // n).astype(np.int64)
     c = (key % n).astype(np.int32)
     row_start = np.zeros(m + 1, dtype=np.int64)
