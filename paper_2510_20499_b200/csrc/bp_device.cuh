@@ -16,7 +16,6 @@ enum { BP_STATUS_UNSET = -1, BP_STATUS_TIGHTENED = 0, BP_STATUS_INFEASIBLE = 1, 
 
 constexpr int kSumSegment = 16384;   // problem.hpp:274
 constexpr int kShortNnz   = 32;      // rows/cols at or below: one lane each
-constexpr int kSegNnz     = 2048;    // rows above: producer/consumer warp pair per 16384-segment
 constexpr double kIntEps  = 1e-6;    // common.hpp:24
 
 // Row record gathered by the tightening sweep: one 32-byte sector, one LDG.256.
@@ -171,6 +170,20 @@ __device__ __forceinline__ void fold_entry(Fold& f, double lo, double up, bool i
   }
 }
 
+// The same rule as fold_entry, returned as this entry's lower-bound candidate (or -inf) and
+// upper-bound candidate (or +inf). Per entry at most one candidate of each kind exists, and the
+// sentinels are never taken by the strict comparisons of the fold, so folding these in CSC order
+// is the reference's tighten_variable loop.
+__device__ __forceinline__ void entry_candidates(double lo, double up, bool integer, double a,
+                                                 const RowRec& r, const double2* aux, int k,
+                                                 double& cl, double& cu)
+{
+  Fold f{-INFINITY, -1, INFINITY, -1};
+  fold_entry(f, lo, up, integer, a, r, aux, k, 0);
+  cl = f.lo;
+  cu = f.up;
+}
+
 // Combine two partial folds of disjoint position sets (lexicographic (value, position)).
 __device__ __forceinline__ void fold_combine(Fold& f, double olo, int olo_pos, double oup,
                                              int oup_pos)
@@ -209,22 +222,32 @@ struct DevProblem {
   const double* col_val;
   const double2* cons;      // (lower, upper) per row
   const uint8_t* is_int;
-  // rows with nnz <= kShortNnz, natural order (lane per row)
-  int n_srow;
-  const int* srow;
-  // rows with kShortNnz < nnz <= kSegNnz, nnz descending (warp per row)
-  int n_mrow;
-  const int* mrow;
-  // segment tasks of rows with nnz > kSegNnz: (row, segment), longest rows first
+  // Short rows (nnz <= kShortNnz) packed contiguously in natural order and grouped into tiles of
+  // <= 32 rows / <= kTile entries: a warp loads a tile coalesced, every lane folds one row.
+  int n_srow, n_srtile;
+  const int* srow;          // packed index -> row id
+  const int* sr_ptr;        // n_srow + 1 offsets into sr_col / sr_val
+  const int* sr_col;
+  const double* sr_val;
+  const int* sr_tile;       // n_srtile + 1 packed-row starts
+  // Long rows (nnz > kShortNnz): one warp task per 16384-entry segment, longest first.
   int n_seg;
-  const int2* seg_task;
-  const int* seg_base;      // per row (m entries; -1 if not segmented): first partial slot
-  // columns: nnz <= kShortNnz natural order (lane per var) / longer, nnz descending (warp per var)
-  int n_scol;
+  const int2* seg_task;     // (row, segment)
+  const int* seg_base;      // per row: first partial slot if the row has > 1 segment, else -1
+  // Short columns, packed the same way (tile lanes fold one variable each).
+  int n_scol, n_sctile;
   const int* scol;
+  const int* sc_ptr;
+  const int* sc_row;
+  const double* sc_val;
+  const uint8_t* sc_own;    // owner's local index inside its tile, per packed entry
+  const int* sc_tile;
+  // Long columns (nnz > kShortNnz), nnz descending: one warp per variable.
   int n_mcol;
   const int* mcol;
 };
+
+constexpr int kTile = 128;  // entries per tile / per streamed chunk (4 per lane)
 
 struct SegPart {
   double min, max;

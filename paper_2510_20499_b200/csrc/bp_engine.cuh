@@ -55,12 +55,11 @@ struct DBuf {
 
 // Per-round frontier/counter block (double-buffered by round parity).
 struct ParCtl {
-  int n_drow_all, n_drow_s, n_drow_m, n_dseg;  // staged together (stage_rows)
-  int n_dvar_s, n_dvar_m;                      // staged together (stage_vars)
-  int n_changed, n_crossed;
-  int any_rows, cur_seg, cur_m, cur_s;
-  int cur_vm, cur_vs, cur_x1, cur_x2;
-  int n_xtask, stop;
+  int n_drow_s, n_dseg, n_drow_all;  // staged together (stage_rows)
+  int n_dvar_s, n_dvar_m;            // staged together (stage_vars)
+  int n_changed, n_crossed, any_rows;
+  int cur_seg, cur_s, cur_vm, cur_vs;
+  int cur_x1, cur_x2, n_xtask, stop;
   unsigned long long colnnz, roww, colw;
   int pad[2];
 };
@@ -80,9 +79,7 @@ struct DevState {
   int* seg_done;
   unsigned* row_stamp;
   unsigned* var_stamp;
-  int* drow_all[2];
   int* drow_s[2];
-  int* drow_m[2];
   int2* dseg[2];
   int2* xtask[2];  // (row, 256-entry chunk) tasks for var expansion
   int* dvar_s[2];
@@ -99,15 +96,20 @@ struct Problem {
   long long nnz = 0;
   // host copies kept for classification of caller-supplied lists
   std::vector<int> h_row_start, h_col_start;
-  std::vector<int> h_seg_base;
-  // device arrays
+  // device arrays: the matrix twice
   DBuf<int> row_start, row_col, col_start, col_row;
   DBuf<double> row_val, col_val;
   DBuf<double2> cons;
   DBuf<uint8_t> is_int;
-  DBuf<int> srow, mrow, scol, mcol, seg_base;
+  // partition tables (see DevProblem)
+  DBuf<int> srow, sr_ptr, sr_col, sr_tile;
+  DBuf<double> sr_val;
+  DBuf<int> scol, sc_ptr, sc_row, sc_tile;
+  DBuf<double> sc_val;
+  DBuf<uint8_t> sc_own;
   DBuf<int2> seg_task;
-  int n_srow = 0, n_mrow = 0, n_scol = 0, n_mcol = 0, n_seg = 0;
+  DBuf<int> seg_base, mcol;
+  int n_srow = 0, n_srtile = 0, n_scol = 0, n_sctile = 0, n_seg = 0, n_mcol = 0, n_part = 0;
   // workspace
   DBuf<double2> bounds;
   DBuf<RowRec> rec;
@@ -140,13 +142,13 @@ struct RunResult {
   int status, rounds, crossed;
 };
 
-// Runs the persistent kernel on the device-resident working bounds P.st.bounds.
-// For MODE_ACTIVITY / MODE_TIGHTEN with lists, the frontier lists of parity 1 must be staged.
 // flags: ENGINE_FORCE_FRONTIER never substitutes a full round for a large frontier (the exact
 // reference trajectory of dirty sets, used to count its work); stats (device, kStatCols per round)
 // receives per-round work counts when non-null.
 enum { ENGINE_FORCE_FRONTIER = 1 };
-constexpr int kStatCols = 6;  // full, |R|, row nnz visits, |V|, col nnz visits, |changed|
+// full, |R|, row nnz visits, |V|, col nnz visits, |changed|, then phase-end times (ns since
+// kernel start): activity, tightening, row expansion, var expansion
+constexpr int kStatCols = 10;
 RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s,
                      int flags = 0, long long* d_stats = nullptr);
 

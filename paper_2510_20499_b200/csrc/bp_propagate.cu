@@ -6,21 +6,27 @@
 //   round r:  Phase A  row activities      (propagation.hpp:226-251)   ─ grid.sync
 //             Phase B  bound tightening    (propagation.hpp:378-412)   ─ grid.sync
 //             decision: infeasible / fixpoint / round cap / empty frontier (uniform on every block)
-//             Phase C  frontier: changed vars → dirty rows (+ segment/expansion tasks)  ─ grid.sync
-//             Phase D  dirty rows → dirty vars                                            ─ grid.sync
+//             Phase C  frontier: changed vars → dirty rows (+ segment / expansion tasks) ─ grid.sync
+//             Phase D  dirty rows → dirty vars                                           ─ grid.sync
 //
-// Work partition (replaces the reference's LRB bins, propagation.hpp:97-141):
-//   rows  nnz <= 32        one lane per row, sequential fold (exact reference order)
-//         32 < nnz <= 2048 one warp per row: lanes gather/multiply, lanes 0/1 fold min/max chains
-//         nnz > 2048       one producer/consumer warp PAIR per 16384-entry segment; the last
-//                          segment to finish sums the partials in segment order (heavy_row_activity,
-//                          propagation.hpp:197-218) — identical bits to the sequential sum.
-//   vars  col nnz <= 32    one lane per var, sequential CSC fold
-//         col nnz > 32     one warp per var; the std::min/max fold is reduced as a lexicographic
-//                          (value, CSC position) min/max, which reproduces "first operand wins on
-//                          ties" (sign of tied zeros) exactly.
+// The path is a sparse gather: its cost is memory-level parallelism, not arithmetic. Work is
+// therefore organised so every warp keeps 4 independent gathers per lane in flight:
+//   rows  nnz <= 32   packed tiles (<= 32 rows, <= 128 entries): the warp loads a tile coalesced,
+//                     gathers all bounds at once, and each lane folds one row in reference order
+//                     from shared memory (exact: same sequential sum).
+//         nnz > 32    one warp per 16384-entry segment (the reference's fixed summation tree,
+//                     problem.hpp:274), software-pipelined in 128-entry chunks (loads two chunks
+//                     ahead, gathers one chunk ahead of the fold); zero contributions are
+//                     compacted away (exact: the running sum starts at +0.0 and is never -0.0);
+//                     lanes 0/1 fold the min/max chains. Multi-segment rows are summed by the
+//                     last segment to finish, in segment order (heavy_row_activity, :197-218).
+//   vars  nnz <= 32   packed tiles; lanes gather row records (one LDG.256 each) and compute
+//                     per-entry candidates; each lane folds one variable in CSC order.
+//         nnz > 32    one warp per variable; the std::min/max fold is reduced as a lexicographic
+//                     (value, CSC position) min/max, which reproduces "first operand wins on
+//                     ties" (sign of tied zeros) exactly.
 // Frontier rounds (propagation.hpp:456-479) touch only dirty rows / dirty vars; when the frontier
-// would cover a large fraction of the matrix the engine runs a full round instead — evaluating a
+// would cost about as much as the whole matrix the engine runs a full round instead — evaluating a
 // superset of the dirty sets yields bit-identical results (SURVEY §8a A12 lemma).
 #include <cooperative_groups.h>
 
@@ -37,11 +43,11 @@ long long g_kernel_launches = 0;
 
 namespace {
 
-constexpr int kThreads   = 256;
-constexpr int kWarps     = kThreads / 32;
-constexpr int kPairs     = kWarps / 2;
-constexpr unsigned FULL  = 0xffffffffu;
-constexpr int kXChunk    = 256;  // entries per var-expansion task
+constexpr int kThreads  = 256;
+constexpr int kWarps    = kThreads / 32;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kXChunk   = 256;  // entries per var-expansion task
+constexpr int kEPL      = kTile / 32;
 
 __device__ __forceinline__ unsigned lanemask_lt()
 {
@@ -49,14 +55,19 @@ __device__ __forceinline__ unsigned lanemask_lt()
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
-__device__ __forceinline__ void named_bar(int id, int count)
-{
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 __device__ __forceinline__ int warp_sum(int v)
 {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_incl_scan(int v, int lane)
+{
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
   return v;
 }
 __device__ __forceinline__ unsigned long long globaltimer()
@@ -65,22 +76,28 @@ __device__ __forceinline__ unsigned long long globaltimer()
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ int ld_volatile(const int* p) { return *(const volatile int*)p; }
-__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p)
+__device__ __forceinline__ int ldv(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ unsigned long long ldv(const unsigned long long* p)
 {
   return *(const volatile unsigned long long*)p;
 }
 
+struct WarpSmem {
+  double b0[kTile];          // min contributions / lower-bound candidates
+  double b1[kTile];          // max contributions / upper-bound candidates
+  unsigned char fl[kTile];   // infinite-contributor flags (bit 0 min, bit 1 max)
+  int off[32];               // list tiles: exclusive entry offsets of the 32 items
+  int st[32];                //             their first entry
+  double2 vb[32];            // tighten tiles: the 32 variables' bounds
+  unsigned char vint[32];    //                and integrality
+  int chg[64];               // changed-var staging before a global append
+};
+
 struct Smem {
-  double pair_buf[kPairs][2][2][64];  // [pair][buffer][chain][entry]
-  int pair_cnt[kPairs][2][2];
-  int pair_inf[kPairs][2];
-  double warp_buf[kWarps][2][128];    // medium-row fold staging
-  int chg[kWarps][64];                // changed-var staging before a global append
+  WarpSmem w[kWarps];
   int blk_crossed;
   int blk_any_rows;
   unsigned long long blk_colnnz;
-  int fetch[kWarps];
 };
 
 struct Ctx {
@@ -88,8 +105,40 @@ struct Ctx {
   const DevState& S;
   const Limits& lim;
   Smem& sm;
-  int lane, warp, gwarp, nwarps;
+  WarpSmem& w;
+  int lane, warp;
 };
+
+// Allocates `cnt` slots per lane in a global list with one atomic per warp; returns this lane's
+// first slot.
+__device__ __forceinline__ int warp_alloc(int* counter, int cnt, int lane)
+{
+  const int incl  = warp_incl_scan(cnt, lane);
+  const int total = __shfl_sync(FULL, incl, 31);
+  int base        = 0;
+  if (total) {
+    if (lane == 31) base = atomicAdd(counter, total);
+    base = __shfl_sync(FULL, base, 31);
+  }
+  return base + incl - cnt;
+}
+
+// Largest o with off[o] <= f (off non-decreasing, off[0] = 0): the list item owning entry f.
+__device__ __forceinline__ int owner_of(const int* off, int f)
+{
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step; step >>= 1)
+    if (off[o + step] <= f) o += step;
+  return o;
+}
+
+__device__ __forceinline__ int warp_fetch(Ctx& c, int* cursor, int step)
+{
+  int t = 0;
+  if (c.lane == 0) t = atomicAdd(cursor, step);
+  return __shfl_sync(FULL, t, 0);
+}
 
 // ------------------------------------------------------------------ row activities
 
@@ -106,263 +155,248 @@ __device__ __forceinline__ void write_rec(const DevProblem& P, const DevState& S
   if (imn | imx) S.aux[k] = make_double2(smn, smx);
 }
 
-// nnz <= 32: one lane, sequential (single segment: total = 0.0 + part = part, part != -0.0).
-__device__ void row_activity_lane(const DevProblem& P, const DevState& S, int k)
-{
-  const int rs = __ldg(P.row_start + k), re = __ldg(P.row_start + k + 1);
-  double smn = 0.0, smx = 0.0;
-  int imn = 0, imx = 0;
-#pragma unroll 4
-  for (int e = rs; e < re; ++e) {
-    const int c    = __ldg(P.row_col + e);
-    const double a = __ldg(P.row_val + e);
-    const double2 b = S.bounds[c];
-    double cmn, cmx;
-    int i1, i2;
-    contrib(a, b.x, b.y, cmn, cmx, i1, i2);
-    smn = __dadd_rn(smn, cmn);
-    smx = __dadd_rn(smx, cmx);
-    imn += i1;
-    imx += i2;
-  }
-  write_rec(P, S, k, smn, smx, imn, imx);
-}
-
-// 32 < nnz <= 2048: one warp; lanes produce 128 contributions per step, lanes 0/1 fold.
-__device__ void row_activity_warp(Ctx& c, int k)
+// One 16384-entry segment of a long row, streamed by one warp.
+__device__ void row_stream(Ctx& c, int k, int seg)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  double(*wb)[128]    = c.sm.warp_buf[c.warp];
+  const int lane      = c.lane;
   const int rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
-  double acc = 0.0;
-  int imn = 0, imx = 0;
-  for (int base = 0; base < L; base += 128) {
+  const int e0 = rs + seg * kSumSegment, e1 = rs + min(L, (seg + 1) * kSumSegment);
+  const int nch = (e1 - e0 + kTile - 1) / kTile;
+  int ca[kEPL], cb[kEPL];
+  double va[kEPL], vb[kEPL];
+  double2 bd[kEPL];
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int j = base + h * 32 + c.lane;
-      double cmn = 0.0, cmx = 0.0;
-      if (j < L) {
-        const int col  = __ldg(P.row_col + rs + j);
-        const double a = __ldg(P.row_val + rs + j);
-        const double2 b = S.bounds[col];
-        int i1, i2;
-        contrib(a, b.x, b.y, cmn, cmx, i1, i2);
-        imn += i1;
-        imx += i2;
-      }
-      wb[0][h * 32 + c.lane] = cmn;
-      wb[1][h * 32 + c.lane] = cmx;
-    }
-    __syncwarp();
-    if (c.lane < 2) {
-      const int cnt     = min(128, L - base);
-      const double* src = wb[c.lane];
-#pragma unroll 8
-      for (int j = 0; j < cnt; ++j) acc = __dadd_rn(acc, src[j]);
-    }
-    __syncwarp();
+  for (int h = 0; h < kEPL; ++h) {
+    const int e = e0 + h * 32 + lane;
+    ca[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
+    va[h]       = e < e1 ? __ldg(P.row_val + e) : 0.0;
   }
-  imn = warp_sum(imn);
-  imx = warp_sum(imx);
-  const double smx = __shfl_sync(FULL, acc, 1);
-  if (c.lane == 0) write_rec(P, S, k, acc, smx, imn, imx);
-}
-
-// nnz > 2048: producer warp computes and zero-compacts contributions of 64 entries per step into a
-// double buffer; consumer lanes 0/1 fold the min/max chains in entry order. Skipping zero
-// contributions is exact: the running sum starts at +0.0 and is never -0.0.
-__device__ void row_segment_pair(Ctx& c, int k, int seg, bool producer, int pair)
-{
-  const DevProblem& P = c.P;
-  const DevState& S   = c.S;
-  double(*pb)[2][64]  = c.sm.pair_buf[pair];
-  int(*pcnt)[2]       = c.sm.pair_cnt[pair];
-  int* pinf           = c.sm.pair_inf[pair];
-  const int bar       = 1 + pair;
-  const int rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
-  const int e0 = seg * kSumSegment, e1 = min(L, e0 + kSumSegment);
-  const int nch = (e1 - e0 + 63) >> 6;
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) bd[h] = ca[h] >= 0 ? S.bounds[ca[h]] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    const int e = e0 + kTile + h * 32 + lane;
+    cb[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
+    vb[h]       = e < e1 ? __ldg(P.row_val + e) : 0.0;
+  }
   double acc = 0.0;
   int imn = 0, imx = 0;
   const unsigned lt = lanemask_lt();
-  for (int step = 0; step <= nch; ++step) {
-    if (producer) {
-      if (step < nch) {
-        const int bb = step & 1, base = e0 + (step << 6);
-        double cm[2], cx[2];
+  for (int s = 0; s < nch; ++s) {
+    double cm[kEPL], cx[kEPL];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int e = base + h * 32 + c.lane;
-          cm[h] = 0.0;
-          cx[h] = 0.0;
-          if (e < e1) {
-            const int col  = __ldg(P.row_col + rs + e);
-            const double a = __ldg(P.row_val + rs + e);
-            const double2 b = S.bounds[col];
-            int i1, i2;
-            contrib(a, b.x, b.y, cm[h], cx[h], i1, i2);
-            imn += i1;
-            imx += i2;
-          }
-        }
-        const unsigned m0 = __ballot_sync(FULL, cm[0] != 0.0);
-        const unsigned m1 = __ballot_sync(FULL, cm[1] != 0.0);
-        const unsigned x0 = __ballot_sync(FULL, cx[0] != 0.0);
-        const unsigned x1 = __ballot_sync(FULL, cx[1] != 0.0);
-        if (cm[0] != 0.0) pb[bb][0][__popc(m0 & lt)] = cm[0];
-        if (cm[1] != 0.0) pb[bb][0][__popc(m0) + __popc(m1 & lt)] = cm[1];
-        if (cx[0] != 0.0) pb[bb][1][__popc(x0 & lt)] = cx[0];
-        if (cx[1] != 0.0) pb[bb][1][__popc(x0) + __popc(x1 & lt)] = cx[1];
-        if (c.lane == 0) {
-          pcnt[bb][0] = __popc(m0) + __popc(m1);
-          pcnt[bb][1] = __popc(x0) + __popc(x1);
-        }
+    for (int h = 0; h < kEPL; ++h) {
+      cm[h] = 0.0;
+      cx[h] = 0.0;
+      if (ca[h] >= 0) {
+        int i1, i2;
+        contrib(va[h], bd[h].x, bd[h].y, cm[h], cx[h], i1, i2);
+        imn += i1;
+        imx += i2;
       }
-    } else if (step >= 1 && c.lane < 2) {
-      const int bb      = (step - 1) & 1;
-      const int cnt     = pcnt[bb][c.lane];
-      const double* src = pb[bb][c.lane];
+    }
+    // gather chunk s+1 (its columns arrived one iteration ago), load chunk s+2
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      bd[h] = cb[h] >= 0 ? S.bounds[cb[h]] : make_double2(0.0, 0.0);
+      ca[h] = cb[h];
+      va[h] = vb[h];
+    }
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int e = e0 + (s + 2) * kTile + h * 32 + lane;
+      cb[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
+      vb[h]       = e < e1 ? __ldg(P.row_val + e) : 0.0;
+    }
+    // order-preserving compaction of the non-zero contributions of each chain
+    int pm = 0, px = 0;
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const unsigned m = __ballot_sync(FULL, cm[h] != 0.0);
+      const unsigned x = __ballot_sync(FULL, cx[h] != 0.0);
+      if (cm[h] != 0.0) c.w.b0[pm + __popc(m & lt)] = cm[h];
+      if (cx[h] != 0.0) c.w.b1[px + __popc(x & lt)] = cx[h];
+      pm += __popc(m);
+      px += __popc(x);
+    }
+    __syncwarp();
+    if (lane < 2) {
+      const int cnt     = lane ? px : pm;
+      const double* src = lane ? c.w.b1 : c.w.b0;
 #pragma unroll 4
       for (int j = 0; j < cnt; ++j) acc = __dadd_rn(acc, src[j]);
     }
-    named_bar(bar, 64);
+    __syncwarp();
   }
-  if (producer) {
-    imn = warp_sum(imn);
-    imx = warp_sum(imx);
-    if (c.lane == 0) {
-      pinf[0] = imn;
-      pinf[1] = imx;
-    }
-  }
-  named_bar(bar, 64);
-  if (!producer) {
-    const double smx = __shfl_sync(FULL, acc, 1);
-    if (c.lane == 0) {
-      const int nseg = (L + kSumSegment - 1) / kSumSegment;
-      if (nseg == 1) {
-        write_rec(P, S, k, acc, smx, pinf[0], pinf[1]);
-      } else {
-        const int base = __ldg(P.seg_base + k);
-        SegPart sp;
-        sp.min  = acc;
-        sp.max  = smx;
-        sp.nmin = pinf[0];
-        sp.nmax = pinf[1];
-        sp.pad0 = sp.pad1 = 0;
-        S.seg_part[base + seg] = sp;
+  imn              = warp_sum(imn);
+  imx              = warp_sum(imx);
+  const double smx = __shfl_sync(FULL, acc, 1);
+  if (lane == 0) {
+    const int nseg = (L + kSumSegment - 1) / kSumSegment;
+    if (nseg == 1) {
+      write_rec(P, S, k, acc, smx, imn, imx);  // 0.0 + part == part (part is never -0.0)
+    } else {
+      const int base = __ldg(P.seg_base + k);
+      SegPart sp;
+      sp.min  = acc;
+      sp.max  = smx;
+      sp.nmin = imn;
+      sp.nmax = imx;
+      sp.pad0 = sp.pad1 = 0;
+      S.seg_part[base + seg] = sp;
+      __threadfence();
+      const int done = atomicAdd(&S.seg_done[k], 1);
+      if (done == nseg - 1) {
         __threadfence();
-        const int done = atomicAdd(&S.seg_done[k], 1);
-        if (done == nseg - 1) {
-          __threadfence();
-          double tmn = 0.0, tmx = 0.0;
-          int cmn = 0, cmx = 0;
-          for (int s = 0; s < nseg; ++s) {  // row_activity's segment fold (propagation.hpp:182-188)
-            const SegPart* q = S.seg_part + base + s;
-            tmn = __dadd_rn(tmn, __ldcg(&q->min));
-            tmx = __dadd_rn(tmx, __ldcg(&q->max));
-            cmn += __ldcg(&q->nmin);
-            cmx += __ldcg(&q->nmax);
-          }
-          write_rec(P, S, k, tmn, tmx, cmn, cmx);
-          S.seg_done[k] = 0;
+        double tmn = 0.0, tmx = 0.0;
+        int cmn = 0, cmx = 0;
+        for (int q = 0; q < nseg; ++q) {  // row_activity's segment fold (propagation.hpp:182-188)
+          const SegPart* p = S.seg_part + base + q;
+          tmn = __dadd_rn(tmn, __ldcg(&p->min));
+          tmx = __dadd_rn(tmx, __ldcg(&p->max));
+          cmn += __ldcg(&p->nmin);
+          cmx += __ldcg(&p->nmax);
         }
+        write_rec(P, S, k, tmn, tmx, cmn, cmx);
+        S.seg_done[k] = 0;
       }
     }
   }
-  named_bar(bar, 64);
 }
 
-// Dynamic work cursor shared by a warp.
-__device__ __forceinline__ int warp_fetch(Ctx& c, int* cursor, int step)
+// Contributions of up to 128 gathered entries into shared memory (slot h*32+lane).
+__device__ __forceinline__ void stage_contribs(Ctx& c, const int* col, const double* a)
 {
-  int t = 0;
-  if (c.lane == 0) t = atomicAdd(cursor, step);
-  return __shfl_sync(FULL, t, 0);
+  double2 bd[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) bd[h] = col[h] >= 0 ? c.S.bounds[col[h]] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    double cm = 0.0, cx = 0.0;
+    int i1 = 0, i2 = 0;
+    if (col[h] >= 0) contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
+    c.w.b0[h * 32 + c.lane] = cm;
+    c.w.b1[h * 32 + c.lane] = cx;
+    c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
+  }
 }
 
-// Phase A. full: every row from the static partition tables; else: the frontier lists.
-__device__ void phase_activity(Ctx& c, ParCtl* pc, bool full)
+// A packed tile of short rows (full rounds).
+__device__ void act_tile_packed(Ctx& c, int t)
+{
+  const DevProblem& P = c.P;
+  const int r0 = __ldg(P.sr_tile + t), r1 = __ldg(P.sr_tile + t + 1);
+  const int p0 = __ldg(P.sr_ptr + r0), p1 = __ldg(P.sr_ptr + r1);
+  int col[kEPL];
+  double a[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    const int f = p0 + h * 32 + c.lane;
+    col[h]      = f < p1 ? __ldg(P.sr_col + f) : -1;
+    a[h]        = f < p1 ? __ldg(P.sr_val + f) : 0.0;
+  }
+  stage_contribs(c, col, a);
+  __syncwarp();
+  if (c.lane < r1 - r0) {
+    const int r  = r0 + c.lane;
+    const int q0 = __ldg(P.sr_ptr + r) - p0, q1 = __ldg(P.sr_ptr + r + 1) - p0;
+    double smn = 0.0, smx = 0.0;
+    int imn = 0, imx = 0;
+    for (int q = q0; q < q1; ++q) {
+      smn = __dadd_rn(smn, c.w.b0[q]);
+      smx = __dadd_rn(smx, c.w.b1[q]);
+      imn += c.w.fl[q] & 1;
+      imx += c.w.fl[q] >> 1;
+    }
+    write_rec(P, c.S, __ldg(P.srow + r), smn, smx, imn, imx);
+  }
+  __syncwarp();
+}
+
+// Up to 32 listed items (rows or columns) as one flattened entry stream: returns this lane's
+// item range [excl, excl + L) and the stream length; fills w.off / w.st.
+__device__ __forceinline__ int list_tile_setup(Ctx& c, int first, int len, int& excl)
+{
+  const int incl = warp_incl_scan(len, c.lane);
+  excl           = incl - len;
+  c.w.off[c.lane] = excl;
+  c.w.st[c.lane]  = first;
+  __syncwarp();
+  return __shfl_sync(FULL, incl, 31);
+}
+
+// Listed short rows (frontier rounds): flattened 128-entry windows, each lane folds its row.
+__device__ void act_list_tile(Ctx& c, const int* ids, int base, int n)
+{
+  const DevProblem& P = c.P;
+  const int j = base + c.lane;
+  const int k = j < n ? ids[j] : -1;
+  int rs = 0, L = 0;
+  if (k >= 0) {
+    rs = __ldg(P.row_start + k);
+    L  = __ldg(P.row_start + k + 1) - rs;
+  }
+  int excl;
+  const int T = list_tile_setup(c, rs, L, excl);
+  double smn = 0.0, smx = 0.0;
+  int imn = 0, imx = 0;
+  for (int w0 = 0; w0 < T; w0 += kTile) {
+    int col[kEPL];
+    double a[kEPL];
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int f = w0 + h * 32 + c.lane;
+      col[h]      = -1;
+      a[h]        = 0.0;
+      if (f < T) {
+        const int o = owner_of(c.w.off, f);
+        const int e = c.w.st[o] + (f - c.w.off[o]);
+        col[h]      = __ldg(P.row_col + e);
+        a[h]        = __ldg(P.row_val + e);
+      }
+    }
+    stage_contribs(c, col, a);
+    __syncwarp();
+    if (k >= 0) {
+      const int q0 = max(excl, w0) - w0, q1 = min(excl + L, w0 + kTile) - w0;
+      for (int q = q0; q < q1; ++q) {
+        smn = __dadd_rn(smn, c.w.b0[q]);
+        smx = __dadd_rn(smx, c.w.b1[q]);
+        imn += c.w.fl[q] & 1;
+        imx += c.w.fl[q] >> 1;
+      }
+    }
+    __syncwarp();
+  }
+  if (k >= 0) write_rec(P, c.S, k, smn, smx, imn, imx);
+}
+
+// Phase A. full: every row from the static partition tables; else the frontier lists.
+__device__ void phase_activity(Ctx& c, ParCtl* pc, int par, bool full)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int par       = (&c.S.ctl->par[1] == pc) ? 1 : 0;
-  // 1) segment tasks (longest rows first) on warp pairs, static stride.
   {
-    const int n_seg   = full ? P.n_seg : ld_volatile(&pc->n_dseg);
+    const int n       = full ? P.n_seg : ldv(&pc->n_dseg);
     const int2* tasks = full ? P.seg_task : S.dseg[par];
-    const int pair    = c.warp >> 1;
-    const bool prod   = (c.warp & 1) == 0;
-    const int gpair   = blockIdx.x * kPairs + pair;
-    const int npairs  = gridDim.x * kPairs;
-    for (int t = gpair; t < n_seg; t += npairs) {
+    for (int t = warp_fetch(c, &pc->cur_seg, 1); t < n; t = warp_fetch(c, &pc->cur_seg, 1)) {
       const int2 tk = tasks[t];
-      row_segment_pair(c, tk.x, tk.y, prod, pair);
+      row_stream(c, tk.x, tk.y);
     }
   }
-  // 2) medium rows, one warp each (dynamic).
-  {
-    const int n    = full ? P.n_mrow : ld_volatile(&pc->n_drow_m);
-    const int* ids = full ? P.mrow : S.drow_m[par];
-    for (int t = warp_fetch(c, &pc->cur_m, 1); t < n; t = warp_fetch(c, &pc->cur_m, 1))
-      row_activity_warp(c, full ? __ldg(ids + t) : ids[t]);
-  }
-  // 3) short rows, one lane each, tiles of 32 (dynamic).
-  {
-    const int n    = full ? P.n_srow : ld_volatile(&pc->n_drow_s);
-    const int* ids = full ? P.srow : S.drow_s[par];
-    for (int t = warp_fetch(c, &pc->cur_s, 32); t < n; t = warp_fetch(c, &pc->cur_s, 32)) {
-      const int j = t + c.lane;
-      if (j < n) row_activity_lane(P, S, full ? __ldg(ids + j) : ids[j]);
-    }
+  if (full) {
+    for (int t = warp_fetch(c, &pc->cur_s, 1); t < P.n_srtile; t = warp_fetch(c, &pc->cur_s, 1))
+      act_tile_packed(c, t);
+  } else {
+    const int n = ldv(&pc->n_drow_s);
+    for (int t = warp_fetch(c, &pc->cur_s, 32); t < n; t = warp_fetch(c, &pc->cur_s, 32))
+      act_list_tile(c, S.drow_s[par], t, n);
   }
 }
 
 // ------------------------------------------------------------------ tightening
-
-__device__ int tighten_lane(const DevProblem& P, const DevState& S, int i, const Limits& lim)
-{
-  const double2 b    = S.bounds[i];
-  const bool integer = __ldg(P.is_int + i) != 0;
-  Fold f{b.x, -1, b.y, -1};
-  const int cs = __ldg(P.col_start + i), ce = __ldg(P.col_start + i + 1);
-#pragma unroll 2
-  for (int e = cs; e < ce; ++e) {
-    const int k    = __ldg(P.col_row + e);
-    const double a = __ldg(P.col_val + e);
-    const RowRec r = ld_rec(S.rec + k);
-    fold_entry(f, b.x, b.y, integer, a, r, S.aux, k, e);
-  }
-  return finish_var(S.bounds + i, b.x, b.y, f.lo, f.up, integer, lim);
-}
-
-__device__ int tighten_warp(Ctx& c, int i)
-{
-  const DevProblem& P = c.P;
-  const DevState& S   = c.S;
-  const double2 b     = S.bounds[i];
-  const bool integer  = __ldg(P.is_int + i) != 0;
-  Fold f{b.x, -1, b.y, -1};
-  const int cs = __ldg(P.col_start + i), ce = __ldg(P.col_start + i + 1);
-  for (int e = cs + c.lane; e < ce; e += 32) {
-    const int k    = __ldg(P.col_row + e);
-    const double a = __ldg(P.col_val + e);
-    const RowRec r = ld_rec(S.rec + k);
-    fold_entry(f, b.x, b.y, integer, a, r, S.aux, k, e);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const double olo = __shfl_xor_sync(FULL, f.lo, o);
-    const int olp    = __shfl_xor_sync(FULL, f.lo_pos, o);
-    const double oup = __shfl_xor_sync(FULL, f.up, o);
-    const int oupp   = __shfl_xor_sync(FULL, f.up_pos, o);
-    fold_combine(f, olo, olp, oup, oupp);
-  }
-  int res = 0;
-  if (c.lane == 0) res = finish_var(S.bounds + i, b.x, b.y, f.lo, f.up, integer, c.lim);
-  return __shfl_sync(FULL, res, 0);
-}
 
 struct Tally {
   int crossed;
@@ -378,7 +412,7 @@ __device__ __forceinline__ void flush_changed(Ctx& c, ParCtl* pc, Tally& t)
   if (c.lane == 0) base = atomicAdd(&pc->n_changed, t.nbuf);
   base = __shfl_sync(FULL, base, 0);
   __syncwarp();
-  for (int j = c.lane; j < t.nbuf; j += 32) c.S.changed[base + j] = c.sm.chg[c.warp][j];
+  for (int j = c.lane; j < t.nbuf; j += 32) c.S.changed[base + j] = c.w.chg[j];
   __syncwarp();
   t.nbuf = 0;
 }
@@ -395,45 +429,192 @@ __device__ __forceinline__ void tally(Ctx& c, ParCtl* pc, Tally& t, int i, int r
   }
   if (ch) {
     if (t.nbuf + __popc(ch) > 64) flush_changed(c, pc, t);
-    if (r > 0) c.sm.chg[c.warp][t.nbuf + __popc(ch & lanemask_lt())] = i;
+    if (r > 0) c.w.chg[t.nbuf + __popc(ch & lanemask_lt())] = i;
     t.nbuf += __popc(ch);
     __syncwarp();
   }
 }
 
-__device__ void phase_tighten(Ctx& c, ParCtl* pc, bool full)
+// Long column: one warp, 4 row-record gathers per lane in flight, (value, position) reduction.
+__device__ int tighten_warp(Ctx& c, int i)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int par       = (&c.S.ctl->par[1] == pc) ? 1 : 0;
+  const double2 b     = S.bounds[i];
+  const bool integer  = __ldg(P.is_int + i) != 0;
+  Fold f{b.x, -1, b.y, -1};
+  const int cs = __ldg(P.col_start + i), ce = __ldg(P.col_start + i + 1);
+  for (int base = cs; base < ce; base += kTile) {
+    int k[kEPL];
+    double a[kEPL];
+    RowRec r[kEPL];
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int e = base + h * 32 + c.lane;
+      k[h]        = e < ce ? __ldg(P.col_row + e) : -1;
+      a[h]        = e < ce ? __ldg(P.col_val + e) : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h)
+      if (k[h] >= 0) r[h] = ld_rec(S.rec + k[h]);
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h)
+      if (k[h] >= 0) fold_entry(f, b.x, b.y, integer, a[h], r[h], S.aux, k[h], base + h * 32 + c.lane);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double olo = __shfl_xor_sync(FULL, f.lo, o);
+    const int olp    = __shfl_xor_sync(FULL, f.lo_pos, o);
+    const double oup = __shfl_xor_sync(FULL, f.up, o);
+    const int oupp   = __shfl_xor_sync(FULL, f.up_pos, o);
+    fold_combine(f, olo, olp, oup, oupp);
+  }
+  int res = 0;
+  if (c.lane == 0) res = finish_var(S.bounds + i, b.x, b.y, f.lo, f.up, integer, c.lim);
+  return __shfl_sync(FULL, res, 0);
+}
+
+// Candidates of up to 128 entries (row k[h], coefficient a[h], owner variable own[h] whose bounds
+// are in w.vb) into shared memory: b0 = lower-bound candidates, b1 = upper-bound candidates.
+__device__ __forceinline__ void stage_candidates(Ctx& c, const int* k, const double* a, const int* own)
+{
+  RowRec r[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h)
+    if (k[h] >= 0) r[h] = ld_rec(c.S.rec + k[h]);
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    double cl = -INFINITY, cu = INFINITY;
+    if (k[h] >= 0) {
+      const double2 b = c.w.vb[own[h]];
+      entry_candidates(b.x, b.y, c.w.vint[own[h]] != 0, a[h], r[h], c.S.aux, k[h], cl, cu);
+    }
+    c.w.b0[h * 32 + c.lane] = cl;
+    c.w.b1[h * 32 + c.lane] = cu;
+  }
+}
+
+// Packed tile of short columns (full rounds).
+__device__ void tighten_tile_packed(Ctx& c, int t, ParCtl* pc, Tally& ty)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int v0 = __ldg(P.sc_tile + t), v1 = __ldg(P.sc_tile + t + 1);
+  const int p0 = __ldg(P.sc_ptr + v0), p1 = __ldg(P.sc_ptr + v1);
+  int i = -1;
+  if (c.lane < v1 - v0) {
+    i                  = __ldg(P.scol + v0 + c.lane);
+    c.w.vb[c.lane]     = S.bounds[i];
+    c.w.vint[c.lane]   = __ldg(P.is_int + i);
+  }
+  int k[kEPL], own[kEPL];
+  double a[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    const int f = p0 + h * 32 + c.lane;
+    k[h]        = f < p1 ? __ldg(P.sc_row + f) : -1;
+    a[h]        = f < p1 ? __ldg(P.sc_val + f) : 0.0;
+    own[h]      = f < p1 ? __ldg(P.sc_own + f) : 0;
+  }
+  __syncwarp();
+  stage_candidates(c, k, a, own);
+  __syncwarp();
+  int res = 0;
+  if (i >= 0) {
+    const double2 b = c.w.vb[c.lane];
+    double nl = b.x, nu = b.y;
+    const int q0 = __ldg(P.sc_ptr + v0 + c.lane) - p0, q1 = __ldg(P.sc_ptr + v0 + c.lane + 1) - p0;
+    for (int q = q0; q < q1; ++q) {
+      const double cl = c.w.b0[q], cu = c.w.b1[q];
+      if (nl < cl) nl = cl;
+      if (cu < nu) nu = cu;
+    }
+    res = finish_var(S.bounds + i, b.x, b.y, nl, nu, c.w.vint[c.lane] != 0, c.lim);
+  }
+  tally(c, pc, ty, i, res);
+  __syncwarp();
+}
+
+// Listed short columns (frontier rounds).
+__device__ void tighten_list_tile(Ctx& c, const int* ids, int base, int n, ParCtl* pc, Tally& ty)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int j = base + c.lane;
+  const int i = j < n ? ids[j] : -1;
+  int cs = 0, L = 0;
+  double2 b = make_double2(0.0, 0.0);
+  bool integer = false;
+  if (i >= 0) {
+    cs      = __ldg(P.col_start + i);
+    L       = __ldg(P.col_start + i + 1) - cs;
+    b       = S.bounds[i];
+    integer = __ldg(P.is_int + i) != 0;
+  }
+  c.w.vb[c.lane]   = b;
+  c.w.vint[c.lane] = integer ? 1 : 0;
+  int excl;
+  const int T = list_tile_setup(c, cs, L, excl);
+  double nl = b.x, nu = b.y;
+  for (int w0 = 0; w0 < T; w0 += kTile) {
+    int k[kEPL], own[kEPL];
+    double a[kEPL];
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int f = w0 + h * 32 + c.lane;
+      k[h]        = -1;
+      a[h]        = 0.0;
+      own[h]      = 0;
+      if (f < T) {
+        const int o = owner_of(c.w.off, f);
+        const int e = c.w.st[o] + (f - c.w.off[o]);
+        k[h]        = __ldg(P.col_row + e);
+        a[h]        = __ldg(P.col_val + e);
+        own[h]      = o;
+      }
+    }
+    stage_candidates(c, k, a, own);
+    __syncwarp();
+    if (i >= 0) {
+      const int q0 = max(excl, w0) - w0, q1 = min(excl + L, w0 + kTile) - w0;
+      for (int q = q0; q < q1; ++q) {
+        const double cl = c.w.b0[q], cu = c.w.b1[q];
+        if (nl < cl) nl = cl;
+        if (cu < nu) nu = cu;
+      }
+    }
+    __syncwarp();
+  }
+  int res = 0;
+  if (i >= 0) res = finish_var(S.bounds + i, b.x, b.y, nl, nu, integer, c.lim);
+  tally(c, pc, ty, i, res);
+}
+
+__device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
   Tally t{0, 0, 0ull, 0};
   {
-    const int n    = full ? P.n_mcol : ld_volatile(&pc->n_dvar_m);
+    const int n    = full ? P.n_mcol : ldv(&pc->n_dvar_m);
     const int* ids = full ? P.mcol : S.dvar_m[par];
     for (int q = warp_fetch(c, &pc->cur_vm, 1); q < n; q = warp_fetch(c, &pc->cur_vm, 1)) {
-      const int i = full ? __ldg(ids + q) : ids[q];
+      const int i = ids[q];
       const int r = tighten_warp(c, i);
-      // lane 0 stands for the var; other lanes report nothing
       tally(c, pc, t, c.lane == 0 ? i : -1, c.lane == 0 ? r : 0);
     }
   }
-  {
-    const int n    = full ? P.n_scol : ld_volatile(&pc->n_dvar_s);
-    const int* ids = full ? P.scol : S.dvar_s[par];
-    for (int q = warp_fetch(c, &pc->cur_vs, 32); q < n; q = warp_fetch(c, &pc->cur_vs, 32)) {
-      const int j = q + c.lane;
-      int i = -1, r = 0;
-      if (j < n) {
-        i = full ? __ldg(ids + j) : ids[j];
-        r = tighten_lane(P, S, i, c.lim);
-      }
-      tally(c, pc, t, i, r);
-    }
+  if (full) {
+    for (int q = warp_fetch(c, &pc->cur_vs, 1); q < P.n_sctile; q = warp_fetch(c, &pc->cur_vs, 1))
+      tighten_tile_packed(c, q, pc, t);
+  } else {
+    const int n = ldv(&pc->n_dvar_s);
+    for (int q = warp_fetch(c, &pc->cur_vs, 32); q < n; q = warp_fetch(c, &pc->cur_vs, 32))
+      tighten_list_tile(c, S.dvar_s[par], q, n, pc, t);
   }
   flush_changed(c, pc, t);
-  // block reduction of the tallies, one global atomic each
-  int cr = warp_sum(t.crossed);
-  int ar = __any_sync(FULL, t.any_rows);
+  const int cr = warp_sum(t.crossed);
+  const int ar = __any_sync(FULL, t.any_rows);
   unsigned long long cn = t.colnnz;
 #pragma unroll
   for (int o = 16; o; o >>= 1) cn += __shfl_xor_sync(FULL, cn, o);
@@ -456,96 +637,104 @@ __device__ void phase_tighten(Ctx& c, ParCtl* pc, bool full)
 
 // ------------------------------------------------------------------ frontier
 
-__device__ __forceinline__ int warp_append(int* counter, bool pred, unsigned lt)
-{
-  const unsigned b = __ballot_sync(FULL, pred);
-  if (!b) return -1;
-  const int leader = __ffs(b) - 1;
-  int base         = 0;
-  if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(counter, __popc(b));
-  base = __shfl_sync(FULL, base, leader);
-  return pred ? base + __popc(b & lt) : -1;
-}
-
-// Phase C: rows(changed) → dirty rows of the next round, classified + var-expansion tasks.
+// Phase C: rows(changed) → next round's dirty rows: short rows, long-row segment tasks, and
+// 256-entry var-expansion tasks. 4 incidences per lane in flight.
 __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int nch       = ld_volatile(&pc->n_changed);
-  const unsigned lt   = lanemask_lt();
+  const int nch       = ldv(&pc->n_changed);
   unsigned long long roww = 0;
   for (int t = warp_fetch(c, &pc->cur_x1, 32); t < nch; t = warp_fetch(c, &pc->cur_x1, 32)) {
-    const int cnt = min(32, nch - t);
-    for (int q = 0; q < cnt; ++q) {
-      const int i  = S.changed[t + q];
-      const int cs = __ldg(P.col_start + i), ce = __ldg(P.col_start + i + 1);
-      for (int base = cs; base < ce; base += 32) {
-        const int e   = base + c.lane;
-        const bool ok = e < ce;
-        const int k   = ok ? __ldg(P.col_row + e) : 0;
-        const bool nw = ok && atomicExch(S.row_stamp + k, stamp) != stamp;
-        if (!__ballot_sync(FULL, nw)) continue;
-        const int L = nw ? __ldg(P.row_start + k + 1) - __ldg(P.row_start + k) : 0;
-        if (nw) roww += (unsigned long long)L;
-        int pos = warp_append(&qc->n_drow_all, nw, lt);
-        if (nw) S.drow_all[qpar][pos] = k;
-        const bool is_s = nw && L <= kShortNnz;
-        const bool is_m = nw && L > kShortNnz && L <= kSegNnz;
-        const bool is_g = nw && L > kSegNnz;
-        pos = warp_append(&qc->n_drow_s, is_s, lt);
-        if (is_s) S.drow_s[qpar][pos] = k;
-        pos = warp_append(&qc->n_drow_m, is_m, lt);
-        if (is_m) S.drow_m[qpar][pos] = k;
-        if (is_g) {
-          const int ns = (L + kSumSegment - 1) / kSumSegment;
-          const int b0 = atomicAdd(&qc->n_dseg, ns);
-          for (int s = 0; s < ns; ++s) S.dseg[qpar][b0 + s] = make_int2(k, s);
-        }
-        if (nw && L > 0) {
-          const int nx = (L + kXChunk - 1) / kXChunk;
-          const int b0 = atomicAdd(&qc->n_xtask, nx);
-          for (int s = 0; s < nx; ++s) S.xtask[qpar][b0 + s] = make_int2(k, s);
+    const int j = t + c.lane;
+    const int i = j < nch ? S.changed[j] : -1;
+    int cs = 0, L = 0;
+    if (i >= 0) {
+      cs = __ldg(P.col_start + i);
+      L  = __ldg(P.col_start + i + 1) - cs;
+    }
+    int excl;
+    const int T = list_tile_setup(c, cs, L, excl);
+    for (int w0 = 0; w0 < T; w0 += kTile) {
+      int k[kEPL];
+      bool nw[kEPL];
+#pragma unroll
+      for (int h = 0; h < kEPL; ++h) {
+        const int f = w0 + h * 32 + c.lane;
+        k[h]        = -1;
+        if (f < T) {
+          const int o = owner_of(c.w.off, f);
+          k[h]        = __ldg(P.col_row + c.w.st[o] + (f - c.w.off[o]));
         }
       }
+#pragma unroll
+      for (int h = 0; h < kEPL; ++h) nw[h] = k[h] >= 0 && atomicExch(S.row_stamp + k[h], stamp) != stamp;
+      int RL[kEPL], n_s = 0, n_g = 0, n_x = 0, n_a = 0;
+#pragma unroll
+      for (int h = 0; h < kEPL; ++h) {
+        RL[h] = nw[h] ? __ldg(P.row_start + k[h] + 1) - __ldg(P.row_start + k[h]) : 0;
+        roww += (unsigned long long)RL[h];
+        n_a += nw[h];
+        n_s += nw[h] && RL[h] <= kShortNnz;
+        n_g += (nw[h] && RL[h] > kShortNnz) ? (RL[h] + kSumSegment - 1) / kSumSegment : 0;
+        n_x += (nw[h] && RL[h] > 0) ? (RL[h] + kXChunk - 1) / kXChunk : 0;
+      }
+      warp_alloc(&qc->n_drow_all, n_a, c.lane);
+      int ps = warp_alloc(&qc->n_drow_s, n_s, c.lane);
+      int pg = warp_alloc(&qc->n_dseg, n_g, c.lane);
+      int px = warp_alloc(&qc->n_xtask, n_x, c.lane);
+#pragma unroll
+      for (int h = 0; h < kEPL; ++h) {
+        if (!nw[h]) continue;
+        if (RL[h] <= kShortNnz) S.drow_s[qpar][ps++] = k[h];
+        else
+          for (int s = 0; s * kSumSegment < RL[h]; ++s) S.dseg[qpar][pg++] = make_int2(k[h], s);
+        for (int s = 0; s * kXChunk < RL[h]; ++s) S.xtask[qpar][px++] = make_int2(k[h], s);
+      }
     }
+    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) roww += __shfl_xor_sync(FULL, roww, o);
   if (c.lane == 0 && roww) atomicAdd(&qc->roww, roww);
 }
 
-// Phase D: dirty rows → dirty vars of the next round (classified by column length).
+// Phase D: dirty rows → next round's dirty vars (classified by column length).
 __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int ntask     = ld_volatile(&qc->n_xtask);
-  const unsigned lt   = lanemask_lt();
+  const int ntask     = ldv(&qc->n_xtask);
   unsigned long long colw = 0;
+  constexpr int H = kXChunk / 32;
   for (int t = warp_fetch(c, &pc->cur_x2, 1); t < ntask; t = warp_fetch(c, &pc->cur_x2, 1)) {
     const int2 tk = S.xtask[qpar][t];
-    const int rs  = __ldg(P.row_start + tk.x), re = __ldg(P.row_start + tk.x + 1);
-    const int e0  = rs + tk.y * kXChunk, e1 = min(re, e0 + kXChunk);
-    bool nw[kXChunk / 32];
-    int vj[kXChunk / 32];
+    const int rs = __ldg(P.row_start + tk.x), re = __ldg(P.row_start + tk.x + 1);
+    const int e0 = rs + tk.y * kXChunk, e1 = min(re, e0 + kXChunk);
+    int vj[H];
+    bool nw[H];
 #pragma unroll
-    for (int h = 0; h < kXChunk / 32; ++h) {
+    for (int h = 0; h < H; ++h) {
       const int e = e0 + h * 32 + c.lane;
       vj[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
-      nw[h]       = vj[h] >= 0 && atomicExch(S.var_stamp + vj[h], stamp) != stamp;
     }
 #pragma unroll
-    for (int h = 0; h < kXChunk / 32; ++h) {
-      if (!__ballot_sync(FULL, nw[h])) continue;
-      const int L     = nw[h] ? __ldg(P.col_start + vj[h] + 1) - __ldg(P.col_start + vj[h]) : 0;
-      const bool is_s = nw[h] && L <= kShortNnz;
-      const bool is_m = nw[h] && L > kShortNnz;
-      colw += (unsigned long long)L;
-      int pos         = warp_append(&qc->n_dvar_s, is_s, lt);
-      if (is_s) S.dvar_s[qpar][pos] = vj[h];
-      pos = warp_append(&qc->n_dvar_m, is_m, lt);
-      if (is_m) S.dvar_m[qpar][pos] = vj[h];
+    for (int h = 0; h < H; ++h) nw[h] = vj[h] >= 0 && atomicExch(S.var_stamp + vj[h], stamp) != stamp;
+    int CL[H], n_s = 0, n_m = 0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      CL[h] = nw[h] ? __ldg(P.col_start + vj[h] + 1) - __ldg(P.col_start + vj[h]) : 0;
+      colw += (unsigned long long)CL[h];
+      n_s += nw[h] && CL[h] <= kShortNnz;
+      n_m += nw[h] && CL[h] > kShortNnz;
+    }
+    int ps = warp_alloc(&qc->n_dvar_s, n_s, c.lane);
+    int pm = warp_alloc(&qc->n_dvar_m, n_m, c.lane);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      if (!nw[h]) continue;
+      if (CL[h] <= kShortNnz) S.dvar_s[qpar][ps++] = vj[h];
+      else S.dvar_m[qpar][pm++] = vj[h];
     }
   }
 #pragma unroll
@@ -559,7 +748,10 @@ __device__ void zero_par(ParCtl* q)
   for (int j = 0; j < (int)(sizeof(ParCtl) / sizeof(int)); ++j) w[j] = 0;
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+#ifndef BP_MIN_BLOCKS
+#define BP_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     k_engine(DevProblem P, DevState S, Limits lim, int mode, int full_first, unsigned stamp_base,
              unsigned long long dense_thr, long long* stats)
 {
@@ -571,20 +763,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     sm.blk_colnnz   = 0;
   }
   __syncthreads();
-  Ctx c{P, S, lim, sm, (int)(threadIdx.x & 31), (int)(threadIdx.x >> 5),
-        (int)((blockIdx.x * kThreads + threadIdx.x) >> 5), (int)(gridDim.x * kWarps)};
+  const int warp = threadIdx.x >> 5;
+  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
 
   if (mode == MODE_ACTIVITY) {
-    phase_activity(c, &S.ctl->par[1], full_first != 0);
+    phase_activity(c, &S.ctl->par[1], 1, full_first != 0);
     return;
   }
   if (mode == MODE_TIGHTEN) {
-    phase_tighten(c, &S.ctl->par[1], full_first != 0);
+    phase_tighten(c, &S.ctl->par[1], 1, full_first != 0);
     return;
   }
 
   const unsigned long long t0 = globaltimer();
   const bool timed            = isfinite(lim.time_limit);
+  const bool lead             = blockIdx.x == 0 && threadIdx.x == 0;
   bool full                   = true;  // round 1 is always a full sweep (propagation.hpp:442)
   bool any_change             = false;
   int status = BP_STATUS_UNSET, crossed_out = 0;
@@ -594,24 +787,27 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int ppar = rounds & 1, qpar = ppar ^ 1;
     ParCtl* pc     = &S.ctl->par[ppar];
     ParCtl* qc     = &S.ctl->par[qpar];
-    phase_activity(c, pc, full || !lim.incremental);
+    long long* st  = stats ? stats + (long long)(rounds - 1) * kStatCols : nullptr;
+    const bool fr  = full || !lim.incremental;
+    phase_activity(c, pc, ppar, fr);
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      zero_par(qc);
+    if (st && lead) st[6] = (long long)(globaltimer() - t0);
+    if (lead) {
+      zero_par(qc);  // safe: every block has finished reading the previous round's counters
       if (timed && (double)(globaltimer() - t0) * 1e-9 >= lim.time_limit) pc->stop = 1;
     }
-    phase_tighten(c, pc, full || !lim.incremental);
+    phase_tighten(c, pc, ppar, fr);
     grid.sync();
-    const int cr = ld_volatile(&pc->n_crossed);
-    const int nc = ld_volatile(&pc->n_changed);
-    if (stats && blockIdx.x == 0 && threadIdx.x == 0) {
-      const bool fr = full || !lim.incremental;
-      long long* st = stats + (long long)(rounds - 1) * kStatCols;
+    const int cr = ldv(&pc->n_crossed);
+    const int nc = ldv(&pc->n_changed);
+    if (st && lead) {
+      st[7] = (long long)(globaltimer() - t0);
+      st[8] = st[9] = st[7];
       st[0] = fr ? 1 : 0;
-      st[1] = fr ? P.m : ld_volatile(&pc->n_drow_all);
-      st[2] = fr ? P.nnz : (long long)ld_volatile(&pc->roww);
-      st[3] = fr ? P.n : ld_volatile(&pc->n_dvar_s) + ld_volatile(&pc->n_dvar_m);
-      st[4] = fr ? P.nnz : (long long)ld_volatile(&pc->colw);
+      st[1] = fr ? P.m : ldv(&pc->n_drow_all);
+      st[2] = fr ? P.nnz : (long long)ldv(&pc->roww);
+      st[3] = fr ? P.n : ldv(&pc->n_dvar_s) + ldv(&pc->n_dvar_m);
+      st[4] = fr ? P.nnz : (long long)ldv(&pc->colw);
       st[5] = nc;
     }
     if (cr > 0) {
@@ -621,25 +817,28 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     if (nc == 0) break;
     any_change = true;
-    if (!ld_volatile(&pc->any_rows)) break;          // dirty_rows.empty() (propagation.hpp:481)
+    if (!ldv(&pc->any_rows)) break;  // dirty_rows.empty() (propagation.hpp:481)
     if (rounds >= lim.max_rounds) break;
-    if (ld_volatile(&pc->stop)) break;             // time limit (propagation.hpp:439)
-    if (!lim.incremental || ld_volatile(&pc->colnnz) > dense_thr) {
+    if (ldv(&pc->stop)) break;       // time limit (propagation.hpp:439)
+    if (!lim.incremental || ldv(&pc->colnnz) > dense_thr) {
       full = true;
       continue;
     }
     const unsigned stamp = stamp_base + (unsigned)rounds;
     phase_expand_rows(c, pc, qc, qpar, stamp);
     grid.sync();
-    if (ld_volatile(&qc->roww) > dense_thr) {
+    if (st && lead) st[8] = st[9] = (long long)(globaltimer() - t0);
+    if (ldv(&qc->roww) > dense_thr) {
       full = true;
       continue;
     }
     phase_expand_vars(c, pc, qc, qpar, stamp);
     grid.sync();
-    full = false;
+    if (st && lead) st[9] = (long long)(globaltimer() - t0);
+    // a frontier round costs ~ its gathers (row nnz + col nnz); a full round ~ 2 N = 8 dense_thr
+    full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 6 * dense_thr;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (lead) {
     if (status == BP_STATUS_UNSET) status = any_change ? BP_STATUS_TIGHTENED : BP_STATUS_UNCHANGED;
     S.ctl->status     = status;
     S.ctl->rounds     = rounds;
@@ -667,18 +866,70 @@ DevProblem Problem::dev() const
   d.cons      = cons.p;
   d.is_int    = is_int.p;
   d.n_srow    = n_srow;
+  d.n_srtile  = n_srtile;
   d.srow      = srow.p;
-  d.n_mrow    = n_mrow;
-  d.mrow      = mrow.p;
+  d.sr_ptr    = sr_ptr.p;
+  d.sr_col    = sr_col.p;
+  d.sr_val    = sr_val.p;
+  d.sr_tile   = sr_tile.p;
   d.n_seg     = n_seg;
   d.seg_task  = seg_task.p;
   d.seg_base  = seg_base.p;
   d.n_scol    = n_scol;
+  d.n_sctile  = n_sctile;
   d.scol      = scol.p;
+  d.sc_ptr    = sc_ptr.p;
+  d.sc_row    = sc_row.p;
+  d.sc_val    = sc_val.p;
+  d.sc_own    = sc_own.p;
+  d.sc_tile   = sc_tile.p;
   d.n_mcol    = n_mcol;
   d.mcol      = mcol.p;
   return d;
 }
+
+namespace {
+
+// Packs the short items (nnz <= kShortNnz) of a compressed matrix view contiguously, in natural
+// order, and groups them into tiles of <= 32 items and <= kTile entries.
+struct Packed {
+  std::vector<int> ids, ptr, idx, tile;
+  std::vector<double> val;
+  std::vector<uint8_t> own;
+};
+
+Packed pack_short(int count, const int* start, const int* idx, const double* val)
+{
+  Packed pk;
+  pk.ptr.push_back(0);
+  for (int k = 0; k < count; ++k) {
+    const int L = start[k + 1] - start[k];
+    if (L > kShortNnz) continue;
+    pk.ids.push_back(k);
+    for (int e = start[k]; e < start[k + 1]; ++e) {
+      pk.idx.push_back(idx[e]);
+      pk.val.push_back(val[e]);
+    }
+    pk.ptr.push_back((int)pk.idx.size());
+  }
+  pk.own.resize(pk.idx.size());
+  const int ns = (int)pk.ids.size();
+  int r = 0;
+  while (r < ns) {
+    pk.tile.push_back(r);
+    const int base = pk.ptr[r];
+    int q          = r;
+    while (q < ns && q - r < 32 && pk.ptr[q + 1] - base <= kTile) {
+      for (int e = pk.ptr[q]; e < pk.ptr[q + 1]; ++e) pk.own[e] = (uint8_t)(q - r);
+      ++q;
+    }
+    r = q;
+  }
+  pk.tile.push_back(ns);
+  return pk;
+}
+
+}  // namespace
 
 void problem_build(Problem& P, int n, int m, const int* row_start, const int* row_col,
                    const double* row_val, const int* col_start_in, const int* col_row_in,
@@ -713,10 +964,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
     col_row_in    = crw.data();
     col_val_in    = cvl.data();
   }
+  const int* col_start = P.h_col_start.data();
   P.row_start.upload(row_start, m + 1);
   P.row_col.upload(row_col, N);
   P.row_val.upload(row_val, N);
-  P.col_start.upload(P.h_col_start.data(), n + 1);
+  P.col_start.upload(col_start, n + 1);
   P.col_row.upload(col_row_in, N);
   P.col_val.upload(col_val_in, N);
   std::vector<double2> cons(m);
@@ -724,71 +976,77 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.cons.upload(cons);
   P.is_int.upload(is_integer, n);
 
-  // Partition tables.
-  std::vector<int> srow, mrow, scol, mcol, seg_base(m, -1);
-  std::vector<std::pair<int, int>> seg_rows;
+  // Short rows / columns: packed tiles.
+  {
+    Packed r = pack_short(m, row_start, row_col, row_val);
+    P.n_srow   = (int)r.ids.size();
+    P.n_srtile = (int)r.tile.size() - 1;
+    P.srow.upload(r.ids);
+    P.sr_ptr.upload(r.ptr);
+    P.sr_col.upload(r.idx);
+    P.sr_val.upload(r.val);
+    P.sr_tile.upload(r.tile);
+    Packed c = pack_short(n, col_start, col_row_in, col_val_in);
+    P.n_scol   = (int)c.ids.size();
+    P.n_sctile = (int)c.tile.size() - 1;
+    P.scol.upload(c.ids);
+    P.sc_ptr.upload(c.ptr);
+    P.sc_row.upload(c.idx);
+    P.sc_val.upload(c.val);
+    P.sc_own.upload(c.own);
+    P.sc_tile.upload(c.tile);
+  }
+  // Long rows: one task per 16384-entry segment, longest segments first (the fold of a segment
+  // is a sequential chain, so long chains must start early).
+  std::vector<int> seg_base(m, -1);
+  std::vector<std::pair<int, int2>> tasks;  // (segment length, task)
+  int slot = 0;
   for (int k = 0; k < m; ++k) {
     const int L = row_start[k + 1] - row_start[k];
-    if (L <= kShortNnz) srow.push_back(k);
-    else if (L <= kSegNnz) mrow.push_back(k);
-    else seg_rows.push_back({L, k});
-  }
-  std::stable_sort(mrow.begin(), mrow.end(), [&](int a, int b) {
-    return row_start[a + 1] - row_start[a] > row_start[b + 1] - row_start[b];
-  });
-  std::stable_sort(seg_rows.begin(), seg_rows.end(),
-                   [](auto& a, auto& b) { return a.first > b.first; });
-  std::vector<int2> seg_task;
-  int slot = 0;
-  // segment-major order: the first segment of every long row first, so all long rows start early
-  int max_seg = 0;
-  for (auto& [L, k] : seg_rows) {
-    seg_base[k] = slot;
+    if (L <= kShortNnz) continue;
     const int ns = (L + kSumSegment - 1) / kSumSegment;
-    slot += ns;
-    max_seg = std::max(max_seg, ns);
+    if (ns > 1) {
+      seg_base[k] = slot;
+      slot += ns;
+    }
+    for (int s = 0; s < ns; ++s)
+      tasks.push_back({std::min(L - s * kSumSegment, kSumSegment), make_int2(k, s)});
   }
-  for (int s = 0; s < max_seg; ++s)
-    for (auto& [L, k] : seg_rows)
-      if (s * kSumSegment < L) seg_task.push_back(make_int2(k, s));
-  for (int i = 0; i < n; ++i) {
-    const int L = P.h_col_start[i + 1] - P.h_col_start[i];
-    if (L <= kShortNnz) scol.push_back(i);
-    else mcol.push_back(i);
-  }
-  std::stable_sort(mcol.begin(), mcol.end(), [&](int a, int b) {
-    return P.h_col_start[a + 1] - P.h_col_start[a] > P.h_col_start[b + 1] - P.h_col_start[b];
-  });
-  P.n_srow = (int)srow.size();
-  P.n_mrow = (int)mrow.size();
+  std::stable_sort(tasks.begin(), tasks.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<int2> seg_task(tasks.size());
+  for (size_t j = 0; j < tasks.size(); ++j) seg_task[j] = tasks[j].second;
   P.n_seg  = (int)seg_task.size();
-  P.n_scol = (int)scol.size();
-  P.n_mcol = (int)mcol.size();
-  P.srow.upload(srow);
-  P.mrow.upload(mrow);
-  P.scol.upload(scol);
-  P.mcol.upload(mcol);
+  P.n_part = slot;
   P.seg_task.upload(seg_task);
   P.seg_base.upload(seg_base);
-  P.h_seg_base = seg_base;
+  // Long columns, longest first.
+  std::vector<int> mcol;
+  for (int i = 0; i < n; ++i)
+    if (col_start[i + 1] - col_start[i] > kShortNnz) mcol.push_back(i);
+  std::stable_sort(mcol.begin(), mcol.end(), [&](int a, int b) {
+    return col_start[a + 1] - col_start[a] > col_start[b + 1] - col_start[b];
+  });
+  P.n_mcol = (int)mcol.size();
+  P.mcol.upload(mcol);
 
   // Workspace.
-  P.bounds.alloc(std::max(n, 1));
-  P.rec.alloc(std::max(m, 1));
-  P.aux.alloc(std::max(m, 1));
-  P.seg_part.alloc(std::max(slot, 1));
-  P.seg_done.alloc(std::max(m, 1));
-  BP_CUDA(cudaMemset(P.seg_done.p, 0, sizeof(int) * std::max(m, 1)));
-  P.row_stamp.alloc(std::max(m, 1));
-  P.var_stamp.alloc(std::max(n, 1));
-  BP_CUDA(cudaMemset(P.row_stamp.p, 0, sizeof(unsigned) * std::max(m, 1)));
-  BP_CUDA(cudaMemset(P.var_stamp.p, 0, sizeof(unsigned) * std::max(n, 1)));
   const size_t mm = (size_t)std::max(m, 1), nn = (size_t)std::max(n, 1);
-  // int lists per parity: drow_all, drow_s, drow_m (m each), dvar_s, dvar_m (n each); changed (n)
-  P.lists_i.alloc(2 * (3 * mm + 2 * nn) + nn);
-  // int2 lists per parity: dseg (slot), xtask (N/256 + m)
-  const size_t nseg_cap = (size_t)std::max(slot, 1);
-  const size_t nx_cap   = (size_t)(N / kXChunk) + mm + 1;
+  P.bounds.alloc(nn);
+  P.rec.alloc(mm);
+  P.aux.alloc(mm);
+  P.seg_part.alloc(std::max(slot, 1));
+  P.seg_done.alloc(mm);
+  BP_CUDA(cudaMemset(P.seg_done.p, 0, sizeof(int) * mm));
+  P.row_stamp.alloc(mm);
+  P.var_stamp.alloc(nn);
+  BP_CUDA(cudaMemset(P.row_stamp.p, 0, sizeof(unsigned) * mm));
+  BP_CUDA(cudaMemset(P.var_stamp.p, 0, sizeof(unsigned) * nn));
+  // int lists per parity: drow_s (m), dvar_s, dvar_m (n each); changed (n)
+  P.lists_i.alloc(2 * (mm + 2 * nn) + nn);
+  // int2 lists per parity: dseg (all segment tasks), xtask (N/256 + m)
+  const size_t nseg_cap = (size_t)std::max(P.n_seg, 1);
+  const size_t nx_cap   = (size_t)(N / 256) + mm + 1;
   P.lists_i2.alloc(2 * (nseg_cap + nx_cap));
   P.ctl.alloc(1);
   DevState& S = P.st;
@@ -802,13 +1060,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   int* pi     = P.lists_i.p;
   int2* pi2   = P.lists_i2.p;
   for (int q = 0; q < 2; ++q) {
-    S.drow_all[q] = pi; pi += mm;
-    S.drow_s[q]   = pi; pi += mm;
-    S.drow_m[q]   = pi; pi += mm;
-    S.dvar_s[q]   = pi; pi += nn;
-    S.dvar_m[q]   = pi; pi += nn;
-    S.dseg[q]     = pi2; pi2 += nseg_cap;
-    S.xtask[q]    = pi2; pi2 += nx_cap;
+    S.drow_s[q] = pi; pi += mm;
+    S.dvar_s[q] = pi; pi += nn;
+    S.dvar_m[q] = pi; pi += nn;
+    S.dseg[q]   = pi2; pi2 += nseg_cap;
+    S.xtask[q]  = pi2; pi2 += nx_cap;
   }
   S.changed = pi;
   S.ctl     = P.ctl.p;
@@ -826,23 +1082,23 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
 RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s, int flags,
                      long long* d_stats)
 {
-  DevProblem d                 = P.dev();
-  DevState st                  = P.st;
-  Limits l                     = lim;
-  int md                       = (int)mode;
-  int ff                       = full ? 1 : 0;
+  DevProblem d = P.dev();
+  DevState st  = P.st;
+  Limits l     = lim;
+  int md       = (int)mode;
+  int ff       = full ? 1 : 0;
   // stamps: one value per round, never reused until wrap-around (then the stamp arrays reset)
-  if (P.stamp_base > 0xF0000000u - (unsigned)lim.max_rounds - 2) {
+  if (P.stamp_base > 0xF0000000u - (unsigned)std::max(lim.max_rounds, 1) - 2) {
     BP_CUDA(cudaMemsetAsync(P.row_stamp.p, 0, sizeof(unsigned) * P.row_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.var_stamp.p, 0, sizeof(unsigned) * P.var_stamp.n, s));
     P.stamp_base = 1;
   }
-  unsigned sb                  = P.stamp_base;
+  unsigned sb = P.stamp_base;
   P.stamp_base += (unsigned)std::max(lim.max_rounds, 1) + 1;
-  unsigned long long dense_thr = (flags & ENGINE_FORCE_FRONTIER) ? ~0ull
-                                                                 : (unsigned long long)(P.nnz / 4);
+  unsigned long long dense_thr =
+      (flags & ENGINE_FORCE_FRONTIER) ? ~0ull : (unsigned long long)(P.nnz / 4);
   long long* stp = d_stats;
-  void* args[] = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp};
+  void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp};
   BP_CUDA(cudaEventRecord(P.ev0, s));
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, 0, s));
   BP_CUDA(cudaEventRecord(P.ev1, s));
@@ -868,27 +1124,23 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
 
 void stage_rows(Problem& P, const int* rows, int nrows, cudaStream_t s)
 {
-  std::vector<int> all, sr, mr;
+  std::vector<int> sr;
   std::vector<int2> sg;
   for (int j = 0; j < nrows; ++j) {
     const int k = rows[j];
     const int L = P.h_row_start[k + 1] - P.h_row_start[k];
-    all.push_back(k);
     if (L <= kShortNnz) sr.push_back(k);
-    else if (L <= kSegNnz) mr.push_back(k);
     else
       for (int q = 0; q * kSumSegment < L; ++q) sg.push_back(make_int2(k, q));
   }
   DevState& S = P.st;
-  auto up = [&](void* dst, const void* src, size_t bytes) {
-    if (bytes) BP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-  };
-  up(S.drow_all[1], all.data(), all.size() * 4);
-  up(S.drow_s[1], sr.data(), sr.size() * 4);
-  up(S.drow_m[1], mr.data(), mr.size() * 4);
-  up(S.dseg[1], sg.data(), sg.size() * 8);
-  int cnt[4] = {(int)all.size(), (int)sr.size(), (int)mr.size(), (int)sg.size()};
-  up(&S.ctl->par[1].n_drow_all, cnt, sizeof(cnt));
+  if (!sr.empty())
+    BP_CUDA(cudaMemcpyAsync(S.drow_s[1], sr.data(), sr.size() * 4, cudaMemcpyHostToDevice, s));
+  if (!sg.empty())
+    BP_CUDA(cudaMemcpyAsync(S.dseg[1], sg.data(), sg.size() * 8, cudaMemcpyHostToDevice, s));
+  int cnt[3] = {(int)sr.size(), (int)sg.size(), nrows};
+  BP_CUDA(cudaMemcpyAsync(&S.ctl->par[1].n_drow_s, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
+  BP_CUDA(cudaStreamSynchronize(s));
 }
 
 void stage_vars(Problem& P, const int* vars, int nvars, cudaStream_t s)
@@ -906,6 +1158,7 @@ void stage_vars(Problem& P, const int* vars, int nvars, cudaStream_t s)
     BP_CUDA(cudaMemcpyAsync(S.dvar_m[1], mv.data(), mv.size() * 4, cudaMemcpyHostToDevice, s));
   int cnt[2] = {(int)sv.size(), (int)mv.size()};
   BP_CUDA(cudaMemcpyAsync(&S.ctl->par[1].n_dvar_s, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
+  BP_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace bp

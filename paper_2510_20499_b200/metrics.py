@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-STAT_COLS = 6  # full, |R|, A (row nnz), |V|, B (col nnz), |C|
+STAT_COLS = 10  # full, |R|, A (row nnz), |V|, B (col nnz), |C|, t_act, t_tight, t_xrow, t_xvar (ns)
 
 
 def trim(stats: np.ndarray, rounds: int) -> np.ndarray:
