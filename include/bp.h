@@ -106,9 +106,9 @@ int bp_propagate_device(bp_problem* p, double* d_bounds2n, int32_t* infeasible,
 /* Device-resident propagate with options. flags: BP_FORCE_FRONTIER (bit 0) disables the engine's
  * full-round substitution for large frontiers, i.e. runs the reference's exact dirty-set
  * trajectory (results are bit-identical either way). d_stats, if non-NULL, is a DEVICE array of
- * 10 * max_rounds int64 receiving per round {full, |dirty rows|, row nnz visited, |dirty vars|,
+ * 12 * max_rounds int64 receiving per round {full, |dirty rows|, row nnz visited, |dirty vars|,
  * col nnz visited, |changed vars|, and the phase-end times in ns since kernel start: activity,
- * tightening, row expansion, var expansion} — the reference's algorithmic work. */
+ * tightening, row expansion, var expansion, gather, spare} — the reference's algorithmic work. */
 #define BP_FORCE_FRONTIER 1
 int bp_propagate_ex(bp_problem* p, double* d_bounds2n, int32_t* infeasible, const bp_limits* lim,
                     bp_result* res, void* stream, int32_t flags, int64_t* d_stats);

@@ -120,68 +120,88 @@ struct Fold {
   int up_pos;
 };
 
-// One CSC entry's contribution to the fold (propagation.hpp:297-352).
-__device__ __forceinline__ void fold_entry(Fold& f, double lo, double up, bool integer, double a,
-                                           const RowRec& r, const double2* aux, int k, int pos)
+// Candidate bounds one row implies for one of its variables (propagation.hpp:297-352), from the
+// row's activity given explicitly: finite parts mnf/mxf and infinite-contributor counts nmn/nmx.
+// cl = lower-bound candidate or -inf, cu = upper-bound candidate or +inf (at most one of each per
+// entry; the sentinels are never taken by the strict comparisons of the fold).
+__device__ __forceinline__ void cand_explicit(double lo, double up, bool integer, double a,
+                                              double mnf, int nmn, double mxf, int nmx, double g,
+                                              double h, double& cl, double& cu)
 {
-  if (isfinite(r.g)) {
-    double rest;
-    bool usable;
-    if (!is_box(r.min)) {
-      rest   = __dsub_rn(r.min, (a > 0.0) ? __dmul_rn(a, lo) : __dmul_rn(a, up));
+  cl = -INFINITY;
+  cu = INFINITY;
+  if (isfinite(g)) {
+    const bool my_inf = (a > 0.0) ? (lo == -INFINITY) : (up == INFINITY);
+    bool usable       = false;
+    double rest       = 0.0;
+    if (nmn == 0) {
+      rest   = __dsub_rn(mnf, (a > 0.0) ? __dmul_rn(a, lo) : __dmul_rn(a, up));
       usable = true;
-    } else {
-      const bool my_inf = (a > 0.0) ? (lo == -INFINITY) : (up == INFINITY);
-      usable            = (box_value(r.min) == 1) && my_inf;
-      rest              = usable ? aux[k].x : 0.0;
+    } else if (nmn == 1 && my_inf) {
+      rest   = mnf;
+      usable = true;
     }
     if (usable) {
-      const double cand = __ddiv_rn(__dsub_rn(r.g, rest), a);
-      if (a > 0.0) {
-        const double c = integer ? floor(__dadd_rn(cand, kIntEps)) : cand;
-        if (c < f.up) { f.up = c; f.up_pos = pos; }
-      } else {
-        const double c = integer ? ceil(__dsub_rn(cand, kIntEps)) : cand;
-        if (f.lo < c) { f.lo = c; f.lo_pos = pos; }
-      }
+      const double cand = __ddiv_rn(__dsub_rn(g, rest), a);
+      if (a > 0.0) cu = integer ? floor(__dadd_rn(cand, kIntEps)) : cand;
+      else cl = integer ? ceil(__dsub_rn(cand, kIntEps)) : cand;
     }
   }
-  if (isfinite(r.h)) {
-    double rest;
-    bool usable;
-    if (!is_box(r.max)) {
-      rest   = __dsub_rn(r.max, (a > 0.0) ? __dmul_rn(a, up) : __dmul_rn(a, lo));
+  if (isfinite(h)) {
+    const bool my_inf = (a > 0.0) ? (up == INFINITY) : (lo == -INFINITY);
+    bool usable       = false;
+    double rest       = 0.0;
+    if (nmx == 0) {
+      rest   = __dsub_rn(mxf, (a > 0.0) ? __dmul_rn(a, up) : __dmul_rn(a, lo));
       usable = true;
-    } else {
-      const bool my_inf = (a > 0.0) ? (up == INFINITY) : (lo == -INFINITY);
-      usable            = (box_value(r.max) == 1) && my_inf;
-      rest              = usable ? aux[k].y : 0.0;
+    } else if (nmx == 1 && my_inf) {
+      rest   = mxf;
+      usable = true;
     }
     if (usable) {
-      const double cand = __ddiv_rn(__dsub_rn(r.h, rest), a);
-      if (a > 0.0) {
-        const double c = integer ? ceil(__dsub_rn(cand, kIntEps)) : cand;
-        if (f.lo < c) { f.lo = c; f.lo_pos = pos; }
-      } else {
-        const double c = integer ? floor(__dadd_rn(cand, kIntEps)) : cand;
-        if (c < f.up) { f.up = c; f.up_pos = pos; }
-      }
+      const double cand = __ddiv_rn(__dsub_rn(h, rest), a);
+      if (a > 0.0) cl = integer ? ceil(__dsub_rn(cand, kIntEps)) : cand;
+      else cu = integer ? floor(__dadd_rn(cand, kIntEps)) : cand;
     }
   }
 }
 
-// The same rule as fold_entry, returned as this entry's lower-bound candidate (or -inf) and
-// upper-bound candidate (or +inf). Per entry at most one candidate of each kind exists, and the
-// sentinels are never taken by the strict comparisons of the fold, so folding these in CSC order
-// is the reference's tighten_variable loop.
+// Decodes a row record (+ its aux finite parts when boxed).
+__device__ __forceinline__ void decode_rec(const RowRec& r, const double2* aux, int k, double& mnf,
+                                           int& nmn, double& mxf, int& nmx)
+{
+  nmn = is_box(r.min) ? box_value(r.min) : 0;
+  nmx = is_box(r.max) ? box_value(r.max) : 0;
+  mnf = r.min;
+  mxf = r.max;
+  if (nmn | nmx) {
+    const double2 x = aux[k];
+    if (nmn) mnf = x.x;
+    if (nmx) mxf = x.y;
+  }
+}
+
+// One CSC entry's contribution to the fold (propagation.hpp:297-352), position-tagged.
+__device__ __forceinline__ void fold_entry(Fold& f, double lo, double up, bool integer, double a,
+                                           const RowRec& r, const double2* aux, int k, int pos)
+{
+  double mnf, mxf, cl, cu;
+  int nmn, nmx;
+  decode_rec(r, aux, k, mnf, nmn, mxf, nmx);
+  cand_explicit(lo, up, integer, a, mnf, nmn, mxf, nmx, r.g, r.h, cl, cu);
+  if (cu < f.up) { f.up = cu; f.up_pos = pos; }
+  if (f.lo < cl) { f.lo = cl; f.lo_pos = pos; }
+}
+
+// Candidates of one CSC entry from the gathered row record.
 __device__ __forceinline__ void entry_candidates(double lo, double up, bool integer, double a,
                                                  const RowRec& r, const double2* aux, int k,
                                                  double& cl, double& cu)
 {
-  Fold f{-INFINITY, -1, INFINITY, -1};
-  fold_entry(f, lo, up, integer, a, r, aux, k, 0);
-  cl = f.lo;
-  cu = f.up;
+  double mnf, mxf;
+  int nmn, nmx;
+  decode_rec(r, aux, k, mnf, nmn, mxf, nmx);
+  cand_explicit(lo, up, integer, a, mnf, nmn, mxf, nmx, r.g, r.h, cl, cu);
 }
 
 // Combine two partial folds of disjoint position sets (lexicographic (value, position)).
@@ -209,6 +229,31 @@ __device__ __forceinline__ int finish_var(double2* b, double lo, double up, doub
   return changed ? 1 : 0;
 }
 
+// Per-variable candidate slot of the fused full round: the minimum upper-bound / maximum
+// lower-bound candidate strictly improving on the round-start bound, published with
+// order-preserving 64-bit atomics. Equal doubles have equal bits except +-0.0, so the only
+// order-dependent case of the reference's std::min/max fold (a tie at zero, first operand kept)
+// is resolved by also recording the smallest row (= first CSC position) with a zero candidate
+// and that candidate's sign: (row << 1) | signbit.
+struct alignas(32) CandSlot {
+  unsigned long long lo_key, up_key;
+  unsigned lo_zero, up_zero;
+  unsigned pad0, pad1;
+};
+constexpr unsigned long long kLoEmpty = 0ull, kUpEmpty = ~0ull;
+constexpr unsigned kZeroEmpty         = 0xFFFFFFFFu;
+
+__device__ __forceinline__ unsigned long long okey(double d)
+{
+  const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dekey(unsigned long long k)
+{
+  const unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
 // Immutable device problem: the matrix twice (CSR + CSC) plus work-partition tables built once
 // at upload (SURVEY §8a A4's LRB bins, re-designed for warps: see DESIGN.md §3).
 struct DevProblem {
@@ -217,6 +262,7 @@ struct DevProblem {
   const int* row_start;
   const int* row_col;
   const double* row_val;
+  const int* row_ci;        // row_col | is_integer(col) << 31 (the fused pass needs integrality)
   const int* col_start;
   const int* col_row;
   const double* col_val;
@@ -226,13 +272,20 @@ struct DevProblem {
   // <= 32 rows / <= kTile entries: a warp loads a tile coalesced, every lane folds one row.
   int n_srow, n_srtile;
   const int* srow;          // packed index -> row id
-  const int* sr_ptr;        // n_srow + 1 offsets into sr_col / sr_val
-  const int* sr_col;
+  const int* sr_ptr;        // n_srow + 1 offsets into sr_ci / sr_val
+  const int* sr_ci;         // column | integrality << 31
   const double* sr_val;
+  const uint8_t* sr_own;    // owner's local row index inside its tile, per packed entry
   const int* sr_tile;       // n_srtile + 1 packed-row starts
-  // Long rows (nnz > kShortNnz): one warp task per 16384-entry segment, longest first.
-  int n_seg;
-  const int2* seg_task;     // (row, segment)
+  // Long rows (nnz > kShortNnz): their bounds are first gathered into a contiguous buffer
+  // (gbuf, pieces of kPiece entries), then one warp per 16384-entry segment folds it streaming.
+  const int* long_off;      // per row: offset of its entries in gbuf, -1 for short rows
+  int n_piece;
+  const int2* piece_task;   // (row, piece), longest rows first
+  int n_fold;
+  const int2* fold_task;    // (row, segment), longest segments first
+  int n_cpiece;
+  const int2* cpiece_task;  // (row, piece) candidate tasks of rows with nnz > kCandSplit
   const int* seg_base;      // per row: first partial slot if the row has > 1 segment, else -1
   // Short columns, packed the same way (tile lanes fold one variable each).
   int n_scol, n_sctile;
@@ -247,7 +300,10 @@ struct DevProblem {
   const int* mcol;
 };
 
-constexpr int kTile = 128;  // entries per tile / per streamed chunk (4 per lane)
+constexpr int kTile      = 128;   // entries per tile / per gathered chunk (4 per lane)
+constexpr int kPiece     = 1024;  // gather / candidate piece of a long row (divides kSumSegment)
+constexpr int kFoldChunk = 256;   // staging chunk of the streamed fold (8 per lane)
+constexpr int kCandSplit = 2048;  // long rows above: candidates by parallel pieces
 
 struct SegPart {
   double min, max;

@@ -55,13 +55,13 @@ struct DBuf {
 
 // Per-round frontier/counter block (double-buffered by round parity).
 struct ParCtl {
-  int n_drow_s, n_dseg, n_drow_all;  // staged together (stage_rows)
-  int n_dvar_s, n_dvar_m;            // staged together (stage_vars)
+  int n_drow_s, n_dpiece, n_dfold, n_drow_all;  // staged together (stage_rows)
+  int n_dvar_s, n_dvar_m;                       // staged together (stage_vars)
   int n_changed, n_crossed, any_rows;
-  int cur_seg, cur_s, cur_vm, cur_vs;
+  int cur_a, cur_b, cur_c, cur_vm, cur_vs;
   int cur_x1, cur_x2, n_xtask, stop;
+  int n_ctask, cur_x3, cur_x4, pad1;
   unsigned long long colnnz, roww, colw;
-  int pad[2];
 };
 
 struct Ctl {
@@ -75,16 +75,21 @@ struct DevState {
   double2* bounds;
   RowRec* rec;
   double2* aux;
+  double2* gbuf;      // gathered bounds of long rows' entries (DevProblem::long_off)
+  CandSlot* slot;     // fused full round: per-var candidate slots
+  unsigned* ready;    // per row: stamp of the round whose activity is published
   SegPart* seg_part;
   int* seg_done;
   unsigned* row_stamp;
   unsigned* var_stamp;
   int* drow_s[2];
-  int2* dseg[2];
-  int2* xtask[2];  // (row, 256-entry chunk) tasks for var expansion
+  int2* dpiece[2];  // (row, piece) gather tasks of dirty long rows
+  int2* dfold[2];   // (row, segment) fold tasks of dirty long rows
+  int2* xtask[2];   // (row, kTile-entry chunk) var-expansion tasks of dirty long rows
   int* dvar_s[2];
   int* dvar_m[2];
   int* changed;
+  int2* ctask;      // (var, kTile-entry column chunk) row-expansion tasks of the changed vars
   Ctl* ctl;
 };
 
@@ -97,23 +102,30 @@ struct Problem {
   // host copies kept for classification of caller-supplied lists
   std::vector<int> h_row_start, h_col_start;
   // device arrays: the matrix twice
-  DBuf<int> row_start, row_col, col_start, col_row;
+  DBuf<int> row_start, row_col, row_ci, col_start, col_row;
   DBuf<double> row_val, col_val;
   DBuf<double2> cons;
   DBuf<uint8_t> is_int;
   // partition tables (see DevProblem)
-  DBuf<int> srow, sr_ptr, sr_col, sr_tile;
+  DBuf<int> srow, sr_ptr, sr_ci, sr_tile;
   DBuf<double> sr_val;
+  DBuf<uint8_t> sr_own;
+  DBuf<int> long_off;
+  DBuf<int2> piece_task, fold_task, cpiece_task;
   DBuf<int> scol, sc_ptr, sc_row, sc_tile;
   DBuf<double> sc_val;
   DBuf<uint8_t> sc_own;
-  DBuf<int2> seg_task;
   DBuf<int> seg_base, mcol;
-  int n_srow = 0, n_srtile = 0, n_scol = 0, n_sctile = 0, n_seg = 0, n_mcol = 0, n_part = 0;
+  int n_srow = 0, n_srtile = 0, n_scol = 0, n_sctile = 0, n_mcol = 0, n_part = 0;
+  int n_piece = 0, n_fold = 0, n_cpiece = 0;
+  long long n_long_entries = 0;
   // workspace
   DBuf<double2> bounds;
   DBuf<RowRec> rec;
   DBuf<double2> aux;
+  DBuf<double2> gbuf;
+  DBuf<CandSlot> slot;
+  DBuf<unsigned> ready;
   DBuf<SegPart> seg_part;
   DBuf<int> seg_done;
   DBuf<unsigned> row_stamp, var_stamp;
@@ -147,8 +159,8 @@ struct RunResult {
 // receives per-round work counts when non-null.
 enum { ENGINE_FORCE_FRONTIER = 1 };
 // full, |R|, row nnz visits, |V|, col nnz visits, |changed|, then phase-end times (ns since
-// kernel start): activity, tightening, row expansion, var expansion
-constexpr int kStatCols = 10;
+// kernel start): activity, tightening, row expansion, var expansion, gather; one spare
+constexpr int kStatCols = 12;
 RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaStream_t s,
                      int flags = 0, long long* d_stats = nullptr);
 

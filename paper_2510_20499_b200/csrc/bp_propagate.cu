@@ -1,33 +1,30 @@
 // Persistent, device-resident bound propagation for sm_100a.
 //
 // One cooperative kernel runs the whole `propagate` loop of the reference
-// (propagation.hpp:418-486) with no host round trip per round:
+// (propagation.hpp:418-486) with no host round trip per round. The path is a sparse fp64 gather
+// whose cost is memory-level parallelism and two serial chains (the reference's sequential
+// activity sums and the std::min/max fold of each column), so the kernel is organised around
+// keeping gathers in flight and taking those chains off the critical path.
 //
-//   round r:  Phase A  row activities      (propagation.hpp:226-251)   ─ grid.sync
-//             Phase B  bound tightening    (propagation.hpp:378-412)   ─ grid.sync
-//             decision: infeasible / fixpoint / round cap / empty frontier (uniform on every block)
-//             Phase C  frontier: changed vars → dirty rows (+ segment / expansion tasks) ─ grid.sync
-//             Phase D  dirty rows → dirty vars                                           ─ grid.sync
-//
-// The path is a sparse gather: its cost is memory-level parallelism, not arithmetic. Work is
-// therefore organised so every warp keeps 4 independent gathers per lane in flight:
-//   rows  nnz <= 32   packed tiles (<= 32 rows, <= 128 entries): the warp loads a tile coalesced,
-//                     gathers all bounds at once, and each lane folds one row in reference order
-//                     from shared memory (exact: same sequential sum).
-//         nnz > 32    one warp per 16384-entry segment (the reference's fixed summation tree,
-//                     problem.hpp:274), software-pipelined in 128-entry chunks (loads two chunks
-//                     ahead, gathers one chunk ahead of the fold); zero contributions are
-//                     compacted away (exact: the running sum starts at +0.0 and is never -0.0);
-//                     lanes 0/1 fold the min/max chains. Multi-segment rows are summed by the
-//                     last segment to finish, in segment order (heavy_row_activity, :197-218).
-//   vars  nnz <= 32   packed tiles; lanes gather row records (one LDG.256 each) and compute
-//                     per-entry candidates; each lane folds one variable in CSC order.
-//         nnz > 32    one warp per variable; the std::min/max fold is reduced as a lexicographic
-//                     (value, CSC position) min/max, which reproduces "first operand wins on
-//                     ties" (sign of tied zeros) exactly.
-// Frontier rounds (propagation.hpp:456-479) touch only dirty rows / dirty vars; when the frontier
-// would cost about as much as the whole matrix the engine runs a full round instead — evaluating a
-// superset of the dirty sets yields bit-identical results (SURVEY §8a A12 lemma).
+// FULL round (round 1, and any round whose frontier is a large part of the matrix):
+//   F1  gather: the bounds of every long row's entries (nnz > 32) are gathered into a contiguous
+//       buffer (gbuf), pieces of 1024 entries, 8 gathers per lane in flight.        ─ grid.sync
+//   F2  rows: per 16384-entry segment of a long row, one warp streams gbuf coalesced while lanes
+//       0/1 run the reference's sequential min/max sums (zero contributions skipped: exact, the
+//       running sum is never -0.0); packed tiles of short rows fold one row per lane. Right after
+//       a row's activity is known, every entry's candidate bounds for its variable are computed
+//       and the ones strictly improving the round-start bound are published into per-variable
+//       slots with order-preserving 64-bit atomics (fused tightening: no CSC pass, no second
+//       gather of row records).                                                    ─ grid.sync
+//   F4  finalize: per variable, the slot gives the std::min/max fold result (ties at +-0.0 are
+//       resolved by the smallest row = first CSC position), then the reference's crossing /
+//       hair-crossing / threshold rules (propagation.hpp:354-369).                  ─ grid.sync
+// FRONTIER round (propagation.hpp:442-447 with dirty rows / dirty vars):
+//   P1 gather (dirty long rows) ─ P2 activities (dirty rows) ─ B tighten the dirty vars over the
+//   CSC (row-record gathers; long columns reduced as a lexicographic (value, CSC position)
+//   min/max) ─ C/D frontier expansion.
+// Evaluating a superset of the reference's dirty sets yields bit-identical results (DESIGN.md §2,
+// SURVEY §8a A12 lemma), so the engine may pick either round type for any round.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -46,8 +43,8 @@ namespace {
 constexpr int kThreads  = 256;
 constexpr int kWarps    = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kXChunk   = 256;  // entries per var-expansion task
 constexpr int kEPL      = kTile / 32;
+constexpr int kIntBit   = (int)0x80000000u;
 
 __device__ __forceinline__ unsigned lanemask_lt()
 {
@@ -77,19 +74,30 @@ __device__ __forceinline__ unsigned long long globaltimer()
   return t;
 }
 __device__ __forceinline__ int ldv(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ unsigned ldv(const unsigned* p) { return *(const volatile unsigned*)p; }
 __device__ __forceinline__ unsigned long long ldv(const unsigned long long* p)
 {
   return *(const volatile unsigned long long*)p;
 }
+__device__ __forceinline__ RowRec ld_rec_cg(const RowRec* p)
+{
+  RowRec r;
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r.min), "=d"(r.max), "=d"(r.g), "=d"(r.h)
+               : "l"(p));
+  return r;
+}
 
 struct WarpSmem {
-  double b0[kTile];          // min contributions / lower-bound candidates
-  double b1[kTile];          // max contributions / upper-bound candidates
+  double b0[kFoldChunk];     // min contributions / lower-bound candidates
+  double b1[kFoldChunk];     // max contributions / upper-bound candidates
   unsigned char fl[kTile];   // infinite-contributor flags (bit 0 min, bit 1 max)
   int off[32];               // list tiles: exclusive entry offsets of the 32 items
   int st[32];                //             their first entry
   double2 vb[32];            // tighten tiles: the 32 variables' bounds
-  unsigned char vint[32];    //                and integrality
+  double ract[32][2];        // short-row tiles: finite parts of each row's min/max activity
+  int rinf[32][2];           //                  and infinite-contributor counts
+  unsigned char vint[32];    // tighten tiles: integrality
   int chg[64];               // changed-var staging before a global append
 };
 
@@ -140,6 +148,35 @@ __device__ __forceinline__ int warp_fetch(Ctx& c, int* cursor, int step)
   return __shfl_sync(FULL, t, 0);
 }
 
+// Up to 32 listed items as one flattened entry stream: returns the stream length and this lane's
+// item offset; fills w.off / w.st.
+__device__ __forceinline__ int list_tile_setup(Ctx& c, int first, int len, int& excl)
+{
+  const int incl  = warp_incl_scan(len, c.lane);
+  excl            = incl - len;
+  c.w.off[c.lane] = excl;
+  c.w.st[c.lane]  = first;
+  __syncwarp();
+  return __shfl_sync(FULL, incl, 31);
+}
+
+// ------------------------------------------------------------------ candidate publication
+
+// Publishes the candidates of one (row k, variable) entry that strictly improve the round-start
+// bounds (lo, up) into the variable's slot.
+__device__ __forceinline__ void publish(CandSlot* s, double cl, double cu, double lo, double up,
+                                       int k)
+{
+  if (cu < up) {
+    atomicMin(&s->up_key, okey(cu == 0.0 ? 0.0 : cu));
+    if (cu == 0.0) atomicMin(&s->up_zero, ((unsigned)k << 1) | (signbit(cu) ? 1u : 0u));
+  }
+  if (lo < cl) {
+    atomicMax(&s->lo_key, okey(cl == 0.0 ? 0.0 : cl));
+    if (cl == 0.0) atomicMin(&s->lo_zero, ((unsigned)k << 1) | (signbit(cl) ? 1u : 0u));
+  }
+}
+
 // ------------------------------------------------------------------ row activities
 
 __device__ __forceinline__ void write_rec(const DevProblem& P, const DevState& S, int k, double smn,
@@ -155,92 +192,131 @@ __device__ __forceinline__ void write_rec(const DevProblem& P, const DevState& S
   if (imn | imx) S.aux[k] = make_double2(smn, smx);
 }
 
-// One 16384-entry segment of a long row, streamed by one warp.
-__device__ void row_stream(Ctx& c, int k, int seg)
+// F1 / P1: gathers the bounds of piece p (kPiece entries) of long row k into gbuf.
+__device__ void long_gather(Ctx& c, int k, int p)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
+  const int e0 = p * kPiece, e1 = min(L, e0 + kPiece);
+  double2* out = S.gbuf + __ldg(P.long_off + k);
+  for (int j0 = e0; j0 < e1; j0 += 2 * kTile) {
+    int col[2 * kEPL];
+#pragma unroll
+    for (int h = 0; h < 2 * kEPL; ++h) {
+      const int e = j0 + h * 32 + c.lane;
+      col[h]      = e < e1 ? __ldg(P.row_col + rs + e) : -1;
+    }
+    double2 bd[2 * kEPL];
+#pragma unroll
+    for (int h = 0; h < 2 * kEPL; ++h) bd[h] = col[h] >= 0 ? S.bounds[col[h]] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int h = 0; h < 2 * kEPL; ++h)
+      if (col[h] >= 0) out[j0 + h * 32 + c.lane] = bd[h];
+  }
+}
+
+// Candidates of entries [e0, e1) of long row k whose activity is (mnf, nmn, mxf, nmx, g, h).
+__device__ void long_candidates(Ctx& c, int k, int e0, int e1, double mnf, int nmn, double mxf,
+                                int nmx, double g, double hh)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int rs        = __ldg(P.row_start + k);
+  const double2* gb   = S.gbuf + __ldg(P.long_off + k);
+  for (int j0 = e0; j0 < e1; j0 += kTile) {
+    int ci[kEPL];
+    double a[kEPL];
+    double2 bd[kEPL];
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int e = j0 + h * 32 + c.lane;
+      ci[h]       = e < e1 ? __ldg(P.row_ci + rs + e) : -1;
+      a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
+      bd[h]       = e < e1 ? gb[e] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      if (ci[h] == -1) continue;
+      double cl, cu;
+      cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], mnf, nmn, mxf, nmx, g, hh, cl, cu);
+      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
+    }
+  }
+}
+
+// F2 / P2: one 16384-entry segment of a long row. All lanes stage contributions of 256 entries
+// (coalesced from gbuf) while lanes 0/1 fold the previous chunk. With `cand`, a single-segment
+// row of <= kCandSplit entries publishes its candidates right away; longer rows publish their
+// activity (ready stamp) for the parallel candidate pieces.
+__device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   const int lane      = c.lane;
   const int rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
-  const int e0 = rs + seg * kSumSegment, e1 = rs + min(L, (seg + 1) * kSumSegment);
-  const int nch = (e1 - e0 + kTile - 1) / kTile;
-  int ca[kEPL], cb[kEPL];
-  double va[kEPL], vb[kEPL];
-  double2 bd[kEPL];
+  const int e0 = seg * kSumSegment, e1 = min(L, e0 + kSumSegment);
+  const double2* gb = S.gbuf + __ldg(P.long_off + k);
+  constexpr int H   = kFoldChunk / 32;
+  double a[H];
+  double2 bd[H];
 #pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
+  for (int h = 0; h < H; ++h) {
     const int e = e0 + h * 32 + lane;
-    ca[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
-    va[h]       = e < e1 ? __ldg(P.row_val + e) : 0.0;
-  }
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) bd[h] = ca[h] >= 0 ? S.bounds[ca[h]] : make_double2(0.0, 0.0);
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    const int e = e0 + kTile + h * 32 + lane;
-    cb[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
-    vb[h]       = e < e1 ? __ldg(P.row_val + e) : 0.0;
+    a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
+    bd[h]       = e < e1 ? gb[e] : make_double2(0.0, 0.0);
   }
   double acc = 0.0;
   int imn = 0, imx = 0;
   const unsigned lt = lanemask_lt();
-  for (int s = 0; s < nch; ++s) {
-    double cm[kEPL], cx[kEPL];
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      cm[h] = 0.0;
-      cx[h] = 0.0;
-      if (ca[h] >= 0) {
-        int i1, i2;
-        contrib(va[h], bd[h].x, bd[h].y, cm[h], cx[h], i1, i2);
-        imn += i1;
-        imx += i2;
-      }
-    }
-    // gather chunk s+1 (its columns arrived one iteration ago), load chunk s+2
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      bd[h] = cb[h] >= 0 ? S.bounds[cb[h]] : make_double2(0.0, 0.0);
-      ca[h] = cb[h];
-      va[h] = vb[h];
-    }
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      const int e = e0 + (s + 2) * kTile + h * 32 + lane;
-      cb[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
-      vb[h]       = e < e1 ? __ldg(P.row_val + e) : 0.0;
-    }
+  for (int base = e0; base < e1; base += kFoldChunk) {
     // order-preserving compaction of the non-zero contributions of each chain
     int pm = 0, px = 0;
 #pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      const unsigned m = __ballot_sync(FULL, cm[h] != 0.0);
-      const unsigned x = __ballot_sync(FULL, cx[h] != 0.0);
-      if (cm[h] != 0.0) c.w.b0[pm + __popc(m & lt)] = cm[h];
-      if (cx[h] != 0.0) c.w.b1[px + __popc(x & lt)] = cx[h];
+    for (int h = 0; h < H; ++h) {
+      double cm = 0.0, cx = 0.0;
+      if (base + h * 32 + lane < e1) {
+        int i1, i2;
+        contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
+        imn += i1;
+        imx += i2;
+      }
+      const unsigned m = __ballot_sync(FULL, cm != 0.0);
+      const unsigned x = __ballot_sync(FULL, cx != 0.0);
+      if (cm != 0.0) c.w.b0[pm + __popc(m & lt)] = cm;
+      if (cx != 0.0) c.w.b1[px + __popc(x & lt)] = cx;
       pm += __popc(m);
       px += __popc(x);
     }
     __syncwarp();
+    // next chunk in flight during the fold
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int e = base + kFoldChunk + h * 32 + lane;
+      a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
+      bd[h]       = e < e1 ? gb[e] : make_double2(0.0, 0.0);
+    }
     if (lane < 2) {
-      const int cnt     = lane ? px : pm;
       const double* src = lane ? c.w.b1 : c.w.b0;
-#pragma unroll 4
+      const int cnt     = lane ? px : pm;
+#pragma unroll 8
       for (int j = 0; j < cnt; ++j) acc = __dadd_rn(acc, src[j]);
     }
     __syncwarp();
   }
-  imn              = warp_sum(imn);
-  imx              = warp_sum(imx);
-  const double smx = __shfl_sync(FULL, acc, 1);
-  if (lane == 0) {
-    const int nseg = (L + kSumSegment - 1) / kSumSegment;
-    if (nseg == 1) {
-      write_rec(P, S, k, acc, smx, imn, imx);  // 0.0 + part == part (part is never -0.0)
-    } else {
+  imn            = warp_sum(imn);
+  imx            = warp_sum(imx);
+  double smn     = __shfl_sync(FULL, acc, 0);
+  double smx     = __shfl_sync(FULL, acc, 1);
+  const int nseg = (L + kSumSegment - 1) / kSumSegment;
+  int final_row  = 0;  // 1 if this warp holds the row's final activity
+  if (nseg == 1) {
+    final_row = 1;
+  } else {
+    if (lane == 0) {
       const int base = __ldg(P.seg_base + k);
       SegPart sp;
-      sp.min  = acc;
+      sp.min  = smn;
       sp.max  = smx;
       sp.nmin = imn;
       sp.nmax = imx;
@@ -253,53 +329,94 @@ __device__ void row_stream(Ctx& c, int k, int seg)
         double tmn = 0.0, tmx = 0.0;
         int cmn = 0, cmx = 0;
         for (int q = 0; q < nseg; ++q) {  // row_activity's segment fold (propagation.hpp:182-188)
-          const SegPart* p = S.seg_part + base + q;
-          tmn = __dadd_rn(tmn, __ldcg(&p->min));
-          tmx = __dadd_rn(tmx, __ldcg(&p->max));
-          cmn += __ldcg(&p->nmin);
-          cmx += __ldcg(&p->nmax);
+          const SegPart* sq = S.seg_part + base + q;
+          tmn = __dadd_rn(tmn, __ldcg(&sq->min));
+          tmx = __dadd_rn(tmx, __ldcg(&sq->max));
+          cmn += __ldcg(&sq->nmin);
+          cmx += __ldcg(&sq->nmax);
         }
-        write_rec(P, S, k, tmn, tmx, cmn, cmx);
+        smn           = tmn;
+        smx           = tmx;
+        imn           = cmn;
+        imx           = cmx;
         S.seg_done[k] = 0;
+        final_row     = 1;
       }
     }
+    final_row = __shfl_sync(FULL, final_row, 0);
+    smn       = __shfl_sync(FULL, smn, 0);
+    smx       = __shfl_sync(FULL, smx, 0);
+    imn       = __shfl_sync(FULL, imn, 0);
+    imx       = __shfl_sync(FULL, imx, 0);
   }
+  if (!final_row) return;
+  if (lane == 0) write_rec(P, S, k, smn, smx, imn, imx);
+  if (!cand) return;
+  if (L > kCandSplit) {
+    if (lane == 0) {
+      __threadfence();
+      atomicExch(S.ready + k, stamp);
+    }
+    return;
+  }
+  const double2 cb = __ldg(&P.cons[k]);
+  long_candidates(c, k, 0, L, smn, imn, smx, imx, cb.y, cb.x);
 }
 
-// Contributions of up to 128 gathered entries into shared memory (slot h*32+lane).
-__device__ __forceinline__ void stage_contribs(Ctx& c, const int* col, const double* a)
-{
-  double2 bd[kEPL];
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) bd[h] = col[h] >= 0 ? c.S.bounds[col[h]] : make_double2(0.0, 0.0);
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    double cm = 0.0, cx = 0.0;
-    int i1 = 0, i2 = 0;
-    if (col[h] >= 0) contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
-    c.w.b0[h * 32 + c.lane] = cm;
-    c.w.b1[h * 32 + c.lane] = cx;
-    c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
-  }
-}
-
-// A packed tile of short rows (full rounds).
-__device__ void act_tile_packed(Ctx& c, int t)
+// F2 tail: candidate piece p of a row with > kCandSplit entries, once its activity is published.
+__device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp)
 {
   const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  if (c.lane == 0)
+    while (ldv(S.ready + k) != stamp) __nanosleep(200);
+  __syncwarp();
+  __threadfence();
+  const RowRec r = ld_rec_cg(S.rec + k);
+  double mnf = r.min, mxf = r.max;
+  const int nmn = is_box(r.min) ? box_value(r.min) : 0;
+  const int nmx = is_box(r.max) ? box_value(r.max) : 0;
+  if (nmn | nmx) {
+    const double2 x = __ldcg(S.aux + k);
+    if (nmn) mnf = x.x;
+    if (nmx) mxf = x.y;
+  }
+  const int L = __ldg(P.row_start + k + 1) - __ldg(P.row_start + k);
+  long_candidates(c, k, p * kPiece, min(L, (p + 1) * kPiece), mnf, nmn, mxf, nmx, r.g, r.h);
+}
+
+// A packed tile of short rows: gathers, per-lane folds, and (with `cand`) the candidates of every
+// entry from the registers that still hold its coefficient and bounds.
+__device__ void short_tile(Ctx& c, int t, bool cand)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
   const int r0 = __ldg(P.sr_tile + t), r1 = __ldg(P.sr_tile + t + 1);
   const int p0 = __ldg(P.sr_ptr + r0), p1 = __ldg(P.sr_ptr + r1);
-  int col[kEPL];
+  int ci[kEPL];
   double a[kEPL];
 #pragma unroll
   for (int h = 0; h < kEPL; ++h) {
     const int f = p0 + h * 32 + c.lane;
-    col[h]      = f < p1 ? __ldg(P.sr_col + f) : -1;
+    ci[h]       = f < p1 ? __ldg(P.sr_ci + f) : -1;
     a[h]        = f < p1 ? __ldg(P.sr_val + f) : 0.0;
   }
-  stage_contribs(c, col, a);
+  double2 bd[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h)
+    bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    double cm = 0.0, cx = 0.0;
+    int i1 = 0, i2 = 0;
+    if (ci[h] != -1) contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
+    c.w.b0[h * 32 + c.lane] = cm;
+    c.w.b1[h * 32 + c.lane] = cx;
+    c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
+  }
   __syncwarp();
-  if (c.lane < r1 - r0) {
+  const int nr = r1 - r0;
+  if (c.lane < nr) {
     const int r  = r0 + c.lane;
     const int q0 = __ldg(P.sr_ptr + r) - p0, q1 = __ldg(P.sr_ptr + r + 1) - p0;
     double smn = 0.0, smx = 0.0;
@@ -310,25 +427,32 @@ __device__ void act_tile_packed(Ctx& c, int t)
       imn += c.w.fl[q] & 1;
       imx += c.w.fl[q] >> 1;
     }
-    write_rec(P, c.S, __ldg(P.srow + r), smn, smx, imn, imx);
+    write_rec(P, S, __ldg(P.srow + r), smn, smx, imn, imx);
+    c.w.ract[c.lane][0] = smn;
+    c.w.ract[c.lane][1] = smx;
+    c.w.rinf[c.lane][0] = imn;
+    c.w.rinf[c.lane][1] = imx;
+  }
+  __syncwarp();
+  if (cand) {
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int f = p0 + h * 32 + c.lane;
+      if (ci[h] == -1) continue;
+      const int o      = __ldg(P.sr_own + f);
+      const int k      = __ldg(P.srow + r0 + o);
+      const double2 cb = __ldg(&P.cons[k]);
+      double cl, cu;
+      cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], c.w.ract[o][0], c.w.rinf[o][0],
+                    c.w.ract[o][1], c.w.rinf[o][1], cb.y, cb.x, cl, cu);
+      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
+    }
   }
   __syncwarp();
 }
 
-// Up to 32 listed items (rows or columns) as one flattened entry stream: returns this lane's
-// item range [excl, excl + L) and the stream length; fills w.off / w.st.
-__device__ __forceinline__ int list_tile_setup(Ctx& c, int first, int len, int& excl)
-{
-  const int incl = warp_incl_scan(len, c.lane);
-  excl           = incl - len;
-  c.w.off[c.lane] = excl;
-  c.w.st[c.lane]  = first;
-  __syncwarp();
-  return __shfl_sync(FULL, incl, 31);
-}
-
 // Listed short rows (frontier rounds): flattened 128-entry windows, each lane folds its row.
-__device__ void act_list_tile(Ctx& c, const int* ids, int base, int n)
+__device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
 {
   const DevProblem& P = c.P;
   const int j = base + c.lane;
@@ -357,7 +481,18 @@ __device__ void act_list_tile(Ctx& c, const int* ids, int base, int n)
         a[h]        = __ldg(P.row_val + e);
       }
     }
-    stage_contribs(c, col, a);
+    double2 bd[kEPL];
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) bd[h] = col[h] >= 0 ? c.S.bounds[col[h]] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      double cm = 0.0, cx = 0.0;
+      int i1 = 0, i2 = 0;
+      if (col[h] >= 0) contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
+      c.w.b0[h * 32 + c.lane] = cm;
+      c.w.b1[h * 32 + c.lane] = cx;
+      c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
+    }
     __syncwarp();
     if (k >= 0) {
       const int q0 = max(excl, w0) - w0, q1 = min(excl + L, w0 + kTile) - w0;
@@ -373,26 +508,47 @@ __device__ void act_list_tile(Ctx& c, const int* ids, int base, int n)
   if (k >= 0) write_rec(P, c.S, k, smn, smx, imn, imx);
 }
 
-// Phase A. full: every row from the static partition tables; else the frontier lists.
-__device__ void phase_activity(Ctx& c, ParCtl* pc, int par, bool full)
+// Phase 1 (F1 / P1): gather pieces of long rows.
+__device__ void phase_gather(Ctx& c, ParCtl* pc, int par, bool full)
+{
+  const int n       = full ? c.P.n_piece : ldv(&pc->n_dpiece);
+  const int2* tasks = full ? c.P.piece_task : c.S.dpiece[par];
+  for (int t = warp_fetch(c, &pc->cur_a, 1); t < n; t = warp_fetch(c, &pc->cur_a, 1)) {
+    const int2 tk = tasks[t];
+    long_gather(c, tk.x, tk.y);
+  }
+}
+
+// Phase 2 (F2 / P2): activities of all rows (full) or the dirty ones; `cand` fuses tightening.
+__device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, unsigned stamp)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  {
-    const int n       = full ? P.n_seg : ldv(&pc->n_dseg);
-    const int2* tasks = full ? P.seg_task : S.dseg[par];
-    for (int t = warp_fetch(c, &pc->cur_seg, 1); t < n; t = warp_fetch(c, &pc->cur_seg, 1)) {
-      const int2 tk = tasks[t];
-      row_stream(c, tk.x, tk.y);
-    }
-  }
+  const int nf        = full ? P.n_fold : ldv(&pc->n_dfold);
+  const int2* folds   = full ? P.fold_task : S.dfold[par];
   if (full) {
-    for (int t = warp_fetch(c, &pc->cur_s, 1); t < P.n_srtile; t = warp_fetch(c, &pc->cur_s, 1))
-      act_tile_packed(c, t);
+    // one cursor over [folds | short tiles | candidate pieces]: the longest chains start first
+    const int ns = P.n_srtile, nc = cand ? P.n_cpiece : 0;
+    const int total = nf + ns + nc;
+    for (int t = warp_fetch(c, &pc->cur_b, 1); t < total; t = warp_fetch(c, &pc->cur_b, 1)) {
+      if (t < nf) {
+        const int2 tk = folds[t];
+        long_fold(c, tk.x, tk.y, cand, stamp);
+      } else if (t < nf + ns) {
+        short_tile(c, t - nf, cand);
+      } else {
+        const int2 tk = P.cpiece_task[t - nf - ns];
+        long_cand_piece(c, tk.x, tk.y, stamp);
+      }
+    }
   } else {
+    for (int t = warp_fetch(c, &pc->cur_b, 1); t < nf; t = warp_fetch(c, &pc->cur_b, 1)) {
+      const int2 tk = folds[t];
+      long_fold(c, tk.x, tk.y, false, stamp);
+    }
     const int n = ldv(&pc->n_drow_s);
-    for (int t = warp_fetch(c, &pc->cur_s, 32); t < n; t = warp_fetch(c, &pc->cur_s, 32))
-      act_list_tile(c, S.drow_s[par], t, n);
+    for (int t = warp_fetch(c, &pc->cur_c, 32); t < n; t = warp_fetch(c, &pc->cur_c, 32))
+      short_list_tile(c, S.drow_s[par], t, n);
   }
 }
 
@@ -405,6 +561,8 @@ struct Tally {
   int nbuf;  // warp-uniform count of staged changed vars
 };
 
+// Appends the staged changed vars to the changed list and their columns, in kTile-entry chunks,
+// to the row-expansion task list (no long serial chain in the frontier expansion).
 __device__ __forceinline__ void flush_changed(Ctx& c, ParCtl* pc, Tally& t)
 {
   if (t.nbuf == 0) return;
@@ -412,7 +570,18 @@ __device__ __forceinline__ void flush_changed(Ctx& c, ParCtl* pc, Tally& t)
   if (c.lane == 0) base = atomicAdd(&pc->n_changed, t.nbuf);
   base = __shfl_sync(FULL, base, 0);
   __syncwarp();
-  for (int j = c.lane; j < t.nbuf; j += 32) c.S.changed[base + j] = c.w.chg[j];
+  for (int j0 = 0; j0 < t.nbuf; j0 += 32) {
+    const int j = j0 + c.lane;
+    int i = -1, nch = 0;
+    if (j < t.nbuf) {
+      i                         = c.w.chg[j];
+      c.S.changed[base + j]     = i;
+      const int L               = __ldg(c.P.col_start + i + 1) - __ldg(c.P.col_start + i);
+      nch                       = L > kTile ? (L + kTile - 1) / kTile : 0;
+    }
+    const int pos = warp_alloc(&pc->n_ctask, nch, c.lane);
+    for (int q = 0; q < nch; ++q) c.S.ctask[pos + q] = make_int2(i, q);
+  }
   __syncwarp();
   t.nbuf = 0;
 }
@@ -433,6 +602,66 @@ __device__ __forceinline__ void tally(Ctx& c, ParCtl* pc, Tally& t, int i, int r
     t.nbuf += __popc(ch);
     __syncwarp();
   }
+}
+
+__device__ void tally_flush_block(Ctx& c, ParCtl* pc, Tally& t)
+{
+  flush_changed(c, pc, t);
+  const int cr = warp_sum(t.crossed);
+  const int ar = __any_sync(FULL, t.any_rows);
+  unsigned long long cn = t.colnnz;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cn += __shfl_xor_sync(FULL, cn, o);
+  if (c.lane == 0) {
+    if (cr) atomicAdd(&c.sm.blk_crossed, cr);
+    if (ar) atomicOr(&c.sm.blk_any_rows, 1);
+    if (cn) atomicAdd(&c.sm.blk_colnnz, cn);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (c.sm.blk_crossed) atomicAdd(&pc->n_crossed, c.sm.blk_crossed);
+    if (c.sm.blk_any_rows) atomicOr(&pc->any_rows, 1);
+    if (c.sm.blk_colnnz) atomicAdd(&pc->colnnz, c.sm.blk_colnnz);
+    c.sm.blk_crossed  = 0;
+    c.sm.blk_any_rows = 0;
+    c.sm.blk_colnnz   = 0;
+  }
+  __syncthreads();
+}
+
+// F4: per variable, the fold result from its candidate slot, then the reference's rules.
+__device__ void phase_finalize(Ctx& c, ParCtl* pc)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  Tally t{0, 0, 0ull, 0};
+  for (int q = warp_fetch(c, &pc->cur_vs, 32); q < P.n; q = warp_fetch(c, &pc->cur_vs, 32)) {
+    const int i = q + c.lane;
+    int res     = 0;
+    if (i < P.n) {
+      CandSlot* s                 = S.slot + i;
+      const unsigned long long uk = s->up_key, lk = s->lo_key;
+      if (uk != kUpEmpty || lk != kLoEmpty) {
+        const double2 b = S.bounds[i];
+        double nl = b.x, nu = b.y;
+        if (uk != kUpEmpty) {
+          nu = dekey(uk);
+          if (nu == 0.0) nu = (s->up_zero & 1u) ? -0.0 : 0.0;
+        }
+        if (lk != kLoEmpty) {
+          nl = dekey(lk);
+          if (nl == 0.0) nl = (s->lo_zero & 1u) ? -0.0 : 0.0;
+        }
+        s->up_key  = kUpEmpty;
+        s->lo_key  = kLoEmpty;
+        s->up_zero = kZeroEmpty;
+        s->lo_zero = kZeroEmpty;
+        res = finish_var(S.bounds + i, b.x, b.y, nl, nu, __ldg(P.is_int + i) != 0, c.lim);
+      }
+    }
+    tally(c, pc, t, i < P.n ? i : -1, res);
+  }
+  tally_flush_block(c, pc, t);
 }
 
 // Long column: one warp, 4 row-record gathers per lane in flight, (value, position) reduction.
@@ -494,7 +723,7 @@ __device__ __forceinline__ void stage_candidates(Ctx& c, const int* k, const dou
   }
 }
 
-// Packed tile of short columns (full rounds).
+// Packed tile of short columns (tighten-only calls with every variable).
 __device__ void tighten_tile_packed(Ctx& c, int t, ParCtl* pc, Tally& ty)
 {
   const DevProblem& P = c.P;
@@ -503,9 +732,9 @@ __device__ void tighten_tile_packed(Ctx& c, int t, ParCtl* pc, Tally& ty)
   const int p0 = __ldg(P.sc_ptr + v0), p1 = __ldg(P.sc_ptr + v1);
   int i = -1;
   if (c.lane < v1 - v0) {
-    i                  = __ldg(P.scol + v0 + c.lane);
-    c.w.vb[c.lane]     = S.bounds[i];
-    c.w.vint[c.lane]   = __ldg(P.is_int + i);
+    i                = __ldg(P.scol + v0 + c.lane);
+    c.w.vb[c.lane]   = S.bounds[i];
+    c.w.vint[c.lane] = __ldg(P.is_int + i);
   }
   int k[kEPL], own[kEPL];
   double a[kEPL];
@@ -543,7 +772,7 @@ __device__ void tighten_list_tile(Ctx& c, const int* ids, int base, int n, ParCt
   const int j = base + c.lane;
   const int i = j < n ? ids[j] : -1;
   int cs = 0, L = 0;
-  double2 b = make_double2(0.0, 0.0);
+  double2 b    = make_double2(0.0, 0.0);
   bool integer = false;
   if (i >= 0) {
     cs      = __ldg(P.col_start + i);
@@ -590,6 +819,7 @@ __device__ void tighten_list_tile(Ctx& c, const int* ids, int base, int n, ParCt
   tally(c, pc, ty, i, res);
 }
 
+// Phase B of frontier rounds (and tighten-only calls): CSC tightening of listed / all variables.
 __device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
 {
   const DevProblem& P = c.P;
@@ -612,39 +842,60 @@ __device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
     for (int q = warp_fetch(c, &pc->cur_vs, 32); q < n; q = warp_fetch(c, &pc->cur_vs, 32))
       tighten_list_tile(c, S.dvar_s[par], q, n, pc, t);
   }
-  flush_changed(c, pc, t);
-  const int cr = warp_sum(t.crossed);
-  const int ar = __any_sync(FULL, t.any_rows);
-  unsigned long long cn = t.colnnz;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) cn += __shfl_xor_sync(FULL, cn, o);
-  if (c.lane == 0) {
-    if (cr) atomicAdd(&c.sm.blk_crossed, cr);
-    if (ar) atomicOr(&c.sm.blk_any_rows, 1);
-    if (cn) atomicAdd(&c.sm.blk_colnnz, cn);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (c.sm.blk_crossed) atomicAdd(&pc->n_crossed, c.sm.blk_crossed);
-    if (c.sm.blk_any_rows) atomicOr(&pc->any_rows, 1);
-    if (c.sm.blk_colnnz) atomicAdd(&pc->colnnz, c.sm.blk_colnnz);
-    c.sm.blk_crossed  = 0;
-    c.sm.blk_any_rows = 0;
-    c.sm.blk_colnnz   = 0;
-  }
-  __syncthreads();
+  tally_flush_block(c, pc, t);
 }
 
 // ------------------------------------------------------------------ frontier
 
-// Phase C: rows(changed) → next round's dirty rows: short rows, long-row segment tasks, and
-// 256-entry var-expansion tasks. 4 incidences per lane in flight.
+// One 128-incidence window of the row expansion: marks rows k[h] dirty for the next round and
+// appends the new ones (short rows to drow_s; long rows as gather / fold / var-expansion tasks).
+__device__ __forceinline__ void expand_rows_window(Ctx& c, ParCtl* qc, int qpar, unsigned stamp,
+                                                   const int* k, unsigned long long& roww, int& nall)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  bool nw[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) nw[h] = k[h] >= 0 && atomicExch(S.row_stamp + k[h], stamp) != stamp;
+  int RL[kEPL], n_s = 0, n_p = 0, n_f = 0, n_x = 0;
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    RL[h] = nw[h] ? __ldg(P.row_start + k[h] + 1) - __ldg(P.row_start + k[h]) : 0;
+    roww += (unsigned long long)RL[h];
+    nall += nw[h];
+    const bool lg = nw[h] && RL[h] > kShortNnz;
+    n_s += nw[h] && !lg;
+    n_p += lg ? (RL[h] + kPiece - 1) / kPiece : 0;
+    n_f += lg ? (RL[h] + kSumSegment - 1) / kSumSegment : 0;
+    n_x += lg ? (RL[h] + kTile - 1) / kTile : 0;
+  }
+  int ps = warp_alloc(&qc->n_drow_s, n_s, c.lane);
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h)
+    if (nw[h] && RL[h] <= kShortNnz) S.drow_s[qpar][ps++] = k[h];
+  if (__any_sync(FULL, n_p > 0)) {  // rare: a long row became dirty
+    int pp = warp_alloc(&qc->n_dpiece, n_p, c.lane);
+    int pf = warp_alloc(&qc->n_dfold, n_f, c.lane);
+    int px = warp_alloc(&qc->n_xtask, n_x, c.lane);
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      if (!nw[h] || RL[h] <= kShortNnz) continue;
+      for (int s = 0; s * kPiece < RL[h]; ++s) S.dpiece[qpar][pp++] = make_int2(k[h], s);
+      for (int s = 0; s * kSumSegment < RL[h]; ++s) S.dfold[qpar][pf++] = make_int2(k[h], s);
+      for (int s = 0; s * kTile < RL[h]; ++s) S.xtask[qpar][px++] = make_int2(k[h], s);
+    }
+  }
+}
+
+// Phase C: rows(changed) → next round's dirty rows. Changed vars with short columns go 32 per
+// warp (flattened 128-entry windows); longer columns were split into chunk tasks at append time.
 __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int nch       = ldv(&pc->n_changed);
   unsigned long long roww = 0;
+  int nall                = 0;
+  const int nch = ldv(&pc->n_changed);
   for (int t = warp_fetch(c, &pc->cur_x1, 32); t < nch; t = warp_fetch(c, &pc->cur_x1, 32)) {
     const int j = t + c.lane;
     const int i = j < nch ? S.changed[j] : -1;
@@ -652,12 +903,12 @@ __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
     if (i >= 0) {
       cs = __ldg(P.col_start + i);
       L  = __ldg(P.col_start + i + 1) - cs;
+      if (L > kTile) L = 0;  // chunk tasks
     }
     int excl;
     const int T = list_tile_setup(c, cs, L, excl);
     for (int w0 = 0; w0 < T; w0 += kTile) {
       int k[kEPL];
-      bool nw[kEPL];
 #pragma unroll
       for (int h = 0; h < kEPL; ++h) {
         const int f = w0 + h * 32 + c.lane;
@@ -667,75 +918,103 @@ __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
           k[h]        = __ldg(P.col_row + c.w.st[o] + (f - c.w.off[o]));
         }
       }
-#pragma unroll
-      for (int h = 0; h < kEPL; ++h) nw[h] = k[h] >= 0 && atomicExch(S.row_stamp + k[h], stamp) != stamp;
-      int RL[kEPL], n_s = 0, n_g = 0, n_x = 0, n_a = 0;
-#pragma unroll
-      for (int h = 0; h < kEPL; ++h) {
-        RL[h] = nw[h] ? __ldg(P.row_start + k[h] + 1) - __ldg(P.row_start + k[h]) : 0;
-        roww += (unsigned long long)RL[h];
-        n_a += nw[h];
-        n_s += nw[h] && RL[h] <= kShortNnz;
-        n_g += (nw[h] && RL[h] > kShortNnz) ? (RL[h] + kSumSegment - 1) / kSumSegment : 0;
-        n_x += (nw[h] && RL[h] > 0) ? (RL[h] + kXChunk - 1) / kXChunk : 0;
-      }
-      warp_alloc(&qc->n_drow_all, n_a, c.lane);
-      int ps = warp_alloc(&qc->n_drow_s, n_s, c.lane);
-      int pg = warp_alloc(&qc->n_dseg, n_g, c.lane);
-      int px = warp_alloc(&qc->n_xtask, n_x, c.lane);
-#pragma unroll
-      for (int h = 0; h < kEPL; ++h) {
-        if (!nw[h]) continue;
-        if (RL[h] <= kShortNnz) S.drow_s[qpar][ps++] = k[h];
-        else
-          for (int s = 0; s * kSumSegment < RL[h]; ++s) S.dseg[qpar][pg++] = make_int2(k[h], s);
-        for (int s = 0; s * kXChunk < RL[h]; ++s) S.xtask[qpar][px++] = make_int2(k[h], s);
-      }
+      expand_rows_window(c, qc, qpar, stamp, k, roww, nall);
     }
     __syncwarp();
   }
+  const int ntask = ldv(&pc->n_ctask);
+  for (int t = warp_fetch(c, &pc->cur_x2, 1); t < ntask; t = warp_fetch(c, &pc->cur_x2, 1)) {
+    const int2 tk = S.ctask[t];
+    const int ce  = __ldg(P.col_start + tk.x + 1);
+    const int e0  = __ldg(P.col_start + tk.x) + tk.y * kTile, e1 = min(ce, e0 + kTile);
+    int k[kEPL];
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int e = e0 + h * 32 + c.lane;
+      k[h]        = e < e1 ? __ldg(P.col_row + e) : -1;
+    }
+    expand_rows_window(c, qc, qpar, stamp, k, roww, nall);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) roww += __shfl_xor_sync(FULL, roww, o);
-  if (c.lane == 0 && roww) atomicAdd(&qc->roww, roww);
+  nall = warp_sum(nall);
+  if (c.lane == 0) {
+    if (roww) atomicAdd(&qc->roww, roww);
+    if (nall) atomicAdd(&qc->n_drow_all, nall);
+  }
 }
 
-// Phase D: dirty rows → next round's dirty vars (classified by column length).
+// One 128-entry window of the var expansion: marks vars v[h] dirty and appends the new ones.
+__device__ __forceinline__ void expand_vars_window(Ctx& c, ParCtl* qc, int qpar, unsigned stamp,
+                                                   const int* v, unsigned long long& colw)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  bool nw[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) nw[h] = v[h] >= 0 && atomicExch(S.var_stamp + v[h], stamp) != stamp;
+  int CL[kEPL], n_s = 0, n_m = 0;
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    CL[h] = nw[h] ? __ldg(P.col_start + v[h] + 1) - __ldg(P.col_start + v[h]) : 0;
+    colw += (unsigned long long)CL[h];
+    n_s += nw[h] && CL[h] <= kShortNnz;
+    n_m += nw[h] && CL[h] > kShortNnz;
+  }
+  int ps = warp_alloc(&qc->n_dvar_s, n_s, c.lane);
+  int pm = warp_alloc(&qc->n_dvar_m, n_m, c.lane);
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    if (!nw[h]) continue;
+    if (CL[h] <= kShortNnz) S.dvar_s[qpar][ps++] = v[h];
+    else S.dvar_m[qpar][pm++] = v[h];
+  }
+}
+
+// Phase D: dirty rows → next round's dirty vars: short rows 32 per warp, long rows by chunk tasks.
 __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int ntask     = ldv(&qc->n_xtask);
   unsigned long long colw = 0;
-  constexpr int H = kXChunk / 32;
-  for (int t = warp_fetch(c, &pc->cur_x2, 1); t < ntask; t = warp_fetch(c, &pc->cur_x2, 1)) {
+  const int nr = ldv(&qc->n_drow_s);
+  for (int t = warp_fetch(c, &pc->cur_x3, 32); t < nr; t = warp_fetch(c, &pc->cur_x3, 32)) {
+    const int j = t + c.lane;
+    const int k = j < nr ? S.drow_s[qpar][j] : -1;
+    int rs = 0, L = 0;
+    if (k >= 0) {
+      rs = __ldg(P.row_start + k);
+      L  = __ldg(P.row_start + k + 1) - rs;
+    }
+    int excl;
+    const int T = list_tile_setup(c, rs, L, excl);
+    for (int w0 = 0; w0 < T; w0 += kTile) {
+      int v[kEPL];
+#pragma unroll
+      for (int h = 0; h < kEPL; ++h) {
+        const int f = w0 + h * 32 + c.lane;
+        v[h]        = -1;
+        if (f < T) {
+          const int o = owner_of(c.w.off, f);
+          v[h]        = __ldg(P.row_col + c.w.st[o] + (f - c.w.off[o]));
+        }
+      }
+      expand_vars_window(c, qc, qpar, stamp, v, colw);
+    }
+    __syncwarp();
+  }
+  const int ntask = ldv(&qc->n_xtask);
+  for (int t = warp_fetch(c, &pc->cur_x4, 1); t < ntask; t = warp_fetch(c, &pc->cur_x4, 1)) {
     const int2 tk = S.xtask[qpar][t];
-    const int rs = __ldg(P.row_start + tk.x), re = __ldg(P.row_start + tk.x + 1);
-    const int e0 = rs + tk.y * kXChunk, e1 = min(re, e0 + kXChunk);
-    int vj[H];
-    bool nw[H];
+    const int re  = __ldg(P.row_start + tk.x + 1);
+    const int e0  = __ldg(P.row_start + tk.x) + tk.y * kTile, e1 = min(re, e0 + kTile);
+    int v[kEPL];
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
+    for (int h = 0; h < kEPL; ++h) {
       const int e = e0 + h * 32 + c.lane;
-      vj[h]       = e < e1 ? __ldg(P.row_col + e) : -1;
+      v[h]        = e < e1 ? __ldg(P.row_col + e) : -1;
     }
-#pragma unroll
-    for (int h = 0; h < H; ++h) nw[h] = vj[h] >= 0 && atomicExch(S.var_stamp + vj[h], stamp) != stamp;
-    int CL[H], n_s = 0, n_m = 0;
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      CL[h] = nw[h] ? __ldg(P.col_start + vj[h] + 1) - __ldg(P.col_start + vj[h]) : 0;
-      colw += (unsigned long long)CL[h];
-      n_s += nw[h] && CL[h] <= kShortNnz;
-      n_m += nw[h] && CL[h] > kShortNnz;
-    }
-    int ps = warp_alloc(&qc->n_dvar_s, n_s, c.lane);
-    int pm = warp_alloc(&qc->n_dvar_m, n_m, c.lane);
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      if (!nw[h]) continue;
-      if (CL[h] <= kShortNnz) S.dvar_s[qpar][ps++] = vj[h];
-      else S.dvar_m[qpar][pm++] = vj[h];
-    }
+    expand_vars_window(c, qc, qpar, stamp, v, colw);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) colw += __shfl_xor_sync(FULL, colw, o);
@@ -767,7 +1046,10 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
 
   if (mode == MODE_ACTIVITY) {
-    phase_activity(c, &S.ctl->par[1], 1, full_first != 0);
+    const bool full = full_first != 0;
+    phase_gather(c, &S.ctl->par[1], 1, full);
+    grid.sync();
+    phase_rows(c, &S.ctl->par[1], 1, full, false, stamp_base);
     return;
   }
   if (mode == MODE_TIGHTEN) {
@@ -784,19 +1066,26 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   int rounds = 0;
   while (rounds < lim.max_rounds) {
     ++rounds;
-    const int ppar = rounds & 1, qpar = ppar ^ 1;
-    ParCtl* pc     = &S.ctl->par[ppar];
-    ParCtl* qc     = &S.ctl->par[qpar];
-    long long* st  = stats ? stats + (long long)(rounds - 1) * kStatCols : nullptr;
-    const bool fr  = full || !lim.incremental;
-    phase_activity(c, pc, ppar, fr);
+    const int ppar       = rounds & 1, qpar = ppar ^ 1;
+    ParCtl* pc           = &S.ctl->par[ppar];
+    ParCtl* qc           = &S.ctl->par[qpar];
+    long long* st        = stats ? stats + (long long)(rounds - 1) * kStatCols : nullptr;
+    const bool fr        = full || !lim.incremental;
+    const unsigned stamp = stamp_base + (unsigned)rounds;
+    if (fr || ldv(&pc->n_dpiece) > 0) {
+      phase_gather(c, pc, ppar, fr);
+      grid.sync();
+    }
+    if (st && lead) st[10] = (long long)(globaltimer() - t0);
+    phase_rows(c, pc, ppar, fr, fr, stamp);
     grid.sync();
     if (st && lead) st[6] = (long long)(globaltimer() - t0);
     if (lead) {
       zero_par(qc);  // safe: every block has finished reading the previous round's counters
       if (timed && (double)(globaltimer() - t0) * 1e-9 >= lim.time_limit) pc->stop = 1;
     }
-    phase_tighten(c, pc, ppar, fr);
+    if (fr) phase_finalize(c, pc);
+    else phase_tighten(c, pc, ppar, false);
     grid.sync();
     const int cr = ldv(&pc->n_crossed);
     const int nc = ldv(&pc->n_changed);
@@ -824,7 +1113,6 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
       full = true;
       continue;
     }
-    const unsigned stamp = stamp_base + (unsigned)rounds;
     phase_expand_rows(c, pc, qc, qpar, stamp);
     grid.sync();
     if (st && lead) st[8] = st[9] = (long long)(globaltimer() - t0);
@@ -835,8 +1123,8 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     phase_expand_vars(c, pc, qc, qpar, stamp);
     grid.sync();
     if (st && lead) st[9] = (long long)(globaltimer() - t0);
-    // a frontier round costs ~ its gathers (row nnz + col nnz); a full round ~ 2 N = 8 dense_thr
-    full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 6 * dense_thr;
+    // a frontier round costs ~ its gathers (row nnz + col nnz); a full round ~ N = 4 dense_thr
+    full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 3 * dense_thr;
   }
   if (lead) {
     if (status == BP_STATUS_UNSET) status = any_change ? BP_STATUS_TIGHTENED : BP_STATUS_UNCHANGED;
@@ -854,37 +1142,44 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
 DevProblem Problem::dev() const
 {
   DevProblem d;
-  d.n         = n;
-  d.m         = m;
-  d.nnz       = nnz;
-  d.row_start = row_start.p;
-  d.row_col   = row_col.p;
-  d.row_val   = row_val.p;
-  d.col_start = col_start.p;
-  d.col_row   = col_row.p;
-  d.col_val   = col_val.p;
-  d.cons      = cons.p;
-  d.is_int    = is_int.p;
-  d.n_srow    = n_srow;
-  d.n_srtile  = n_srtile;
-  d.srow      = srow.p;
-  d.sr_ptr    = sr_ptr.p;
-  d.sr_col    = sr_col.p;
-  d.sr_val    = sr_val.p;
-  d.sr_tile   = sr_tile.p;
-  d.n_seg     = n_seg;
-  d.seg_task  = seg_task.p;
-  d.seg_base  = seg_base.p;
-  d.n_scol    = n_scol;
-  d.n_sctile  = n_sctile;
-  d.scol      = scol.p;
-  d.sc_ptr    = sc_ptr.p;
-  d.sc_row    = sc_row.p;
-  d.sc_val    = sc_val.p;
-  d.sc_own    = sc_own.p;
-  d.sc_tile   = sc_tile.p;
-  d.n_mcol    = n_mcol;
-  d.mcol      = mcol.p;
+  d.n           = n;
+  d.m           = m;
+  d.nnz         = nnz;
+  d.row_start   = row_start.p;
+  d.row_col     = row_col.p;
+  d.row_val     = row_val.p;
+  d.row_ci      = row_ci.p;
+  d.col_start   = col_start.p;
+  d.col_row     = col_row.p;
+  d.col_val     = col_val.p;
+  d.cons        = cons.p;
+  d.is_int      = is_int.p;
+  d.n_srow      = n_srow;
+  d.n_srtile    = n_srtile;
+  d.srow        = srow.p;
+  d.sr_ptr      = sr_ptr.p;
+  d.sr_ci       = sr_ci.p;
+  d.sr_val      = sr_val.p;
+  d.sr_own      = sr_own.p;
+  d.sr_tile     = sr_tile.p;
+  d.long_off    = long_off.p;
+  d.n_piece     = n_piece;
+  d.piece_task  = piece_task.p;
+  d.n_fold      = n_fold;
+  d.fold_task   = fold_task.p;
+  d.n_cpiece    = n_cpiece;
+  d.cpiece_task = cpiece_task.p;
+  d.seg_base    = seg_base.p;
+  d.n_scol      = n_scol;
+  d.n_sctile    = n_sctile;
+  d.scol        = scol.p;
+  d.sc_ptr      = sc_ptr.p;
+  d.sc_row      = sc_row.p;
+  d.sc_val      = sc_val.p;
+  d.sc_own      = sc_own.p;
+  d.sc_tile     = sc_tile.p;
+  d.n_mcol      = n_mcol;
+  d.mcol        = mcol.p;
   return d;
 }
 
@@ -898,7 +1193,8 @@ struct Packed {
   std::vector<uint8_t> own;
 };
 
-Packed pack_short(int count, const int* start, const int* idx, const double* val)
+Packed pack_short(int count, const int* start, const int* idx, const double* val,
+                  const uint8_t* int_flag)
 {
   Packed pk;
   pk.ptr.push_back(0);
@@ -907,7 +1203,7 @@ Packed pack_short(int count, const int* start, const int* idx, const double* val
     if (L > kShortNnz) continue;
     pk.ids.push_back(k);
     for (int e = start[k]; e < start[k + 1]; ++e) {
-      pk.idx.push_back(idx[e]);
+      pk.idx.push_back(int_flag && int_flag[idx[e]] ? (idx[e] | kIntBit) : idx[e]);
       pk.val.push_back(val[e]);
     }
     pk.ptr.push_back((int)pk.idx.size());
@@ -968,6 +1264,12 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.row_start.upload(row_start, m + 1);
   P.row_col.upload(row_col, N);
   P.row_val.upload(row_val, N);
+  {
+    std::vector<int> ci(N);
+    for (long long e = 0; e < N; ++e)
+      ci[e] = is_integer[row_col[e]] ? (row_col[e] | kIntBit) : row_col[e];
+    P.row_ci.upload(ci);
+  }
   P.col_start.upload(col_start, n + 1);
   P.col_row.upload(col_row_in, N);
   P.col_val.upload(col_val_in, N);
@@ -978,15 +1280,16 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
 
   // Short rows / columns: packed tiles.
   {
-    Packed r = pack_short(m, row_start, row_col, row_val);
+    Packed r   = pack_short(m, row_start, row_col, row_val, is_integer);
     P.n_srow   = (int)r.ids.size();
     P.n_srtile = (int)r.tile.size() - 1;
     P.srow.upload(r.ids);
     P.sr_ptr.upload(r.ptr);
-    P.sr_col.upload(r.idx);
+    P.sr_ci.upload(r.idx);
     P.sr_val.upload(r.val);
+    P.sr_own.upload(r.own);
     P.sr_tile.upload(r.tile);
-    Packed c = pack_short(n, col_start, col_row_in, col_val_in);
+    Packed c   = pack_short(n, col_start, col_row_in, col_val_in, nullptr);
     P.n_scol   = (int)c.ids.size();
     P.n_sctile = (int)c.tile.size() - 1;
     P.scol.upload(c.ids);
@@ -996,29 +1299,51 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
     P.sc_own.upload(c.own);
     P.sc_tile.upload(c.tile);
   }
-  // Long rows: one task per 16384-entry segment, longest segments first (the fold of a segment
-  // is a sequential chain, so long chains must start early).
-  std::vector<int> seg_base(m, -1);
-  std::vector<std::pair<int, int2>> tasks;  // (segment length, task)
-  int slot = 0;
+  // Long rows: gather pieces, fold tasks per 16384-segment (longest first: the fold is a
+  // sequential chain), candidate pieces for rows above kCandSplit.
+  std::vector<int> long_off(m, -1), seg_base(m, -1), order;
+  long long goff = 0;
+  int slot       = 0;
   for (int k = 0; k < m; ++k) {
     const int L = row_start[k + 1] - row_start[k];
     if (L <= kShortNnz) continue;
+    long_off[k] = (int)goff;
+    goff += L;
     const int ns = (L + kSumSegment - 1) / kSumSegment;
     if (ns > 1) {
       seg_base[k] = slot;
       slot += ns;
     }
-    for (int s = 0; s < ns; ++s)
-      tasks.push_back({std::min(L - s * kSumSegment, kSumSegment), make_int2(k, s)});
+    order.push_back(k);
   }
-  std::stable_sort(tasks.begin(), tasks.end(),
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return row_start[a + 1] - row_start[a] > row_start[b + 1] - row_start[b];
+  });
+  std::vector<int2> piece, cpiece;
+  std::vector<std::pair<int, int2>> folds;
+  for (int k : order) {
+    const int L = row_start[k + 1] - row_start[k];
+    for (int p = 0; p * kPiece < L; ++p) {
+      piece.push_back(make_int2(k, p));
+      if (L > kCandSplit) cpiece.push_back(make_int2(k, p));
+    }
+    for (int s = 0; s * kSumSegment < L; ++s)
+      folds.push_back({std::min(L - s * kSumSegment, kSumSegment), make_int2(k, s)});
+  }
+  std::stable_sort(folds.begin(), folds.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
-  std::vector<int2> seg_task(tasks.size());
-  for (size_t j = 0; j < tasks.size(); ++j) seg_task[j] = tasks[j].second;
-  P.n_seg  = (int)seg_task.size();
-  P.n_part = slot;
-  P.seg_task.upload(seg_task);
+  std::vector<int2> fold(folds.size());
+  for (size_t j = 0; j < folds.size(); ++j) fold[j] = folds[j].second;
+  if (goff > 0x7FFFFFFFll) throw std::runtime_error("long-row entries exceed int32 offsets");
+  P.n_long_entries = goff;
+  P.n_piece        = (int)piece.size();
+  P.n_fold         = (int)fold.size();
+  P.n_cpiece       = (int)cpiece.size();
+  P.n_part         = slot;
+  P.long_off.upload(long_off);
+  P.piece_task.upload(piece);
+  P.fold_task.upload(fold);
+  P.cpiece_task.upload(cpiece);
   P.seg_base.upload(seg_base);
   // Long columns, longest first.
   std::vector<int> mcol;
@@ -1035,6 +1360,21 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.bounds.alloc(nn);
   P.rec.alloc(mm);
   P.aux.alloc(mm);
+  P.gbuf.alloc((size_t)std::max(goff, 1ll));
+  P.slot.alloc(nn);
+  {
+    std::vector<CandSlot> empty(nn);
+    for (auto& s : empty) {
+      s.lo_key  = kLoEmpty;
+      s.up_key  = kUpEmpty;
+      s.lo_zero = kZeroEmpty;
+      s.up_zero = kZeroEmpty;
+      s.pad0 = s.pad1 = 0;
+    }
+    BP_CUDA(cudaMemcpy(P.slot.p, empty.data(), sizeof(CandSlot) * nn, cudaMemcpyHostToDevice));
+  }
+  P.ready.alloc(mm);
+  BP_CUDA(cudaMemset(P.ready.p, 0, sizeof(unsigned) * mm));
   P.seg_part.alloc(std::max(slot, 1));
   P.seg_done.alloc(mm);
   BP_CUDA(cudaMemset(P.seg_done.p, 0, sizeof(int) * mm));
@@ -1044,15 +1384,19 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   BP_CUDA(cudaMemset(P.var_stamp.p, 0, sizeof(unsigned) * nn));
   // int lists per parity: drow_s (m), dvar_s, dvar_m (n each); changed (n)
   P.lists_i.alloc(2 * (mm + 2 * nn) + nn);
-  // int2 lists per parity: dseg (all segment tasks), xtask (N/256 + m)
-  const size_t nseg_cap = (size_t)std::max(P.n_seg, 1);
-  const size_t nx_cap   = (size_t)(N / 256) + mm + 1;
-  P.lists_i2.alloc(2 * (nseg_cap + nx_cap));
+  // int2 lists per parity: dpiece, dfold (all long-row tasks), xtask (N/256 + m)
+  const size_t np_cap = (size_t)std::max(P.n_piece, 1);
+  const size_t nf_cap = (size_t)std::max(P.n_fold, 1);
+  const size_t nx_cap = (size_t)(N / kTile) + mm + 1;
+  P.lists_i2.alloc(2 * (np_cap + nf_cap + nx_cap) + (size_t)(N / kTile) + nn + 1);
   P.ctl.alloc(1);
   DevState& S = P.st;
   S.bounds    = P.bounds.p;
   S.rec       = P.rec.p;
   S.aux       = P.aux.p;
+  S.gbuf      = P.gbuf.p;
+  S.slot      = P.slot.p;
+  S.ready     = P.ready.p;
   S.seg_part  = P.seg_part.p;
   S.seg_done  = P.seg_done.p;
   S.row_stamp = P.row_stamp.p;
@@ -1060,13 +1404,21 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   int* pi     = P.lists_i.p;
   int2* pi2   = P.lists_i2.p;
   for (int q = 0; q < 2; ++q) {
-    S.drow_s[q] = pi; pi += mm;
-    S.dvar_s[q] = pi; pi += nn;
-    S.dvar_m[q] = pi; pi += nn;
-    S.dseg[q]   = pi2; pi2 += nseg_cap;
-    S.xtask[q]  = pi2; pi2 += nx_cap;
+    S.drow_s[q] = pi;
+    pi += mm;
+    S.dvar_s[q] = pi;
+    pi += nn;
+    S.dvar_m[q] = pi;
+    pi += nn;
+    S.dpiece[q] = pi2;
+    pi2 += np_cap;
+    S.dfold[q] = pi2;
+    pi2 += nf_cap;
+    S.xtask[q] = pi2;
+    pi2 += nx_cap;
   }
   S.changed = pi;
+  S.ctask   = pi2;  // sum over vars of ceil(col nnz / kTile) <= N / kTile + n
   S.ctl     = P.ctl.p;
 
   int dev_sms = 0, per_sm = 0;
@@ -1091,6 +1443,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   if (P.stamp_base > 0xF0000000u - (unsigned)std::max(lim.max_rounds, 1) - 2) {
     BP_CUDA(cudaMemsetAsync(P.row_stamp.p, 0, sizeof(unsigned) * P.row_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.var_stamp.p, 0, sizeof(unsigned) * P.var_stamp.n, s));
+    BP_CUDA(cudaMemsetAsync(P.ready.p, 0, sizeof(unsigned) * P.ready.n, s));
     P.stamp_base = 1;
   }
   unsigned sb = P.stamp_base;
@@ -1125,20 +1478,25 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
 void stage_rows(Problem& P, const int* rows, int nrows, cudaStream_t s)
 {
   std::vector<int> sr;
-  std::vector<int2> sg;
+  std::vector<int2> pc, fd;
   for (int j = 0; j < nrows; ++j) {
     const int k = rows[j];
     const int L = P.h_row_start[k + 1] - P.h_row_start[k];
-    if (L <= kShortNnz) sr.push_back(k);
-    else
-      for (int q = 0; q * kSumSegment < L; ++q) sg.push_back(make_int2(k, q));
+    if (L <= kShortNnz) {
+      sr.push_back(k);
+    } else {
+      for (int q = 0; q * kPiece < L; ++q) pc.push_back(make_int2(k, q));
+      for (int q = 0; q * kSumSegment < L; ++q) fd.push_back(make_int2(k, q));
+    }
   }
   DevState& S = P.st;
   if (!sr.empty())
     BP_CUDA(cudaMemcpyAsync(S.drow_s[1], sr.data(), sr.size() * 4, cudaMemcpyHostToDevice, s));
-  if (!sg.empty())
-    BP_CUDA(cudaMemcpyAsync(S.dseg[1], sg.data(), sg.size() * 8, cudaMemcpyHostToDevice, s));
-  int cnt[3] = {(int)sr.size(), (int)sg.size(), nrows};
+  if (!pc.empty())
+    BP_CUDA(cudaMemcpyAsync(S.dpiece[1], pc.data(), pc.size() * 8, cudaMemcpyHostToDevice, s));
+  if (!fd.empty())
+    BP_CUDA(cudaMemcpyAsync(S.dfold[1], fd.data(), fd.size() * 8, cudaMemcpyHostToDevice, s));
+  int cnt[4] = {(int)sr.size(), (int)pc.size(), (int)fd.size(), nrows};
   BP_CUDA(cudaMemcpyAsync(&S.ctl->par[1].n_drow_s, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
   BP_CUDA(cudaStreamSynchronize(s));
 }

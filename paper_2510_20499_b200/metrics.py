@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-STAT_COLS = 10  # full, |R|, A (row nnz), |V|, B (col nnz), |C|, t_act, t_tight, t_xrow, t_xvar (ns)
+STAT_COLS = 12  # full, |R|, A (row nnz), |V|, B (col nnz), |C|, t_act, t_tight, t_xrow, t_xvar, t_gather (ns), spare
 
 
 def trim(stats: np.ndarray, rounds: int) -> np.ndarray:
