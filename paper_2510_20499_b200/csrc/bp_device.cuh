@@ -276,7 +276,7 @@ struct DevProblem {
   const int* sr_ci;         // column | integrality << 31
   const double* sr_val;
   const uint8_t* sr_own;    // owner's local row index inside its tile, per packed entry
-  const int* sr_tile;       // n_srtile + 1 packed-row starts
+  const int* sr_tile;       // (n_srtile + 1) x {first packed row, first packed entry}
   // Long rows (nnz > kShortNnz): their bounds are first gathered into a contiguous buffer
   // (gbuf, pieces of kPiece entries), then one warp per 16384-entry segment folds it streaming.
   const int* long_off;      // per row: offset of its entries in gbuf, -1 for short rows

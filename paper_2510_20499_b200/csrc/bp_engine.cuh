@@ -91,6 +91,7 @@ struct DevState {
   int* changed;
   int2* ctask;      // (var, kTile-entry column chunk) row-expansion tasks of the changed vars
   Ctl* ctl;
+  unsigned long long* dbg;  // optional debug counters (BP_DEBUG=1)
 };
 
 enum Mode { MODE_PROPAGATE = 0, MODE_ACTIVITY = 1, MODE_TIGHTEN = 2 };
@@ -132,6 +133,7 @@ struct Problem {
   DBuf<int> lists_i;  // backing store for int lists
   DBuf<int2> lists_i2;
   DBuf<Ctl> ctl;
+  DBuf<unsigned long long> dbg;
   DevState st{};
   unsigned stamp_base = 1;
   int grid_blocks = 0;

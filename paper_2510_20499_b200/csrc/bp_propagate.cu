@@ -29,6 +29,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "bp_engine.cuh"
 
@@ -97,6 +99,7 @@ struct WarpSmem {
   double2 vb[32];            // tighten tiles: the 32 variables' bounds
   double ract[32][2];        // short-row tiles: finite parts of each row's min/max activity
   int rinf[32][2];           //                  and infinite-contributor counts
+  int rk[32];                //                  and row ids (row bounds go to vb)
   unsigned char vint[32];    // tighten tiles: integrality
   int chg[64];               // changed-var staging before a global append
 };
@@ -147,6 +150,28 @@ __device__ __forceinline__ int warp_fetch(Ctx& c, int* cursor, int step)
   if (c.lane == 0) t = atomicAdd(cursor, step);
   return __shfl_sync(FULL, t, 0);
 }
+
+// Dynamic work cursor with the next fetch in flight while the current task runs.
+struct Prefetch {
+  Ctx& c;
+  int* cur;
+  int step, t, nx;
+  __device__ Prefetch(Ctx& c_, int* cur_, int step_) : c(c_), cur(cur_), step(step_)
+  {
+    t = warp_fetch(c, cur, step);
+    issue();
+  }
+  __device__ __forceinline__ void issue()
+  {
+    nx = 0;
+    if (c.lane == 0) nx = atomicAdd(cur, step);
+  }
+  __device__ __forceinline__ void advance()
+  {
+    t = __shfl_sync(FULL, nx, 0);
+    issue();
+  }
+};
 
 // Up to 32 listed items as one flattened entry stream: returns the stream length and this lane's
 // item offset; fills w.off / w.st.
@@ -200,18 +225,19 @@ __device__ void long_gather(Ctx& c, int k, int p)
   const int rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
   const int e0 = p * kPiece, e1 = min(L, e0 + kPiece);
   double2* out = S.gbuf + __ldg(P.long_off + k);
-  for (int j0 = e0; j0 < e1; j0 += 2 * kTile) {
-    int col[2 * kEPL];
+  constexpr int G = 4 * kEPL;  // 16 gathers per lane in flight
+  for (int j0 = e0; j0 < e1; j0 += 32 * G) {
+    int col[G];
 #pragma unroll
-    for (int h = 0; h < 2 * kEPL; ++h) {
+    for (int h = 0; h < G; ++h) {
       const int e = j0 + h * 32 + c.lane;
       col[h]      = e < e1 ? __ldg(P.row_col + rs + e) : -1;
     }
-    double2 bd[2 * kEPL];
+    double2 bd[G];
 #pragma unroll
-    for (int h = 0; h < 2 * kEPL; ++h) bd[h] = col[h] >= 0 ? S.bounds[col[h]] : make_double2(0.0, 0.0);
+    for (int h = 0; h < G; ++h) bd[h] = col[h] >= 0 ? S.bounds[col[h]] : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int h = 0; h < 2 * kEPL; ++h)
+    for (int h = 0; h < G; ++h)
       if (col[h] >= 0) out[j0 + h * 32 + c.lane] = bd[h];
   }
 }
@@ -243,6 +269,31 @@ __device__ void long_candidates(Ctx& c, int k, int e0, int e1, double mnf, int n
       publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
     }
   }
+}
+
+// Sequential left-to-right sum of src[0..cnt) onto acc (the reference's fold order), with the
+// shared-memory loads of the next 8 values in flight while the current 8 are added.
+__device__ __forceinline__ double fold_seq(const double* src, int cnt, double acc)
+{
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  int j             = 0;
+  if (cnt >= 8) {
+    double2 v0 = s2[0], v1 = s2[1], v2 = s2[2], v3 = s2[3];
+    for (j = 8; j + 8 <= cnt; j += 8) {
+      const double2 w0 = s2[j / 2], w1 = s2[j / 2 + 1], w2 = s2[j / 2 + 2], w3 = s2[j / 2 + 3];
+      acc = __dadd_rn(acc, v0.x); acc = __dadd_rn(acc, v0.y);
+      acc = __dadd_rn(acc, v1.x); acc = __dadd_rn(acc, v1.y);
+      acc = __dadd_rn(acc, v2.x); acc = __dadd_rn(acc, v2.y);
+      acc = __dadd_rn(acc, v3.x); acc = __dadd_rn(acc, v3.y);
+      v0 = w0; v1 = w1; v2 = w2; v3 = w3;
+    }
+    acc = __dadd_rn(acc, v0.x); acc = __dadd_rn(acc, v0.y);
+    acc = __dadd_rn(acc, v1.x); acc = __dadd_rn(acc, v1.y);
+    acc = __dadd_rn(acc, v2.x); acc = __dadd_rn(acc, v2.y);
+    acc = __dadd_rn(acc, v3.x); acc = __dadd_rn(acc, v3.y);
+  }
+  for (; j < cnt; ++j) acc = __dadd_rn(acc, src[j]);
+  return acc;
 }
 
 // F2 / P2: one 16384-entry segment of a long row. All lanes stage contributions of 256 entries
@@ -296,12 +347,7 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
       a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
       bd[h]       = e < e1 ? gb[e] : make_double2(0.0, 0.0);
     }
-    if (lane < 2) {
-      const double* src = lane ? c.w.b1 : c.w.b0;
-      const int cnt     = lane ? px : pm;
-#pragma unroll 8
-      for (int j = 0; j < cnt; ++j) acc = __dadd_rn(acc, src[j]);
-    }
+    if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
     __syncwarp();
   }
   imn            = warp_sum(imn);
@@ -386,25 +432,36 @@ __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp)
 }
 
 // A packed tile of short rows: gathers, per-lane folds, and (with `cand`) the candidates of every
-// entry from the registers that still hold its coefficient and bounds.
+// entry from the registers that still hold its coefficient and bounds. Three dependent memory
+// levels: tile descriptor -> (entries, per-lane row info) -> (bounds gathers, row bounds).
 __device__ void short_tile(Ctx& c, int t, bool cand)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int r0 = __ldg(P.sr_tile + t), r1 = __ldg(P.sr_tile + t + 1);
-  const int p0 = __ldg(P.sr_ptr + r0), p1 = __ldg(P.sr_ptr + r1);
-  int ci[kEPL];
+  const int2 d0 = __ldg(reinterpret_cast<const int2*>(P.sr_tile) + t);      // (r0, p0)
+  const int2 d1 = __ldg(reinterpret_cast<const int2*>(P.sr_tile) + t + 1);  // (r1, p1)
+  const int r0 = d0.x, p0 = d0.y, r1 = d1.x, p1 = d1.y;
+  const int nr = r1 - r0;
+  int ci[kEPL], own[kEPL];
   double a[kEPL];
 #pragma unroll
   for (int h = 0; h < kEPL; ++h) {
     const int f = p0 + h * 32 + c.lane;
     ci[h]       = f < p1 ? __ldg(P.sr_ci + f) : -1;
     a[h]        = f < p1 ? __ldg(P.sr_val + f) : 0.0;
+    own[h]      = f < p1 ? __ldg(P.sr_own + f) : 0;
+  }
+  int k = -1, q0 = 0, q1 = 0;
+  if (c.lane < nr) {
+    k  = __ldg(P.srow + r0 + c.lane);
+    q0 = __ldg(P.sr_ptr + r0 + c.lane) - p0;
+    q1 = __ldg(P.sr_ptr + r0 + c.lane + 1) - p0;
   }
   double2 bd[kEPL];
 #pragma unroll
   for (int h = 0; h < kEPL; ++h)
     bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+  const double2 cb = k >= 0 ? __ldg(&P.cons[k]) : make_double2(0.0, 0.0);
 #pragma unroll
   for (int h = 0; h < kEPL; ++h) {
     double cm = 0.0, cx = 0.0;
@@ -415,10 +472,7 @@ __device__ void short_tile(Ctx& c, int t, bool cand)
     c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
   }
   __syncwarp();
-  const int nr = r1 - r0;
-  if (c.lane < nr) {
-    const int r  = r0 + c.lane;
-    const int q0 = __ldg(P.sr_ptr + r) - p0, q1 = __ldg(P.sr_ptr + r + 1) - p0;
+  if (k >= 0) {
     double smn = 0.0, smx = 0.0;
     int imn = 0, imx = 0;
     for (int q = q0; q < q1; ++q) {
@@ -427,25 +481,31 @@ __device__ void short_tile(Ctx& c, int t, bool cand)
       imn += c.w.fl[q] & 1;
       imx += c.w.fl[q] >> 1;
     }
-    write_rec(P, S, __ldg(P.srow + r), smn, smx, imn, imx);
+    RowRec r;
+    r.min = imn ? box_count(imn) : smn;
+    r.max = imx ? box_count(imx) : smx;
+    r.g   = cb.y;
+    r.h   = cb.x;
+    st_rec(S.rec + k, r);
+    if (imn | imx) S.aux[k] = make_double2(smn, smx);
     c.w.ract[c.lane][0] = smn;
     c.w.ract[c.lane][1] = smx;
     c.w.rinf[c.lane][0] = imn;
     c.w.rinf[c.lane][1] = imx;
+    c.w.rk[c.lane]      = k;
+    c.w.vb[c.lane]      = cb;
   }
   __syncwarp();
   if (cand) {
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
-      const int f = p0 + h * 32 + c.lane;
       if (ci[h] == -1) continue;
-      const int o      = __ldg(P.sr_own + f);
-      const int k      = __ldg(P.srow + r0 + o);
-      const double2 cb = __ldg(&P.cons[k]);
+      const int o       = own[h];
+      const double2 rcb = c.w.vb[o];
       double cl, cu;
       cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], c.w.ract[o][0], c.w.rinf[o][0],
-                    c.w.ract[o][1], c.w.rinf[o][1], cb.y, cb.x, cl, cu);
-      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
+                    c.w.ract[o][1], c.w.rinf[o][1], rcb.y, rcb.x, cl, cu);
+      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, c.w.rk[o]);
     }
   }
   __syncwarp();
@@ -513,7 +573,8 @@ __device__ void phase_gather(Ctx& c, ParCtl* pc, int par, bool full)
 {
   const int n       = full ? c.P.n_piece : ldv(&pc->n_dpiece);
   const int2* tasks = full ? c.P.piece_task : c.S.dpiece[par];
-  for (int t = warp_fetch(c, &pc->cur_a, 1); t < n; t = warp_fetch(c, &pc->cur_a, 1)) {
+  for (Prefetch it_t(c, &pc->cur_a, 1); it_t.t < n; it_t.advance()) {
+    const int t = it_t.t;
     const int2 tk = tasks[t];
     long_gather(c, tk.x, tk.y);
   }
@@ -530,25 +591,38 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     // one cursor over [folds | short tiles | candidate pieces]: the longest chains start first
     const int ns = P.n_srtile, nc = cand ? P.n_cpiece : 0;
     const int total = nf + ns + nc;
-    for (int t = warp_fetch(c, &pc->cur_b, 1); t < total; t = warp_fetch(c, &pc->cur_b, 1)) {
+    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < total; it_t.advance()) {
+      const int t                = it_t.t;
+      const long long c0         = S.dbg ? clock64() : 0;
+      int kind;
       if (t < nf) {
         const int2 tk = folds[t];
         long_fold(c, tk.x, tk.y, cand, stamp);
+        kind = 0;
       } else if (t < nf + ns) {
         short_tile(c, t - nf, cand);
+        kind = 1;
       } else {
         const int2 tk = P.cpiece_task[t - nf - ns];
         long_cand_piece(c, tk.x, tk.y, stamp);
+        kind = 2;
+      }
+      if (S.dbg && c.lane == 0) {  // debug counters: per task kind total / max cycles, count
+        const unsigned long long d = (unsigned long long)(clock64() - c0);
+        atomicAdd(S.dbg + 3 * kind, d);
+        atomicMax(S.dbg + 3 * kind + 1, d);
+        atomicAdd(S.dbg + 3 * kind + 2, 1ull);
       }
     }
   } else {
-    for (int t = warp_fetch(c, &pc->cur_b, 1); t < nf; t = warp_fetch(c, &pc->cur_b, 1)) {
+    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nf; it_t.advance()) {
+    const int t = it_t.t;
       const int2 tk = folds[t];
       long_fold(c, tk.x, tk.y, false, stamp);
     }
     const int n = ldv(&pc->n_drow_s);
-    for (int t = warp_fetch(c, &pc->cur_c, 32); t < n; t = warp_fetch(c, &pc->cur_c, 32))
-      short_list_tile(c, S.drow_s[par], t, n);
+    for (Prefetch it_t(c, &pc->cur_c, 32); it_t.t < n; it_t.advance())
+      short_list_tile(c, S.drow_s[par], it_t.t, n);
   }
 }
 
@@ -635,7 +709,8 @@ __device__ void phase_finalize(Ctx& c, ParCtl* pc)
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   Tally t{0, 0, 0ull, 0};
-  for (int q = warp_fetch(c, &pc->cur_vs, 32); q < P.n; q = warp_fetch(c, &pc->cur_vs, 32)) {
+  for (Prefetch it_q(c, &pc->cur_vs, 32); it_q.t < P.n; it_q.advance()) {
+    const int q = it_q.t;
     const int i = q + c.lane;
     int res     = 0;
     if (i < P.n) {
@@ -828,19 +903,20 @@ __device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
   {
     const int n    = full ? P.n_mcol : ldv(&pc->n_dvar_m);
     const int* ids = full ? P.mcol : S.dvar_m[par];
-    for (int q = warp_fetch(c, &pc->cur_vm, 1); q < n; q = warp_fetch(c, &pc->cur_vm, 1)) {
+    for (Prefetch it_q(c, &pc->cur_vm, 1); it_q.t < n; it_q.advance()) {
+    const int q = it_q.t;
       const int i = ids[q];
       const int r = tighten_warp(c, i);
       tally(c, pc, t, c.lane == 0 ? i : -1, c.lane == 0 ? r : 0);
     }
   }
   if (full) {
-    for (int q = warp_fetch(c, &pc->cur_vs, 1); q < P.n_sctile; q = warp_fetch(c, &pc->cur_vs, 1))
-      tighten_tile_packed(c, q, pc, t);
+    for (Prefetch it_q(c, &pc->cur_vs, 1); it_q.t < P.n_sctile; it_q.advance())
+      tighten_tile_packed(c, it_q.t, pc, t);
   } else {
     const int n = ldv(&pc->n_dvar_s);
-    for (int q = warp_fetch(c, &pc->cur_vs, 32); q < n; q = warp_fetch(c, &pc->cur_vs, 32))
-      tighten_list_tile(c, S.dvar_s[par], q, n, pc, t);
+    for (Prefetch it_q(c, &pc->cur_vs, 32); it_q.t < n; it_q.advance())
+      tighten_list_tile(c, S.dvar_s[par], it_q.t, n, pc, t);
   }
   tally_flush_block(c, pc, t);
 }
@@ -896,7 +972,8 @@ __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
   unsigned long long roww = 0;
   int nall                = 0;
   const int nch = ldv(&pc->n_changed);
-  for (int t = warp_fetch(c, &pc->cur_x1, 32); t < nch; t = warp_fetch(c, &pc->cur_x1, 32)) {
+  for (Prefetch it_t(c, &pc->cur_x1, 32); it_t.t < nch; it_t.advance()) {
+    const int t = it_t.t;
     const int j = t + c.lane;
     const int i = j < nch ? S.changed[j] : -1;
     int cs = 0, L = 0;
@@ -923,7 +1000,8 @@ __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
     __syncwarp();
   }
   const int ntask = ldv(&pc->n_ctask);
-  for (int t = warp_fetch(c, &pc->cur_x2, 1); t < ntask; t = warp_fetch(c, &pc->cur_x2, 1)) {
+  for (Prefetch it_t(c, &pc->cur_x2, 1); it_t.t < ntask; it_t.advance()) {
+    const int t = it_t.t;
     const int2 tk = S.ctask[t];
     const int ce  = __ldg(P.col_start + tk.x + 1);
     const int e0  = __ldg(P.col_start + tk.x) + tk.y * kTile, e1 = min(ce, e0 + kTile);
@@ -978,7 +1056,8 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
   const DevState& S   = c.S;
   unsigned long long colw = 0;
   const int nr = ldv(&qc->n_drow_s);
-  for (int t = warp_fetch(c, &pc->cur_x3, 32); t < nr; t = warp_fetch(c, &pc->cur_x3, 32)) {
+  for (Prefetch it_t(c, &pc->cur_x3, 32); it_t.t < nr; it_t.advance()) {
+    const int t = it_t.t;
     const int j = t + c.lane;
     const int k = j < nr ? S.drow_s[qpar][j] : -1;
     int rs = 0, L = 0;
@@ -1004,7 +1083,8 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
     __syncwarp();
   }
   const int ntask = ldv(&qc->n_xtask);
-  for (int t = warp_fetch(c, &pc->cur_x4, 1); t < ntask; t = warp_fetch(c, &pc->cur_x4, 1)) {
+  for (Prefetch it_t(c, &pc->cur_x4, 1); it_t.t < ntask; it_t.advance()) {
+    const int t = it_t.t;
     const int2 tk = S.xtask[qpar][t];
     const int re  = __ldg(P.row_start + tk.x + 1);
     const int e0  = __ldg(P.row_start + tk.x) + tk.y * kTile, e1 = min(re, e0 + kTile);
@@ -1034,7 +1114,8 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     k_engine(DevProblem P, DevState S, Limits lim, int mode, int full_first, unsigned stamp_base,
              unsigned long long dense_thr, long long* stats)
 {
-  __shared__ Smem sm;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  Smem& sm            = *reinterpret_cast<Smem*>(dyn_smem);
   cg::grid_group grid = cg::this_grid();
   if (threadIdx.x == 0) {
     sm.blk_crossed  = 0;
@@ -1123,8 +1204,9 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     phase_expand_vars(c, pc, qc, qpar, stamp);
     grid.sync();
     if (st && lead) st[9] = (long long)(globaltimer() - t0);
-    // a frontier round costs ~ its gathers (row nnz + col nnz); a full round ~ N = 4 dense_thr
-    full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 3 * dense_thr;
+    // a frontier round costs ~ its gathers (row nnz + col nnz); a fused full round ~ N = 4 dense_thr
+    // gathers but with far better memory-level parallelism
+    full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 2 * dense_thr;
   }
   if (lead) {
     if (status == BP_STATUS_UNSET) status = any_change ? BP_STATUS_TIGHTENED : BP_STATUS_UNCHANGED;
@@ -1288,7 +1370,12 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
     P.sr_ci.upload(r.idx);
     P.sr_val.upload(r.val);
     P.sr_own.upload(r.own);
-    P.sr_tile.upload(r.tile);
+    std::vector<int> desc(2 * r.tile.size());  // (first packed row, first packed entry) per tile
+    for (size_t t = 0; t < r.tile.size(); ++t) {
+      desc[2 * t]     = r.tile[t];
+      desc[2 * t + 1] = r.ptr[r.tile[t]];
+    }
+    P.sr_tile.upload(desc);
     Packed c   = pack_short(n, col_start, col_row_in, col_val_in, nullptr);
     P.n_scol   = (int)c.ids.size();
     P.n_sctile = (int)c.tile.size() - 1;
@@ -1420,12 +1507,20 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.changed = pi;
   S.ctask   = pi2;  // sum over vars of ceil(col nnz / kTile) <= N / kTile + n
   S.ctl     = P.ctl.p;
+  S.dbg     = nullptr;
+  if (getenv("BP_DEBUG")) {
+    P.dbg.alloc(16);
+    BP_CUDA(cudaMemset(P.dbg.p, 0, 16 * sizeof(unsigned long long)));
+    S.dbg = P.dbg.p;
+  }
 
   int dev_sms = 0, per_sm = 0;
   BP_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, P.device));
-  BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine, kThreads, 0));
+  BP_CUDA(cudaFuncSetAttribute(k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(Smem)));
+  BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine, kThreads, sizeof(Smem)));
   if (per_sm < 1) throw cuda_error("engine kernel cannot be resident (occupancy 0)");
-  P.grid_blocks = dev_sms * std::min(per_sm, 2);
+  P.grid_blocks = dev_sms * std::min(per_sm, 4);
   BP_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
   BP_CUDA(cudaEventCreate(&P.ev0));
   BP_CUDA(cudaEventCreate(&P.ev1));
@@ -1453,7 +1548,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   long long* stp = d_stats;
   void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp};
   BP_CUDA(cudaEventRecord(P.ev0, s));
-  BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, 0, s));
+  BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
   BP_CUDA(cudaEventRecord(P.ev1, s));
   ++g_kernel_launches;
   RunResult r{0, 0, 0};
@@ -1466,6 +1561,16 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
     r.crossed = h[2];
   } else {
     BP_CUDA(cudaStreamSynchronize(s));
+  }
+  if (P.st.dbg) {
+    unsigned long long h[16];
+    BP_CUDA(cudaMemcpy(h, P.st.dbg, sizeof(h), cudaMemcpyDeviceToHost));
+    const char* nm[3] = {"fold", "short_tile", "cand_piece"};
+    for (int q = 0; q < 3; ++q)
+      fprintf(stderr, "[bp dbg] %-10s n=%llu avg=%.1f us max=%.1f us total=%.1f warp-ms\n", nm[q],
+              h[3 * q + 2], h[3 * q + 2] ? h[3 * q] / 1965.0 / h[3 * q + 2] : 0.0,
+              h[3 * q + 1] / 1965.0, h[3 * q] / 1965.0 / 1e3);
+    BP_CUDA(cudaMemset(P.st.dbg, 0, sizeof(h)));
   }
   float ms = 0.f;
   BP_CUDA(cudaEventElapsedTime(&ms, P.ev0, P.ev1));
