@@ -113,6 +113,44 @@ int bp_propagate_device(bp_problem* p, double* d_bounds2n, int32_t* infeasible,
 int bp_propagate_ex(bp_problem* p, double* d_bounds2n, int32_t* infeasible, const bp_limits* lim,
                     bp_result* res, void* stream, int32_t flags, int64_t* d_stats);
 
+/* ---------------------------------------------------------------- probing cache
+ * pulse::ProbingCache (probing.hpp:87-98) as an opaque host object built on the GPU. */
+typedef struct bp_cache bp_cache;
+
+/* Batched double probing: both branches of every listed variable, from root2n (NULL = the
+ * problem's original bounds). Entries follow pulse::probe_variable (probing.hpp:225-238),
+ * including default entries for variables without a branch spec. */
+int bp_probe_variables(bp_problem* p, const double* root2n, const int32_t* vars, int32_t nvars,
+                       bp_cache** out);
+/* pulse::prioritize_probe_vars (probing.hpp:105-190): integer vars in probing priority order. */
+int bp_prioritize_probe_vars(bp_problem* p, int32_t* order, int32_t* n_order);
+/* pulse::build_cache (probing.hpp:243-281): root = original bounds; candidates = priority order
+ * minus root-fixed vars; stops launching batches once budget_sec has elapsed. */
+int bp_build_cache(bp_problem* p, double budget_sec, bp_cache** out);
+int bp_cache_destroy(bp_cache* c);
+/* Stats: n_probed / n_infeasible_branches as ProbingCache; n_fallback = branches that ran on the
+ * full engine (uncertified root or overlay overflow); probe_ms = device time of the batch. */
+int bp_cache_info(const bp_cache* c, int32_t* n_vars, int32_t* n_probed,
+                  int32_t* n_infeasible_branches, int64_t* n_deltas, int32_t* n_fallback,
+                  int32_t* certified, double* probe_ms);
+/* Entry of v: *present = 0 if absent; hdr7 = {kind, forces_down, forces_up, down.feasible,
+ * up.feasible, n_down_deltas, n_up_deltas}; br4 = {down lo, down up, up lo, up up}. */
+int bp_cache_entry(const bp_cache* c, int32_t v, int32_t* present, int32_t* hdr7, double* br4);
+/* Deltas of branch side (0 down, 1 up) of v, ascending by var (probing.hpp:213-217). */
+int bp_cache_deltas(const bp_cache* c, int32_t v, int32_t side, int32_t* vars, double* lo,
+                    double* up);
+int bp_cache_root(const bp_cache* c, double* root2n);
+int bp_cache_create_empty(int32_t n_vars, const double* root2n, bp_cache** out);
+/* Serialisation of a cache slice for the multi-GPU gather (NCCL) and merge on rank 0. */
+int bp_cache_pack_size(const bp_cache* c, int64_t* bytes);
+int bp_cache_pack(const bp_cache* c, void* buf, int64_t bytes);
+int bp_cache_merge_packed(bp_cache* dst, const void* buf, int64_t bytes);
+/* pulse::assemble_bulk_warm_start (probing.hpp:292-352): merged bounds (2n), conflicts as
+ * (kept, evicted) pairs (capacity 2 * n), evicted vars (capacity n). */
+int bp_assemble_bulk_warm_start(const bp_cache* c, const int32_t* vars, const double* vals,
+                                int32_t n, double* bounds2n, int32_t* conflicts,
+                                int32_t* n_conflicts, int32_t* evicted, int32_t* n_evicted);
+
 /* Number of engine kernels launched by this process. */
 int64_t bp_kernel_launches(void);
 

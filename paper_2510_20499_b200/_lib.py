@@ -71,6 +71,26 @@ _SIGS = [
     ("bp_propagate_ex", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32),
                                   C.POINTER(bp_limits), C.POINTER(bp_result), C.c_void_p, C.c_int32,
                                   C.c_void_p]),
+    ("bp_probe_variables", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                     C.POINTER(C.c_void_p)]),
+    ("bp_prioritize_probe_vars", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
+    ("bp_build_cache", C.c_int, [C.c_void_p, C.c_double, C.POINTER(C.c_void_p)]),
+    ("bp_cache_destroy", C.c_int, [C.c_void_p]),
+    ("bp_cache_info", C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+    ("bp_cache_entry", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
+                                 C.c_void_p]),
+    ("bp_cache_deltas", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]),
+    ("bp_cache_root", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("bp_cache_create_empty", C.c_int, [C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("bp_cache_pack_size", C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    ("bp_cache_pack", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    ("bp_cache_merge_packed", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    ("bp_assemble_bulk_warm_start", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                              C.c_void_p, C.c_void_p, C.POINTER(C.c_int32),
+                                              C.c_void_p, C.POINTER(C.c_int32)]),
     ("bp_kernel_launches", C.c_int64, []),
     ("bp_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                  C.POINTER(C.c_int64)]),

@@ -1,0 +1,794 @@
+// Probing cache: host driver of the batched probe kernel, fallback path, priority order,
+// warm-start merge, and (de)serialisation for the multi-GPU gather. C-ABI in include/bp.h.
+//
+// References: probing.hpp:30-60 make_branch_spec, :105-190 prioritize_probe_vars,
+// :225-238 probe_variable, :243-281 build_cache, :292-352 assemble_bulk_warm_start.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bp.h"
+#include "bp_engine.cuh"
+#include "bp_probe.cuh"
+#include "bp_capi_internal.h"
+
+namespace bp {
+
+void HostCache::finalize_stats()
+{
+  n_probed              = (int)e_var.size();
+  n_infeasible_branches = 0;
+  for (size_t e = 0; e < e_var.size(); ++e)
+    n_infeasible_branches += (e_feas[2 * e] ? 0 : 1) + (e_feas[2 * e + 1] ? 0 : 1);
+}
+
+namespace {
+
+// probing.hpp:30-60. Returns 0 (no spec) or kind + 1; s = {down lo, down up, up lo, up up}.
+int branch_spec(double lo, double up, double* s)
+{
+  if (lo == up) return 0;
+  if (std::isfinite(lo) && std::isfinite(up)) {
+    const double mid = std::ceil((lo + up) / 2.0);
+    s[0] = lo; s[1] = mid - 1.0; s[2] = mid; s[3] = up;
+    return 1;
+  }
+  if (std::isfinite(lo)) {
+    s[0] = lo; s[1] = lo; s[2] = lo + 1.0; s[3] = up;
+    return 2;
+  }
+  if (std::isfinite(up)) {
+    s[0] = lo; s[1] = up - 1.0; s[2] = up; s[3] = up;
+    return 3;
+  }
+  return 0;
+}
+
+__global__ void k_diff(const double2* b, const double2* root, int n, int* cnt, int cap, int* var,
+                       double* lo, double* up)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2 x = b[i], r = root[i];
+    if (x.x != r.x || x.y != r.y) {
+      const int p = atomicAdd(cnt, 1);
+      if (p < cap) {
+        var[p] = i;
+        lo[p]  = x.x;
+        up[p]  = x.y;
+      }
+    }
+  }
+}
+
+Limits default_limits()
+{
+  Limits l;
+  l.max_rounds    = 64;
+  l.time_limit    = INFINITY;
+  l.abs_threshold = 1e-7;
+  l.rel_threshold = 1e-4;
+  l.incremental   = 1;
+  return l;
+}
+
+struct Branch {
+  int feasible = 1;
+  std::vector<int> var;
+  std::vector<double> lo, up;
+};
+
+// Full-engine branch (probing.hpp:194-219 verbatim semantics, any root).
+Branch engine_branch(Problem& P, const DBuf<double2>& d_root, int v, double blo, double bup,
+                     const std::vector<double>& root, cudaStream_t s)
+{
+  Branch br;
+  // std::max(root.lower(v), branch_lo) / std::min(root.upper(v), branch_up)
+  const double nlo = (root[2 * v] < blo) ? blo : root[2 * v];
+  const double nup = (bup < root[2 * v + 1]) ? bup : root[2 * v + 1];
+  if (nlo > nup) {
+    br.feasible = 0;
+    return br;
+  }
+  BP_CUDA(cudaMemcpyAsync(P.st.bounds, d_root.p, sizeof(double2) * P.n, cudaMemcpyDeviceToDevice, s));
+  const double2 nb = make_double2(nlo, nup);
+  BP_CUDA(cudaMemcpyAsync(P.st.bounds + v, &nb, sizeof(double2), cudaMemcpyHostToDevice, s));
+  BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+  const RunResult r = run_engine(P, MODE_PROPAGATE, true, default_limits(), s);
+  if (r.status == BP_STATUS_INFEASIBLE) {
+    br.feasible = 0;
+    return br;
+  }
+  int cap = 1 << 16;
+  for (;;) {
+    DBuf<int> cnt, var;
+    DBuf<double> dl, du;
+    cnt.alloc(1);
+    var.alloc(cap);
+    dl.alloc(cap);
+    du.alloc(cap);
+    BP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
+    k_diff<<<256, 256, 0, s>>>(P.st.bounds, d_root.p, P.n, cnt.p, cap, var.p, dl.p, du.p);
+    BP_CUDA(cudaGetLastError());
+    int h = 0;
+    BP_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaStreamSynchronize(s));
+    if (h > cap) {
+      cap = h;
+      continue;
+    }
+    std::vector<int> vv(h);
+    std::vector<double> l(h), u(h);
+    if (h) {
+      BP_CUDA(cudaMemcpy(vv.data(), var.p, sizeof(int) * h, cudaMemcpyDeviceToHost));
+      BP_CUDA(cudaMemcpy(l.data(), dl.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
+      BP_CUDA(cudaMemcpy(u.data(), du.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int> ord(h);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](int a, int b) { return vv[a] < vv[b]; });
+    for (int j : ord) {
+      br.var.push_back(vv[j]);
+      br.lo.push_back(l[j]);
+      br.up.push_back(u[j]);
+    }
+    return br;
+  }
+}
+
+}  // namespace
+
+// Probes `vars` (both branches each) from `root`; entries follow probe_variable semantics.
+HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vector<int>& vars,
+                     double budget_sec)
+{
+  const auto t_start = std::chrono::steady_clock::now();
+  auto elapsed       = [&] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  BP_CUDA(cudaSetDevice(P.device));
+  cudaStream_t s = P.stream;
+  const int n    = P.n;
+  HostCache C;
+  C.n    = n;
+  C.root = root;
+  C.entry_of.assign(n, -1);
+  DBuf<double2> d_root;
+  d_root.alloc(std::max(n, 1));
+  if (n) BP_CUDA(cudaMemcpy(d_root.p, root.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+  // certification: one full round from the root changes nothing (fixpoint) -> frontier starts
+  // are exact. Leaves the root activities in P.st.rec / aux.
+  bool certified = false;
+  if (n) {
+    BP_CUDA(cudaMemcpyAsync(P.st.bounds, d_root.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+    BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+    Limits one       = default_limits();
+    one.max_rounds   = 1;
+    const RunResult r = run_engine(P, MODE_PROPAGATE, true, one, s);
+    certified         = r.status == BP_STATUS_UNCHANGED;
+  }
+  C.certified = certified;
+
+  // tasks: down then up branch of every var with a spec (probing.hpp:228-234)
+  std::vector<int> tv, tslot;
+  std::vector<double> tlo, tup;
+  for (int v : vars) {
+    if (v < 0 || v >= n) throw std::out_of_range("probe var out of range");
+    int e = C.entry_of[v];
+    if (e < 0) {
+      e            = (int)C.e_var.size();
+      C.entry_of[v] = e;
+      C.e_var.push_back(v);
+      C.e_kind.push_back(0);
+      C.e_feas.insert(C.e_feas.end(), {1, 1});
+      C.e_force.insert(C.e_force.end(), {0, 0});
+      C.e_branch.insert(C.e_branch.end(), {0.0, 0.0, 0.0, 0.0});
+    }
+    double sp[4];
+    const int kind = branch_spec(root[2 * v], root[2 * v + 1], sp);
+    if (!kind) continue;  // default entry: no spec (probing.hpp:231)
+    C.e_kind[e] = kind - 1;
+    for (int q = 0; q < 4; ++q) C.e_branch[4 * e + q] = sp[q];
+    for (int side = 0; side < 2; ++side) {
+      tv.push_back(v);
+      tlo.push_back(sp[2 * side]);
+      tup.push_back(sp[2 * side + 1]);
+      tslot.push_back(2 * e + side);
+    }
+  }
+  const int ne = (int)C.e_var.size();
+  std::vector<Branch> res(2 * (size_t)ne);
+  std::vector<uint8_t> done(2 * (size_t)ne, 0);
+  for (int e = 0; e < ne; ++e) done[2 * e] = done[2 * e + 1] = 1;
+  for (int slot : tslot) done[slot] = 0;
+
+  const int ntask = (int)tv.size();
+  std::vector<int> fallback;
+  if (certified && ntask) {
+    const int chunk = 1 << 18;
+    DBuf<int> dvar, dcur, dstat, dcnt;
+    DBuf<double> dlo, dup;
+    DBuf<long long> doff;
+    DBuf<unsigned long long> dpc;
+    long long pool_cap = 32ll * std::min(ntask, chunk) + 4096;
+    DBuf<int> pvar;
+    DBuf<double> plo, pup;
+    pvar.alloc(pool_cap);
+    plo.alloc(pool_cap);
+    pup.alloc(pool_cap);
+    ProbeRoot R{d_root.p, P.st.rec, P.st.aux};
+    for (int t0 = 0; t0 < ntask; t0 += chunk) {
+      if (t0 > 0 && elapsed() >= budget_sec) break;
+      const int nt = std::min(chunk, ntask - t0);
+      dvar.upload(tv.data() + t0, nt);
+      dlo.upload(tlo.data() + t0, nt);
+      dup.upload(tup.data() + t0, nt);
+      dcur.alloc(1);
+      dstat.alloc(nt);
+      dcnt.alloc(nt);
+      doff.alloc(nt);
+      dpc.alloc(1);
+      for (;;) {
+        BP_CUDA(cudaMemsetAsync(dcur.p, 0, sizeof(int), s));
+        BP_CUDA(cudaMemsetAsync(dpc.p, 0, sizeof(unsigned long long), s));
+        ProbeBatch B{nt, dvar.p, dlo.p, dup.p, dcur.p, dstat.p, dcnt.p, doff.p, dpc.p,
+                     pool_cap, pvar.p, plo.p, pup.p};
+        BP_CUDA(cudaEventRecord(P.ev0, s));
+        probe_launch(P, R, B, default_limits(), s);
+        BP_CUDA(cudaEventRecord(P.ev1, s));
+        unsigned long long used = 0;
+        BP_CUDA(cudaMemcpyAsync(&used, dpc.p, sizeof(used), cudaMemcpyDeviceToHost, s));
+        BP_CUDA(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        BP_CUDA(cudaEventElapsedTime(&ms, P.ev0, P.ev1));
+        C.probe_ms += ms;
+        if ((long long)used > pool_cap) {  // grow the delta pool and rerun the chunk
+          pool_cap = (long long)used + 4096;
+          pvar.alloc(pool_cap);
+          plo.alloc(pool_cap);
+          pup.alloc(pool_cap);
+          continue;
+        }
+        std::vector<int> st(nt), cn(nt);
+        std::vector<long long> of(nt);
+        BP_CUDA(cudaMemcpy(st.data(), dstat.p, sizeof(int) * nt, cudaMemcpyDeviceToHost));
+        BP_CUDA(cudaMemcpy(cn.data(), dcnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost));
+        BP_CUDA(cudaMemcpy(of.data(), doff.p, sizeof(long long) * nt, cudaMemcpyDeviceToHost));
+        std::vector<int> hv(used);
+        std::vector<double> hl(used), hu(used);
+        if (used) {
+          BP_CUDA(cudaMemcpy(hv.data(), pvar.p, sizeof(int) * used, cudaMemcpyDeviceToHost));
+          BP_CUDA(cudaMemcpy(hl.data(), plo.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
+          BP_CUDA(cudaMemcpy(hu.data(), pup.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
+        }
+        for (int j = 0; j < nt; ++j) {
+          const int t = t0 + j;
+          Branch& br  = res[tslot[t]];
+          if (st[j] == 0) {
+            br.feasible = 1;
+            br.var.assign(hv.begin() + of[j], hv.begin() + of[j] + cn[j]);
+            br.lo.assign(hl.begin() + of[j], hl.begin() + of[j] + cn[j]);
+            br.up.assign(hu.begin() + of[j], hu.begin() + of[j] + cn[j]);
+            done[tslot[t]] = 1;
+          } else if (st[j] == 1) {
+            br.feasible    = 0;
+            done[tslot[t]] = 1;
+          } else {
+            fallback.push_back(t);
+          }
+        }
+        break;
+      }
+    }
+  } else {
+    for (int t = 0; t < ntask; ++t) fallback.push_back(t);
+  }
+  for (int t : fallback) {
+    if (elapsed() >= budget_sec) break;
+    res[tslot[t]]  = engine_branch(P, d_root, tv[t], tlo[t], tup[t], root, s);
+    done[tslot[t]] = 1;
+    C.n_fallback++;
+  }
+  // assemble (entries whose branches were not both computed within the budget are dropped)
+  HostCache out;
+  out.n         = n;
+  out.root      = root;
+  out.certified = certified;
+  out.probe_ms  = C.probe_ms;
+  out.n_fallback = C.n_fallback;
+  out.entry_of.assign(n, -1);
+  out.d_off.push_back(0);
+  for (int e = 0; e < ne; ++e) {
+    if (!done[2 * e] || !done[2 * e + 1]) continue;
+    const int v    = C.e_var[e];
+    const int ne2  = (int)out.e_var.size();
+    out.entry_of[v] = ne2;
+    out.e_var.push_back(v);
+    out.e_kind.push_back(C.e_kind[e]);
+    for (int q = 0; q < 4; ++q) out.e_branch.push_back(C.e_branch[4 * e + q]);
+    const Branch& dn = res[2 * e];
+    const Branch& upb = res[2 * e + 1];
+    out.e_feas.push_back((uint8_t)dn.feasible);
+    out.e_feas.push_back((uint8_t)upb.feasible);
+    out.e_force.push_back((uint8_t)(!upb.feasible && dn.feasible));  // forces_down
+    out.e_force.push_back((uint8_t)(!dn.feasible && upb.feasible));  // forces_up
+    for (const Branch* b : {&dn, &upb}) {
+      out.d_var.insert(out.d_var.end(), b->var.begin(), b->var.end());
+      out.d_lo.insert(out.d_lo.end(), b->lo.begin(), b->lo.end());
+      out.d_up.insert(out.d_up.end(), b->up.begin(), b->up.end());
+      out.d_off.push_back((long long)out.d_var.size());
+    }
+  }
+  out.finalize_stats();
+  return out;
+}
+
+// probing.hpp:105-190 from the original bounds' activities.
+std::vector<int> prioritize(const std::vector<int>& row_start, const std::vector<int>& col_start,
+                            const int* col_row, const double* col_val, const uint8_t* is_int,
+                            const double* var_lower, const double* var_upper,
+                            const double* cons_lower, const double* cons_upper,
+                            const std::vector<double>& act, const std::vector<int>& nmin,
+                            const std::vector<int>& nmax)
+{
+  const int n = (int)col_start.size() - 1;
+  struct Key {
+    int violated;
+    double max_violation, min_unit_slack;
+    int var;
+  };
+  std::vector<Key> keys;
+  const double kFeasTol = 1e-6;
+  for (int i = 0; i < n; ++i) {
+    if (!is_int[i]) continue;
+    Key key{0, 0.0, INFINITY, i};
+    bool pos = false, neg = false;
+    for (int e = col_start[i]; e < col_start[i + 1]; ++e) (col_val[e] > 0 ? pos : neg) = true;
+    const double lo = var_lower[i], up = var_upper[i];
+    for (int e = col_start[i]; e < col_start[i + 1]; ++e) {
+      const int k    = col_row[e];
+      const double a = col_val[e];
+      if (pos && neg) {
+        const double min_c = a > 0 ? a * lo : a * up;
+        const double max_c = a > 0 ? a * up : a * lo;
+        const bool min_inf = a > 0 ? lo == -INFINITY : up == INFINITY;
+        const bool max_inf = a > 0 ? up == INFINITY : lo == -INFINITY;
+        if (std::isfinite(cons_upper[k]) && nmin[k] - (min_inf ? 1 : 0) == 0) {
+          const double fm = max_inf ? INFINITY : act[2 * k] - (min_inf ? 0.0 : min_c) + max_c;
+          if (fm > cons_upper[k] + kFeasTol) {
+            key.violated++;
+            key.max_violation = std::max(key.max_violation, fm - cons_upper[k]);
+          }
+        }
+        if (std::isfinite(cons_lower[k]) && nmax[k] - (max_inf ? 1 : 0) == 0) {
+          const double fx = min_inf ? -INFINITY : act[2 * k + 1] - (max_inf ? 0.0 : max_c) + min_c;
+          if (fx < cons_lower[k] - kFeasTol) {
+            key.violated++;
+            key.max_violation = std::max(key.max_violation, cons_lower[k] - fx);
+          }
+        }
+      }
+      if (std::isfinite(cons_upper[k]) && nmin[k] == 0) {
+        const double slack = cons_upper[k] - act[2 * k];
+        if (slack > 0.0) key.min_unit_slack = std::min(key.min_unit_slack, std::abs(a) / slack);
+      }
+      if (std::isfinite(cons_lower[k]) && nmax[k] == 0) {
+        const double slack = act[2 * k + 1] - cons_lower[k];
+        if (slack > 0.0) key.min_unit_slack = std::min(key.min_unit_slack, std::abs(a) / slack);
+      }
+    }
+    keys.push_back(key);
+  }
+  std::stable_sort(keys.begin(), keys.end(), [](const Key& x, const Key& y) {
+    if (x.violated != y.violated) return x.violated > y.violated;
+    if (x.max_violation != y.max_violation) return x.max_violation > y.max_violation;
+    return x.min_unit_slack < y.min_unit_slack;
+  });
+  std::vector<int> order;
+  for (const auto& k : keys) order.push_back(k.var);
+  (void)row_start;
+  return order;
+}
+
+// probing.hpp:292-352 over the flat cache. Returns merged bounds; fills conflicts / evicted.
+void warm_start(const HostCache& C, const int* vars, const double* vals, int na,
+                std::vector<double>& bounds, std::vector<int>& conflicts, std::vector<int>& evicted)
+{
+  bounds = C.root;
+  conflicts.clear();
+  evicted.clear();
+  std::vector<int> last_writer(C.n, -1);
+  std::vector<uint8_t> ev(C.n, 0);
+  struct Undo {
+    int var;
+    double lo, up;
+    int writer;
+  };
+  std::vector<Undo> undo;
+  for (int j = 0; j < na; ++j) {
+    const int v = vars[j];
+    const int e = (v >= 0 && v < C.n) ? C.entry_of[v] : -1;
+    if (e < 0) continue;
+    const int side = (vals[j] <= C.e_branch[4 * e + 1]) ? 0 : 1;
+    if (!C.e_feas[2 * e + side]) {
+      conflicts.push_back(v);
+      conflicts.push_back(v);
+      if (!ev[v]) {
+        ev[v] = 1;
+        evicted.push_back(v);
+      }
+      continue;
+    }
+    undo.clear();
+    bool conflict   = false;
+    int conflicting = -1;
+    for (long long d = C.d_off[2 * e + side]; d < C.d_off[2 * e + side + 1]; ++d) {
+      const int dv    = C.d_var[d];
+      const double cl = bounds[2 * dv], cu = bounds[2 * dv + 1];
+      const double nl = (cl < C.d_lo[d]) ? C.d_lo[d] : cl;  // std::max(cur, delta)
+      const double nu = (C.d_up[d] < cu) ? C.d_up[d] : cu;  // std::min(cur, delta)
+      if (nl > nu + 1e-9) {
+        conflict    = true;
+        conflicting = last_writer[dv] >= 0 ? last_writer[dv] : v;
+        break;
+      }
+      if (nl != cl || nu != cu) {
+        undo.push_back({dv, cl, cu, last_writer[dv]});
+        bounds[2 * dv]     = nl;
+        bounds[2 * dv + 1] = nu;
+        last_writer[dv]    = v;
+      }
+    }
+    if (conflict) {
+      for (auto it = undo.rbegin(); it != undo.rend(); ++it) {
+        bounds[2 * it->var]     = it->lo;
+        bounds[2 * it->var + 1] = it->up;
+        last_writer[it->var]    = it->writer;
+      }
+      conflicts.push_back(conflicting);
+      conflicts.push_back(v);
+      if (!ev[v]) {
+        ev[v] = 1;
+        evicted.push_back(v);
+      }
+    }
+  }
+}
+
+}  // namespace bp
+
+// ------------------------------------------------------------------ C-ABI
+
+struct bp_cache {
+  bp::HostCache c;
+};
+
+namespace {
+
+template <class F>
+int cguard(F&& f)
+{
+  try {
+    f();
+    return BP_OK;
+  } catch (const std::invalid_argument& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_OUT_OF_RANGE;
+  } catch (const bp::cuda_error& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_CUDA;
+  } catch (const std::exception& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_RUNTIME;
+  }
+}
+
+void need(bool ok, const char* what)
+{
+  if (!ok) throw std::invalid_argument(what);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bp_probe_variables(bp_problem* p, const double* root2n, const int32_t* vars, int32_t nvars,
+                       bp_cache** out)
+{
+  return cguard([&] {
+    need(p && out && (nvars == 0 || vars), "null argument");
+    bp::Problem& P = bp_problem_impl(p);
+    std::lock_guard<std::mutex> lk(P.mu);
+    std::vector<double> root(2 * (size_t)P.n);
+    if (root2n) std::memcpy(root.data(), root2n, sizeof(double) * root.size());
+    else bp_problem_root(p, root.data());
+    std::vector<int> v(vars, vars + nvars);
+    auto c = std::make_unique<bp_cache>();
+    c->c   = bp::probe_vars(P, root, v, INFINITY);
+    *out   = c.release();
+  });
+}
+
+int bp_prioritize_probe_vars(bp_problem* p, int32_t* order, int32_t* n_order)
+{
+  return cguard([&] {
+    need(p && order && n_order, "null argument");
+    bp::Problem& P = bp_problem_impl(p);
+    std::vector<double> root(2 * (size_t)P.n);
+    bp_problem_root(p, root.data());
+    std::vector<double> act(2 * (size_t)P.m);
+    std::vector<int> nmin(P.m), nmax(P.m);
+    if (int rc = bp_compute_activities(p, root.data(), nullptr, -1, act.data(), nmin.data(), nmax.data()))
+      throw std::runtime_error(bp_last_error());
+    std::lock_guard<std::mutex> lk(P.mu);
+    const bp_problem_host& H = bp_problem_hostdata(p);
+    const auto o = bp::prioritize(P.h_row_start, P.h_col_start, H.col_row.data(), H.col_val.data(),
+                                  H.is_integer.data(), H.var_lower.data(), H.var_upper.data(),
+                                  H.cons_lower.data(), H.cons_upper.data(), act, nmin, nmax);
+    std::copy(o.begin(), o.end(), order);
+    *n_order = (int32_t)o.size();
+  });
+}
+
+int bp_build_cache(bp_problem* p, double budget_sec, bp_cache** out)
+{
+  return cguard([&] {
+    need(p && out, "null argument");
+    bp::Problem& P = bp_problem_impl(p);
+    std::vector<double> root(2 * (size_t)P.n);
+    bp_problem_root(p, root.data());
+    auto c = std::make_unique<bp_cache>();
+    c->c.n    = P.n;
+    c->c.root = root;
+    c->c.entry_of.assign(P.n, -1);
+    c->c.d_off.push_back(0);
+    if (budget_sec > 0.0) {  // probing.hpp:248
+      std::vector<int> order(P.n);
+      int32_t no = 0;
+      if (int rc = bp_prioritize_probe_vars(p, order.data(), &no)) throw std::runtime_error(bp_last_error());
+      std::vector<int> cand;
+      for (int j = 0; j < no; ++j)
+        if (root[2 * order[j]] != root[2 * order[j] + 1]) cand.push_back(order[j]);
+      std::lock_guard<std::mutex> lk(P.mu);
+      c->c = bp::probe_vars(P, root, cand, budget_sec);
+    }
+    *out = c.release();
+  });
+}
+
+int bp_cache_destroy(bp_cache* c)
+{
+  delete c;
+  return BP_OK;
+}
+
+int bp_cache_info(const bp_cache* c, int32_t* n_vars, int32_t* n_probed,
+                  int32_t* n_infeasible_branches, int64_t* n_deltas, int32_t* n_fallback,
+                  int32_t* certified, double* probe_ms)
+{
+  return cguard([&] {
+    need(c, "null cache");
+    if (n_vars) *n_vars = c->c.n;
+    if (n_probed) *n_probed = c->c.n_probed;
+    if (n_infeasible_branches) *n_infeasible_branches = c->c.n_infeasible_branches;
+    if (n_deltas) *n_deltas = (int64_t)c->c.d_var.size();
+    if (n_fallback) *n_fallback = c->c.n_fallback;
+    if (certified) *certified = c->c.certified ? 1 : 0;
+    if (probe_ms) *probe_ms = c->c.probe_ms;
+  });
+}
+
+int bp_cache_entry(const bp_cache* c, int32_t v, int32_t* present, int32_t* hdr7, double* br4)
+{
+  return cguard([&] {
+    need(c && present && hdr7 && br4, "null argument");
+    if (v < 0 || v >= c->c.n) throw std::out_of_range("var out of range");
+    const int e = c->c.entry_of[v];
+    *present    = e >= 0;
+    if (e < 0) return;
+    hdr7[0] = c->c.e_kind[e];
+    hdr7[1] = c->c.e_force[2 * e];
+    hdr7[2] = c->c.e_force[2 * e + 1];
+    hdr7[3] = c->c.e_feas[2 * e];
+    hdr7[4] = c->c.e_feas[2 * e + 1];
+    hdr7[5] = (int32_t)(c->c.d_off[2 * e + 1] - c->c.d_off[2 * e]);
+    hdr7[6] = (int32_t)(c->c.d_off[2 * e + 2] - c->c.d_off[2 * e + 1]);
+    for (int q = 0; q < 4; ++q) br4[q] = c->c.e_branch[4 * e + q];
+  });
+}
+
+int bp_cache_deltas(const bp_cache* c, int32_t v, int32_t side, int32_t* vars, double* lo,
+                    double* up)
+{
+  return cguard([&] {
+    need(c && vars && lo && up && (side == 0 || side == 1), "bad argument");
+    if (v < 0 || v >= c->c.n) throw std::out_of_range("var out of range");
+    const int e = c->c.entry_of[v];
+    if (e < 0) throw std::out_of_range("var has no cache entry");
+    for (long long d = c->c.d_off[2 * e + side], j = 0; d < c->c.d_off[2 * e + side + 1]; ++d, ++j) {
+      vars[j] = c->c.d_var[d];
+      lo[j]   = c->c.d_lo[d];
+      up[j]   = c->c.d_up[d];
+    }
+  });
+}
+
+int bp_cache_root(const bp_cache* c, double* root2n)
+{
+  return cguard([&] {
+    need(c && root2n, "null argument");
+    std::memcpy(root2n, c->c.root.data(), sizeof(double) * c->c.root.size());
+  });
+}
+
+int bp_cache_create_empty(int32_t n_vars, const double* root2n, bp_cache** out)
+{
+  return cguard([&] {
+    need(out && n_vars >= 0 && (n_vars == 0 || root2n), "bad argument");
+    auto c   = std::make_unique<bp_cache>();
+    c->c.n   = n_vars;
+    c->c.root.assign(root2n, root2n + 2 * (size_t)n_vars);
+    c->c.entry_of.assign(n_vars, -1);
+    c->c.d_off.push_back(0);
+    *out = c.release();
+  });
+}
+
+// Packed slice: [i64 n_entries, i64 n_deltas, i64 n_fallback, i64 certified]
+//   entries: i32 var, i32 kind, u8 feas[2], u8 force[2], f64 branch[4], i64 count[2]
+//   deltas:  i32 var[], f64 lo[], f64 up[]
+int bp_cache_pack_size(const bp_cache* c, int64_t* bytes)
+{
+  return cguard([&] {
+    need(c && bytes, "null argument");
+    const int64_t ne = (int64_t)c->c.e_var.size(), nd = (int64_t)c->c.d_var.size();
+    *bytes = 32 + ne * (4 + 4 + 2 + 2 + 32 + 16) + nd * (4 + 8 + 8);
+  });
+}
+
+int bp_cache_pack(const bp_cache* c, void* buf, int64_t bytes)
+{
+  return cguard([&] {
+    int64_t need_b = 0;
+    bp_cache_pack_size(c, &need_b);
+    need(buf && bytes >= need_b, "buffer too small");
+    char* p  = static_cast<char*>(buf);
+    auto put = [&](const void* src, size_t nb) {
+      std::memcpy(p, src, nb);
+      p += nb;
+    };
+    const auto& C     = c->c;
+    const int64_t hdr[4] = {(int64_t)C.e_var.size(), (int64_t)C.d_var.size(), C.n_fallback,
+                            C.certified ? 1 : 0};
+    put(hdr, sizeof(hdr));
+    for (size_t e = 0; e < C.e_var.size(); ++e) {
+      put(&C.e_var[e], 4);
+      put(&C.e_kind[e], 4);
+      put(&C.e_feas[2 * e], 2);
+      put(&C.e_force[2 * e], 2);
+      put(&C.e_branch[4 * e], 32);
+      const int64_t cnt[2] = {C.d_off[2 * e + 1] - C.d_off[2 * e], C.d_off[2 * e + 2] - C.d_off[2 * e + 1]};
+      put(cnt, 16);
+    }
+    if (!C.d_var.empty()) {
+      put(C.d_var.data(), 4 * C.d_var.size());
+      put(C.d_lo.data(), 8 * C.d_lo.size());
+      put(C.d_up.data(), 8 * C.d_up.size());
+    }
+  });
+}
+
+// Merges a packed slice (from any rank) into `dst`; entries of the same variable are identical
+// by determinism, later slices overwrite earlier ones.
+int bp_cache_merge_packed(bp_cache* dst, const void* buf, int64_t bytes)
+{
+  return cguard([&] {
+    need(dst && buf && bytes >= 32, "bad argument");
+    const char* p = static_cast<const char*>(buf);
+    auto get      = [&](void* d, size_t nb) {
+      std::memcpy(d, p, nb);
+      p += nb;
+    };
+    int64_t hdr[4];
+    get(hdr, sizeof(hdr));
+    const int64_t ne = hdr[0], nd = hdr[1];
+    struct E {
+      int var, kind;
+      uint8_t feas[2], force[2];
+      double br[4];
+      int64_t cnt[2];
+    };
+    std::vector<E> es(ne);
+    for (auto& e : es) {
+      get(&e.var, 4);
+      get(&e.kind, 4);
+      get(e.feas, 2);
+      get(e.force, 2);
+      get(e.br, 32);
+      get(e.cnt, 16);
+    }
+    std::vector<int> dv(nd);
+    std::vector<double> dl(nd), du(nd);
+    if (nd) {
+      get(dv.data(), 4 * nd);
+      get(dl.data(), 8 * nd);
+      get(du.data(), 8 * nd);
+    }
+    // rebuild: existing entries not overwritten + the new ones, in arrival order
+    bp::HostCache& C = dst->c;
+    bp::HostCache M;
+    M.n         = C.n;
+    M.root      = C.root;
+    M.certified = C.certified || hdr[3];
+    M.n_fallback = C.n_fallback + (int)hdr[2];
+    M.probe_ms  = C.probe_ms;
+    M.entry_of.assign(C.n, -1);
+    M.d_off.push_back(0);
+    std::vector<uint8_t> over(C.n, 0);
+    for (const auto& e : es) {
+      if (e.var < 0 || e.var >= C.n) throw std::out_of_range("packed entry var out of range");
+      over[e.var] = 1;
+    }
+    auto add = [&](int var, int kind, const uint8_t* feas, const uint8_t* force, const double* br,
+                   const int* v0, const double* l0, const double* u0, int64_t c0, const int* v1,
+                   const double* l1, const double* u1, int64_t c1) {
+      M.entry_of[var] = (int)M.e_var.size();
+      M.e_var.push_back(var);
+      M.e_kind.push_back(kind);
+      M.e_feas.insert(M.e_feas.end(), feas, feas + 2);
+      M.e_force.insert(M.e_force.end(), force, force + 2);
+      M.e_branch.insert(M.e_branch.end(), br, br + 4);
+      M.d_var.insert(M.d_var.end(), v0, v0 + c0);
+      M.d_lo.insert(M.d_lo.end(), l0, l0 + c0);
+      M.d_up.insert(M.d_up.end(), u0, u0 + c0);
+      M.d_off.push_back((long long)M.d_var.size());
+      M.d_var.insert(M.d_var.end(), v1, v1 + c1);
+      M.d_lo.insert(M.d_lo.end(), l1, l1 + c1);
+      M.d_up.insert(M.d_up.end(), u1, u1 + c1);
+      M.d_off.push_back((long long)M.d_var.size());
+    };
+    for (size_t e = 0; e < C.e_var.size(); ++e) {
+      if (over[C.e_var[e]]) continue;
+      const long long a = C.d_off[2 * e], b = C.d_off[2 * e + 1], d = C.d_off[2 * e + 2];
+      add(C.e_var[e], C.e_kind[e], &C.e_feas[2 * e], &C.e_force[2 * e], &C.e_branch[4 * e],
+          C.d_var.data() + a, C.d_lo.data() + a, C.d_up.data() + a, b - a, C.d_var.data() + b,
+          C.d_lo.data() + b, C.d_up.data() + b, d - b);
+    }
+    int64_t off = 0;
+    for (const auto& e : es) {
+      add(e.var, e.kind, e.feas, e.force, e.br, dv.data() + off, dl.data() + off, du.data() + off,
+          e.cnt[0], dv.data() + off + e.cnt[0], dl.data() + off + e.cnt[0],
+          du.data() + off + e.cnt[0], e.cnt[1]);
+      off += e.cnt[0] + e.cnt[1];
+    }
+    M.finalize_stats();
+    C = std::move(M);
+  });
+}
+
+int bp_assemble_bulk_warm_start(const bp_cache* c, const int32_t* vars, const double* vals,
+                                int32_t n, double* bounds2n, int32_t* conflicts,
+                                int32_t* n_conflicts, int32_t* evicted, int32_t* n_evicted)
+{
+  return cguard([&] {
+    need(c && bounds2n && n_conflicts && n_evicted && (n == 0 || (vars && vals)), "null argument");
+    std::vector<double> b;
+    std::vector<int> cf, ev;
+    bp::warm_start(c->c, vars, vals, n, b, cf, ev);
+    std::memcpy(bounds2n, b.data(), sizeof(double) * b.size());
+    if (conflicts) std::copy(cf.begin(), cf.end(), conflicts);
+    *n_conflicts = (int32_t)(cf.size() / 2);
+    if (evicted) std::copy(ev.begin(), ev.end(), evicted);
+    *n_evicted = (int32_t)ev.size();
+  });
+}
+
+}  // extern "C"

@@ -11,6 +11,7 @@
 
 #include "../../include/bp.h"
 #include "bp_engine.cuh"
+#include "bp_capi_internal.h"
 
 namespace {
 
@@ -129,7 +130,19 @@ void reset_ctl(bp::Problem& P, cudaStream_t s)
 struct bp_problem {
   bp::Problem impl;
   std::vector<double> cons_lower, cons_upper;
+  bp_problem_host host;
 };
+
+bp::Problem& bp_problem_impl(bp_problem* p) { return p->impl; }
+const bp_problem_host& bp_problem_hostdata(bp_problem* p) { return p->host; }
+void bp_problem_root(bp_problem* p, double* root2n)
+{
+  for (int i = 0; i < p->impl.n; ++i) {
+    root2n[2 * i]     = p->host.var_lower[i];
+    root2n[2 * i + 1] = p->host.var_upper[i];
+  }
+}
+void bp_set_last_error(const char* msg) { g_last_error = msg; }
 
 extern "C" {
 
@@ -198,6 +211,29 @@ int bp_problem_create(const bp_problem_desc* d, int32_t device, bp_problem** out
     bp::problem_build(p->impl, d->n_vars, d->n_cons, d->row_start, d->row_col, d->row_val,
                       d->col_start, d->col_row, d->col_val, d->var_lower, d->var_upper,
                       d->is_integer, d->cons_lower, d->cons_upper);
+    bp_problem_host& H = p->host;
+    H.var_lower.assign(d->var_lower, d->var_lower + d->n_vars);
+    H.var_upper.assign(d->var_upper, d->var_upper + d->n_vars);
+    H.is_integer.assign(d->is_integer, d->is_integer + d->n_vars);
+    H.cons_lower = p->cons_lower;
+    H.cons_upper = p->cons_upper;
+    H.row_col.assign(d->row_col, d->row_col + N);
+    H.row_val.assign(d->row_val, d->row_val + N);
+    // CSC on the host (the stable transpose, problem.hpp:211-225)
+    {
+      const int n = d->n_vars, m = d->n_cons;
+      const std::vector<int>& cs = p->impl.h_col_start;
+      H.col_row.resize(N);
+      H.col_val.resize(N);
+      std::vector<int> cur(cs.begin(), cs.end() - 1);
+      for (int k = 0; k < m; ++k)
+        for (int e = d->row_start[k]; e < d->row_start[k + 1]; ++e) {
+          const int dst  = cur[d->row_col[e]]++;
+          H.col_row[dst] = k;
+          H.col_val[dst] = d->row_val[e];
+        }
+      (void)n;
+    }
     *out = p.release();
   });
 }

@@ -1,0 +1,21 @@
+// Internal glue shared by the C-ABI translation units (not part of the public ABI).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/bp.h"
+#include "bp_engine.cuh"
+
+// Host copies of the problem kept for host-side steps (priority keys, rounding driver).
+struct bp_problem_host {
+  std::vector<int> col_row;
+  std::vector<double> col_val, var_lower, var_upper, cons_lower, cons_upper;
+  std::vector<uint8_t> is_integer;
+  std::vector<int> row_col;
+  std::vector<double> row_val;
+};
+
+bp::Problem& bp_problem_impl(bp_problem* p);
+const bp_problem_host& bp_problem_hostdata(bp_problem* p);
+void bp_problem_root(bp_problem* p, double* root2n);
+void bp_set_last_error(const char* msg);
