@@ -151,6 +151,39 @@ int bp_assemble_bulk_warm_start(const bp_cache* c, const int32_t* vars, const do
                                 int32_t n, double* bounds2n, int32_t* conflicts,
                                 int32_t* n_conflicts, int32_t* evicted, int32_t* n_evicted);
 
+/* ---------------------------------------------------------------- fix-and-propagate
+ * pulse::RoundingConfig (rounding.hpp:18-31); the lp_polish fields are out of scope. */
+typedef struct {
+  double random_band;         /* 0.25 */
+  int32_t single_var_tail;    /* 36 */
+  int32_t repair_enabled;     /* 0 (repair is not implemented: non-zero is rejected) */
+  int32_t repair_attempt_cap; /* 16 */
+  int32_t repair_shift_cap;   /* 64 */
+} bp_rounding_config;
+
+/* pulse::RoundingOutcome (rounding.hpp:347-355) minus the polished point; bounds_feasible = the
+ * reference's lp_polish condition (completed && !rounding_infeasible && !ws.infeasible()). */
+typedef struct {
+  int32_t rounding_infeasible;
+  int32_t timed_out;
+  int32_t completed;
+  int32_t repair_attempts;
+  int32_t bulks_committed;
+  int32_t set_count;
+  int32_t bounds_feasible;
+  int32_t bp_calls;   /* engine propagate launches */
+  double device_ms;   /* device time of engine launches */
+} bp_rounding_outcome;
+
+void bp_rounding_config_default(bp_rounding_config* cfg);
+
+/* pulse::propagation_round (rounding.hpp:393-558) with Rng(seed); deadline_sec <= 0 = never.
+ * out_values (n_vars) receives the point before lp_polish: integer vars from the fixed bounds
+ * (else nearest rounding), continuous vars clamped into their original bounds. cache may be NULL. */
+int bp_propagation_round(bp_problem* p, const double* start_values, const bp_cache* cache,
+                         uint64_t seed, double deadline_sec, const bp_rounding_config* cfg,
+                         double* out_values, bp_rounding_outcome* out);
+
 /* Number of engine kernels launched by this process. */
 int64_t bp_kernel_launches(void);
 

@@ -297,3 +297,55 @@ class PortProblem:
             out.append((bool(feas[s]), dv[o:o + nd[s]].copy(), dl[o:o + nd[s]].copy(),
                         du[o:o + nd[s]].copy()))
         return kind, out
+
+
+# ------------------------------------------------------------------ reference rounding / cache
+
+
+class RefCache:
+    """A pulse::ProbingCache inside the reference library."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            Ref.lib().ref_cache_free(self.h)
+        except Exception:
+            pass
+
+    @classmethod
+    def build(cls, rp, budget=1e9):
+        return cls(Ref.lib().ref_build_cache(rp.h, budget))
+
+    @classmethod
+    def from_gpu(cls, rp, gpu_cache):
+        """Installs every entry of an engine-built cache into a reference ProbingCache."""
+        L = Ref.lib()
+        c = cls(L.ref_cache_new_empty(rp.h))
+        for v in range(gpu_cache.n_vars):
+            raw = gpu_cache._entry_raw(v)
+            if raw is None:
+                continue
+            hdr, br = raw
+            d0 = gpu_cache.deltas(v, 0)
+            d1 = gpu_cache.deltas(v, 1)
+            dv = np.ascontiguousarray(np.concatenate([d0[0], d1[0]]), dtype=np.int32)
+            dl = np.ascontiguousarray(np.concatenate([d0[1], d1[1]]))
+            du = np.ascontiguousarray(np.concatenate([d0[2], d1[2]]))
+            L.ref_cache_set_entry(c.h, v, _p(np.ascontiguousarray(hdr, dtype=np.int32)),
+                                  _p(np.ascontiguousarray(br)), _p(dv), _p(dl), _p(du))
+        return c
+
+
+def ref_propagation_round(rp, n_vars, start, cache=None, seed=0, deadline=0.0, band=0.25,
+                          repair=False):
+    """rounding.hpp:393 with Rng(seed); returns (values, flags dict). lp_polish runs inside."""
+    vals = np.zeros(max(n_vars, 1))
+    fl = np.zeros(6, np.int32)
+    Ref.lib().ref_propagation_round(rp.h, _p(np.ascontiguousarray(start, dtype=np.float64)),
+                                    None if cache is None else cache.h, seed, deadline, band,
+                                    int(repair), _p(vals), _p(fl))
+    keys = ["rounding_infeasible", "timed_out", "completed", "repair_attempts", "bulks_committed",
+            "set_count"]
+    return vals[:n_vars], dict(zip(keys, (int(x) for x in fl)))

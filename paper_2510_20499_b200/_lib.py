@@ -43,6 +43,20 @@ class bp_limits(C.Structure):
                 ("incremental", C.c_int32)]
 
 
+class bp_rounding_config(C.Structure):
+    _fields_ = [("random_band", C.c_double), ("single_var_tail", C.c_int32),
+                ("repair_enabled", C.c_int32), ("repair_attempt_cap", C.c_int32),
+                ("repair_shift_cap", C.c_int32)]
+
+
+class bp_rounding_outcome(C.Structure):
+    _fields_ = [("rounding_infeasible", C.c_int32), ("timed_out", C.c_int32),
+                ("completed", C.c_int32), ("repair_attempts", C.c_int32),
+                ("bulks_committed", C.c_int32), ("set_count", C.c_int32),
+                ("bounds_feasible", C.c_int32), ("bp_calls", C.c_int32),
+                ("device_ms", C.c_double)]
+
+
 class bp_result(C.Structure):
     _fields_ = [("status", C.c_int32), ("rounds", C.c_int32), ("crossed_vars", C.c_int32)]
 
@@ -91,6 +105,10 @@ _SIGS = [
     ("bp_assemble_bulk_warm_start", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                               C.c_void_p, C.c_void_p, C.POINTER(C.c_int32),
                                               C.c_void_p, C.POINTER(C.c_int32)]),
+    ("bp_rounding_config_default", None, [C.POINTER(bp_rounding_config)]),
+    ("bp_propagation_round", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double,
+                                       C.POINTER(bp_rounding_config), C.c_void_p,
+                                       C.POINTER(bp_rounding_outcome)]),
     ("bp_kernel_launches", C.c_int64, []),
     ("bp_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                  C.POINTER(C.c_int64)]),

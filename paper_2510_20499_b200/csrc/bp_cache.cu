@@ -460,13 +460,116 @@ void warm_start(const HostCache& C, const int* vars, const double* vals, int na,
   }
 }
 
+// Sparse form of the same merge: only the variables whose merged bounds differ from the root are
+// returned (O(bulk deltas) instead of an O(n) copy of the root per call).
+void warm_start_sparse(const HostCache& C, const int* vars, const double* vals, int na,
+                       std::vector<int>& dv, std::vector<double>& dl, std::vector<double>& du,
+                       std::vector<int>& conflicts, std::vector<int>& evicted)
+{
+  thread_local std::vector<double> cur;
+  thread_local std::vector<int> writer;
+  thread_local std::vector<uint8_t> has, ev;
+  thread_local std::vector<int> touched;
+  if ((int)has.size() != C.n) {
+    cur.assign(2 * (size_t)C.n, 0.0);
+    writer.assign(C.n, -1);
+    has.assign(C.n, 0);
+    ev.assign(C.n, 0);
+  }
+  touched.clear();
+  dv.clear();
+  dl.clear();
+  du.clear();
+  conflicts.clear();
+  evicted.clear();
+  auto touch = [&](int v) {
+    if (!has[v]) {
+      has[v]         = 1;
+      cur[2 * v]     = C.root[2 * v];
+      cur[2 * v + 1] = C.root[2 * v + 1];
+      touched.push_back(v);
+    }
+  };
+  struct Undo {
+    int var;
+    double lo, up;
+    int writer;
+  };
+  std::vector<Undo> undo;
+  for (int j = 0; j < na; ++j) {
+    const int v = vars[j];
+    const int e = (v >= 0 && v < C.n) ? C.entry_of[v] : -1;
+    if (e < 0) continue;
+    const int side = (vals[j] <= C.e_branch[4 * e + 1]) ? 0 : 1;
+    if (!C.e_feas[2 * e + side]) {
+      conflicts.push_back(v);
+      conflicts.push_back(v);
+      touch(v);
+      if (!ev[v]) {
+        ev[v] = 1;
+        evicted.push_back(v);
+      }
+      continue;
+    }
+    undo.clear();
+    bool conflict   = false;
+    int conflicting = -1;
+    for (long long d = C.d_off[2 * e + side]; d < C.d_off[2 * e + side + 1]; ++d) {
+      const int x = C.d_var[d];
+      touch(x);
+      const double cl = cur[2 * x], cu = cur[2 * x + 1];
+      const double nl = (cl < C.d_lo[d]) ? C.d_lo[d] : cl;
+      const double nu = (C.d_up[d] < cu) ? C.d_up[d] : cu;
+      if (nl > nu + 1e-9) {
+        conflict    = true;
+        conflicting = writer[x] >= 0 ? writer[x] : v;
+        break;
+      }
+      if (nl != cl || nu != cu) {
+        undo.push_back({x, cl, cu, writer[x]});
+        cur[2 * x]     = nl;
+        cur[2 * x + 1] = nu;
+        writer[x]      = v;
+      }
+    }
+    if (conflict) {
+      for (auto it = undo.rbegin(); it != undo.rend(); ++it) {
+        cur[2 * it->var]     = it->lo;
+        cur[2 * it->var + 1] = it->up;
+        writer[it->var]      = it->writer;
+      }
+      conflicts.push_back(conflicting);
+      conflicts.push_back(v);
+      touch(v);
+      if (!ev[v]) {
+        ev[v] = 1;
+        evicted.push_back(v);
+      }
+    }
+  }
+  for (int x : touched) {
+    if (cur[2 * x] != C.root[2 * x] || cur[2 * x + 1] != C.root[2 * x + 1]) {
+      dv.push_back(x);
+      dl.push_back(cur[2 * x]);
+      du.push_back(cur[2 * x + 1]);
+    }
+    has[x]    = 0;
+    writer[x] = -1;
+    ev[x]     = 0;
+  }
+}
+
 }  // namespace bp
+
+const bp::HostCache* bp_cache_host(const bp_cache* c);
 
 // ------------------------------------------------------------------ C-ABI
 
 struct bp_cache {
   bp::HostCache c;
 };
+
+const bp::HostCache* bp_cache_host(const bp_cache* c) { return &c->c; }
 
 namespace {
 

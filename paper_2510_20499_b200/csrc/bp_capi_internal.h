@@ -19,3 +19,11 @@ bp::Problem& bp_problem_impl(bp_problem* p);
 const bp_problem_host& bp_problem_hostdata(bp_problem* p);
 void bp_problem_root(bp_problem* p, double* root2n);
 void bp_set_last_error(const char* msg);
+
+namespace bp {
+struct HostCache;
+void warm_start_sparse(const HostCache& C, const int* vars, const double* vals, int na,
+                       std::vector<int>& dv, std::vector<double>& dl, std::vector<double>& du,
+                       std::vector<int>& conflicts, std::vector<int>& evicted);
+}  // namespace bp
+const bp::HostCache* bp_cache_host(const bp_cache* c);

@@ -67,7 +67,8 @@ struct ParCtl {
 struct Ctl {
   ParCtl par[2];
   int status, rounds, crossed, any_change;
-  int pad[12];
+  int fixpoint;  // 1 if the loop ended at a fixpoint (no change / no dirty row): certifies the bounds
+  int pad[11];
 };
 
 // Mutable per-problem workspace (one propagate at a time per problem; calls serialized).
@@ -153,13 +154,15 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
                    const uint8_t* is_integer, const double* cons_lower, const double* cons_upper);
 
 struct RunResult {
-  int status, rounds, crossed;
+  int status, rounds, crossed, fixpoint;
 };
 
 // flags: ENGINE_FORCE_FRONTIER never substitutes a full round for a large frontier (the exact
 // reference trajectory of dirty sets, used to count its work); stats (device, kStatCols per round)
 // receives per-round work counts when non-null.
-enum { ENGINE_FORCE_FRONTIER = 1 };
+// ENGINE_START_FRONTIER: the bounds are a certified fixpoint except for the variables staged in
+// par[0]'s changed list (stage_changed); round 1 starts from their frontier.
+enum { ENGINE_FORCE_FRONTIER = 1, ENGINE_START_FRONTIER = 2 };
 // full, |R|, row nnz visits, |V|, col nnz visits, |changed|, then phase-end times (ns since
 // kernel start): activity, tightening, row expansion, var expansion, gather; one spare
 constexpr int kStatCols = 12;
@@ -169,6 +172,8 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
 // Stage caller row/var lists into the parity-1 frontier buffers (host-classified).
 void stage_rows(Problem& P, const int* rows, int nrows, cudaStream_t s);
 void stage_vars(Problem& P, const int* vars, int nvars, cudaStream_t s);
+// Stage the changed-variable list of a frontier start (ENGINE_START_FRONTIER).
+void stage_changed(Problem& P, const int* vars, int nvars, cudaStream_t s);
 
 extern long long g_kernel_launches;
 

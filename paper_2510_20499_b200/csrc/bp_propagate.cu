@@ -1143,8 +1143,27 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   const bool lead             = blockIdx.x == 0 && threadIdx.x == 0;
   bool full                   = true;  // round 1 is always a full sweep (propagation.hpp:442)
   bool any_change             = false;
+  bool fixpoint               = false;
   int status = BP_STATUS_UNSET, crossed_out = 0;
   int rounds = 0;
+  if (full_first == 2) {
+    // frontier start from a certified fixpoint: rows(changed) / vars(rows) of the staged list
+    ParCtl* p0 = &S.ctl->par[0];
+    ParCtl* p1 = &S.ctl->par[1];
+    phase_expand_rows(c, p0, p1, 1, stamp_base);
+    grid.sync();
+    phase_expand_vars(c, p0, p1, 1, stamp_base);
+    grid.sync();
+    full = dense_thr != ~0ull && ldv(&p1->roww) + ldv(&p1->colw) > 2 * dense_thr;
+    if (ldv(&p1->n_drow_all) == 0) {  // nothing to revisit: the fixpoint stands
+      full     = false;
+      rounds   = lim.max_rounds;  // skip the loop; result = Unchanged after one round below
+      fixpoint = true;
+    }
+  }
+  if (rounds == lim.max_rounds && fixpoint) {
+    rounds = 1;  // the reference's first (full) round finds no change
+  } else {
   while (rounds < lim.max_rounds) {
     ++rounds;
     const int ppar       = rounds & 1, qpar = ppar ^ 1;
@@ -1185,9 +1204,15 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
       crossed_out = cr;
       break;
     }
-    if (nc == 0) break;
+    if (nc == 0) {
+      fixpoint = true;
+      break;
+    }
     any_change = true;
-    if (!ldv(&pc->any_rows)) break;  // dirty_rows.empty() (propagation.hpp:481)
+    if (!ldv(&pc->any_rows)) {  // dirty_rows.empty() (propagation.hpp:481)
+      fixpoint = true;
+      break;
+    }
     if (rounds >= lim.max_rounds) break;
     if (ldv(&pc->stop)) break;       // time limit (propagation.hpp:439)
     if (!lim.incremental || ldv(&pc->colnnz) > dense_thr) {
@@ -1208,12 +1233,14 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     // gathers but with far better memory-level parallelism
     full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 2 * dense_thr;
   }
+  }
   if (lead) {
     if (status == BP_STATUS_UNSET) status = any_change ? BP_STATUS_TIGHTENED : BP_STATUS_UNCHANGED;
     S.ctl->status     = status;
     S.ctl->rounds     = rounds;
     S.ctl->crossed    = crossed_out;
     S.ctl->any_change = any_change ? 1 : 0;
+    S.ctl->fixpoint   = fixpoint ? 1 : 0;
   }
 }
 
@@ -1533,7 +1560,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   DevState st  = P.st;
   Limits l     = lim;
   int md       = (int)mode;
-  int ff       = full ? 1 : 0;
+  int ff       = (mode == MODE_PROPAGATE && (flags & ENGINE_START_FRONTIER)) ? 2 : (full ? 1 : 0);
   // stamps: one value per round, never reused until wrap-around (then the stamp arrays reset)
   if (P.stamp_base > 0xF0000000u - (unsigned)std::max(lim.max_rounds, 1) - 2) {
     BP_CUDA(cudaMemsetAsync(P.row_stamp.p, 0, sizeof(unsigned) * P.row_stamp.n, s));
@@ -1551,14 +1578,15 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
   BP_CUDA(cudaEventRecord(P.ev1, s));
   ++g_kernel_launches;
-  RunResult r{0, 0, 0};
+  RunResult r{0, 0, 0, 0};
   if (mode == MODE_PROPAGATE) {
-    int h[4];
+    int h[5];
     BP_CUDA(cudaMemcpyAsync(h, &P.st.ctl->status, sizeof(h), cudaMemcpyDeviceToHost, s));
     BP_CUDA(cudaStreamSynchronize(s));
-    r.status  = h[0];
-    r.rounds  = h[1];
-    r.crossed = h[2];
+    r.status   = h[0];
+    r.rounds   = h[1];
+    r.crossed  = h[2];
+    r.fixpoint = h[4];
   } else {
     BP_CUDA(cudaStreamSynchronize(s));
   }
@@ -1621,6 +1649,26 @@ void stage_vars(Problem& P, const int* vars, int nvars, cudaStream_t s)
     BP_CUDA(cudaMemcpyAsync(S.dvar_m[1], mv.data(), mv.size() * 4, cudaMemcpyHostToDevice, s));
   int cnt[2] = {(int)sv.size(), (int)mv.size()};
   BP_CUDA(cudaMemcpyAsync(&S.ctl->par[1].n_dvar_s, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
+  BP_CUDA(cudaStreamSynchronize(s));
+}
+
+void stage_changed(Problem& P, const int* vars, int nvars, cudaStream_t s)
+{
+  std::vector<int2> ct;
+  for (int j = 0; j < nvars; ++j) {
+    const int i = vars[j];
+    const int L = P.h_col_start[i + 1] - P.h_col_start[i];
+    if (L > kTile)
+      for (int q = 0; q * kTile < L; ++q) ct.push_back(make_int2(i, q));
+  }
+  DevState& S = P.st;
+  if (nvars)
+    BP_CUDA(cudaMemcpyAsync(S.changed, vars, sizeof(int) * nvars, cudaMemcpyHostToDevice, s));
+  if (!ct.empty())
+    BP_CUDA(cudaMemcpyAsync(S.ctask, ct.data(), ct.size() * 8, cudaMemcpyHostToDevice, s));
+  const int nc = nvars, nt = (int)ct.size();
+  BP_CUDA(cudaMemcpyAsync(&S.ctl->par[0].n_changed, &nc, sizeof(int), cudaMemcpyHostToDevice, s));
+  BP_CUDA(cudaMemcpyAsync(&S.ctl->par[0].n_ctask, &nt, sizeof(int), cudaMemcpyHostToDevice, s));
   BP_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -1,0 +1,700 @@
+// Fix-and-propagate bulk rounding (rounding.hpp:393-558) with device-resident working bounds.
+//
+// The control flow is the reference's, step for step, on the host (same RNG stream:
+// std::mt19937_64 + std::uniform_real_distribution from the same libstdc++, rounding.hpp:127-152;
+// the same stable sorts; the same probe-0 preference, forcing, recovery and terminal phases).
+// Everything O(n) or O(N) per bulk runs on the GPU:
+//   - the working bounds `ws` never leave the device;
+//   - compute_activities + implied_slack_sort keys (rounding.hpp:71-115) + a stable radix sort of
+//     the unset list (CUB) and its stable compaction (drop_fixed);
+//   - both candidate probes (run_probe, rounding.hpp:167-207): warm start merged on the host from
+//     the packed cache (sparse), met with `ws` on the device, fixings scattered, then the engine's
+//     propagate. When `ws` is a certified fixpoint (its last propagate ended at a fixpoint) the
+//     first round starts from the frontier of the changed variables, which turns
+//     the reference's O(N) first round into O(frontier);
+//   - count_envelope_violations (rounding.hpp:361-383).
+// lp_polish (PDHG, rounding.hpp:315-345) is out of scope: the outcome reports `bounds_feasible`
+// (the condition under which the reference would polish) and returns the pre-polish point.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/bp.h"
+#include "bp_capi_internal.h"
+#include "bp_engine.cuh"
+#include "bp_probe.cuh"
+
+namespace bp {
+
+namespace {
+
+constexpr double kFeasTol = 1e-6;  // common.hpp:20
+
+__global__ void k_meet_root(double2* b, const double2* root, int n, int* flags)
+{
+  int fl = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2 x = b[i], r = root[i];
+    const double lo = (x.x < r.x) ? r.x : x.x;  // std::max(b, other)
+    const double up = (r.y < x.y) ? r.y : x.y;  // std::min(b, other)
+    if (lo != x.x || up != x.y) {
+      fl |= 1;
+      b[i] = make_double2(lo, up);
+    }
+    if (lo > up) fl |= 2;
+  }
+  if (fl) atomicOr(flags, fl);
+}
+
+// Meet of listed vars with the given bounds; new values + per-var "changed" written back.
+__global__ void k_meet_list(double2* b, const int* var, const double* lo, const double* up, int k,
+                            int* changed, int* flags)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    const int i    = var[j];
+    const double2 x = b[i];
+    const double nl = (x.x < lo[j]) ? lo[j] : x.x;
+    const double nu = (up[j] < x.y) ? up[j] : x.y;
+    changed[j]      = (nl != x.x || nu != x.y) ? 1 : 0;
+    b[i]            = make_double2(nl, nu);
+    if (nl > nu) atomicOr(flags, 2);
+  }
+}
+
+__global__ void k_gather(const double2* b, const int* var, int k, double2* out)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+    out[j] = b[var[j]];
+}
+
+__global__ void k_scatter(double2* b, const int* var, const double2* val, int k)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+    b[var[j]] = val[j];
+}
+
+// rounding.hpp:71-115 keys: S_i = sum over rows of (a / slack)^2 in CSC order, +inf on a
+// non-positive slack; returned as order-preserving 64-bit keys (S >= +0.0, never -0.0).
+__global__ void k_slack_keys(DevProblem P, const RowRec* rec, const double2* aux, const int* vars,
+                             int k, unsigned long long* keys, int* pos)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    const int i  = vars[j];
+    double total = 0.0;
+    for (int e = P.col_start[i]; e < P.col_start[i + 1]; ++e) {
+      const int r    = P.col_row[e];
+      const double a = P.col_val[e];
+      const RowRec q = rec[r];
+      double mnf, mxf;
+      int nmn, nmx;
+      decode_rec(q, aux, r, mnf, nmn, mxf, nmx);
+      if (isfinite(q.g) && nmn == 0) {
+        const double slack = __dsub_rn(q.g, mnf);
+        if (slack <= 0.0) {
+          total = INFINITY;
+          break;
+        }
+        const double s = __ddiv_rn(a, slack);
+        total          = __dadd_rn(total, __dmul_rn(s, s));
+      }
+      if (isfinite(q.h) && nmx == 0) {
+        const double slack = __dsub_rn(mxf, q.h);
+        if (slack <= 0.0) {
+          total = INFINITY;
+          break;
+        }
+        const double s = __ddiv_rn(a, slack);
+        total          = __dadd_rn(total, __dmul_rn(s, s));
+      }
+    }
+    keys[j] = okey(total);
+    pos[j]  = j;
+  }
+}
+
+__global__ void k_permute(const int* src, const int* pos, int k, int* dst)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+    dst[j] = src[pos[j]];
+}
+
+// rounding.hpp:372-381: rows violated by the fixed-value envelope.
+__global__ void k_count_violations(DevProblem P, const RowRec* rec, const double2* aux, int* out)
+{
+  int cnt = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < P.m; k += gridDim.x * blockDim.x) {
+    const RowRec q = rec[k];
+    double mnf, mxf;
+    int nmn, nmx;
+    decode_rec(q, aux, k, mnf, nmn, mxf, nmx);
+    if (isfinite(q.g) && nmn == 0 && mnf > __dadd_rn(q.g, kFeasTol)) ++cnt;
+    else if (isfinite(q.h) && nmx == 0 && mxf < __dsub_rn(q.h, kFeasTol)) ++cnt;
+  }
+  if (cnt) atomicAdd(out, cnt);
+}
+
+struct NotFixed {
+  const double2* ws;
+  __device__ __forceinline__ bool operator()(const int& v) const { return ws[v].x != ws[v].y; }
+};
+
+inline int blocks_for(long long n) { return (int)std::max(1ll, std::min(4096ll, (n + 255) / 256)); }
+
+double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+}  // namespace
+
+// Persistent per-call device context of the rounding driver.
+struct RoundCtx {
+  Problem& P;
+  const bp_problem_host& H;
+  cudaStream_t s;
+  DBuf<double2> ws, root, tmp2;
+  DBuf<RowRec> ws_rec;   // activity records consistent with ws while ws_cert holds
+  DBuf<double2> ws_aux;
+  DBuf<int> unset, unset_alt, pos_in, pos_out, sel_count, flags, ivar, ichg;
+  DBuf<unsigned long long> keys_in, keys_out;
+  DBuf<double> dlo, dup;
+  DBuf<unsigned char> cub_tmp;
+  int n_unset = 0;
+  bool ws_infeasible = false;
+  bool ws_cert       = false;
+  long long bp_calls = 0;
+  double dev_ms      = 0.0;
+
+  RoundCtx(Problem& P_, const bp_problem_host& H_) : P(P_), H(H_), s(P_.stream) {}
+
+  Limits limits() const
+  {
+    Limits l;
+    l.max_rounds    = 64;
+    l.time_limit    = INFINITY;
+    l.abs_threshold = 1e-7;
+    l.rel_threshold = 1e-4;
+    l.incremental   = 1;
+    return l;
+  }
+
+  void sync() { BP_CUDA(cudaStreamSynchronize(s)); }
+
+  // Stream-ordered upload (the engine stream is non-blocking: a plain cudaMemcpy would race with
+  // kernels still reading the buffer).
+  template <class T>
+  void put(DBuf<T>& b, const std::vector<T>& v)
+  {
+    if (b.n < v.size()) b.alloc(std::max(v.size(), 2 * b.n));
+    if (!v.empty())
+      BP_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
+  }
+  template <class T>
+  void reserve(DBuf<T>& b, size_t k)
+  {
+    if (b.n < k) b.alloc(std::max(k, 2 * b.n));
+  }
+
+  std::vector<double2> gather(const DBuf<double2>& b, const std::vector<int>& vars)
+  {
+    std::vector<double2> out(vars.size());
+    if (vars.empty()) return out;
+    put(ivar, vars);
+    reserve(tmp2, vars.size());
+    k_gather<<<blocks_for(vars.size()), 256, 0, s>>>(b.p, ivar.p, (int)vars.size(), tmp2.p);
+    BP_CUDA(cudaMemcpyAsync(out.data(), tmp2.p, sizeof(double2) * vars.size(), cudaMemcpyDeviceToHost, s));
+    sync();
+    return out;
+  }
+
+  void scatter(double2* b, const std::vector<int>& vars, const std::vector<double2>& vals)
+  {
+    if (vars.empty()) return;
+    put(ivar, vars);
+    put(tmp2, vals);
+    k_scatter<<<blocks_for(vars.size()), 256, 0, s>>>(b, ivar.p, tmp2.p, (int)vars.size());
+  }
+
+  // After a propagate that ended at a fixpoint, P.st.rec / aux describe its final bounds for
+  // every row; keep them as the certified state's activities.
+  void snapshot_ws_activities()
+  {
+    reserve(ws_rec, (size_t)std::max(P.m, 1));
+    reserve(ws_aux, (size_t)std::max(P.m, 1));
+    if (P.m) {
+      BP_CUDA(cudaMemcpyAsync(ws_rec.p, P.st.rec, sizeof(RowRec) * P.m, cudaMemcpyDeviceToDevice, s));
+      BP_CUDA(cudaMemcpyAsync(ws_aux.p, P.st.aux, sizeof(double2) * P.m, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+
+  RunResult propagate_engine(bool start_frontier, const std::vector<int>& changed)
+  {
+    BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+    int flags = 0;
+    if (start_frontier) {
+      // a frontier round reads the activities of rows it does not recompute: they must be the
+      // certified state's, whatever the previous engine call left behind
+      if (P.m) {
+        BP_CUDA(cudaMemcpyAsync(P.st.rec, ws_rec.p, sizeof(RowRec) * P.m, cudaMemcpyDeviceToDevice, s));
+        BP_CUDA(cudaMemcpyAsync(P.st.aux, ws_aux.p, sizeof(double2) * P.m, cudaMemcpyDeviceToDevice, s));
+      }
+      stage_changed(P, changed.data(), (int)changed.size(), s);
+      flags = ENGINE_START_FRONTIER;
+    }
+    const RunResult r = run_engine(P, MODE_PROPAGATE, true, limits(), s, flags);
+    bp_calls++;
+    dev_ms += P.last_kernel_ms;
+    return r;
+  }
+
+  // compute_activities(p, b, nullptr, acts) of bounds `b` (device) into P.st.rec / aux.
+  void activities(const double2* b)
+  {
+    BP_CUDA(cudaMemcpyAsync(P.st.bounds, b, sizeof(double2) * P.n, cudaMemcpyDeviceToDevice, s));
+    BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+    run_engine(P, MODE_ACTIVITY, true, limits(), s);
+    dev_ms += P.last_kernel_ms;
+  }
+
+  // implied_slack_sort of the unset list, in place (stable).
+  void slack_sort()
+  {
+    activities(ws.p);
+    const int k = n_unset;
+    k_slack_keys<<<blocks_for(k), 256, 0, s>>>(P.dev(), P.st.rec, P.st.aux, unset.p, k, keys_in.p,
+                                               pos_in.p);
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, keys_in.p, keys_out.p, pos_in.p, pos_out.p, k, 0,
+                                    64, s);
+    if (need > cub_tmp.n) cub_tmp.alloc(need);
+    size_t have = cub_tmp.n;
+    cub::DeviceRadixSort::SortPairs(cub_tmp.p, have, keys_in.p, keys_out.p, pos_in.p, pos_out.p, k,
+                                    0, 64, s);
+    k_permute<<<blocks_for(k), 256, 0, s>>>(unset.p, pos_out.p, k, unset_alt.p);
+    std::swap(unset.p, unset_alt.p);
+    std::swap(unset.n, unset_alt.n);
+  }
+
+  // unset.erase(remove_if(ws.fixed(v))) (stable).
+  void drop_fixed()
+  {
+    size_t need = 0;
+    NotFixed pred{ws.p};
+    cub::DeviceSelect::If(nullptr, need, unset.p, unset_alt.p, sel_count.p, n_unset, pred, s);
+    if (need > cub_tmp.n) cub_tmp.alloc(need);
+    size_t have = cub_tmp.n;
+    cub::DeviceSelect::If(cub_tmp.p, have, unset.p, unset_alt.p, sel_count.p, n_unset, pred, s);
+    std::swap(unset.p, unset_alt.p);
+    std::swap(unset.n, unset_alt.n);
+    BP_CUDA(cudaMemcpyAsync(&n_unset, sel_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sync();
+  }
+
+  std::vector<int> take_first(int k)
+  {
+    std::vector<int> t(k);
+    if (k) BP_CUDA(cudaMemcpyAsync(t.data(), unset.p, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
+    sync();
+    return t;
+  }
+
+  struct Probe {
+    int infeas_count = 0;
+    bool infeasible  = false;
+    bool cert        = false;
+    std::vector<int> evicted;
+    std::vector<std::pair<int, double>> fixed;
+  };
+
+  // rounding.hpp:167-207 with the result bounds left in P.st.bounds.
+  Probe run_probe(const std::vector<int>& vars, const std::vector<double>& values,
+                  const HostCache* cache)
+  {
+    Probe out;
+    BP_CUDA(cudaMemcpyAsync(P.st.bounds, ws.p, sizeof(double2) * P.n, cudaMemcpyDeviceToDevice, s));
+    bool inf          = ws_infeasible;
+    bool root_changed = false;
+    std::vector<int> changed;
+    std::vector<uint8_t> evm;
+    if (cache) {
+      // warm start on the host (sparse deltas over the cache root), meet on the device
+      std::vector<int> conflicts, dv;
+      std::vector<double> dl, du;
+      bp::warm_start_sparse(*cache, vars.data(), values.data(), (int)vars.size(), dv, dl, du,
+                            conflicts, out.evicted);
+      reserve(flags, 1);
+      BP_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), s));
+      k_meet_root<<<blocks_for(P.n), 256, 0, s>>>(P.st.bounds, root.p, P.n, flags.p);
+      if (!dv.empty()) {
+        put(ivar, dv);
+        put(dlo, dl);
+        put(dup, du);
+        reserve(ichg, dv.size());
+        k_meet_list<<<blocks_for(dv.size()), 256, 0, s>>>(P.st.bounds, ivar.p, dlo.p, dup.p,
+                                                          (int)dv.size(), ichg.p, flags.p);
+      }
+      int fl = 0;
+      BP_CUDA(cudaMemcpyAsync(&fl, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      std::vector<int> ch(dv.size());
+      if (!dv.empty())
+        BP_CUDA(cudaMemcpyAsync(ch.data(), ichg.p, sizeof(int) * dv.size(), cudaMemcpyDeviceToHost, s));
+      sync();
+      root_changed = (fl & 1) != 0;
+      if (fl & 2) inf = true;
+      for (size_t j = 0; j < dv.size(); ++j)
+        if (ch[j]) changed.push_back(dv[j]);
+    }
+    evm.assign(P.n, 0);
+    for (int v : out.evicted) evm[v] = 1;
+    // fixings (rounding.hpp:186-195) on the post-meet bounds of the bulk vars
+    const std::vector<double2> cur = [&] {
+      std::vector<double2> o(vars.size());
+      if (!vars.empty()) {
+        put(ivar, vars);
+        reserve(tmp2, vars.size());
+        k_gather<<<blocks_for(vars.size()), 256, 0, s>>>(P.st.bounds, ivar.p, (int)vars.size(), tmp2.p);
+        BP_CUDA(cudaMemcpyAsync(o.data(), tmp2.p, sizeof(double2) * vars.size(), cudaMemcpyDeviceToHost, s));
+        sync();
+      }
+      return o;
+    }();
+    int crossings = inf ? 1 : 0;
+    std::vector<int> fv;
+    std::vector<double2> fb;
+    std::vector<double2> now = cur;  // repeated vars: later assignments see earlier fixings
+    for (size_t j = 0; j < vars.size(); ++j) {
+      const int v = vars[j];
+      if (evm[v]) continue;
+      double2 b = now[j];
+      for (size_t q = 0; q < j; ++q)
+        if (vars[q] == v) b = now[q];
+      const double val = values[j];
+      if (val < b.x - 1e-9 || val > b.y + 1e-9) {
+        ++crossings;
+        continue;
+      }
+      if (b.x != val || b.y != val) changed.push_back(v);
+      now[j] = make_double2(val, val);
+      for (size_t q = 0; q < j; ++q)
+        if (vars[q] == v) now[q] = now[j];
+      fv.push_back(v);
+      fb.push_back(now[j]);
+      out.fixed.push_back({v, val});
+    }
+    if (crossings > 0) {
+      out.infeasible   = true;
+      out.infeas_count = crossings;
+      return out;
+    }
+    scatter(P.st.bounds, fv, fb);
+    std::sort(changed.begin(), changed.end());
+    changed.erase(std::unique(changed.begin(), changed.end()), changed.end());
+    const bool frontier = ws_cert && !root_changed;
+    const RunResult r   = propagate_engine(frontier, changed);
+    if (r.status == BP_STATUS_INFEASIBLE) {
+      out.infeasible   = true;
+      out.infeas_count = std::max(1, r.crossed);
+    }
+    out.cert = r.fixpoint != 0;
+    return out;
+  }
+
+  // rounding.hpp:361-383
+  int count_envelope_violations(const std::vector<int>& vars, const std::vector<double>& values)
+  {
+    BP_CUDA(cudaMemcpyAsync(P.st.bounds, ws.p, sizeof(double2) * P.n, cudaMemcpyDeviceToDevice, s));
+    std::vector<double2> vals(vars.size());
+    for (size_t j = 0; j < vars.size(); ++j) {
+      const int v     = vars[j];
+      const double lo = std::max(H.var_lower[v], std::min(values[j], H.var_upper[v]));
+      vals[j]         = make_double2(lo, lo);
+    }
+    // repeated vars: the last fixing wins, as in the sequential loop
+    scatter(P.st.bounds, vars, vals);
+    BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+    run_engine(P, MODE_ACTIVITY, true, limits(), s);
+    dev_ms += P.last_kernel_ms;
+    reserve(flags, 1);
+    BP_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), s));
+    k_count_violations<<<blocks_for(P.m), 256, 0, s>>>(P.dev(), P.st.rec, P.st.aux, flags.p);
+    int h = 0;
+    BP_CUDA(cudaMemcpyAsync(&h, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sync();
+    return h;
+  }
+};
+
+// rounding.hpp:35-65
+std::vector<int> initial_sort(const bp_problem_host& H, const double* values, int n)
+{
+  struct Item {
+    int var, cls;
+    double frac;
+  };
+  std::vector<Item> items;
+  for (int i = 0; i < n; ++i) {
+    if (!H.is_integer[i]) continue;
+    const double w = H.var_upper[i] - H.var_lower[i];
+    const int cls  = (w == 1.0) ? 0 : (w == 2.0 ? 1 : 2);
+    const double v = values[i];
+    items.push_back({i, cls, std::abs(v - std::round(v))});
+  }
+  std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
+    if (a.cls != b.cls) return a.cls < b.cls;
+    return a.frac < b.frac;
+  });
+  std::vector<int> o;
+  for (const auto& it : items) o.push_back(it.var);
+  return o;
+}
+
+// rounding.hpp:119-123
+int get_bulk_size(int remaining, bool recovery, int tail)
+{
+  if (recovery || remaining <= tail) return 1;
+  return (int)std::lround(std::sqrt(double(remaining)));
+}
+
+// rounding.hpp:127-152 (host RNG; identical stream to the reference)
+void candidate_values(const double* sv, const std::vector<int>& vars,
+                      const std::vector<double2>& bounds, std::mt19937_64& rng, double band,
+                      std::vector<double>& v0, std::vector<double>& v1)
+{
+  v0.clear();
+  v1.clear();
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  for (size_t j = 0; j < vars.size(); ++j) {
+    const double v  = sv[vars[j]];
+    const double fl = std::floor(v);
+    const double f  = v - fl;
+    double d0, d1;
+    if (std::abs(f - 0.5) >= band) {
+      d0 = d1 = std::round(v);
+    } else {
+      d0 = fl + (unit(rng) < f ? 1.0 : 0.0);
+      d1 = fl + (unit(rng) < f ? 1.0 : 0.0);
+    }
+    const double lo = std::ceil(bounds[j].x - 1e-9);
+    const double hi = std::floor(bounds[j].y + 1e-9);
+    v0.push_back(clampd(d0, lo, hi));
+    v1.push_back(clampd(d1, lo, hi));
+  }
+}
+
+}  // namespace bp
+
+extern "C" {
+
+void bp_rounding_config_default(bp_rounding_config* c)
+{
+  c->random_band        = 0.25;
+  c->single_var_tail    = 36;
+  c->repair_enabled     = 0;
+  c->repair_attempt_cap = 16;
+  c->repair_shift_cap   = 64;
+}
+
+int bp_propagation_round(bp_problem* p, const double* start_values, const bp_cache* cache,
+                         uint64_t seed, double deadline_sec, const bp_rounding_config* cfg_in,
+                         double* out_values, bp_rounding_outcome* out)
+{
+  try {
+    if (!p || !start_values || !out_values || !out) throw std::invalid_argument("null argument");
+    bp_rounding_config cfg;
+    bp_rounding_config_default(&cfg);
+    if (cfg_in) cfg = *cfg_in;
+    if (cfg.repair_enabled) throw std::invalid_argument("repair is not supported by this engine yet");
+    bp::Problem& P                 = bp_problem_impl(p);
+    const bp_problem_host& H       = bp_problem_hostdata(p);
+    const bp::HostCache* hc        = cache ? bp_cache_host(cache) : nullptr;
+    std::lock_guard<std::mutex> lk(P.mu);
+    BP_CUDA(cudaSetDevice(P.device));
+    const int n = P.n;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto expired  = [&] {
+      if (!(deadline_sec > 0.0)) return false;
+      return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() >= deadline_sec;
+    };
+    std::mt19937_64 rng(seed);
+    bp::RoundCtx X(P, H);
+    std::vector<double> orig(2 * (size_t)n);
+    bp_problem_root(p, orig.data());
+    X.ws.upload(reinterpret_cast<const double2*>(orig.data()), n);
+    X.root.alloc(std::max(n, 1));
+    if (hc) BP_CUDA(cudaMemcpy(X.root.p, hc->root.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+    // is the original-bounds state a certified fixpoint? (one full round changes nothing)
+    {
+      BP_CUDA(cudaMemcpyAsync(P.st.bounds, X.ws.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, X.s));
+      BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(bp::Ctl), X.s));
+      bp::Limits one   = X.limits();
+      one.max_rounds   = 1;
+      const auto r     = bp::run_engine(P, bp::MODE_PROPAGATE, true, one, X.s);
+      X.ws_cert        = r.status == bp::BP_STATUS_UNCHANGED;
+      if (X.ws_cert) X.snapshot_ws_activities();
+    }
+    // unset = initial_sort minus fixed (rounding.hpp:400-404)
+    std::vector<int> unset0;
+    for (int v : bp::initial_sort(H, start_values, n))
+      if (orig[2 * v] != orig[2 * v + 1]) unset0.push_back(v);
+    X.n_unset = (int)unset0.size();
+    const size_t cap = std::max<size_t>(unset0.size(), 1);
+    X.unset.upload(unset0.data(), unset0.size());
+    if (X.unset.n < cap) X.unset.alloc(cap);
+    X.unset_alt.alloc(cap);
+    X.pos_in.alloc(cap);
+    X.pos_out.alloc(cap);
+    X.keys_in.alloc(cap);
+    X.keys_out.alloc(cap);
+    X.sel_count.alloc(1);
+    std::vector<std::pair<int, double>> committed;
+    bool recovery = false, force = false;
+    bp_rounding_outcome o;
+    std::memset(&o, 0, sizeof(o));
+    std::vector<double> pv0, pv1;
+    while (X.n_unset > 0) {
+      if (expired()) {
+        o.timed_out = 1;
+        break;
+      }
+      const int bulk = bp::get_bulk_size(X.n_unset, recovery && !force, cfg.single_var_tail);
+      if (!force) {
+        if (bulk > 1) X.slack_sort();
+        const std::vector<int> take = X.take_first(bulk);
+        const auto tb               = X.gather(X.ws, take);
+        bp::candidate_values(start_values, take, tb, rng, cfg.random_band, pv0, pv1);
+        auto pr0   = X.run_probe(take, pv0, hc);
+        int sel    = -1;
+        bp::RoundCtx::Probe pr1;
+        if (pr0.infeas_count == 0) {
+          sel = 0;
+        } else {
+          pr1 = X.run_probe(take, pv1, hc);
+          if (pr1.infeas_count == 0) sel = 1;
+        }
+        if (sel >= 0) {
+          auto& pr = sel == 0 ? pr0 : pr1;
+          if (!pr.fixed.empty()) {  // commit (rounding.hpp:436-443)
+            BP_CUDA(cudaMemcpyAsync(X.ws.p, P.st.bounds, sizeof(double2) * n, cudaMemcpyDeviceToDevice, X.s));
+            X.ws_infeasible = false;
+            X.ws_cert       = pr.cert;
+            if (X.ws_cert) X.snapshot_ws_activities();
+            for (const auto& fv : pr.fixed) committed.push_back(fv);
+            X.drop_fixed();
+            recovery = false;
+            o.bulks_committed++;
+            continue;
+          }
+          // every bulk var evicted: apply the cache's forced branches (rounding.hpp:447-478)
+          bool narrowed = false;
+          for (int v : pr.evicted) {
+            const int e = (hc && v < hc->n) ? hc->entry_of[v] : -1;
+            if (e < 0) continue;
+            const double2 b = X.gather(X.ws, {v})[0];
+            double lo = b.x, up = b.y;
+            if (hc->e_force[2 * e] && up > hc->e_branch[4 * e + 1]) {
+              up       = std::min(up, hc->e_branch[4 * e + 1]);
+              narrowed = true;
+            } else if (hc->e_force[2 * e + 1] && lo < hc->e_branch[4 * e + 2]) {
+              lo       = std::max(lo, hc->e_branch[4 * e + 2]);
+              narrowed = true;
+            }
+            X.scatter(X.ws.p, {v}, {make_double2(lo, up)});
+            X.ws_cert = false;
+            if (lo > up) {
+              o.rounding_infeasible = 1;
+              force                 = true;
+              break;
+            }
+          }
+          if (narrowed && !force) {
+            BP_CUDA(cudaMemcpyAsync(P.st.bounds, X.ws.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, X.s));
+            const auto r = X.propagate_engine(false, {});
+            BP_CUDA(cudaMemcpyAsync(X.ws.p, P.st.bounds, sizeof(double2) * n, cudaMemcpyDeviceToDevice, X.s));
+            X.ws_cert = r.fixpoint != 0;
+            if (X.ws_cert) X.snapshot_ws_activities();
+            if (r.status == bp::BP_STATUS_INFEASIBLE) {
+              X.ws_infeasible       = true;
+              o.rounding_infeasible = 1;
+              force                 = true;
+            }
+            X.drop_fixed();
+            continue;
+          }
+          if (!force) {
+            o.rounding_infeasible = 1;
+            force                 = true;
+          }
+          continue;
+        }
+        if (!recovery && !o.rounding_infeasible) {
+          recovery = true;  // backtrack, single-variable mode (rounding.hpp:480-483)
+          continue;
+        }
+        o.rounding_infeasible = 1;
+        const int v      = take[0];
+        const double val = bp::clampd(pv0[0], H.var_lower[v], H.var_upper[v]);
+        committed.push_back({v, val});
+        X.scatter(X.ws.p, {v}, {make_double2(val, val)});
+        X.ws_cert = false;
+        X.drop_fixed();
+        force = true;  // repair disabled (rounding.hpp:505-507)
+        continue;
+      }
+      // terminal phase (rounding.hpp:511-528)
+      const std::vector<int> take = X.take_first(bulk);
+      const auto tb               = X.gather(X.ws, take);
+      bp::candidate_values(start_values, take, tb, rng, cfg.random_band, pv0, pv1);
+      for (size_t j = 0; j < take.size(); ++j) {
+        pv0[j] = bp::clampd(pv0[j], H.var_lower[take[j]], H.var_upper[take[j]]);
+        pv1[j] = bp::clampd(pv1[j], H.var_lower[take[j]], H.var_upper[take[j]]);
+      }
+      const int viol0 = X.count_envelope_violations(take, pv0);
+      const int viol1 = viol0 == 0 ? 1 : X.count_envelope_violations(take, pv1);
+      const auto& pv  = viol1 < viol0 ? pv1 : pv0;
+      std::vector<double2> fx(take.size());
+      for (size_t j = 0; j < take.size(); ++j) {
+        fx[j] = make_double2(pv[j], pv[j]);
+        committed.push_back({take[j], pv[j]});
+      }
+      X.scatter(X.ws.p, take, fx);
+      X.ws_cert = false;
+      X.drop_fixed();
+    }
+    // value extraction (rounding.hpp:533-549)
+    std::vector<double> wsb(2 * (size_t)n);
+    if (n) BP_CUDA(cudaMemcpy(wsb.data(), X.ws.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) {
+      const double v = start_values[i];
+      if (!H.is_integer[i]) {
+        out_values[i] = bp::clampd(v, H.var_lower[i], H.var_upper[i]);
+        continue;
+      }
+      if (wsb[2 * i] == wsb[2 * i + 1]) out_values[i] = wsb[2 * i];
+      else out_values[i] = bp::clampd(std::round(v), H.var_lower[i], H.var_upper[i]);
+      if (wsb[2 * i] == wsb[2 * i + 1]) o.set_count++;
+    }
+    o.completed       = X.n_unset == 0;
+    o.bounds_feasible = o.completed && !o.rounding_infeasible && !X.ws_infeasible;
+    o.bp_calls        = (int32_t)X.bp_calls;
+    o.device_ms       = X.dev_ms;
+    *out              = o;
+    return BP_OK;
+  } catch (const std::invalid_argument& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_OUT_OF_RANGE;
+  } catch (const bp::cuda_error& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_CUDA;
+  } catch (const std::exception& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_RUNTIME;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+"""Python mirror of the reference fix-and-propagate API (pulse/rounding.hpp), on the GPU driver.
+
+* ``RoundingConfig`` (rounding.hpp:18-31), ``RoundingOutcome`` (:347-355)
+* ``initial_sort`` (:35-65) and ``get_bulk_size`` (:119-123) (host helpers)
+* ``propagation_round`` (:393-558): the whole bulk loop runs in libbp's driver with device-resident
+  bounds; the host RNG stream is the reference's (std::mt19937_64(seed)).
+
+``lp_polish`` (PDHG) is out of scope: ``propagation_round`` returns the point the reference would
+polish, and ``outcome.bounds_feasible`` tells whether it would.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .problem import ProblemDef
+from .probing import ProbingCache
+from .propagation import device_problem
+
+
+@dataclass
+class RoundingConfig:
+    random_band: float = 0.25
+    single_var_tail: int = 36
+    repair_enabled: bool = False
+    repair_attempt_cap: int = 16
+    repair_shift_cap: int = 64
+
+
+@dataclass
+class RoundingOutcome:
+    values: np.ndarray
+    rounding_infeasible: bool
+    timed_out: bool
+    completed: bool
+    repair_attempts: int
+    bulks_committed: int
+    set_count: int
+    bounds_feasible: bool
+    bp_calls: int
+    device_ms: float
+
+
+def initial_sort(p: ProblemDef, values) -> list:
+    """rounding.hpp:35-65 (stable: width class, then distance to the nearest integer)."""
+    items = []
+    for i in range(p.n_vars):
+        if not p.is_integer[i]:
+            continue
+        w = p.var_upper[i] - p.var_lower[i]
+        cls = 0 if w == 1.0 else (1 if w == 2.0 else 2)
+        v = float(values[i])
+        items.append((cls, abs(v - _round_half_away(v)), i))
+    items.sort(key=lambda t: (t[0], t[1]))  # Python's sort is stable
+    return [t[2] for t in items]
+
+
+def _round_half_away(v: float) -> float:
+    """std::round (half away from zero)."""
+    return math.copysign(math.floor(abs(v) + 0.5), v)
+
+
+def get_bulk_size(remaining: int, recovery: bool, single_var_tail: int = 36) -> int:
+    """rounding.hpp:119-123 (std::lround: half away from zero)."""
+    if recovery or remaining <= single_var_tail:
+        return 1
+    return int(_round_half_away(math.sqrt(float(remaining))))
+
+
+def propagation_round(p: ProblemDef, start_values, cache: ProbingCache | None, seed: int,
+                      deadline_sec: float = math.inf, cfg: RoundingConfig | None = None) -> RoundingOutcome:
+    """rounding.hpp:393 with Rng(seed) and Deadline(deadline_sec) (inf = never)."""
+    cfg = cfg or RoundingConfig()
+    dp = device_problem(p)
+    L = _lib.lib()
+    c = _lib.bp_rounding_config()
+    L.bp_rounding_config_default(C.byref(c))
+    c.random_band = cfg.random_band
+    c.single_var_tail = cfg.single_var_tail
+    c.repair_enabled = 1 if cfg.repair_enabled else 0
+    c.repair_attempt_cap = cfg.repair_attempt_cap
+    c.repair_shift_cap = cfg.repair_shift_cap
+    sv = np.ascontiguousarray(start_values, dtype=np.float64)
+    out = np.zeros(max(p.n_vars, 1))
+    o = _lib.bp_rounding_outcome()
+    dl = 0.0 if not math.isfinite(deadline_sec) else float(deadline_sec)
+    _lib.check(L.bp_propagation_round(dp.h, _lib.ptr(sv), cache.h if cache is not None else None,
+                                      C.c_uint64(seed), dl, C.byref(c), _lib.ptr(out), C.byref(o)))
+    return RoundingOutcome(out[: p.n_vars], bool(o.rounding_infeasible), bool(o.timed_out),
+                           bool(o.completed), int(o.repair_attempts), int(o.bulks_committed),
+                           int(o.set_count), bool(o.bounds_feasible), int(o.bp_calls),
+                           float(o.device_ms))

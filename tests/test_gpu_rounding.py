@@ -1,0 +1,88 @@
+"""GPU fix-and-propagate driver vs the reference's propagation_round (rounding.hpp:393) on the
+same instances, start points, seeds and caches: identical integer outputs and flags. Mirrors
+test_rounding.cpp and acceptance.cpp criterion 4 (rounding integrality, 1000-instance stream)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2510_20499_b200 import make_problem, synth
+from paper_2510_20499_b200.probing import build_cache
+from paper_2510_20499_b200.rounding import get_bulk_size, initial_sort, propagation_round
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+FLAGS = ("rounding_infeasible", "timed_out", "completed", "bulks_committed", "set_count")
+
+
+def test_host_helpers_known_answers():
+    assert get_bulk_size(100, False) == 10 and get_bulk_size(36, False) == 1
+    assert get_bulk_size(10000, True) == 1 and get_bulk_size(37, False) == 6
+    p = make_problem([(0, 1, True), (0, 1, True), (0, 9, True)], [([(0, 1.0), (1, 1.0), (2, 1.0)], -INF, 100.0)])
+    assert initial_sort(p, [0.1, 0.5, 0.2]) == [0, 1, 2]
+    p = make_problem([(0, 9, True), (0, 2, True), (0, 1, True)], [([(0, 1.0), (1, 1.0), (2, 1.0)], -INF, 100.0)])
+    assert initial_sort(p, [1.0, 1.0, 1.0]) == [2, 1, 0]
+
+
+def test_rounding_known_answers():
+    p = make_problem([(0, 1, True, -1), (0, 1, True, -1)], [([(0, 1.0), (1, 1.0)], -INF, 1.0)])
+    out = propagation_round(p, [0.5, 0.5], build_cache(p, 1e9), seed=3)
+    assert out.completed and not out.rounding_infeasible
+    x, y = out.values
+    assert x + y <= 1.0 + 1e-9 and x in (0.0, 1.0) and y in (0.0, 1.0)
+    out = propagation_round(p, [1.0, 0.0], None, seed=3)
+    assert list(out.values) == [1.0, 0.0]
+    q = make_problem([(0, 1, True)], [([(0, 1.0)], 1.0, INF), ([(0, 1.0)], -INF, 0.0)])
+    out = propagation_round(q, [0.5], None, seed=3, deadline_sec=5.0)
+    assert out.rounding_infeasible
+
+
+def _compare(rp, p, start, seed, use_cache, tag):
+    from oracle.bind import RefCache, ref_propagation_round
+    gcache = build_cache(p, 1e9) if use_cache else None
+    rcache = RefCache.from_gpu(rp, gcache) if use_cache else None
+    rv, rf = ref_propagation_round(rp, p.n_vars, start, rcache, seed)
+    g = propagation_round(p, start, gcache, seed)
+    got = {k: int(getattr(g, k)) for k in FLAGS}
+    assert got == {k: rf[k] for k in FLAGS}, tag
+    isint = p.is_integer.astype(bool)
+    assert np.array_equal(g.values[isint], rv[isint]), tag
+    return g
+
+
+def test_acceptance_rounding_stream_matches_reference(oracle_built):
+    """acceptance.cpp:121-150 instance stream (seed 5150), GPU cache fed to both drivers."""
+    from oracle.bind import Ref, RefCache, RefRng
+    if not Ref.available():
+        pytest.skip("reference library missing")
+    rng = RefRng(5150)
+    for t in range(300):
+        rp = rng.random_instance()
+        p = rp.to_def()
+        start = np.array([p.var_lower[i] + rng.uniform_real(0.0, 1.0) * (p.var_upper[i] - p.var_lower[i])
+                          for i in range(p.n_vars)])
+        g = _compare(rp, p, start, t, True, f"inst{t}")
+        assert np.all(np.abs(g.values - np.round(g.values)) <= 1e-9)
+
+
+def test_gpu_cache_equals_reference_cache_in_rounding(oracle_built):
+    from oracle.bind import Ref, RefCache, RefRng, ref_propagation_round
+    rng = RefRng(42)
+    for t in range(100):
+        rp = rng.random_instance()
+        p = rp.to_def()
+        start = np.array([p.var_lower[i] + rng.uniform_real(0.0, 1.0) * (p.var_upper[i] - p.var_lower[i])
+                          for i in range(p.n_vars)])
+        gv = propagation_round(p, start, build_cache(p, 1e9), 1000 + t).values
+        rv, _ = ref_propagation_round(rp, p.n_vars, start, RefCache.build(rp), 1000 + t)
+        assert np.array_equal(gv, rv), t
+
+
+def test_mixed_instance_rounding(oracle_built):
+    from oracle.bind import RefProblem
+    p = synth.c1(n=3000, m=3000)
+    rp = RefProblem.from_def(p)
+    rng = np.random.default_rng(7)
+    start = p.var_lower + rng.random(p.n_vars) * (p.var_upper - p.var_lower)
+    for use_cache in (False, True):
+        _compare(rp, p, start, 11, use_cache, f"C1-3000 cache={use_cache}")
