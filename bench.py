@@ -191,6 +191,116 @@ def reference_visits(p):
     return visits
 
 
+def _max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_probing(args, rank, world, local):
+    """configs[2]: batched double probing of all 200k binaries of C3 (500k x 500k set covering),
+    candidates sharded over the ranks, packed slices gathered to rank 0 (NCCL), merged there.
+    probes/s = variables probed (both branches) / wall time of probe + gather + merge."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_20499_b200 import synth
+    from paper_2510_20499_b200.distributed import build_cache_sharded
+    from paper_2510_20499_b200.probing import probe_variables
+
+    p = synth.c3()
+    vars_ = list(range(200_000))  # the binaries (every one is probed: order is immaterial)
+    probe_variables(p, None, vars_[:2000])  # warm-up: kernels loaded, problem uploaded
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    if world > 1:
+        cache, dev_ms = build_cache_sharded(p, vars_, device=torch.device("cuda", local))
+    else:
+        cache = probe_variables(p, None, vars_)
+        dev_ms = cache.probe_ms
+    if world > 1:
+        dist.barrier()
+    el = _max_over_ranks(time.perf_counter() - t0, world)
+    dev_ms = _max_over_ranks(dev_ms, world)
+    if rank != 0:
+        return None
+    out = {"workload": "C3: set covering 500k x 500k (200k binaries + 300k continuous), N=%d" % p.nnz(),
+           "probes_per_s": len(vars_) / el, "variables_probed": cache.n_probed,
+           "branches": 2 * cache.n_probed, "infeasible_branches": cache.n_infeasible_branches,
+           "deltas": cache.n_deltas, "fallback_branches": cache.n_fallback,
+           "root_certified_fixpoint": cache.certified, "wall_ms": el * 1e3,
+           "probe_kernel_ms_max_rank": dev_ms, "n_gpus": world,
+           "parallelism": f"candidates sharded x{world}, NCCL gather to rank 0"}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.bind import Ref, RefCache, RefProblem
+        if Ref.available():
+            rp = RefProblem.from_def(p)
+            L = Ref.lib()
+            t0 = time.perf_counter()
+            h = L.ref_build_cache(rp.h, args.cpu_sample_sec)
+            el_cpu = time.perf_counter() - t0
+            import ctypes as C
+            npb, ninf = C.c_int(), C.c_int()
+            L.ref_cache_stats(h, C.byref(npb), C.byref(ninf))
+            L.ref_cache_free(h)
+            out["cpu_baseline"] = {"value": npb.value / args.cpu_sample_sec, "unit": "probes/s",
+                                   "cores": int(L.ref_max_threads()), "kind": "reference",
+                                   "sample": f"build_cache(p, {args.cpu_sample_sec:g} s): "
+                                             f"{npb.value} vars probed ({el_cpu:.1f} s incl. "
+                                             "prioritization)"}
+    return out
+
+
+def run_rounding(args, rank, world, local):
+    """configs[3]: fix-and-propagate bulk rounding with a probing cache on the 2M x 2M
+    knapsack/assignment mix (presolved to its propagation fixpoint), one replica per rank."""
+    import torch
+
+    from paper_2510_20499_b200 import BoundsState, propagate, synth
+    from paper_2510_20499_b200.probing import build_cache
+    from paper_2510_20499_b200.rounding import propagation_round
+
+    p0, start = synth.c4()
+    b = BoundsState(p0)
+    r0 = propagate(p0, b)
+    p = synth.with_bounds(p0, b.raw())
+    t0 = time.perf_counter()
+    cache = build_cache(p, 1e9)
+    cache_s = _max_over_ranks(time.perf_counter() - t0, world)
+    t0 = time.perf_counter()
+    out = propagation_round(p, start, cache, seed=4 + rank)
+    el = _max_over_ranks(time.perf_counter() - t0, world)
+    if rank != 0:
+        return None
+    res = {"workload": "C4: knapsack/assignment 2M x 2M (N=%d), presolved root (%d BP rounds)"
+                       % (p.nnz(), r0.rounds),
+           "cache_build_s": cache_s, "cache_vars": cache.n_probed,
+           "cache_probes_per_s": cache.n_probed / cache_s, "round_s": el,
+           "bulks_committed": out.bulks_committed, "bp_calls": out.bp_calls,
+           "bp_calls_per_s": world * out.bp_calls / el, "completed": out.completed,
+           "rounding_infeasible": out.rounding_infeasible, "set_count": out.set_count,
+           "engine_device_ms": out.device_ms, "n_gpus": world, "parallelism": f"replicas x{world}"}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.bind import Ref, RefProblem, ref_propagation_round
+        if Ref.available():
+            rp = RefProblem.from_def(p)
+            t0 = time.perf_counter()
+            _, fl = ref_propagation_round(rp, p.n_vars, start, None, 4, deadline=args.cpu_sample_sec)
+            el_cpu = time.perf_counter() - t0
+            res["cpu_baseline"] = {"value": fl["bulks_committed"] / el_cpu, "unit": "bulks committed/s",
+                                   "cores": int(Ref.lib().ref_max_threads()), "kind": "reference",
+                                   "sample": f"propagation_round without cache, deadline "
+                                             f"{args.cpu_sample_sec:g} s: {fl['bulks_committed']} bulks"}
+            res["bulks_committed_per_s"] = out.bulks_committed / el
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -200,6 +310,9 @@ def main():
     ap.add_argument("--workload", default="C2", choices=["C2", "C1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-probing", action="store_true")
+    ap.add_argument("--no-rounding", action="store_true")
+    ap.add_argument("--cpu-sample-sec", type=float, default=20.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -304,6 +417,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    probing = None if args.no_probing else run_probing(args, rank, world, local)
+    rounding = None if args.no_rounding else run_rounding(args, rank, world, local)
+
     if rank == 0:
         peak, peak_kind = peaks()
         achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
@@ -345,6 +461,8 @@ def main():
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks,
+            "probing": probing,
+            "rounding": rounding,
         }
         print(json.dumps(line))
     if world > 1:

@@ -1,0 +1,63 @@
+"""Multi-GPU probing-cache construction: candidates are sharded across ranks with no
+data-path collective; each rank probes its slice on its own GPU (problem replicated per GPU),
+packs it (bp_cache_pack) and the slices are gathered to rank 0 with one collective pair over
+torch.distributed (NCCL over NVLink on GPUs; gloo in the CPU tests):
+
+  1. all_gather of the per-rank packed byte counts (int64)
+  2. all_gather_into_tensor of the byte slices padded to the largest count
+
+Rank 0 merges the slices (bp_cache_merge_packed). Entries are deterministic per variable, so any
+partition gives the same cache.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard(items, rank: int, world: int):
+    """Strided interleave of a priority-ordered candidate list (balances skewed probe costs)."""
+    return list(items[rank::world])
+
+
+def gather_packed(buf: np.ndarray, device=None, group=None) -> list | None:
+    """Gathers every rank's packed slice; returns the list of slices on rank 0, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = device if device is not None else torch.device("cpu")
+    n = torch.tensor([int(buf.size)], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(max(sizes), 1)
+    send = torch.zeros(mx, dtype=torch.uint8, device=dev)
+    if buf.size:
+        send[: buf.size] = torch.from_numpy(np.ascontiguousarray(buf, dtype=np.uint8)).to(dev)
+    recv = torch.zeros(world * mx, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    if rank != 0:
+        return None
+    host = recv.cpu().numpy()
+    return [host[r * mx: r * mx + sizes[r]] for r in range(world)]
+
+
+def build_cache_sharded(p, vars_, root=None, device=None, group=None):
+    """Probes ``vars_`` sharded over the ranks of ``group``; returns the merged ProbingCache on
+    rank 0 (None on other ranks) and this rank's local device time (ms)."""
+    import torch.distributed as dist
+
+    from .probing import ProbingCache, probe_variables
+    from .propagation import BoundsState
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    local = probe_variables(p, root, shard(vars_, rank, world))
+    slices = gather_packed(local.pack(), device=device, group=group)
+    if rank != 0:
+        return None, local.probe_ms
+    merged = ProbingCache.empty(root if root is not None else BoundsState(p))
+    for s in slices:
+        merged.merge_packed(s)
+    return merged, local.probe_ms

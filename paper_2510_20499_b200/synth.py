@@ -150,3 +150,91 @@ def c3(seed=3, n_bin=200_000, n_cont=300_000, n_cover=400_000, n_link=100_000) -
 
 
 CONFIGS = {"C1": c1, "C2": c2, "C3": c3}
+
+
+def c4(seed=4, n=2_000_000, m=2_000_000, bin_frac=0.8, n_long=100, long_len=20_000):
+    """configs[3]: knapsack/assignment mix. Binaries are partitioned into
+    assignment blocks of 4..16 (sum = 1 equalities); the other rows are knapsacks
+    sum w_j x_j <= C with integer weights 1..99 over random binaries / integers [0, 10] (a few
+    long ones), capacities planted around a feasible point. Returns (problem, start point U(lb, ub))."""
+    rng = np.random.default_rng(seed + 4000)
+    nb = int(n * bin_frac)
+    lo = np.zeros(n)
+    up = np.concatenate([np.ones(nb), np.full(n - nb, 10.0)])
+    isint = np.ones(n, np.uint8)
+    # assignment blocks over the binaries
+    sizes = []
+    tot = 0
+    while tot < nb:
+        s = int(rng.integers(4, 17))
+        s = min(s, nb - tot)
+        sizes.append(s)
+        tot += s
+    sizes = np.array(sizes, dtype=np.int64)
+    n_asg = sizes.size
+    x = np.zeros(n)
+    starts = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    pick = starts + np.floor(rng.random(n_asg) * sizes).astype(np.int64)
+    x[pick] = 1.0
+    x[nb:] = rng.integers(0, 11, size=n - nb)
+    m_k = max(m - n_asg, 0)
+    lens = 6 + rng.poisson(6, size=m_k)
+    if n_long and m_k > n_long:
+        lens[rng.choice(m_k, size=n_long, replace=False)] = min(long_len, n)
+    rs_k, cols_k = _distinct_cols(rng, lens, n, lambda size: rng.integers(0, n, size=size))
+    w = rng.integers(1, 100, size=cols_k.size).astype(np.float64)
+    lhs = np.add.reduceat(w * x[cols_k], rs_k[:-1]) if cols_k.size else np.zeros(m_k)
+    lhs[np.diff(rs_k) == 0] = 0.0
+    cap_max = np.add.reduceat(w * up[cols_k], rs_k[:-1]) if cols_k.size else np.zeros(m_k)
+    cap = np.floor(lhs + rng.uniform(0.0, 0.15, size=m_k) * (cap_max - lhs))
+    # assemble: assignment rows first, then knapsacks
+    a_cols = np.arange(nb, dtype=np.int32)
+    row_start = np.concatenate([starts, [nb], nb + rs_k[1:]]).astype(np.int64)
+    cols = np.concatenate([a_cols, cols_k]).astype(np.int32)
+    vals = np.concatenate([np.ones(nb), w])
+    cl = np.concatenate([np.ones(n_asg), np.full(m_k, -math.inf)])
+    cu = np.concatenate([np.ones(n_asg), cap])
+    p = problem_from_csr(n, n_asg + m_k, row_start.astype(np.int32), cols, vals, lo, up, isint, cl,
+                         cu, name=f"C4-{n}x{n_asg + m_k}")
+    start = lo + rng.random(n) * (up - lo)
+    return p, start
+
+
+def c5(seed=100, count=64, lo_nnz=10_000, hi_nnz=5_000_000):
+    """configs[4]: `count` heterogeneous instances, nnz log-uniform in [lo_nnz, hi_nnz], drawn from
+    the C1-C4 generators with row/col ratio U(0.5, 2). Yields (seed, problem)."""
+    for j in range(count):
+        rng = np.random.default_rng(seed + j)
+        nnz = float(np.exp(rng.uniform(np.log(lo_nnz), np.log(hi_nnz))))
+        ratio = float(rng.uniform(0.5, 2.0))
+        kind = int(rng.integers(0, 4))
+        if kind == 0:  # C1-like: ~8 nnz per row
+            m = max(int(nnz / 8), 10)
+            n = max(int(m / ratio), 10)
+            lengths = np.minimum(6 + rng.binomial(4, 0.5, size=m), n)
+            yield seed + j, mixed_instance(n, m, lengths, seed + j, name=f"C5-{j}-C1")
+        elif kind == 1:  # C2-like power law
+            m = max(int(nnz / 19), 10)
+            n = max(int(m / ratio), 10)
+            lengths = pareto_lengths(rng, m, cap=min(100_000, n), n_heavy=min(8, max(m // 1000, 1)))
+            yield seed + j, mixed_instance(n, m, lengths, seed + j, name=f"C5-{j}-C2")
+        elif kind == 2:  # C3-like covering
+            nb = max(int(nnz / 36), 100)
+            yield seed + j, c3(seed + j, n_bin=nb, n_cont=int(1.5 * nb), n_cover=max(int(2 * nb / ratio), 10),
+                               n_link=max(nb // 2, 1))
+        else:  # C4-like knapsack/assignment
+            n = max(int(nnz / 12), 100)
+            yield seed + j, c4(seed + j, n=n, m=max(int(n * ratio), 50), n_long=0)[0]
+
+
+CONFIGS["C4"] = c4
+
+
+def with_bounds(p, bounds) -> ProblemDef:
+    """The same instance with its variable bounds replaced by ``bounds`` (interleaved 2n), e.g. a
+    propagated fixpoint ("presolved" root: probing and rounding then start from a certified
+    fixpoint, so every branch starts from its own frontier)."""
+    b = np.asarray(bounds, dtype=np.float64)
+    return problem_from_csr(p.n_vars, p.n_cons, p.row_start, p.row_col, p.row_val, b[0::2].copy(),
+                            b[1::2].copy(), p.is_integer, p.cons_lower, p.cons_upper,
+                            name=p.name + "-presolved", apply_integral=False, validate=False)
