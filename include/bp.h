@@ -141,6 +141,14 @@ int bp_cache_deltas(const bp_cache* c, int32_t v, int32_t side, int32_t* vars, d
                     double* up);
 int bp_cache_root(const bp_cache* c, double* root2n);
 int bp_cache_create_empty(int32_t n_vars, const double* root2n, bp_cache** out);
+/* Adds the entry of v (pulse::ProbeEntry, probing.hpp:80-85) to a cache, e.g. to hand a host-built
+ * pulse::ProbingCache to the engine: hdr5 = {kind, forces_down, forces_up, down.feasible,
+ * up.feasible}, br4 = {down lo, down up, up lo, up up}, deltas ascending by var. An existing entry
+ * of v is an error (BP_ERR_INVALID_ARGUMENT). */
+int bp_cache_set_entry(bp_cache* c, int32_t v, const int32_t* hdr5, const double* br4,
+                       int32_t n_down, const int32_t* down_vars, const double* down_lo,
+                       const double* down_up, int32_t n_up, const int32_t* up_vars,
+                       const double* up_lo, const double* up_up);
 /* Serialisation of a cache slice for the multi-GPU gather (NCCL) and merge on rank 0. */
 int bp_cache_pack_size(const bp_cache* c, int64_t* bytes);
 int bp_cache_pack(const bp_cache* c, void* buf, int64_t bytes);
@@ -183,6 +191,26 @@ void bp_rounding_config_default(bp_rounding_config* cfg);
 int bp_propagation_round(bp_problem* p, const double* start_values, const bp_cache* cache,
                          uint64_t seed, double deadline_sec, const bp_rounding_config* cfg,
                          double* out_values, bp_rounding_outcome* out);
+
+/* Same with the caller's generator instead of a seed (pulse::propagation_round takes Rng&): the
+ * std::mt19937_64 text representation (`os << rng`) is read from rng_state and the advanced
+ * state written back, so the caller's stream continues exactly as after the reference call. */
+#define BP_RNG_STATE_BYTES 8192
+int bp_propagation_round_rng(bp_problem* p, const double* start_values, const bp_cache* cache,
+                             char* rng_state, int64_t rng_state_bytes, double deadline_sec,
+                             const bp_rounding_config* cfg, double* out_values,
+                             bp_rounding_outcome* out);
+
+/* pulse::parallel_propagate (rounding.hpp:213-224; detail::run_probe :167-207): both candidate
+ * vectors v0 / v1 for `vars` from host bounds base2n (+ its infeasible flag), warm-started from
+ * `cache` when non-NULL. Per probe q in {0, 1}: out_bounds2n[q*2n .. (q+1)*2n) = ProbeResult.bounds,
+ * out_infeasible[q] = bounds.infeasible(), infeas_count[q], evicted[q*nvars ..] / n_evicted[q],
+ * fixed_vars / fixed_vals[q*nvars ..] / n_fixed[q] (ProbeResult.fixed). */
+int bp_parallel_propagate(bp_problem* p, const double* base2n, int32_t base_infeasible,
+                          const int32_t* vars, int32_t nvars, const double* v0, const double* v1,
+                          const bp_cache* cache, double* out_bounds2n, int32_t* out_infeasible,
+                          int32_t* infeas_count, int32_t* evicted, int32_t* n_evicted,
+                          int32_t* fixed_vars, double* fixed_vals, int32_t* n_fixed);
 
 /* Number of engine kernels launched by this process. */
 int64_t bp_kernel_launches(void);

@@ -99,6 +99,9 @@ _SIGS = [
                                   C.c_void_p]),
     ("bp_cache_root", C.c_int, [C.c_void_p, C.c_void_p]),
     ("bp_cache_create_empty", C.c_int, [C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("bp_cache_set_entry", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                     C.c_void_p, C.c_void_p]),
     ("bp_cache_pack_size", C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     ("bp_cache_pack", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
     ("bp_cache_merge_packed", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
@@ -109,6 +112,13 @@ _SIGS = [
     ("bp_propagation_round", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_double,
                                        C.POINTER(bp_rounding_config), C.c_void_p,
                                        C.POINTER(bp_rounding_outcome)]),
+    ("bp_propagation_round_rng", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p,
+                                           C.c_int64, C.c_double, C.POINTER(bp_rounding_config),
+                                           C.c_void_p, C.POINTER(bp_rounding_outcome)]),
+    ("bp_parallel_propagate", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]),
     ("bp_kernel_launches", C.c_int64, []),
     ("bp_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                  C.POINTER(C.c_int64)]),

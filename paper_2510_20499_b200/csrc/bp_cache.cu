@@ -745,6 +745,43 @@ int bp_cache_create_empty(int32_t n_vars, const double* root2n, bp_cache** out)
   });
 }
 
+int bp_cache_set_entry(bp_cache* c, int32_t v, const int32_t* hdr5, const double* br4,
+                       int32_t n_down, const int32_t* down_vars, const double* down_lo,
+                       const double* down_up, int32_t n_up, const int32_t* up_vars,
+                       const double* up_lo, const double* up_up)
+{
+  return cguard([&] {
+    need(c && hdr5 && br4 && n_down >= 0 && n_up >= 0, "bad argument");
+    need((n_down == 0 || (down_vars && down_lo && down_up)) && (n_up == 0 || (up_vars && up_lo && up_up)),
+         "null delta array");
+    bp::HostCache& C = c->c;
+    if (v < 0 || v >= C.n) throw std::out_of_range("var out of range");
+    if (C.entry_of[v] >= 0) throw std::invalid_argument("var already has a cache entry");
+    for (int j = 0; j < n_down; ++j)
+      if (down_vars[j] < 0 || down_vars[j] >= C.n) throw std::out_of_range("delta var out of range");
+    for (int j = 0; j < n_up; ++j)
+      if (up_vars[j] < 0 || up_vars[j] >= C.n) throw std::out_of_range("delta var out of range");
+    C.entry_of[v] = (int)C.e_var.size();
+    C.e_var.push_back(v);
+    C.e_kind.push_back(hdr5[0]);
+    C.e_force.push_back((uint8_t)(hdr5[1] != 0));
+    C.e_force.push_back((uint8_t)(hdr5[2] != 0));
+    C.e_feas.push_back((uint8_t)(hdr5[3] != 0));
+    C.e_feas.push_back((uint8_t)(hdr5[4] != 0));
+    C.e_branch.insert(C.e_branch.end(), br4, br4 + 4);
+    C.d_var.insert(C.d_var.end(), down_vars, down_vars + n_down);
+    C.d_lo.insert(C.d_lo.end(), down_lo, down_lo + n_down);
+    C.d_up.insert(C.d_up.end(), down_up, down_up + n_down);
+    C.d_off.push_back((long long)C.d_var.size());
+    C.d_var.insert(C.d_var.end(), up_vars, up_vars + n_up);
+    C.d_lo.insert(C.d_lo.end(), up_lo, up_lo + n_up);
+    C.d_up.insert(C.d_up.end(), up_up, up_up + n_up);
+    C.d_off.push_back((long long)C.d_var.size());
+    C.n_probed++;  // probing.hpp:274-278, incrementally
+    C.n_infeasible_branches += (hdr5[3] ? 0 : 1) + (hdr5[4] ? 0 : 1);
+  });
+}
+
 // Packed slice: [i64 n_entries, i64 n_deltas, i64 n_fallback, i64 certified]
 //   entries: i32 var, i32 kind, u8 feas[2], u8 force[2], f64 branch[4], i64 count[2]
 //   deltas:  i32 var[], f64 lo[], f64 up[]

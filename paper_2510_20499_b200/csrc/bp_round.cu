@@ -22,6 +22,8 @@
 #include <cmath>
 #include <cstring>
 #include <random>
+#include <sstream>
+#include <string>
 #include <stdexcept>
 #include <vector>
 
@@ -384,12 +386,12 @@ struct RoundCtx {
       fb.push_back(now[j]);
       out.fixed.push_back({v, val});
     }
+    scatter(P.st.bounds, fv, fb);  // applied even when crossing, as in the reference's out.bounds
     if (crossings > 0) {
       out.infeasible   = true;
       out.infeas_count = crossings;
       return out;
     }
-    scatter(P.st.bounds, fv, fb);
     std::sort(changed.begin(), changed.end());
     changed.erase(std::unique(changed.begin(), changed.end()), changed.end());
     const bool frontier = ws_cert && !root_changed;
@@ -486,9 +488,7 @@ void candidate_values(const double* sv, const std::vector<int>& vars,
 
 }  // namespace bp
 
-extern "C" {
-
-void bp_rounding_config_default(bp_rounding_config* c)
+extern "C" void bp_rounding_config_default(bp_rounding_config* c)
 {
   c->random_band        = 0.25;
   c->single_var_tail    = 36;
@@ -497,9 +497,12 @@ void bp_rounding_config_default(bp_rounding_config* c)
   c->repair_shift_cap   = 64;
 }
 
-int bp_propagation_round(bp_problem* p, const double* start_values, const bp_cache* cache,
-                         uint64_t seed, double deadline_sec, const bp_rounding_config* cfg_in,
-                         double* out_values, bp_rounding_outcome* out)
+namespace {
+
+// propagation_round with the caller's generator (consumed exactly like the reference's Rng&).
+int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
+               std::mt19937_64& rng, double deadline_sec, const bp_rounding_config* cfg_in,
+               double* out_values, bp_rounding_outcome* out)
 {
   try {
     if (!p || !start_values || !out_values || !out) throw std::invalid_argument("null argument");
@@ -518,7 +521,6 @@ int bp_propagation_round(bp_problem* p, const double* start_values, const bp_cac
       if (!(deadline_sec > 0.0)) return false;
       return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() >= deadline_sec;
     };
-    std::mt19937_64 rng(seed);
     bp::RoundCtx X(P, H);
     std::vector<double> orig(2 * (size_t)n);
     bp_problem_root(p, orig.data());
@@ -681,6 +683,109 @@ int bp_propagation_round(bp_problem* p, const double* start_values, const bp_cac
     o.bp_calls        = (int32_t)X.bp_calls;
     o.device_ms       = X.dev_ms;
     *out              = o;
+    return BP_OK;
+  } catch (const std::invalid_argument& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_OUT_OF_RANGE;
+  } catch (const bp::cuda_error& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_CUDA;
+  } catch (const std::exception& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_RUNTIME;
+  }
+}
+
+
+}  // namespace
+
+extern "C" {
+
+int bp_propagation_round(bp_problem* p, const double* start_values, const bp_cache* cache,
+                         uint64_t seed, double deadline_sec, const bp_rounding_config* cfg_in,
+                         double* out_values, bp_rounding_outcome* out)
+{
+  std::mt19937_64 rng(seed);
+  return round_impl(p, start_values, cache, rng, deadline_sec, cfg_in, out_values, out);
+}
+
+int bp_propagation_round_rng(bp_problem* p, const double* start_values, const bp_cache* cache,
+                             char* rng_state, int64_t rng_state_bytes, double deadline_sec,
+                             const bp_rounding_config* cfg, double* out_values,
+                             bp_rounding_outcome* out)
+{
+  if (!rng_state || rng_state_bytes <= 0) {
+    bp_set_last_error("null rng state");
+    return BP_ERR_INVALID_ARGUMENT;
+  }
+  std::mt19937_64 rng;
+  {
+    std::istringstream is(std::string(rng_state, strnlen(rng_state, (size_t)rng_state_bytes)));
+    is >> rng;
+    if (!is) {
+      bp_set_last_error("rng state is not a std::mt19937_64 text representation");
+      return BP_ERR_INVALID_ARGUMENT;
+    }
+  }
+  const int rc = round_impl(p, start_values, cache, rng, deadline_sec, cfg, out_values, out);
+  if (rc != BP_OK) return rc;
+  std::ostringstream os;
+  os << rng;
+  const std::string st = os.str();
+  if ((int64_t)st.size() + 1 > rng_state_bytes) {
+    bp_set_last_error("rng state buffer too small (BP_RNG_STATE_BYTES)");
+    return BP_ERR_INVALID_ARGUMENT;
+  }
+  std::memcpy(rng_state, st.c_str(), st.size() + 1);
+  return BP_OK;
+}
+
+int bp_parallel_propagate(bp_problem* p, const double* base2n, int32_t base_infeasible,
+                          const int32_t* vars, int32_t nvars, const double* v0, const double* v1,
+                          const bp_cache* cache, double* out_bounds2n, int32_t* out_infeasible,
+                          int32_t* infeas_count, int32_t* evicted, int32_t* n_evicted,
+                          int32_t* fixed_vars, double* fixed_vals, int32_t* n_fixed)
+{
+  try {
+    if (!p || !base2n || !out_bounds2n || !out_infeasible || !infeas_count || !n_evicted || !n_fixed ||
+        (nvars > 0 && (!vars || !v0 || !v1 || !evicted || !fixed_vars || !fixed_vals)) || nvars < 0)
+      throw std::invalid_argument("null argument");
+    bp::Problem& P           = bp_problem_impl(p);
+    const bp_problem_host& H = bp_problem_hostdata(p);
+    const bp::HostCache* hc  = cache ? bp_cache_host(cache) : nullptr;
+    const int n              = P.n;
+    for (int j = 0; j < nvars; ++j)
+      if (vars[j] < 0 || vars[j] >= n) throw std::out_of_range("var out of range");
+    if (hc && hc->n != n) throw std::invalid_argument("cache does not belong to this problem");
+    std::lock_guard<std::mutex> lk(P.mu);
+    BP_CUDA(cudaSetDevice(P.device));
+    bp::RoundCtx X(P, H);
+    X.ws.upload(reinterpret_cast<const double2*>(base2n), n);
+    X.ws_infeasible = base_infeasible != 0;
+    X.ws_cert       = false;  // an arbitrary base: every probe runs the reference's full first round
+    X.root.alloc(std::max(n, 1));
+    if (hc && n) BP_CUDA(cudaMemcpy(X.root.p, hc->root.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+    const std::vector<int> vv(vars, vars + nvars);
+    for (int q = 0; q < 2; ++q) {
+      const double* val = q ? v1 : v0;
+      const auto pr     = X.run_probe(vv, std::vector<double>(val, val + nvars), hc);
+      if (n)
+        BP_CUDA(cudaMemcpyAsync(out_bounds2n + 2 * (size_t)n * q, P.st.bounds, sizeof(double2) * n,
+                                cudaMemcpyDeviceToHost, X.s));
+      X.sync();
+      out_infeasible[q] = pr.infeasible ? 1 : 0;
+      infeas_count[q]   = pr.infeas_count;
+      n_evicted[q]      = (int32_t)pr.evicted.size();
+      std::copy(pr.evicted.begin(), pr.evicted.end(), evicted + (size_t)nvars * q);
+      n_fixed[q] = (int32_t)pr.fixed.size();
+      for (size_t j = 0; j < pr.fixed.size(); ++j) {
+        fixed_vars[(size_t)nvars * q + j] = pr.fixed[j].first;
+        fixed_vals[(size_t)nvars * q + j] = pr.fixed[j].second;
+      }
+    }
     return BP_OK;
   } catch (const std::invalid_argument& e) {
     bp_set_last_error(e.what());

@@ -94,3 +94,44 @@ def propagation_round(p: ProblemDef, start_values, cache: ProbingCache | None, s
                            bool(o.completed), int(o.repair_attempts), int(o.bulks_committed),
                            int(o.set_count), bool(o.bounds_feasible), int(o.bp_calls),
                            float(o.device_ms))
+
+
+@dataclass
+class ProbeResult:
+    """rounding.hpp:154-159."""
+    bounds: "object"          # BoundsState
+    infeas_count: int
+    evicted: list
+    fixed: list               # [(var, value)]
+
+
+def parallel_propagate(p: ProblemDef, base, vars_, probe_vec_0, probe_vec_1,
+                       cache: ProbingCache | None = None, plan=None):
+    """rounding.hpp:213-224 (both probes of detail::run_probe, :167-207, on the engine). Returns
+    the pair of ProbeResult; the plan argument is accepted for signature parity only."""
+    from .propagation import BoundsState
+    dp = device_problem(p)
+    L = _lib.lib()
+    n, k = p.n_vars, len(vars_)
+    if len(probe_vec_0) != k or len(probe_vec_1) != k:
+        raise ValueError("candidate vector size mismatch")
+    vv = np.ascontiguousarray(vars_, dtype=np.int32)
+    a = np.ascontiguousarray(probe_vec_0, dtype=np.float64)
+    b = np.ascontiguousarray(probe_vec_1, dtype=np.float64)
+    out = np.zeros(max(4 * n, 1))
+    inf, cnt, nev, nfx = (np.zeros(2, dtype=np.int32) for _ in range(4))
+    ev = np.zeros(max(2 * k, 1), dtype=np.int32)
+    fv = np.zeros(max(2 * k, 1), dtype=np.int32)
+    fx = np.zeros(max(2 * k, 1))
+    base_raw = np.ascontiguousarray(base.raw(), dtype=np.float64)
+    _lib.check(L.bp_parallel_propagate(dp.h, _lib.ptr(base_raw), 1 if base.infeasible() else 0,
+                                       _lib.ptr(vv), k, _lib.ptr(a), _lib.ptr(b),
+                                       cache.h if cache is not None else None, _lib.ptr(out),
+                                       _lib.ptr(inf), _lib.ptr(cnt), _lib.ptr(ev), _lib.ptr(nev),
+                                       _lib.ptr(fv), _lib.ptr(fx), _lib.ptr(nfx)))
+    res = []
+    for q in range(2):
+        bs = BoundsState(raw=out[2 * n * q: 2 * n * (q + 1)], infeasible=bool(inf[q]))
+        res.append(ProbeResult(bs, int(cnt[q]), ev[k * q: k * q + nev[q]].tolist(),
+                               [(int(fv[k * q + j]), float(fx[k * q + j])) for j in range(nfx[q])]))
+    return res

@@ -1,0 +1,334 @@
+// TEST INFRASTRUCTURE — the C++ drop-in (include/pulse_gpu.hpp) against the UNMODIFIED reference,
+// side by side in one process: every pulse:: hot-path function is called on the CPU (reference
+// headers from /root/reference, compiled in place by oracle/Makefile) and through pulse::gpu:: on
+// the B200 engine, on the reference's own instance streams (tests/testkit.hpp:69 random_instance,
+// seeds of acceptance.cpp:40 / :89 and test_rounding.cpp), plus larger mixed instances with heavy
+// rows. Everything is compared bit for bit. One PASS/FAIL line per criterion, like acceptance.cpp;
+// exit status = number of failures.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "pulse_gpu.hpp"
+#include "testkit.hpp"
+
+using namespace pulse;
+namespace pg = pulse::gpu;
+
+namespace {
+
+int g_failures = 0;
+
+void report(const std::string& name, bool pass, const std::string& detail)
+{
+  std::printf("%s  %s (%s)\n", pass ? "PASS" : "FAIL", name.c_str(), detail.c_str());
+  std::fflush(stdout);
+  if (!pass) ++g_failures;
+}
+
+bool same_bits(const std::vector<double>& a, const std::vector<double>& b)
+{
+  return a.size() == b.size() && (a.empty() || std::memcmp(a.data(), b.data(), 8 * a.size()) == 0);
+}
+
+bool same_state(const BoundsState& a, const BoundsState& b)
+{
+  return a.infeasible() == b.infeasible() && same_bits(a.raw(), b.raw());
+}
+
+bool same_result(const PropagationResult& a, const PropagationResult& b)
+{
+  return a.status == b.status && a.rounds == b.rounds && a.crossed_vars == b.crossed_vars;
+}
+
+bool same_branch(const ProbeBranch& a, const ProbeBranch& b)
+{
+  if (a.feasible != b.feasible || a.deltas.size() != b.deltas.size()) return false;
+  if (std::memcmp(&a.branch_lower, &b.branch_lower, 8) || std::memcmp(&a.branch_upper, &b.branch_upper, 8))
+    return false;
+  for (size_t d = 0; d < a.deltas.size(); ++d) {
+    if (a.deltas[d].var != b.deltas[d].var) return false;
+    if (std::memcmp(&a.deltas[d].new_lower, &b.deltas[d].new_lower, 8)) return false;
+    if (std::memcmp(&a.deltas[d].new_upper, &b.deltas[d].new_upper, 8)) return false;
+  }
+  return true;
+}
+
+bool same_entry(const ProbeEntry& a, const ProbeEntry& b)
+{
+  return a.var == b.var && a.kind == b.kind && a.forces_down == b.forces_down &&
+         a.forces_up == b.forces_up && same_branch(a.down, b.down) && same_branch(a.up, b.up);
+}
+
+bool same_cache(const ProbingCache& a, const ProbingCache& b)
+{
+  if (a.entries.size() != b.entries.size() || a.n_probed != b.n_probed ||
+      a.n_infeasible_branches != b.n_infeasible_branches || !same_state(a.root, b.root))
+    return false;
+  for (size_t v = 0; v < a.entries.size(); ++v) {
+    if (a.entries[v].has_value() != b.entries[v].has_value()) return false;
+    if (a.entries[v] && !same_entry(*a.entries[v], *b.entries[v])) return false;
+  }
+  return true;
+}
+
+// Mixed instance with fractional data (binary / integer / continuous, one- and two-sided rows) and
+// optionally a few rows longer than kSumSegment, so activities take the 16384-segment tree.
+ProblemDef mixed_instance(uint64_t seed, int n, int m, int heavy_rows, int heavy_len)
+{
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  ProblemBuilder b;
+  std::vector<double> pt(n);
+  std::vector<int> kind(n);
+  for (int i = 0; i < n; ++i) {
+    const double r = U(rng);
+    kind[i]        = r < 0.5 ? 0 : (r < 0.8 ? 1 : 2);
+    const double up = kind[i] == 0 ? 1.0 : (kind[i] == 1 ? 10.0 : 1.0 + 99.0 * U(rng));
+    b.add_var("x" + std::to_string(i), 0.0, up, kind[i] != 2, 0.0);
+    pt[i] = kind[i] == 2 ? up * U(rng) : std::floor((up + 1.0) * U(rng));
+    if (pt[i] > up) pt[i] = up;
+  }
+  for (int k = 0; k < m; ++k) {
+    const int len = k < heavy_rows ? heavy_len : 2 + (int)(10 * U(rng));
+    std::vector<std::pair<int, double>> ent;
+    double lhs = 0.0;
+    for (int j = 0; j < len; ++j) {
+      const int c  = (int)(n * U(rng)) % n;
+      double a     = kind[c] == 2 ? 0.1 + 9.9 * U(rng) : 1.0 + std::floor(9.0 * U(rng));
+      if (U(rng) < 0.5) a = -a;
+      ent.push_back({c, a});
+      lhs += a * pt[c];
+    }
+    const double r  = U(rng);
+    const double lo = r < 0.7 ? -kInf : lhs - 3.0 * U(rng);
+    const double up = r < 0.7 || r > 0.9 ? lhs + 3.0 * U(rng) : kInf;
+    b.add_row("c" + std::to_string(k), lo, up);
+    for (auto& [c, a] : ent) b.add_entry(k, c, a);
+  }
+  return b.build();
+}
+
+// ---------------------------------------------------------------- criteria
+
+void propagation_stream()
+{
+  std::mt19937_64 rng(20240501);  // acceptance.cpp:40
+  int bad = 0, acts_bad = 0, tight_bad = 0;
+  for (int t = 0; t < 1000; ++t) {
+    const ProblemDef p = testkit::random_instance(rng);
+    for (int inc = 0; inc < 2; ++inc) {
+      PropagationLimits lim;
+      lim.incremental = inc == 1;
+      BoundsState a(p), g(p);
+      const auto ra = propagate(p, a, lim);
+      const auto rg = pg::propagate(p, g, lim);
+      if (!same_result(ra, rg) || !same_state(a, g)) ++bad;
+    }
+    // one activity + tightening sweep, full and over a subset
+    BoundsState a(p), g(p);
+    ActivityState aa, ga;
+    compute_activities(p, a, nullptr, aa);
+    pg::compute_activities(p, g, nullptr, ga);
+    if (!same_bits(aa.act, ga.act) || aa.n_inf_min != ga.n_inf_min || aa.n_inf_max != ga.n_inf_max) ++acts_bad;
+    int ca = 0, cg = 0;
+    const auto cha = tighten_bounds(p, a, aa, nullptr, {}, &ca);
+    const auto chg = pg::tighten_bounds(p, g, ga, nullptr, {}, &cg);
+    if (cha != chg || ca != cg || !same_state(a, g)) ++tight_bad;
+    std::vector<int> rows, vars;
+    for (int k = 0; k < p.n_cons; k += 2) rows.push_back(k);
+    for (int i = 1; i < p.n_vars; i += 2) vars.push_back(i);
+    compute_activities(p, a, &rows, aa);
+    pg::compute_activities(p, g, &rows, ga);
+    if (!same_bits(aa.act, ga.act) || aa.n_inf_min != ga.n_inf_min) ++acts_bad;
+    const auto sa = tighten_bounds(p, a, aa, &vars, {}, &ca);
+    const auto sg = pg::tighten_bounds(p, g, ga, &vars, {}, &cg);
+    if (sa != sg || ca != cg || !same_state(a, g)) ++tight_bad;
+  }
+  report("propagate / compute_activities / tighten_bounds on the acceptance stream",
+         bad == 0 && acts_bad == 0 && tight_bad == 0,
+         "1000 instances x {incremental, full}: " + std::to_string(bad) + " propagate, " +
+             std::to_string(acts_bad) + " activity, " + std::to_string(tight_bad) + " tightening mismatches");
+}
+
+void propagation_mixed()
+{
+  int bad = 0, runs = 0;
+  for (uint64_t s = 0; s < 24; ++s) {
+    const bool heavy   = s % 4 == 3;
+    const ProblemDef p = mixed_instance(1000 + s, 3000, 3000, heavy ? 3 : 0, 20000);
+    for (double thr : {1e-7, 0.0}) {
+      PropagationLimits lim;
+      lim.abs_threshold = thr;
+      lim.rel_threshold = thr == 0.0 ? 0.0 : 1e-4;
+      BoundsState a(p), g(p);
+      const auto ra = propagate(p, a, lim);
+      const auto rg = pg::propagate(p, g, lim);
+      ++runs;
+      if (!same_result(ra, rg) || !same_state(a, g)) ++bad;
+    }
+  }
+  report("propagate on mixed fractional instances (incl. rows > 16384 nnz)", bad == 0,
+         std::to_string(runs) + " runs, " + std::to_string(bad) + " mismatches");
+}
+
+void probing_stream()
+{
+  std::mt19937_64 rng(7771);  // acceptance.cpp:89
+  int bad_cache = 0, bad_probe = 0, bad_prio = 0;
+  for (int t = 0; t < 200; ++t) {
+    const ProblemDef p = testkit::random_instance(rng);
+    const auto ca      = build_cache(p, 1e9);
+    const auto cg      = pg::build_cache(p, 1e9);
+    if (!same_cache(ca, cg)) ++bad_cache;
+    if (prioritize_probe_vars(p) != pg::prioritize_probe_vars(p)) ++bad_prio;
+    BoundsState root(p);
+    propagate(p, root);  // a propagated root too (certified-fixpoint path of the batched kernel)
+    if (root.infeasible()) continue;
+    for (int v = 0; v < p.n_vars; ++v)
+      if (!same_entry(probe_variable(p, root, v), pg::probe_variable(p, root, v))) ++bad_probe;
+  }
+  report("build_cache / probe_variable / prioritize_probe_vars on the probing stream",
+         bad_cache == 0 && bad_probe == 0 && bad_prio == 0,
+         "200 instances: " + std::to_string(bad_cache) + " cache, " + std::to_string(bad_probe) +
+             " entry, " + std::to_string(bad_prio) + " priority mismatches");
+}
+
+void warm_start_and_pairs()
+{
+  std::mt19937_64 rng(4242);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  int bad_ws = 0, bad_pp = 0, cases = 0;
+  for (int t = 0; t < 150; ++t) {
+    const ProblemDef p = testkit::random_instance(rng);
+    const auto cache   = build_cache(p, 1e9);
+    const WorkPlan plan = build_work_plan(p);
+    std::vector<int> vars;
+    std::vector<double> v0, v1;
+    std::vector<std::pair<int, double>> asg;
+    for (int i = 0; i < p.n_vars; ++i) {
+      if (U(rng) < 0.4) continue;
+      const double lo = p.var_lower[i], up = p.var_upper[i];
+      const double a = std::floor(lo + (up - lo + 1) * U(rng)), b = std::floor(lo + (up - lo + 1) * U(rng));
+      vars.push_back(i);
+      v0.push_back(std::min(a, up));
+      v1.push_back(std::min(b, up));
+      asg.push_back({i, v0.back()});
+    }
+    const auto wa = assemble_bulk_warm_start(cache, asg);
+    const auto wg = pg::assemble_bulk_warm_start(cache, asg);
+    if (!same_state(wa.bounds, wg.bounds) || wa.conflicts != wg.conflicts || wa.evicted != wg.evicted) ++bad_ws;
+    BoundsState base(p);
+    for (int use_cache = 0; use_cache < 2; ++use_cache) {
+      const ProbingCache* c = use_cache ? &cache : nullptr;
+      const auto ra = parallel_propagate(p, base, vars, v0, v1, c, plan);
+      const auto rg = pg::parallel_propagate(p, base, vars, v0, v1, c, plan);
+      ++cases;
+      for (int q = 0; q < 2; ++q) {
+        const auto& x = ra.probe[q];
+        const auto& y = rg.probe[q];
+        if (!same_state(x.bounds, y.bounds) || x.infeas_count != y.infeas_count || x.evicted != y.evicted ||
+            x.fixed != y.fixed)
+          ++bad_pp;
+      }
+    }
+  }
+  report("assemble_bulk_warm_start / parallel_propagate", bad_ws == 0 && bad_pp == 0,
+         std::to_string(cases) + " paired probes: " + std::to_string(bad_ws) + " warm-start, " +
+             std::to_string(bad_pp) + " probe mismatches");
+}
+
+void rounding_stream()
+{
+  std::mt19937_64 gen(99);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  int bad = 0, runs = 0;
+  for (int t = 0; t < 200; ++t) {
+    testkit::RandomInstanceOptions opt;
+    opt.force_feasible = t % 2 == 0;
+    const ProblemDef p = testkit::random_instance(gen, opt);
+    SolutionVector s;
+    for (int i = 0; i < p.n_vars; ++i) s.values.push_back(p.var_lower[i] + (p.var_upper[i] - p.var_lower[i]) * U(gen));
+    const auto cache = build_cache(p, 1e9);
+    for (int use_cache = 0; use_cache < 2; ++use_cache) {
+      Rng ra(1000 + t), rg(1000 + t);
+      const ProbingCache* c = use_cache ? &cache : nullptr;
+      const auto oa = propagation_round(p, s, c, Deadline::never(), ra);
+      const auto og = pg::propagation_round(p, s, c, Deadline::never(), rg);
+      ++runs;
+      const bool same = oa.rounding_infeasible == og.rounding_infeasible && oa.timed_out == og.timed_out &&
+                        oa.completed == og.completed && oa.bulks_committed == og.bulks_committed &&
+                        oa.set_count == og.set_count && same_bits(oa.point.values, og.point.values) &&
+                        ra == rg;  // the caller's generator advanced identically
+      if (!same) ++bad;
+    }
+  }
+  report("propagation_round (with and without cache; caller Rng state)", bad == 0,
+         std::to_string(runs) + " runs, " + std::to_string(bad) + " mismatches");
+}
+
+void rounding_mixed()
+{
+  int bad = 0, runs = 0;
+  for (uint64_t s = 0; s < 4; ++s) {
+    const ProblemDef p = mixed_instance(500 + s, 2000, 1500, 0, 0);
+    std::mt19937_64 g(s);
+    std::uniform_real_distribution<double> U(0.0, 1.0);
+    SolutionVector sv;
+    for (int i = 0; i < p.n_vars; ++i) sv.values.push_back(p.var_upper[i] * U(g));
+    const auto cache = pg::build_cache(p, 1e9);
+    Rng ra(s), rg(s);
+    const auto oa = propagation_round(p, sv, &cache, Deadline::never(), ra);
+    const auto og = pg::propagation_round(p, sv, &cache, Deadline::never(), rg);
+    ++runs;
+    // continuous values come from the reference's own lp_polish (PDHG, wall-clock budgeted):
+    // compare integer variables bitwise, plus every flag and counter
+    bool same = oa.rounding_infeasible == og.rounding_infeasible && oa.completed == og.completed &&
+                oa.bulks_committed == og.bulks_committed && oa.set_count == og.set_count && ra == rg;
+    for (int i = 0; i < p.n_vars && same; ++i)
+      if (p.is_integer[i] && std::memcmp(&oa.point.values[i], &og.point.values[i], 8)) same = false;
+    if (!same) ++bad;
+  }
+  report("propagation_round on mixed 2000-var instances with a GPU-built cache", bad == 0,
+         std::to_string(runs) + " runs, " + std::to_string(bad) + " mismatches");
+}
+
+void errors()
+{
+  const ProblemDef p = testkit::tiny_knapsack();
+  BoundsState b(p);
+  bool oor = false;
+  try {
+    pg::probe_variable(p, b, 7);
+  } catch (const std::out_of_range&) {
+    oor = true;
+  }
+  BoundsState inf(p);
+  inf.mark_infeasible();
+  const auto r = pg::propagate(p, inf);
+  report("error taxonomy and infeasible short-circuit",
+         oor && r.status == PropagationStatus::Infeasible && r.rounds == 0, "out_of_range, Infeasible/0 rounds");
+}
+
+}  // namespace
+
+int main()
+{
+  int32_t ndev = 0;
+  if (bp_device_count(&ndev) != BP_OK || ndev == 0) {
+    std::printf("FAIL  no CUDA device (%s)\n", bp_last_error());
+    return 1;
+  }
+  errors();
+  propagation_stream();
+  propagation_mixed();
+  probing_stream();
+  warm_start_and_pairs();
+  rounding_stream();
+  rounding_mixed();
+  std::printf("%d failure(s)\n", g_failures);
+  return g_failures;
+}

@@ -86,3 +86,55 @@ def test_mixed_instance_rounding(oracle_built):
     start = p.var_lower + rng.random(p.n_vars) * (p.var_upper - p.var_lower)
     for use_cache in (False, True):
         _compare(rp, p, start, 11, use_cache, f"C1-3000 cache={use_cache}")
+
+
+def _ref_parallel_propagate(rp, n, base, vars_, v0, v1, cache):
+    """pulse::parallel_propagate through oracle/_ref (ref_shim.cpp ref_parallel_propagate)."""
+    import ctypes as C
+
+    from oracle.bind import Ref
+    k = len(vars_)
+    ob = [np.zeros(max(2 * n, 1)) for _ in range(2)]
+    info = np.zeros(8, np.int32)
+    ev = [np.zeros(max(k, 1), np.int32) for _ in range(2)]
+    fv = [np.zeros(max(k, 1), np.int32) for _ in range(2)]
+    fx = [np.zeros(max(k, 1)) for _ in range(2)]
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    Ref.lib().ref_parallel_propagate(rp.h, P(base), 0, P(np.asarray(vars_, np.int32)), k,
+                                     P(np.asarray(v0, float)), P(np.asarray(v1, float)),
+                                     None if cache is None else cache.h, P(ob[0]), P(ob[1]), P(info),
+                                     P(ev[0]), P(ev[1]), P(fv[0]), P(fx[0]), P(fv[1]), P(fx[1]))
+    out = []
+    for q in range(2):
+        inf, cnt, nev, nfx = (int(x) for x in info[4 * q: 4 * q + 4])
+        out.append((ob[q][: 2 * n], bool(inf), cnt, ev[q][:nev].tolist(),
+                    [(int(fv[q][j]), float(fx[q][j])) for j in range(nfx)]))
+    return out
+
+
+def test_parallel_propagate_matches_reference(oracle_built):
+    """rounding.hpp:213-224 (test_rounding.cpp:144-176): both probes, with and without a cache,
+    bounds / infeasibility / infeas_count / evicted / fixed identical (bounds bitwise)."""
+    from oracle.bind import RefCache, RefRng
+
+    from paper_2510_20499_b200 import BoundsState
+    from paper_2510_20499_b200.rounding import parallel_propagate
+    rng = RefRng(4242)
+    gen = np.random.default_rng(5)
+    for t in range(120):
+        rp = rng.random_instance()
+        p = rp.to_def()
+        vars_ = [i for i in range(p.n_vars) if gen.random() < 0.6]
+        lo, up = p.var_lower[vars_], p.var_upper[vars_]
+        v0 = np.minimum(np.floor(lo + (up - lo + 1) * gen.random(len(vars_))), up)
+        v1 = np.minimum(np.floor(lo + (up - lo + 1) * gen.random(len(vars_))), up)
+        gc, rc = build_cache(p, 1e9), RefCache.build(rp)
+        for use_cache in (False, True):
+            g = parallel_propagate(p, BoundsState(p), vars_, v0, v1, gc if use_cache else None)
+            r = _ref_parallel_propagate(rp, p.n_vars, p.root_bounds(), vars_, v0, v1,
+                                        rc if use_cache else None)
+            for q in range(2):
+                rb, rinf, rcnt, rev, rfx = r[q]
+                assert np.array_equal(g[q].bounds.raw().view(np.uint64), rb.view(np.uint64)), (t, q)
+                assert (g[q].bounds.infeasible(), g[q].infeas_count, g[q].evicted, g[q].fixed) == \
+                    (rinf, rcnt, rev, rfx), (t, q, use_cache)
