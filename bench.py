@@ -33,6 +33,14 @@ sys.path.insert(0, str(ROOT))
 HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    """Progress on stderr (the JSON line is the only stdout output)."""
+    print(f"[bench {time.perf_counter() - _T0:8.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -212,6 +220,7 @@ def run_probing(args, rank, world, local):
     from paper_2510_20499_b200.distributed import build_cache_sharded
     from paper_2510_20499_b200.probing import probe_variables
 
+    log("probing: generating C3")
     p = synth.c3()
     vars_ = list(range(200_000))  # the binaries (every one is probed: order is immaterial)
     probe_variables(p, None, vars_[:2000])  # warm-up: kernels loaded, problem uploaded
@@ -271,8 +280,10 @@ def run_rounding(args, rank, world, local):
     r0 = propagate(p0, b)
     p = synth.with_bounds(p0, b.raw())
     t0 = time.perf_counter()
+    log(f"rounding: C4 presolved in {r0.rounds} rounds; building cache")
     cache = build_cache(p, 1e9)
     cache_s = _max_over_ranks(time.perf_counter() - t0, world)
+    log(f"rounding: cache {cache.n_probed} vars in {cache_s:.1f} s")
     t0 = time.perf_counter()
     out = propagation_round(p, start, cache, seed=4 + rank)
     el = _max_over_ranks(time.perf_counter() - t0, world)
@@ -331,7 +342,9 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    log(f"generating {args.workload}")
     p, desc = make_workload(args.workload)
+    log(f"generated n={p.n_vars} m={p.n_cons} nnz={p.nnz()}; uploading")
     dp = device_problem(p, device=local)
     n, m, N = p.n_vars, p.n_cons, p.nnz()
     stream = torch.cuda.current_stream()
@@ -345,6 +358,7 @@ def main():
     r_stats, _ = propagate_device(p, d_work.data_ptr(), False, None, sptr, FORCE_FRONTIER,
                                   d_stats.data_ptr())
     stats = metrics.trim(d_stats.cpu().numpy(), r_stats.rounds)
+    log(f"stats pass done: rounds={r_stats.rounds}")
     ref_bits = d_work.cpu().numpy().view(np.uint64).copy()
     visits = metrics.nnz_visits(stats)
     alg_bytes = metrics.algorithmic_bytes(stats, n, m)
@@ -396,6 +410,7 @@ def main():
         dist.all_reduce(kt, op=dist.ReduceOp.MAX)
         kern_ms = float(kt.item())
 
+    log(f"timed region done: {ms / args.steps:.3f} ms/step")
     # 2) e2e: host (pinned) bounds through the C-ABI call bp_propagate, H2D + D2H every step
     host_root = p.root_bounds()
     pinned = torch.empty(host_root.size, dtype=torch.float64).pin_memory()
@@ -417,8 +432,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    log("e2e done")
     probing = None if args.no_probing else run_probing(args, rank, world, local)
+    log("probing done")
     rounding = None if args.no_rounding else run_rounding(args, rank, world, local)
+    log("rounding done")
 
     if rank == 0:
         peak, peak_kind = peaks()
