@@ -280,13 +280,14 @@ def run_rounding(args, rank, world, local):
     r0 = propagate(p0, b)
     p = synth.with_bounds(p0, b.raw())
     t0 = time.perf_counter()
-    log(f"rounding: C4 presolved in {r0.rounds} rounds; building cache")
-    cache = build_cache(p, 1e9)
+    log(f"rounding: C4 presolved in {r0.rounds} rounds; building cache ({args.cache_budget:g} s budget)")
+    cache = build_cache(p, args.cache_budget)  # fp.hpp:263 with probing_budget_sec (fp.hpp:37)
     cache_s = _max_over_ranks(time.perf_counter() - t0, world)
     log(f"rounding: cache {cache.n_probed} vars in {cache_s:.1f} s")
     t0 = time.perf_counter()
     out = propagation_round(p, start, cache, seed=4 + rank)
     el = _max_over_ranks(time.perf_counter() - t0, world)
+    log(f"rounding: {out.bulks_committed} bulks, {out.bp_calls} BP calls in {el:.1f} s")
     if rank != 0:
         return None
     res = {"workload": "C4: knapsack/assignment 2M x 2M (N=%d), presolved root (%d BP rounds)"
@@ -312,6 +313,96 @@ def run_rounding(args, rank, world, local):
     return res
 
 
+def run_batch(args, rank, world, local):
+    """configs[4]: 64 heterogeneous MIPLIB-shaped instances (10k-5M nnz), LPT-partitioned by size
+    over the ranks; each rank uploads its instances and propagates them one after another on its
+    GPU (device-resident bounds), one full `propagate` each. value = Σ reference-trajectory nnz
+    visits of all instances / max-over-ranks device time."""
+    import torch
+
+    from paper_2510_20499_b200 import metrics, synth
+    from paper_2510_20499_b200.propagation import FORCE_FRONTIER, device_problem, propagate_device
+
+    specs = synth.c5_specs(count=args.c5_count)
+    mine = synth.lpt_partition([sp[1] for sp in specs], world)[rank]
+    log(f"batch: building {len(mine)} of {len(specs)} C5 instances")
+    insts = []
+    for j in mine:
+        p = synth.c5_instance(specs[j])
+        device_problem(p, device=local)
+        insts.append(p)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    work = []
+    visits = 0
+    for p in insts:
+        root = torch.from_numpy(p.root_bounds()).cuda()
+        w = torch.empty_like(root)
+        st = torch.zeros(64 * metrics.STAT_COLS, dtype=torch.int64, device="cuda")
+        w.copy_(root)
+        r, _ = propagate_device(p, w.data_ptr(), False, None, sptr, FORCE_FRONTIER, st.data_ptr())
+        v = metrics.nnz_visits(metrics.trim(st.cpu().numpy(), r.rounds))
+        visits += v
+        work.append((p, root, w, v))
+    log(f"batch: stats pass done, {visits} nnz visits")
+
+    def sweep():
+        for p, root, w, _ in work:
+            w.copy_(root)
+            propagate_device(p, w.data_ptr(), False, None, sptr)
+
+    sweep()  # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.c5_reps):
+        sweep()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(e0.elapsed_time(e1) / args.c5_reps, world)
+    tot_visits = _sum_over_ranks(visits, world)
+    tot_nnz = int(_sum_over_ranks(sum(p.nnz() for p in insts), world))
+    if rank != 0:
+        return None
+    out = {"workload": f"C5: {len(specs)} heterogeneous instances (C1-C4 generators, nnz log-uniform "
+                       f"10k-5M), total nnz {tot_nnz}", "nnz_visits_per_s": tot_visits / (ms * 1e-3),
+           "ms_per_sweep": ms, "nnz_visits_per_sweep": tot_visits, "n_gpus": world,
+           "parallelism": f"LPT instance partition x{world}, no collective"}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.bind import Ref, RefProblem, ref_propagate
+        if Ref.available():
+            done, v_cpu, el = 0, 0, 0.0
+            for p, _, _, v in sorted(work, key=lambda x: x[0].nnz()):
+                if el > args.cpu_sample_sec / 2:  # bounded sample: smallest instances first
+                    break
+                rp = RefProblem.from_def(p)
+                root = p.root_bounds()
+                t1 = time.perf_counter()
+                ref_propagate(rp, root)
+                el += time.perf_counter() - t1
+                v_cpu += v
+                done += 1
+                del rp
+            out["cpu_baseline"] = {"value": v_cpu / el, "unit": "nnz/s", "cores": int(Ref.lib().ref_max_threads()),
+                                   "kind": "reference", "sample": f"reference propagate on {done} of "
+                                                                  f"{len(work)} instances ({el:.1f} s)"}
+    return out
+
+
+def _sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -324,6 +415,11 @@ def main():
     ap.add_argument("--no-probing", action="store_true")
     ap.add_argument("--no-rounding", action="store_true")
     ap.add_argument("--cpu-sample-sec", type=float, default=20.0)
+    ap.add_argument("--no-batch", action="store_true")
+    ap.add_argument("--cache-budget", type=float, default=5.0,
+                    help="C4 probing-cache time budget (the reference FP's probing_budget_sec)")
+    ap.add_argument("--c5-count", type=int, default=64)
+    ap.add_argument("--c5-reps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -437,6 +533,8 @@ def main():
     log("probing done")
     rounding = None if args.no_rounding else run_rounding(args, rank, world, local)
     log("rounding done")
+    batch = None if args.no_batch else run_batch(args, rank, world, local)
+    log("batch done")
 
     if rank == 0:
         peak, peak_kind = peaks()
@@ -481,6 +579,7 @@ def main():
             "clocks": clocks,
             "probing": probing,
             "rounding": rounding,
+            "batch": batch,
         }
         print(json.dumps(line))
     if world > 1:

@@ -166,6 +166,41 @@ __device__ __forceinline__ void cand_explicit(double lo, double up, bool integer
   }
 }
 
+// Candidate gating. An entry (a, lo, up) of a row can only publish a candidate
+// from side g (cons upper, min activity) if the row's slack g - act_min is below |a|·(width + 1
+// for integers): its exact candidate is lo + slack/a (a > 0) or up - slack/|a| (a < 0), and the
+// computed one differs from it by at most 5u(|a·x| + |act| + |g|)/|a|. So when
+//   slack >= tw·(1 + 1e-12) + 1e-12·(|g| + |act| + pm),  tw = |a|(w + int), pm = |a|max(|lo|,|up|)
+// the computed candidate is provably not strictly improving (for integers: floor/ceil land at or
+// beyond the bound), i.e. cand_explicit would publish nothing from that side. The same holds for
+// side h with slack act_max - h. Gating only skips work whose outcome is known: results are
+// bit-identical with or without it.
+__device__ __forceinline__ void entry_reach(double a, double lo, double up, bool integer, double& tw,
+                                            double& pm)
+{
+  const double aa = fabs(a);
+  const double w  = __dsub_rn(up, lo);  // +inf when either bound is infinite
+  tw              = __dmul_rn(aa, integer ? __dadd_rn(w, 1.0) : w);
+  pm              = __dmul_rn(aa, fmax(fabs(lo), fabs(up)));
+}
+
+// Side with slack `slack` (finite rhs, no infinite contributor) cannot yield a candidate for an
+// entry of reach (tw, pm).
+__device__ __forceinline__ bool side_quiet(double slack, double tw, double pm, double rhs, double act)
+{
+  const double margin = __dmul_rn(1e-12, __dadd_rn(__dadd_rn(fabs(rhs), fabs(act)), pm));
+  return slack >= __dadd_rn(__dmul_rn(tw, 1.0 + 1e-12), margin) + 1e-300;
+}
+
+// True when neither side of the row can give this entry a candidate (see entry_reach).
+__device__ __forceinline__ bool entry_quiet(double tw, double pm, double mnf, int nmn, double mxf,
+                                            int nmx, double g, double h)
+{
+  const bool qg = !isfinite(g) || nmn >= 2 || (nmn == 0 && side_quiet(__dsub_rn(g, mnf), tw, pm, g, mnf));
+  const bool qh = !isfinite(h) || nmx >= 2 || (nmx == 0 && side_quiet(__dsub_rn(mxf, h), tw, pm, h, mxf));
+  return qg && qh;
+}
+
 // Decodes a row record (+ its aux finite parts when boxed).
 __device__ __forceinline__ void decode_rec(const RowRec& r, const double2* aux, int k, double& mnf,
                                            int& nmn, double& mxf, int& nmx)
@@ -188,6 +223,9 @@ __device__ __forceinline__ void fold_entry(Fold& f, double lo, double up, bool i
   double mnf, mxf, cl, cu;
   int nmn, nmx;
   decode_rec(r, aux, k, mnf, nmn, mxf, nmx);
+  double tw, pm;
+  entry_reach(a, lo, up, integer, tw, pm);
+  if (entry_quiet(tw, pm, mnf, nmn, mxf, nmx, r.g, r.h)) return;
   cand_explicit(lo, up, integer, a, mnf, nmn, mxf, nmx, r.g, r.h, cl, cu);
   if (cu < f.up) { f.up = cu; f.up_pos = pos; }
   if (f.lo < cl) { f.lo = cl; f.lo_pos = pos; }
@@ -201,6 +239,13 @@ __device__ __forceinline__ void entry_candidates(double lo, double up, bool inte
   double mnf, mxf;
   int nmn, nmx;
   decode_rec(r, aux, k, mnf, nmn, mxf, nmx);
+  double tw, pm;
+  entry_reach(a, lo, up, integer, tw, pm);
+  if (entry_quiet(tw, pm, mnf, nmn, mxf, nmx, r.g, r.h)) {
+    cl = -INFINITY;
+    cu = INFINITY;
+    return;
+  }
   cand_explicit(lo, up, integer, a, mnf, nmn, mxf, nmx, r.g, r.h, cl, cu);
 }
 
@@ -307,8 +352,8 @@ constexpr int kCandSplit = 2048;  // long rows above: candidates by parallel pie
 
 struct SegPart {
   double min, max;
+  double tmax, pmax;  // row-level candidate gating: max |a|(w + 1), max |a|max(|lo|,|up|)
   int nmin, nmax;
-  int pad0, pad1;
 };
 
 }  // namespace bp

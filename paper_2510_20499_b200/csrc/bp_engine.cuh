@@ -79,6 +79,7 @@ struct DevState {
   double2* gbuf;      // gathered bounds of long rows' entries (DevProblem::long_off)
   CandSlot* slot;     // fused full round: per-var candidate slots
   unsigned* ready;    // per row: stamp of the round whose activity is published
+  unsigned char* rquiet;  // per row: 1 if no entry can publish a candidate (set before `ready`)
   SegPart* seg_part;
   int* seg_done;
   unsigned* row_stamp;
@@ -128,6 +129,7 @@ struct Problem {
   DBuf<double2> gbuf;
   DBuf<CandSlot> slot;
   DBuf<unsigned> ready;
+  DBuf<unsigned char> rquiet;
   DBuf<SegPart> seg_part;
   DBuf<int> seg_done;
   DBuf<unsigned> row_stamp, var_stamp;

@@ -264,6 +264,9 @@ __device__ void long_candidates(Ctx& c, int k, int e0, int e1, double mnf, int n
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
       if (ci[h] == -1) continue;
+      double tw, pm;
+      entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pm);
+      if (entry_quiet(tw, pm, mnf, nmn, mxf, nmx, g, hh)) continue;
       double cl, cu;
       cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], mnf, nmn, mxf, nmx, g, hh, cl, cu);
       publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
@@ -319,6 +322,7 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   }
   double acc = 0.0;
   int imn = 0, imx = 0;
+  double gtw = 0.0, gpm = 0.0;  // row-level gating maxima (integrality unknown here: +1 for all)
   const unsigned lt = lanemask_lt();
   for (int base = e0; base < e1; base += kFoldChunk) {
     // order-preserving compaction of the non-zero contributions of each chain
@@ -331,6 +335,12 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
         contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
         imn += i1;
         imx += i2;
+        if (cand) {
+          double tw, pw;
+          entry_reach(a[h], bd[h].x, bd[h].y, true, tw, pw);
+          gtw = fmax(gtw, tw);
+          gpm = fmax(gpm, pw);
+        }
       }
       const unsigned m = __ballot_sync(FULL, cm != 0.0);
       const unsigned x = __ballot_sync(FULL, cx != 0.0);
@@ -352,6 +362,13 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   }
   imn            = warp_sum(imn);
   imx            = warp_sum(imx);
+  if (cand) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      gtw = fmax(gtw, __shfl_xor_sync(FULL, gtw, o));
+      gpm = fmax(gpm, __shfl_xor_sync(FULL, gpm, o));
+    }
+  }
   double smn     = __shfl_sync(FULL, acc, 0);
   double smx     = __shfl_sync(FULL, acc, 1);
   const int nseg = (L + kSumSegment - 1) / kSumSegment;
@@ -366,7 +383,8 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
       sp.max  = smx;
       sp.nmin = imn;
       sp.nmax = imx;
-      sp.pad0 = sp.pad1 = 0;
+      sp.tmax = gtw;
+      sp.pmax = gpm;
       S.seg_part[base + seg] = sp;
       __threadfence();
       const int done = atomicAdd(&S.seg_done[k], 1);
@@ -380,6 +398,8 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
           tmx = __dadd_rn(tmx, __ldcg(&sq->max));
           cmn += __ldcg(&sq->nmin);
           cmx += __ldcg(&sq->nmax);
+          gtw = fmax(gtw, __ldcg(&sq->tmax));
+          gpm = fmax(gpm, __ldcg(&sq->pmax));
         }
         smn           = tmn;
         smx           = tmx;
@@ -394,18 +414,24 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
     smx       = __shfl_sync(FULL, smx, 0);
     imn       = __shfl_sync(FULL, imn, 0);
     imx       = __shfl_sync(FULL, imx, 0);
+    gtw       = __shfl_sync(FULL, gtw, 0);
+    gpm       = __shfl_sync(FULL, gpm, 0);
   }
   if (!final_row) return;
   if (lane == 0) write_rec(P, S, k, smn, smx, imn, imx);
   if (!cand) return;
+  const double2 cb = __ldg(&P.cons[k]);
+  // row-level gating: no entry of the row can publish a candidate -> skip the candidate pass
+  const bool quiet = entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x);
   if (L > kCandSplit) {
     if (lane == 0) {
+      S.rquiet[k] = quiet ? 1 : 0;
       __threadfence();
       atomicExch(S.ready + k, stamp);
     }
     return;
   }
-  const double2 cb = __ldg(&P.cons[k]);
+  if (quiet) return;
   long_candidates(c, k, 0, L, smn, imn, smx, imx, cb.y, cb.x);
 }
 
@@ -418,6 +444,7 @@ __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp)
     while (ldv(S.ready + k) != stamp) __nanosleep(200);
   __syncwarp();
   __threadfence();
+  if (*(const volatile unsigned char*)(S.rquiet + k)) return;  // the whole row is quiet
   const RowRec r = ld_rec_cg(S.rec + k);
   double mnf = r.min, mxf = r.max;
   const int nmn = is_box(r.min) ? box_value(r.min) : 0;
@@ -502,6 +529,11 @@ __device__ void short_tile(Ctx& c, int t, bool cand)
       if (ci[h] == -1) continue;
       const int o       = own[h];
       const double2 rcb = c.w.vb[o];
+      double tw, pm;
+      entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pm);
+      if (entry_quiet(tw, pm, c.w.ract[o][0], c.w.rinf[o][0], c.w.ract[o][1], c.w.rinf[o][1], rcb.y,
+                      rcb.x))
+        continue;
       double cl, cu;
       cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], c.w.ract[o][0], c.w.rinf[o][0],
                     c.w.ract[o][1], c.w.rinf[o][1], rcb.y, rcb.x, cl, cu);
@@ -1489,6 +1521,8 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   }
   P.ready.alloc(mm);
   BP_CUDA(cudaMemset(P.ready.p, 0, sizeof(unsigned) * mm));
+  P.rquiet.alloc(mm);
+  BP_CUDA(cudaMemset(P.rquiet.p, 0, mm));
   P.seg_part.alloc(std::max(slot, 1));
   P.seg_done.alloc(mm);
   BP_CUDA(cudaMemset(P.seg_done.p, 0, sizeof(int) * mm));
@@ -1511,6 +1545,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.gbuf      = P.gbuf.p;
   S.slot      = P.slot.p;
   S.ready     = P.ready.p;
+  S.rquiet    = P.rquiet.p;
   S.seg_part  = P.seg_part.p;
   S.seg_done  = P.seg_done.p;
   S.row_stamp = P.row_stamp.p;

@@ -200,31 +200,59 @@ def c4(seed=4, n=2_000_000, m=2_000_000, bin_frac=0.8, n_long=100, long_len=20_0
     return p, start
 
 
-def c5(seed=100, count=64, lo_nnz=10_000, hi_nnz=5_000_000):
-    """configs[4]: `count` heterogeneous instances, nnz log-uniform in [lo_nnz, hi_nnz], drawn from
-    the C1-C4 generators with row/col ratio U(0.5, 2). Yields (seed, problem)."""
+def c5_specs(seed=100, count=64, lo_nnz=10_000, hi_nnz=5_000_000):
+    """configs[4] instance list without building anything: (seed, target nnz, kind, row/col ratio)
+    per instance; nnz log-uniform in [lo_nnz, hi_nnz], kind = which of the C1-C4 generators,
+    ratio U(0.5, 2). Lets ranks LPT-partition by size and build only their own."""
+    out = []
     for j in range(count):
         rng = np.random.default_rng(seed + j)
         nnz = float(np.exp(rng.uniform(np.log(lo_nnz), np.log(hi_nnz))))
         ratio = float(rng.uniform(0.5, 2.0))
         kind = int(rng.integers(0, 4))
-        if kind == 0:  # C1-like: ~8 nnz per row
-            m = max(int(nnz / 8), 10)
-            n = max(int(m / ratio), 10)
-            lengths = np.minimum(6 + rng.binomial(4, 0.5, size=m), n)
-            yield seed + j, mixed_instance(n, m, lengths, seed + j, name=f"C5-{j}-C1")
-        elif kind == 1:  # C2-like power law
-            m = max(int(nnz / 19), 10)
-            n = max(int(m / ratio), 10)
-            lengths = pareto_lengths(rng, m, cap=min(100_000, n), n_heavy=min(8, max(m // 1000, 1)))
-            yield seed + j, mixed_instance(n, m, lengths, seed + j, name=f"C5-{j}-C2")
-        elif kind == 2:  # C3-like covering
-            nb = max(int(nnz / 36), 100)
-            yield seed + j, c3(seed + j, n_bin=nb, n_cont=int(1.5 * nb), n_cover=max(int(2 * nb / ratio), 10),
-                               n_link=max(nb // 2, 1))
-        else:  # C4-like knapsack/assignment
-            n = max(int(nnz / 12), 100)
-            yield seed + j, c4(seed + j, n=n, m=max(int(n * ratio), 50), n_long=0)[0]
+        out.append((seed + j, nnz, kind, ratio))
+    return out
+
+
+def c5_instance(spec) -> ProblemDef:
+    """Builds one C5 instance from its spec (see c5_specs)."""
+    s, nnz, kind, ratio = spec
+    rng = np.random.default_rng(s)
+    rng.uniform(), rng.uniform(), rng.integers(0, 4)  # the draws c5_specs consumed
+    j = s
+    if kind == 0:  # C1-like: ~8 nnz per row
+        m = max(int(nnz / 8), 10)
+        n = max(int(m / ratio), 10)
+        lengths = np.minimum(6 + rng.binomial(4, 0.5, size=m), n)
+        return mixed_instance(n, m, lengths, s, name=f"C5-{j}-C1")
+    if kind == 1:  # C2-like power law
+        m = max(int(nnz / 19), 10)
+        n = max(int(m / ratio), 10)
+        lengths = pareto_lengths(rng, m, cap=min(100_000, n), n_heavy=min(8, max(m // 1000, 1)))
+        return mixed_instance(n, m, lengths, s, name=f"C5-{j}-C2")
+    if kind == 2:  # C3-like covering
+        nb = max(int(nnz / 36), 100)
+        return c3(s, n_bin=nb, n_cont=int(1.5 * nb), n_cover=max(int(2 * nb / ratio), 10),
+                  n_link=max(nb // 2, 1))
+    n = max(int(nnz / 12), 100)  # C4-like knapsack/assignment
+    return c4(s, n=n, m=max(int(n * ratio), 50), n_long=0)[0]
+
+
+def c5(seed=100, count=64, lo_nnz=10_000, hi_nnz=5_000_000):
+    """configs[4]: `count` heterogeneous instances (c5_specs), yields (seed, problem)."""
+    for spec in c5_specs(seed, count, lo_nnz, hi_nnz):
+        yield spec[0], c5_instance(spec)
+
+
+def lpt_partition(sizes, world):
+    """Longest-processing-time assignment of items (by size) to `world` bins: list of index lists."""
+    bins = [[] for _ in range(world)]
+    load = [0.0] * world
+    for i in sorted(range(len(sizes)), key=lambda i: -sizes[i]):
+        b = min(range(world), key=lambda r: load[r])
+        bins[b].append(i)
+        load[b] += sizes[i]
+    return bins
 
 
 CONFIGS["C4"] = c4

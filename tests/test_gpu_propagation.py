@@ -225,3 +225,15 @@ def test_infinite_bounds_mixed(oracle_built):
         vars_.append((lo, up, bool(rng.random() < 0.6)))
     p = make_problem(vars_, rows)
     _compare_with_oracle(p, lims=(Lim(), Lim(incremental=False)))
+
+
+def test_c5_small_instances_bitwise(oracle_built):
+    """configs[4] (C5): the smallest instances of the 64-instance batch (all four generator kinds
+    occur among them), each propagated on the engine and compared with the oracle bitwise."""
+    specs = sorted(synth.c5_specs(), key=lambda s: s[1])
+    kinds = set()
+    for sp in specs[:12]:
+        p = synth.c5_instance(sp)
+        kinds.add(sp[2])
+        _compare_with_oracle(p, lims=(Lim(),))
+    assert len(kinds) >= 3

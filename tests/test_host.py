@@ -139,3 +139,19 @@ def test_work_plan_bins_like_reference():
     assert size_class_of(16384) == 14 and size_class_of(16385) == 15
     empty = build_work_plan(ProblemBuilder().build())
     assert empty.row_bins == [] and empty.var_bins == []
+
+
+def test_c5_specs_and_lpt_partition():
+    """C5 instance list is deterministic; LPT partitions every instance exactly once and balances."""
+    from paper_2510_20499_b200 import synth
+    a, b = synth.c5_specs(), synth.c5_specs()
+    assert a == b and len(a) == 64
+    sizes = [s[1] for s in a]
+    assert 10_000 <= min(sizes) and max(sizes) <= 5_000_000
+    for world in (1, 2, 4, 8):
+        parts = synth.lpt_partition(sizes, world)
+        assert sorted(i for p in parts for i in p) == list(range(64))
+        loads = [sum(sizes[i] for i in p) for p in parts]
+        assert max(loads) - min(loads) <= max(sizes)
+    p = synth.c5_instance(min(a, key=lambda s: s[1]))
+    assert p.nnz() > 0
