@@ -285,17 +285,19 @@ def run_rounding(args, rank, world, local):
     cache_s = _max_over_ranks(time.perf_counter() - t0, world)
     log(f"rounding: cache {cache.n_probed} vars in {cache_s:.1f} s")
     t0 = time.perf_counter()
-    out = propagation_round(p, start, cache, seed=4 + rank)
+    out = propagation_round(p, start, cache, seed=4 + rank, deadline_sec=args.round_deadline)
     el = _max_over_ranks(time.perf_counter() - t0, world)
     log(f"rounding: {out.bulks_committed} bulks, {out.bp_calls} BP calls in {el:.1f} s")
     if rank != 0:
         return None
     res = {"workload": "C4: knapsack/assignment 2M x 2M (N=%d), presolved root (%d BP rounds)"
                        % (p.nnz(), r0.rounds),
-           "cache_build_s": cache_s, "cache_vars": cache.n_probed,
+           "cache_build_s": cache_s, "cache_budget_s": args.cache_budget, "cache_vars": cache.n_probed,
+           "cache_fallback_branches": cache.n_fallback,
            "cache_probes_per_s": cache.n_probed / cache_s, "round_s": el,
            "bulks_committed": out.bulks_committed, "bp_calls": out.bp_calls,
            "bp_calls_per_s": world * out.bp_calls / el, "completed": out.completed,
+           "timed_out": out.timed_out, "deadline_s": args.round_deadline,
            "rounding_infeasible": out.rounding_infeasible, "set_count": out.set_count,
            "engine_device_ms": out.device_ms, "n_gpus": world, "parallelism": f"replicas x{world}"}
     if world == 1 and not args.no_cpu_baseline:
@@ -416,6 +418,8 @@ def main():
     ap.add_argument("--no-rounding", action="store_true")
     ap.add_argument("--cpu-sample-sec", type=float, default=20.0)
     ap.add_argument("--no-batch", action="store_true")
+    ap.add_argument("--round-deadline", type=float, default=30.0,
+                    help="C4 propagation_round deadline (s), as the reference's Deadline")
     ap.add_argument("--cache-budget", type=float, default=5.0,
                     help="C4 probing-cache time budget (the reference FP's probing_budget_sec)")
     ap.add_argument("--c5-count", type=int, default=64)

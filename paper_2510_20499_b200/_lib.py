@@ -13,7 +13,9 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libbp.so"
+# BP_LIB selects an alternative in-tree build of the same library (A/B experiments of build
+# variants, e.g. a different occupancy target); default: the production build.
+LIB_PATH = Path(os.environ["BP_LIB"]).resolve() if os.environ.get("BP_LIB") else _HERE / "libbp.so"
 
 BP_OK, BP_ERR_INVALID_ARGUMENT, BP_ERR_OUT_OF_RANGE, BP_ERR_RUNTIME, BP_ERR_CUDA = 0, 1, 2, 3, 4
 TIGHTENED, INFEASIBLE, UNCHANGED = 0, 1, 2

@@ -141,6 +141,118 @@ Branch engine_branch(Problem& P, const DBuf<double2>& d_root, int v, double blo,
   }
 }
 
+// Restores the root state after a frontier-start branch: the bounds of every variable that
+// differs from the root, and the activity records of every row containing one (the only rows
+// whose activity the branch can have changed: dirty rows are rows of changed variables).
+__global__ void k_restore(DevProblem P, double2* b, const double2* root, const RowRec* root_rec,
+                          const double2* root_aux, RowRec* rec, double2* aux, const int* var, int h)
+{
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw   = (gridDim.x * blockDim.x) >> 5;
+  for (int j = warp; j < h; j += nw) {
+    const int i = var[j];
+    if (lane == 0) b[i] = root[i];
+    for (int e = P.col_start[i] + lane; e < P.col_start[i + 1]; e += 32) {
+      const int k = P.col_row[e];
+      rec[k]      = root_rec[k];
+      aux[k]      = root_aux[k];
+    }
+  }
+}
+
+// Device scratch of the fallback branches (allocated once per probe_vars call).
+struct FallbackBufs {
+  DBuf<int> cnt, var;
+  DBuf<double> lo, up;
+  DBuf<RowRec> root_rec;
+  DBuf<double2> root_aux;
+  int cap = 0;
+};
+
+// Diff of P.st.bounds against the root, ascending by var (probing.hpp:213-217).
+void diff_root(Problem& P, const DBuf<double2>& d_root, FallbackBufs& F, cudaStream_t s,
+               std::vector<int>& vv, std::vector<double>& l, std::vector<double>& u)
+{
+  if (F.cap == 0) {
+    F.cap = 1 << 16;
+    F.cnt.alloc(1);
+    F.var.alloc(F.cap);
+    F.lo.alloc(F.cap);
+    F.up.alloc(F.cap);
+  }
+  for (;;) {
+    BP_CUDA(cudaMemsetAsync(F.cnt.p, 0, sizeof(int), s));
+    k_diff<<<592, 256, 0, s>>>(P.st.bounds, d_root.p, P.n, F.cnt.p, F.cap, F.var.p, F.lo.p, F.up.p);
+    BP_CUDA(cudaGetLastError());
+    int h = 0;
+    BP_CUDA(cudaMemcpyAsync(&h, F.cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaStreamSynchronize(s));
+    if (h > F.cap) {
+      F.cap = h;
+      F.var.alloc(F.cap);
+      F.lo.alloc(F.cap);
+      F.up.alloc(F.cap);
+      continue;
+    }
+    std::vector<int> v(h);
+    std::vector<double> a(h), b(h);
+    if (h) {
+      BP_CUDA(cudaMemcpy(v.data(), F.var.p, sizeof(int) * h, cudaMemcpyDeviceToHost));
+      BP_CUDA(cudaMemcpy(a.data(), F.lo.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
+      BP_CUDA(cudaMemcpy(b.data(), F.up.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int> ord(h);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return v[x] < v[y]; });
+    vv.clear();
+    l.clear();
+    u.clear();
+    for (int j : ord) {
+      vv.push_back(v[j]);
+      l.push_back(a[j]);
+      u.push_back(b[j]);
+    }
+    return;
+  }
+}
+
+// Branch on the full engine from a CERTIFIED root, starting from the frontier rows(v) (exact:
+// SURVEY §8a A12). Invariant between calls: P.st.bounds = root, P.st.rec/aux = root activities;
+// restored sparsely afterwards (k_restore) instead of O(n + m) copies.
+Branch engine_branch_cert(Problem& P, const DBuf<double2>& d_root, FallbackBufs& F, int v,
+                          double blo, double bup, const std::vector<double>& root, cudaStream_t s)
+{
+  Branch br;
+  const double nlo = (root[2 * v] < blo) ? blo : root[2 * v];
+  const double nup = (bup < root[2 * v + 1]) ? bup : root[2 * v + 1];
+  if (nlo > nup) {
+    br.feasible = 0;
+    return br;
+  }
+  const double2 nb = make_double2(nlo, nup);
+  BP_CUDA(cudaMemcpyAsync(P.st.bounds + v, &nb, sizeof(double2), cudaMemcpyHostToDevice, s));
+  BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+  const int changed[1] = {v};
+  stage_changed(P, changed, 1, s);
+  const RunResult r = run_engine(P, MODE_PROPAGATE, true, default_limits(), s, ENGINE_START_FRONTIER);
+  std::vector<int> vv;
+  std::vector<double> l, u;
+  diff_root(P, d_root, F, s, vv, l, u);
+  if (!vv.empty()) {
+    k_restore<<<148, 256, 0, s>>>(P.dev(), P.st.bounds, d_root.p, F.root_rec.p, F.root_aux.p,
+                                  P.st.rec, P.st.aux, F.var.p, (int)vv.size());
+    BP_CUDA(cudaGetLastError());
+  }
+  if (r.status == BP_STATUS_INFEASIBLE) {
+    br.feasible = 0;
+    return br;
+  }
+  br.var = std::move(vv);
+  br.lo  = std::move(l);
+  br.up  = std::move(u);
+  return br;
+}
+
 }  // namespace
 
 // Probes `vars` (both branches each) from `root`; entries follow probe_variable semantics.
@@ -288,9 +400,19 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   } else {
     for (int t = 0; t < ntask; ++t) fallback.push_back(t);
   }
+  FallbackBufs F;
+  if (certified && !fallback.empty() && P.m) {
+    // snapshot of the root activities (left in P.st.rec / aux by the certification round)
+    F.root_rec.alloc(P.m);
+    F.root_aux.alloc(P.m);
+    BP_CUDA(cudaMemcpyAsync(F.root_rec.p, P.st.rec, sizeof(RowRec) * P.m, cudaMemcpyDeviceToDevice, s));
+    BP_CUDA(cudaMemcpyAsync(F.root_aux.p, P.st.aux, sizeof(double2) * P.m, cudaMemcpyDeviceToDevice, s));
+    BP_CUDA(cudaMemcpyAsync(P.st.bounds, d_root.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+  }
   for (int t : fallback) {
     if (elapsed() >= budget_sec) break;
-    res[tslot[t]]  = engine_branch(P, d_root, tv[t], tlo[t], tup[t], root, s);
+    res[tslot[t]]  = certified ? engine_branch_cert(P, d_root, F, tv[t], tlo[t], tup[t], root, s)
+                               : engine_branch(P, d_root, tv[t], tlo[t], tup[t], root, s);
     done[tslot[t]] = 1;
     C.n_fallback++;
   }

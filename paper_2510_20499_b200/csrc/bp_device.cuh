@@ -313,8 +313,9 @@ struct DevProblem {
   const double* col_val;
   const double2* cons;      // (lower, upper) per row
   const uint8_t* is_int;
-  // Short rows (nnz <= kShortNnz) packed contiguously in natural order and grouped into tiles of
-  // <= 32 rows / <= kTile entries: a warp loads a tile coalesced, every lane folds one row.
+  // Rows with nnz <= kPackNnz packed contiguously in natural order and grouped into tiles of
+  // <= 32 rows / <= kPackTile entries: a warp streams a tile coalesced in 128-entry windows and
+  // every lane folds one row.
   int n_srow, n_srtile;
   const int* srow;          // packed index -> row id
   const int* sr_ptr;        // n_srow + 1 offsets into sr_ci / sr_val
@@ -349,6 +350,14 @@ constexpr int kTile      = 128;   // entries per tile / per gathered chunk (4 pe
 constexpr int kPiece     = 1024;  // gather / candidate piece of a long row (divides kSumSegment)
 constexpr int kFoldChunk = 256;   // staging chunk of the streamed fold (8 per lane)
 constexpr int kCandSplit = 2048;  // long rows above: candidates by parallel pieces
+#ifndef BP_PACK_NNZ
+#define BP_PACK_NNZ 32
+#endif
+#ifndef BP_PACK_TILE
+#define BP_PACK_TILE 128
+#endif
+constexpr int kPackNnz   = BP_PACK_NNZ;   // full rounds: rows up to this length go to packed tiles
+constexpr int kPackTile  = BP_PACK_TILE;  // packed row tiles: <= 32 rows and <= this many entries
 
 struct SegPart {
   double min, max;

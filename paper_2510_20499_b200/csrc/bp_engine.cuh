@@ -60,7 +60,7 @@ struct ParCtl {
   int n_changed, n_crossed, any_rows;
   int cur_a, cur_b, cur_c, cur_vm, cur_vs;
   int cur_x1, cur_x2, n_xtask, stop;
-  int n_ctask, cur_x3, cur_x4, pad1;
+  int n_ctask, cur_x3, cur_x4, xabort;  // xabort: a frontier expansion stopped early (full next)
   unsigned long long colnnz, roww, colw;
 };
 
@@ -68,7 +68,11 @@ struct Ctl {
   ParCtl par[2];
   int status, rounds, crossed, any_change;
   int fixpoint;  // 1 if the loop ended at a fixpoint (no change / no dirty row): certifies the bounds
-  int pad[11];
+  // hand-off of a full round's row phase to k_rows_full (engine state kept across launches)
+  int need_full;              // the engine exited to have round `rounds` run its F2 externally
+  int pad0, pad1;
+  unsigned long long t0;      // globaltimer at the start of the propagate (time limit, stats)
+  int pad[4];
 };
 
 // Mutable per-problem workspace (one propagate at a time per problem; calls serialized).
@@ -140,6 +144,7 @@ struct Problem {
   DevState st{};
   unsigned stamp_base = 1;
   int grid_blocks = 0;
+  int f2_blocks   = 0;  // k_rows_full grid (its own occupancy)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket every engine launch on its stream
   double last_kernel_ms = 0.0;

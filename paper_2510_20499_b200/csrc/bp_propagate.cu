@@ -7,20 +7,19 @@
 // keeping gathers in flight and taking those chains off the critical path.
 //
 // FULL round (round 1, and any round whose frontier is a large part of the matrix):
-//   F1  gather: the bounds of every long row's entries (nnz > 32) are gathered into a contiguous
-//       buffer (gbuf), pieces of 1024 entries, 8 gathers per lane in flight.        ─ grid.sync
-//   F2  rows: per 16384-entry segment of a long row, one warp streams gbuf coalesced while lanes
-//       0/1 run the reference's sequential min/max sums (zero contributions skipped: exact, the
-//       running sum is never -0.0); packed tiles of short rows fold one row per lane. Right after
-//       a row's activity is known, every entry's candidate bounds for its variable are computed
-//       and the ones strictly improving the round-start bound are published into per-variable
-//       slots with order-preserving 64-bit atomics (fused tightening: no CSC pass, no second
-//       gather of row records).                                                    ─ grid.sync
+//   F2  rows: per 16384-entry segment of a long row, one warp streams the row's indices and
+//       coefficients coalesced and gathers its bounds (two chunks in flight) while lanes 0/1 run
+//       the reference's sequential min/max sums (zero contributions skipped: exact, the running
+//       sum is never -0.0); packed tiles of short rows fold one row per lane. Right after a
+//       row's activity is known, every entry's candidate bounds for its variable are computed
+//       (unless provably non-improving: candidate gating) and the ones strictly improving the
+//       round-start bound are published into per-variable slots with order-preserving 64-bit
+//       atomics (fused tightening: no CSC pass, no second gather of row records). ─ grid.sync
 //   F4  finalize: per variable, the slot gives the std::min/max fold result (ties at +-0.0 are
 //       resolved by the smallest row = first CSC position), then the reference's crossing /
 //       hair-crossing / threshold rules (propagation.hpp:354-369).                  ─ grid.sync
 // FRONTIER round (propagation.hpp:442-447 with dirty rows / dirty vars):
-//   P1 gather (dirty long rows) ─ P2 activities (dirty rows) ─ B tighten the dirty vars over the
+//   P2 activities (dirty rows) ─ B tighten the dirty vars over the
 //   CSC (row-record gathers; long columns reduced as a lexicographic (value, CSC position)
 //   min/max) ─ C/D frontier expansion.
 // Evaluating a superset of the reference's dirty sets yields bit-identical results (DESIGN.md §2,
@@ -217,39 +216,14 @@ __device__ __forceinline__ void write_rec(const DevProblem& P, const DevState& S
   if (imn | imx) S.aux[k] = make_double2(smn, smx);
 }
 
-// F1 / P1: gathers the bounds of piece p (kPiece entries) of long row k into gbuf.
-__device__ void long_gather(Ctx& c, int k, int p)
-{
-  const DevProblem& P = c.P;
-  const DevState& S   = c.S;
-  const int rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
-  const int e0 = p * kPiece, e1 = min(L, e0 + kPiece);
-  double2* out = S.gbuf + __ldg(P.long_off + k);
-  constexpr int G = 4 * kEPL;  // 16 gathers per lane in flight
-  for (int j0 = e0; j0 < e1; j0 += 32 * G) {
-    int col[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const int e = j0 + h * 32 + c.lane;
-      col[h]      = e < e1 ? __ldg(P.row_col + rs + e) : -1;
-    }
-    double2 bd[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) bd[h] = col[h] >= 0 ? S.bounds[col[h]] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int h = 0; h < G; ++h)
-      if (col[h] >= 0) out[j0 + h * 32 + c.lane] = bd[h];
-  }
-}
-
 // Candidates of entries [e0, e1) of long row k whose activity is (mnf, nmn, mxf, nmx, g, h).
+// Bounds are gathered straight from the (L2-resident) bounds array.
 __device__ void long_candidates(Ctx& c, int k, int e0, int e1, double mnf, int nmn, double mxf,
                                 int nmx, double g, double hh)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   const int rs        = __ldg(P.row_start + k);
-  const double2* gb   = S.gbuf + __ldg(P.long_off + k);
   for (int j0 = e0; j0 < e1; j0 += kTile) {
     int ci[kEPL];
     double a[kEPL];
@@ -259,8 +233,10 @@ __device__ void long_candidates(Ctx& c, int k, int e0, int e1, double mnf, int n
       const int e = j0 + h * 32 + c.lane;
       ci[h]       = e < e1 ? __ldg(P.row_ci + rs + e) : -1;
       a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
-      bd[h]       = e < e1 ? gb[e] : make_double2(0.0, 0.0);
     }
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h)
+      bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
       if (ci[h] == -1) continue;
@@ -299,10 +275,12 @@ __device__ __forceinline__ double fold_seq(const double* src, int cnt, double ac
   return acc;
 }
 
-// F2 / P2: one 16384-entry segment of a long row. All lanes stage contributions of 256 entries
-// (coalesced from gbuf) while lanes 0/1 fold the previous chunk. With `cand`, a single-segment
-// row of <= kCandSplit entries publishes its candidates right away; longer rows publish their
-// activity (ready stamp) for the parallel candidate pieces.
+// F2 / P2: one 16384-entry segment of a long row, streamed in 128-entry chunks: the indices of
+// chunk j+2 and the bound gathers of chunk j+1 are in flight while lanes 0/1 run the reference's
+// sequential min/max sums over chunk j (zero contributions skipped: exact, the running sum is
+// never -0.0). With `cand`, a single-segment row of <= kCandSplit entries publishes its
+// candidates right away; longer rows publish their activity (ready stamp) for the parallel
+// candidate pieces.
 __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
 {
   const DevProblem& P = c.P;
@@ -310,34 +288,39 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   const int lane      = c.lane;
   const int rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
   const int e0 = seg * kSumSegment, e1 = min(L, e0 + kSumSegment);
-  const double2* gb = S.gbuf + __ldg(P.long_off + k);
-  constexpr int H   = kFoldChunk / 32;
-  double a[H];
+  constexpr int H = kEPL;
+  int ci[H], ci2[H];
+  double a[H], a2[H];
   double2 bd[H];
 #pragma unroll
   for (int h = 0; h < H; ++h) {
-    const int e = e0 + h * 32 + lane;
-    a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
-    bd[h]       = e < e1 ? gb[e] : make_double2(0.0, 0.0);
+    const int e  = e0 + h * 32 + lane;
+    const int e2 = e + kTile;
+    ci[h]        = e < e1 ? __ldg(P.row_ci + rs + e) : -1;
+    a[h]         = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
+    ci2[h]       = e2 < e1 ? __ldg(P.row_ci + rs + e2) : -1;
+    a2[h]        = e2 < e1 ? __ldg(P.row_val + rs + e2) : 0.0;
   }
+#pragma unroll
+  for (int h = 0; h < H; ++h) bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
   double acc = 0.0;
   int imn = 0, imx = 0;
-  double gtw = 0.0, gpm = 0.0;  // row-level gating maxima (integrality unknown here: +1 for all)
+  double gtw = 0.0, gpm = 0.0;  // row-level gating maxima
   const unsigned lt = lanemask_lt();
-  for (int base = e0; base < e1; base += kFoldChunk) {
+  for (int base = e0; base < e1; base += kTile) {
     // order-preserving compaction of the non-zero contributions of each chain
     int pm = 0, px = 0;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       double cm = 0.0, cx = 0.0;
-      if (base + h * 32 + lane < e1) {
+      if (ci[h] != -1) {
         int i1, i2;
         contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
         imn += i1;
         imx += i2;
         if (cand) {
           double tw, pw;
-          entry_reach(a[h], bd[h].x, bd[h].y, true, tw, pw);
+          entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pw);
           gtw = fmax(gtw, tw);
           gpm = fmax(gpm, pw);
         }
@@ -350,18 +333,23 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
       px += __popc(x);
     }
     __syncwarp();
-    // next chunk in flight during the fold
+    // next chunk's gathers and the chunk after's indices in flight during the fold
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      const int e = base + kFoldChunk + h * 32 + lane;
-      a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
-      bd[h]       = e < e1 ? gb[e] : make_double2(0.0, 0.0);
+      ci[h] = ci2[h];
+      a[h]  = a2[h];
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int e2 = base + 2 * kTile + h * 32 + lane;
+      ci2[h]       = e2 < e1 ? __ldg(P.row_ci + rs + e2) : -1;
+      a2[h]        = e2 < e1 ? __ldg(P.row_val + rs + e2) : 0.0;
     }
     if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
     __syncwarp();
   }
-  imn            = warp_sum(imn);
-  imx            = warp_sum(imx);
   if (cand) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -369,6 +357,8 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
       gpm = fmax(gpm, __shfl_xor_sync(FULL, gpm, o));
     }
   }
+  imn            = warp_sum(imn);
+  imx            = warp_sum(imx);
   double smn     = __shfl_sync(FULL, acc, 0);
   double smx     = __shfl_sync(FULL, acc, 1);
   const int nseg = (L + kSumSegment - 1) / kSumSegment;
@@ -458,9 +448,48 @@ __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp)
   long_candidates(c, k, p * kPiece, min(L, (p + 1) * kPiece), mnf, nmn, mxf, nmx, r.g, r.h);
 }
 
-// A packed tile of short rows: gathers, per-lane folds, and (with `cand`) the candidates of every
-// entry from the registers that still hold its coefficient and bounds. Three dependent memory
-// levels: tile descriptor -> (entries, per-lane row info) -> (bounds gathers, row bounds).
+// Loads window w0 of a packed row tile (entries p0 + w0 + [0, 128)) and gathers its bounds.
+__device__ __forceinline__ void tile_window(const Ctx& c, int p0, int p1, int w0, int* ci, double* a,
+                                            int* own, double2* bd)
+{
+  const DevProblem& P = c.P;
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    const int f = p0 + w0 + h * 32 + c.lane;
+    ci[h]       = f < p1 ? __ldg(P.sr_ci + f) : -1;
+    a[h]        = f < p1 ? __ldg(P.sr_val + f) : 0.0;
+    own[h]      = f < p1 ? __ldg(P.sr_own + f) : 0;
+  }
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) bd[h] = ci[h] != -1 ? c.S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+}
+
+// Candidates of one loaded window of a packed row tile (row activities in w.ract / w.rinf).
+__device__ __forceinline__ void tile_candidates(Ctx& c, const int* ci, const double* a, const int* own,
+                                                const double2* bd)
+{
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    if (ci[h] == -1) continue;
+    const int o       = own[h];
+    const double2 rcb = c.w.vb[o];
+    double tw, pm;
+    entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pm);
+    if (entry_quiet(tw, pm, c.w.ract[o][0], c.w.rinf[o][0], c.w.ract[o][1], c.w.rinf[o][1], rcb.y,
+                    rcb.x))
+      continue;
+    double cl, cu;
+    cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], c.w.ract[o][0], c.w.rinf[o][0],
+                  c.w.ract[o][1], c.w.rinf[o][1], rcb.y, rcb.x, cl, cu);
+    publish(c.S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, c.w.rk[o]);
+  }
+}
+
+// A packed tile of <= 32 rows of <= kPackNnz entries each (<= kPackTile entries): the warp
+// streams it coalesced in 128-entry windows (bounds gathered per window), every lane folds its
+// own row in the reference's order across the windows, then (with `cand`) the candidates of every
+// entry are computed -- from the registers that still hold the window when the tile is a single
+// window, else from a second streamed pass.
 __device__ void short_tile(Ctx& c, int t, bool cand)
 {
   const DevProblem& P = c.P;
@@ -468,46 +497,46 @@ __device__ void short_tile(Ctx& c, int t, bool cand)
   const int2 d0 = __ldg(reinterpret_cast<const int2*>(P.sr_tile) + t);      // (r0, p0)
   const int2 d1 = __ldg(reinterpret_cast<const int2*>(P.sr_tile) + t + 1);  // (r1, p1)
   const int r0 = d0.x, p0 = d0.y, r1 = d1.x, p1 = d1.y;
-  const int nr = r1 - r0;
+  const int nr = r1 - r0, T = p1 - p0;
   int ci[kEPL], own[kEPL];
   double a[kEPL];
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    const int f = p0 + h * 32 + c.lane;
-    ci[h]       = f < p1 ? __ldg(P.sr_ci + f) : -1;
-    a[h]        = f < p1 ? __ldg(P.sr_val + f) : 0.0;
-    own[h]      = f < p1 ? __ldg(P.sr_own + f) : 0;
-  }
+  double2 bd[kEPL];
+  tile_window(c, p0, p1, 0, ci, a, own, bd);
   int k = -1, q0 = 0, q1 = 0;
   if (c.lane < nr) {
     k  = __ldg(P.srow + r0 + c.lane);
     q0 = __ldg(P.sr_ptr + r0 + c.lane) - p0;
     q1 = __ldg(P.sr_ptr + r0 + c.lane + 1) - p0;
   }
-  double2 bd[kEPL];
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h)
-    bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
   const double2 cb = k >= 0 ? __ldg(&P.cons[k]) : make_double2(0.0, 0.0);
+  double smn = 0.0, smx = 0.0;
+  int imn = 0, imx = 0;
+  for (int w0 = 0;;) {
 #pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    double cm = 0.0, cx = 0.0;
-    int i1 = 0, i2 = 0;
-    if (ci[h] != -1) contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
-    c.w.b0[h * 32 + c.lane] = cm;
-    c.w.b1[h * 32 + c.lane] = cx;
-    c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
-  }
-  __syncwarp();
-  if (k >= 0) {
-    double smn = 0.0, smx = 0.0;
-    int imn = 0, imx = 0;
-    for (int q = q0; q < q1; ++q) {
-      smn = __dadd_rn(smn, c.w.b0[q]);
-      smx = __dadd_rn(smx, c.w.b1[q]);
-      imn += c.w.fl[q] & 1;
-      imx += c.w.fl[q] >> 1;
+    for (int h = 0; h < kEPL; ++h) {
+      double cm = 0.0, cx = 0.0;
+      int i1 = 0, i2 = 0;
+      if (ci[h] != -1) contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
+      c.w.b0[h * 32 + c.lane] = cm;
+      c.w.b1[h * 32 + c.lane] = cx;
+      c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
     }
+    __syncwarp();
+    if (k >= 0) {
+      const int qa = max(q0, w0) - w0, qb = min(q1, w0 + kTile) - w0;
+      for (int q = qa; q < qb; ++q) {
+        smn = __dadd_rn(smn, c.w.b0[q]);
+        smx = __dadd_rn(smx, c.w.b1[q]);
+        imn += c.w.fl[q] & 1;
+        imx += c.w.fl[q] >> 1;
+      }
+    }
+    __syncwarp();
+    w0 += kTile;
+    if (w0 >= T) break;
+    tile_window(c, p0, p1, w0, ci, a, own, bd);
+  }
+  if (k >= 0) {
     RowRec r;
     r.min = imn ? box_count(imn) : smn;
     r.max = imx ? box_count(imx) : smx;
@@ -524,20 +553,13 @@ __device__ void short_tile(Ctx& c, int t, bool cand)
   }
   __syncwarp();
   if (cand) {
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      if (ci[h] == -1) continue;
-      const int o       = own[h];
-      const double2 rcb = c.w.vb[o];
-      double tw, pm;
-      entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pm);
-      if (entry_quiet(tw, pm, c.w.ract[o][0], c.w.rinf[o][0], c.w.ract[o][1], c.w.rinf[o][1], rcb.y,
-                      rcb.x))
-        continue;
-      double cl, cu;
-      cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], c.w.ract[o][0], c.w.rinf[o][0],
-                    c.w.ract[o][1], c.w.rinf[o][1], rcb.y, rcb.x, cl, cu);
-      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, c.w.rk[o]);
+    if (T <= kTile) {
+      tile_candidates(c, ci, a, own, bd);
+    } else {
+      for (int w0 = 0; w0 < T; w0 += kTile) {
+        tile_window(c, p0, p1, w0, ci, a, own, bd);
+        tile_candidates(c, ci, a, own, bd);
+      }
     }
   }
   __syncwarp();
@@ -598,18 +620,6 @@ __device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
     __syncwarp();
   }
   if (k >= 0) write_rec(P, c.S, k, smn, smx, imn, imx);
-}
-
-// Phase 1 (F1 / P1): gather pieces of long rows.
-__device__ void phase_gather(Ctx& c, ParCtl* pc, int par, bool full)
-{
-  const int n       = full ? c.P.n_piece : ldv(&pc->n_dpiece);
-  const int2* tasks = full ? c.P.piece_task : c.S.dpiece[par];
-  for (Prefetch it_t(c, &pc->cur_a, 1); it_t.t < n; it_t.advance()) {
-    const int t = it_t.t;
-    const int2 tk = tasks[t];
-    long_gather(c, tk.x, tk.y);
-  }
 }
 
 // Phase 2 (F2 / P2): activities of all rows (full) or the dirty ones; `cand` fuses tightening.
@@ -973,7 +983,7 @@ __device__ __forceinline__ void expand_rows_window(Ctx& c, ParCtl* qc, int qpar,
     nall += nw[h];
     const bool lg = nw[h] && RL[h] > kShortNnz;
     n_s += nw[h] && !lg;
-    n_p += lg ? (RL[h] + kPiece - 1) / kPiece : 0;
+    n_p += lg ? 1 : 0;
     n_f += lg ? (RL[h] + kSumSegment - 1) / kSumSegment : 0;
     n_x += lg ? (RL[h] + kTile - 1) / kTile : 0;
   }
@@ -982,29 +992,54 @@ __device__ __forceinline__ void expand_rows_window(Ctx& c, ParCtl* qc, int qpar,
   for (int h = 0; h < kEPL; ++h)
     if (nw[h] && RL[h] <= kShortNnz) S.drow_s[qpar][ps++] = k[h];
   if (__any_sync(FULL, n_p > 0)) {  // rare: a long row became dirty
-    int pp = warp_alloc(&qc->n_dpiece, n_p, c.lane);
     int pf = warp_alloc(&qc->n_dfold, n_f, c.lane);
     int px = warp_alloc(&qc->n_xtask, n_x, c.lane);
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
       if (!nw[h] || RL[h] <= kShortNnz) continue;
-      for (int s = 0; s * kPiece < RL[h]; ++s) S.dpiece[qpar][pp++] = make_int2(k[h], s);
       for (int s = 0; s * kSumSegment < RL[h]; ++s) S.dfold[qpar][pf++] = make_int2(k[h], s);
       for (int s = 0; s * kTile < RL[h]; ++s) S.xtask[qpar][px++] = make_int2(k[h], s);
     }
   }
 }
 
+// Adds this warp's accumulated expansion work to *total. Returns (warp-uniform) whether the
+// expansion should stop early: the total crossed `budget` (the next round will be a full round, so
+// the frontier lists are not needed) or another warp already stopped. budget = ~0: never stops.
+__device__ __forceinline__ bool flush_work(Ctx& c, unsigned long long& acc, unsigned long long* total,
+                                           int* abort_flag, unsigned long long budget)
+{
+  unsigned long long w = acc;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(FULL, w, o);
+  acc      = 0;
+  int stop = 0;
+  if (c.lane == 0) {
+    if (w) {
+      const unsigned long long old = atomicAdd(total, w);
+      if (budget != ~0ull && old + w > budget) {
+        stop = 1;
+        atomicExch(abort_flag, 1);
+      }
+    }
+    if (!stop && budget != ~0ull) stop = ldv(abort_flag);
+  }
+  return __shfl_sync(FULL, stop, 0) != 0;
+}
+
 // Phase C: rows(changed) → next round's dirty rows. Changed vars with short columns go 32 per
 // warp (flattened 128-entry windows); longer columns were split into chunk tasks at append time.
-__device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp)
+__device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp,
+                                  unsigned long long budget)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   unsigned long long roww = 0;
   int nall                = 0;
+  bool stop               = false;
+  const bool eager        = budget != ~0ull;  // early exit enabled: flush per task
   const int nch = ldv(&pc->n_changed);
-  for (Prefetch it_t(c, &pc->cur_x1, 32); it_t.t < nch; it_t.advance()) {
+  for (Prefetch it_t(c, &pc->cur_x1, 32); it_t.t < nch && !stop; it_t.advance()) {
     const int t = it_t.t;
     const int j = t + c.lane;
     const int i = j < nch ? S.changed[j] : -1;
@@ -1030,9 +1065,10 @@ __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
       expand_rows_window(c, qc, qpar, stamp, k, roww, nall);
     }
     __syncwarp();
+    if (eager) stop = flush_work(c, roww, &qc->roww, &qc->xabort, budget);
   }
-  const int ntask = ldv(&pc->n_ctask);
-  for (Prefetch it_t(c, &pc->cur_x2, 1); it_t.t < ntask; it_t.advance()) {
+  const int ntask = stop ? 0 : ldv(&pc->n_ctask);
+  for (Prefetch it_t(c, &pc->cur_x2, 1); it_t.t < ntask && !stop; it_t.advance()) {
     const int t = it_t.t;
     const int2 tk = S.ctask[t];
     const int ce  = __ldg(P.col_start + tk.x + 1);
@@ -1044,14 +1080,11 @@ __device__ void phase_expand_rows(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
       k[h]        = e < e1 ? __ldg(P.col_row + e) : -1;
     }
     expand_rows_window(c, qc, qpar, stamp, k, roww, nall);
+    if (eager) stop = flush_work(c, roww, &qc->roww, &qc->xabort, budget);
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) roww += __shfl_xor_sync(FULL, roww, o);
+  flush_work(c, roww, &qc->roww, &qc->xabort, ~0ull);
   nall = warp_sum(nall);
-  if (c.lane == 0) {
-    if (roww) atomicAdd(&qc->roww, roww);
-    if (nall) atomicAdd(&qc->n_drow_all, nall);
-  }
+  if (c.lane == 0 && nall) atomicAdd(&qc->n_drow_all, nall);
 }
 
 // One 128-entry window of the var expansion: marks vars v[h] dirty and appends the new ones.
@@ -1082,13 +1115,16 @@ __device__ __forceinline__ void expand_vars_window(Ctx& c, ParCtl* qc, int qpar,
 }
 
 // Phase D: dirty rows → next round's dirty vars: short rows 32 per warp, long rows by chunk tasks.
-__device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp)
+__device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsigned stamp,
+                                  unsigned long long budget)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   unsigned long long colw = 0;
+  bool stop               = false;
+  const bool eager        = budget != ~0ull;
   const int nr = ldv(&qc->n_drow_s);
-  for (Prefetch it_t(c, &pc->cur_x3, 32); it_t.t < nr; it_t.advance()) {
+  for (Prefetch it_t(c, &pc->cur_x3, 32); it_t.t < nr && !stop; it_t.advance()) {
     const int t = it_t.t;
     const int j = t + c.lane;
     const int k = j < nr ? S.drow_s[qpar][j] : -1;
@@ -1113,9 +1149,10 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
       expand_vars_window(c, qc, qpar, stamp, v, colw);
     }
     __syncwarp();
+    if (eager) stop = flush_work(c, colw, &qc->colw, &qc->xabort, budget);
   }
-  const int ntask = ldv(&qc->n_xtask);
-  for (Prefetch it_t(c, &pc->cur_x4, 1); it_t.t < ntask; it_t.advance()) {
+  const int ntask = stop ? 0 : ldv(&qc->n_xtask);
+  for (Prefetch it_t(c, &pc->cur_x4, 1); it_t.t < ntask && !stop; it_t.advance()) {
     const int t = it_t.t;
     const int2 tk = S.xtask[qpar][t];
     const int re  = __ldg(P.row_start + tk.x + 1);
@@ -1127,10 +1164,9 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
       v[h]        = e < e1 ? __ldg(P.row_col + e) : -1;
     }
     expand_vars_window(c, qc, qpar, stamp, v, colw);
+    if (eager) stop = flush_work(c, colw, &qc->colw, &qc->xabort, budget);
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) colw += __shfl_xor_sync(FULL, colw, o);
-  if (c.lane == 0 && colw) atomicAdd(&qc->colw, colw);
+  flush_work(c, colw, &qc->colw, &qc->xabort, ~0ull);
 }
 
 __device__ void zero_par(ParCtl* q)
@@ -1142,9 +1178,25 @@ __device__ void zero_par(ParCtl* q)
 #ifndef BP_MIN_BLOCKS
 #define BP_MIN_BLOCKS 2
 #endif
+// F2 of a full round as its own launch: the row phase is a latency-bound stream of independent
+// warp tasks, so it runs at the occupancy its own register budget allows instead of the
+// cooperative engine's (whose allocation is the maximum over every phase).
+#ifndef BP_F2_MIN_BLOCKS
+#define BP_F2_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
+    k_rows_full(DevProblem P, DevState S, Limits lim, int par, unsigned stamp)
+{
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
+  const int warp = threadIdx.x >> 5;
+  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
+  phase_rows(c, &S.ctl->par[par], par, true, true, stamp);
+}
+
 __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     k_engine(DevProblem P, DevState S, Limits lim, int mode, int full_first, unsigned stamp_base,
-             unsigned long long dense_thr, long long* stats)
+             unsigned long long dense_thr, long long* stats, int ext_f2, int resume)
 {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm            = *reinterpret_cast<Smem*>(dyn_smem);
@@ -1160,8 +1212,6 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
 
   if (mode == MODE_ACTIVITY) {
     const bool full = full_first != 0;
-    phase_gather(c, &S.ctl->par[1], 1, full);
-    grid.sync();
     phase_rows(c, &S.ctl->par[1], 1, full, false, stamp_base);
     return;
   }
@@ -1170,7 +1220,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     return;
   }
 
-  const unsigned long long t0 = globaltimer();
+  const unsigned long long t0 = resume ? ldv(&S.ctl->t0) : globaltimer();
   const bool timed            = isfinite(lim.time_limit);
   const bool lead             = blockIdx.x == 0 && threadIdx.x == 0;
   bool full                   = true;  // round 1 is always a full sweep (propagation.hpp:442)
@@ -1178,14 +1228,26 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   bool fixpoint               = false;
   int status = BP_STATUS_UNSET, crossed_out = 0;
   int rounds = 0;
-  if (full_first == 2) {
+  bool resumed = false;  // first iteration after k_rows_full ran this round's F2
+  if (resume) {
+    rounds     = ldv(&S.ctl->rounds);
+    any_change = ldv(&S.ctl->any_change) != 0;
+    resumed    = true;
+  } else if (lead) {
+    S.ctl->t0 = t0;
+  }
+  if (!resume && full_first == 2) {
     // frontier start from a certified fixpoint: rows(changed) / vars(rows) of the staged list
     ParCtl* p0 = &S.ctl->par[0];
     ParCtl* p1 = &S.ctl->par[1];
-    phase_expand_rows(c, p0, p1, 1, stamp_base);
+    const unsigned long long dense2 = dense_thr == ~0ull ? ~0ull : 2 * dense_thr;
+    phase_expand_rows(c, p0, p1, 1, stamp_base, dense2);
     grid.sync();
-    phase_expand_vars(c, p0, p1, 1, stamp_base);
-    grid.sync();
+    const unsigned long long rw0 = ldv(&p1->roww);
+    if (rw0 <= dense2) {
+      phase_expand_vars(c, p0, p1, 1, stamp_base, dense2 == ~0ull ? ~0ull : dense2 - rw0);
+      grid.sync();
+    }
     full = dense_thr != ~0ull && ldv(&p1->roww) + ldv(&p1->colw) > 2 * dense_thr;
     if (ldv(&p1->n_drow_all) == 0) {  // nothing to revisit: the fixpoint stands
       full     = false;
@@ -1196,21 +1258,30 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   if (rounds == lim.max_rounds && fixpoint) {
     rounds = 1;  // the reference's first (full) round finds no change
   } else {
-  while (rounds < lim.max_rounds) {
-    ++rounds;
+  while (rounds < lim.max_rounds || resumed) {
+    if (!resumed) ++rounds;
     const int ppar       = rounds & 1, qpar = ppar ^ 1;
     ParCtl* pc           = &S.ctl->par[ppar];
     ParCtl* qc           = &S.ctl->par[qpar];
     long long* st        = stats ? stats + (long long)(rounds - 1) * kStatCols : nullptr;
     const bool fr        = full || !lim.incremental;
     const unsigned stamp = stamp_base + (unsigned)rounds;
-    if (fr || ldv(&pc->n_dpiece) > 0) {
-      phase_gather(c, pc, ppar, fr);
+    if (resumed) {
+      resumed = false;  // this round's F2 (fused rows + candidates) ran in k_rows_full
+    } else if (fr && ext_f2) {
+      // hand the full round's row phase to k_rows_full; the host relaunches us with resume=1
+      if (lead) {
+        if (st) st[10] = (long long)(globaltimer() - t0);
+        S.ctl->rounds     = rounds;
+        S.ctl->any_change = any_change ? 1 : 0;
+        S.ctl->need_full  = 1;
+      }
+      return;
+    } else {
+      if (st && lead) st[10] = (long long)(globaltimer() - t0);
+      phase_rows(c, pc, ppar, fr, fr, stamp);
       grid.sync();
     }
-    if (st && lead) st[10] = (long long)(globaltimer() - t0);
-    phase_rows(c, pc, ppar, fr, fr, stamp);
-    grid.sync();
     if (st && lead) st[6] = (long long)(globaltimer() - t0);
     if (lead) {
       zero_par(qc);  // safe: every block has finished reading the previous round's counters
@@ -1251,14 +1322,16 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
       full = true;
       continue;
     }
-    phase_expand_rows(c, pc, qc, qpar, stamp);
+    // both expansions stop early once the next round is known to be a full round
+    phase_expand_rows(c, pc, qc, qpar, stamp, dense_thr);
     grid.sync();
     if (st && lead) st[8] = st[9] = (long long)(globaltimer() - t0);
     if (ldv(&qc->roww) > dense_thr) {
       full = true;
       continue;
     }
-    phase_expand_vars(c, pc, qc, qpar, stamp);
+    phase_expand_vars(c, pc, qc, qpar, stamp,
+                      dense_thr == ~0ull ? ~0ull : 2 * dense_thr - ldv(&qc->roww));
     grid.sync();
     if (st && lead) st[9] = (long long)(globaltimer() - t0);
     // a frontier round costs ~ its gathers (row nnz + col nnz); a fused full round ~ N = 4 dense_thr
@@ -1335,13 +1408,13 @@ struct Packed {
 };
 
 Packed pack_short(int count, const int* start, const int* idx, const double* val,
-                  const uint8_t* int_flag)
+                  const uint8_t* int_flag, int max_len, int tile_entries)
 {
   Packed pk;
   pk.ptr.push_back(0);
   for (int k = 0; k < count; ++k) {
     const int L = start[k + 1] - start[k];
-    if (L > kShortNnz) continue;
+    if (L > max_len) continue;
     pk.ids.push_back(k);
     for (int e = start[k]; e < start[k + 1]; ++e) {
       pk.idx.push_back(int_flag && int_flag[idx[e]] ? (idx[e] | kIntBit) : idx[e]);
@@ -1356,7 +1429,7 @@ Packed pack_short(int count, const int* start, const int* idx, const double* val
     pk.tile.push_back(r);
     const int base = pk.ptr[r];
     int q          = r;
-    while (q < ns && q - r < 32 && pk.ptr[q + 1] - base <= kTile) {
+    while (q < ns && q - r < 32 && pk.ptr[q + 1] - base <= tile_entries) {
       for (int e = pk.ptr[q]; e < pk.ptr[q + 1]; ++e) pk.own[e] = (uint8_t)(q - r);
       ++q;
     }
@@ -1421,7 +1494,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
 
   // Short rows / columns: packed tiles.
   {
-    Packed r   = pack_short(m, row_start, row_col, row_val, is_integer);
+    Packed r   = pack_short(m, row_start, row_col, row_val, is_integer, kPackNnz, kPackTile);
     P.n_srow   = (int)r.ids.size();
     P.n_srtile = (int)r.tile.size() - 1;
     P.srow.upload(r.ids);
@@ -1435,7 +1508,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
       desc[2 * t + 1] = r.ptr[r.tile[t]];
     }
     P.sr_tile.upload(desc);
-    Packed c   = pack_short(n, col_start, col_row_in, col_val_in, nullptr);
+    Packed c   = pack_short(n, col_start, col_row_in, col_val_in, nullptr, kShortNnz, kTile);
     P.n_scol   = (int)c.ids.size();
     P.n_sctile = (int)c.tile.size() - 1;
     P.scol.upload(c.ids);
@@ -1447,32 +1520,32 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   }
   // Long rows: gather pieces, fold tasks per 16384-segment (longest first: the fold is a
   // sequential chain), candidate pieces for rows above kCandSplit.
-  std::vector<int> long_off(m, -1), seg_base(m, -1), order;
-  long long goff = 0;
-  int slot       = 0;
+  // Full-round fold tasks (rows > kPackNnz, per 16384-segment, longest segments first: the fold
+  // is a sequential chain) and candidate pieces of rows above kCandSplit; frontier rounds fold
+  // every dirty row > kShortNnz (capacity nf_cap).
+  std::vector<int> seg_base(m, -1), order;
+  int slot = 0;
+  long long nf_front = 0;
   for (int k = 0; k < m; ++k) {
     const int L = row_start[k + 1] - row_start[k];
     if (L <= kShortNnz) continue;
-    long_off[k] = (int)goff;
-    goff += L;
     const int ns = (L + kSumSegment - 1) / kSumSegment;
+    nf_front += ns;
     if (ns > 1) {
       seg_base[k] = slot;
       slot += ns;
     }
-    order.push_back(k);
+    if (L > kPackNnz) order.push_back(k);
   }
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     return row_start[a + 1] - row_start[a] > row_start[b + 1] - row_start[b];
   });
-  std::vector<int2> piece, cpiece;
+  std::vector<int2> cpiece;
   std::vector<std::pair<int, int2>> folds;
   for (int k : order) {
     const int L = row_start[k + 1] - row_start[k];
-    for (int p = 0; p * kPiece < L; ++p) {
-      piece.push_back(make_int2(k, p));
-      if (L > kCandSplit) cpiece.push_back(make_int2(k, p));
-    }
+    if (L > kCandSplit)
+      for (int p = 0; p * kPiece < L; ++p) cpiece.push_back(make_int2(k, p));
     for (int s = 0; s * kSumSegment < L; ++s)
       folds.push_back({std::min(L - s * kSumSegment, kSumSegment), make_int2(k, s)});
   }
@@ -1480,14 +1553,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
                    [](const auto& a, const auto& b) { return a.first > b.first; });
   std::vector<int2> fold(folds.size());
   for (size_t j = 0; j < folds.size(); ++j) fold[j] = folds[j].second;
-  if (goff > 0x7FFFFFFFll) throw std::runtime_error("long-row entries exceed int32 offsets");
-  P.n_long_entries = goff;
-  P.n_piece        = (int)piece.size();
+  P.n_long_entries = 0;
+  P.n_piece        = 0;
   P.n_fold         = (int)fold.size();
   P.n_cpiece       = (int)cpiece.size();
   P.n_part         = slot;
-  P.long_off.upload(long_off);
-  P.piece_task.upload(piece);
   P.fold_task.upload(fold);
   P.cpiece_task.upload(cpiece);
   P.seg_base.upload(seg_base);
@@ -1506,7 +1576,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.bounds.alloc(nn);
   P.rec.alloc(mm);
   P.aux.alloc(mm);
-  P.gbuf.alloc((size_t)std::max(goff, 1ll));
+  P.gbuf.alloc(1);  // unused since folds gather directly (kept for the DevState layout)
   P.slot.alloc(nn);
   {
     std::vector<CandSlot> empty(nn);
@@ -1533,8 +1603,8 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   // int lists per parity: drow_s (m), dvar_s, dvar_m (n each); changed (n)
   P.lists_i.alloc(2 * (mm + 2 * nn) + nn);
   // int2 lists per parity: dpiece, dfold (all long-row tasks), xtask (N/256 + m)
-  const size_t np_cap = (size_t)std::max(P.n_piece, 1);
-  const size_t nf_cap = (size_t)std::max(P.n_fold, 1);
+  const size_t np_cap = 1;  // gather pieces: unused
+  const size_t nf_cap = (size_t)std::max(nf_front, 1ll);
   const size_t nx_cap = (size_t)(N / kTile) + mm + 1;
   P.lists_i2.alloc(2 * (np_cap + nf_cap + nx_cap) + (size_t)(N / kTile) + nn + 1);
   P.ctl.alloc(1);
@@ -1583,6 +1653,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine, kThreads, sizeof(Smem)));
   if (per_sm < 1) throw cuda_error("engine kernel cannot be resident (occupancy 0)");
   P.grid_blocks = dev_sms * std::min(per_sm, 4);
+  int per_sm2   = 0;
+  BP_CUDA(cudaFuncSetAttribute(k_rows_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(Smem)));
+  BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_rows_full, kThreads, sizeof(Smem)));
+  P.f2_blocks = dev_sms * std::max(per_sm2, 1);
   BP_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
   BP_CUDA(cudaEventCreate(&P.ev0));
   BP_CUDA(cudaEventCreate(&P.ev1));
@@ -1608,11 +1683,29 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   unsigned long long dense_thr =
       (flags & ENGINE_FORCE_FRONTIER) ? ~0ull : (unsigned long long)(P.nnz / 4);
   long long* stp = d_stats;
-  void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp};
+  static const bool no_ext = getenv("BP_NO_EXT_F2") != nullptr;
+  int ext        = (mode == MODE_PROPAGATE && !no_ext) ? 1 : 0;
+  int resume     = 0;
+  void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume};
   BP_CUDA(cudaEventRecord(P.ev0, s));
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
-  BP_CUDA(cudaEventRecord(P.ev1, s));
   ++g_kernel_launches;
+  while (ext) {  // full rounds: the row phase runs in k_rows_full, then the engine resumes
+    int h[2];
+    BP_CUDA(cudaMemcpyAsync(h, &P.st.ctl->rounds, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaMemcpyAsync(h + 1, &P.st.ctl->need_full, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaStreamSynchronize(s));
+    if (!h[1]) break;
+    BP_CUDA(cudaMemsetAsync(&P.st.ctl->need_full, 0, sizeof(int), s));
+    const int par           = h[0] & 1;
+    const unsigned stamp    = sb + (unsigned)h[0];
+    k_rows_full<<<P.f2_blocks, kThreads, sizeof(Smem), s>>>(d, st, l, par, stamp);
+    BP_CUDA(cudaGetLastError());
+    resume = 1;
+    BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
+    g_kernel_launches += 2;
+  }
+  BP_CUDA(cudaEventRecord(P.ev1, s));
   RunResult r{0, 0, 0, 0};
   if (mode == MODE_PROPAGATE) {
     int h[5];
@@ -1653,7 +1746,6 @@ void stage_rows(Problem& P, const int* rows, int nrows, cudaStream_t s)
     if (L <= kShortNnz) {
       sr.push_back(k);
     } else {
-      for (int q = 0; q * kPiece < L; ++q) pc.push_back(make_int2(k, q));
       for (int q = 0; q * kSumSegment < L; ++q) fd.push_back(make_int2(k, q));
     }
   }
