@@ -313,21 +313,23 @@ struct DevProblem {
   const double* col_val;
   const double2* cons;      // (lower, upper) per row
   const uint8_t* is_int;
-  // Rows with nnz <= kPackNnz packed contiguously in natural order and grouped into tiles of
-  // <= 32 rows / <= kPackTile entries: a warp streams a tile coalesced in 128-entry windows and
-  // every lane folds one row.
+  // Rows with nnz <= kPackNnz in SELL-32 slices (build: problem_build): n_srtile slices, slice s
+  // has 32 rows srow[32 s + i] (-1 padding) and entries sr_ci / sr_val[sr_tile[s] + 32 j + i].
   int n_srow, n_srtile;
-  const int* srow;          // packed index -> row id
-  const int* sr_ptr;        // n_srow + 1 offsets into sr_ci / sr_val
-  const int* sr_ci;         // column | integrality << 31
+  const int* srow;          // slice lane -> row id
+  const int* sr_ptr;        // unused
+  const int* sr_ci;         // column | integrality << 31, -1 = padding
   const double* sr_val;
-  const uint8_t* sr_own;    // owner's local row index inside its tile, per packed entry
-  const int* sr_tile;       // (n_srtile + 1) x {first packed row, first packed entry}
-  // Long rows (nnz > kShortNnz): their bounds are first gathered into a contiguous buffer
-  // (gbuf, pieces of kPiece entries), then one warp per 16384-entry segment folds it streaming.
-  const int* long_off;      // per row: offset of its entries in gbuf, -1 for short rows
+  const uint8_t* sr_own;    // unused
+  const int* sr_tile;       // n_srtile + 1 slice offsets
+  // Heavy rows (nnz > kHeavyFold): pieces of kPiece entries compute their contributions in
+  // parallel into gbuf (+ per-128-chunk aggregates in chunk_info), then one warp per
+  // 16384-entry segment streams gbuf and runs the reference's sequential sums: the sequential
+  // chain is the only serial part of a full round, so it is fed from a pure stream.
+  const int* long_off;      // per row: 128-aligned offset of its entries in gbuf, -1 otherwise
+  const int* hpiece;        // per heavy row: index of its first piece in piece_task
   int n_piece;
-  const int2* piece_task;   // (row, piece), longest rows first
+  const int2* piece_task;   // (row, piece) of heavy rows, longest rows first
   int n_fold;
   const int2* fold_task;    // (row, segment), longest segments first
   int n_cpiece;
@@ -350,6 +352,13 @@ constexpr int kTile      = 128;   // entries per tile / per gathered chunk (4 pe
 constexpr int kPiece     = 1024;  // gather / candidate piece of a long row (divides kSumSegment)
 constexpr int kFoldChunk = 256;   // staging chunk of the streamed fold (8 per lane)
 constexpr int kCandSplit = 2048;  // long rows above: candidates by parallel pieces
+constexpr int kHeavyFold = 1024;  // rows above: buffered fold (contribution pieces + stream)
+
+// Aggregates of one 128-entry chunk of a heavy row (infinite contributors, gating maxima).
+struct ChunkInfo {
+  double gtw, gpm;
+  int imn, imx;
+};
 #ifndef BP_PACK_NNZ
 #define BP_PACK_NNZ 32
 #endif

@@ -61,6 +61,7 @@ struct ParCtl {
   int cur_a, cur_b, cur_c, cur_vm, cur_vs;
   int cur_x1, cur_x2, n_xtask, stop;
   int n_ctask, cur_x3, cur_x4, xabort;  // xabort: a frontier expansion stopped early (full next)
+  int cur_p, pad2;                      // cur_p: heavy-row contribution pieces (full rounds)
   unsigned long long colnnz, roww, colw;
 };
 
@@ -84,6 +85,8 @@ struct DevState {
   CandSlot* slot;     // fused full round: per-var candidate slots
   unsigned* ready;    // per row: stamp of the round whose activity is published
   unsigned char* rquiet;  // per row: 1 if no entry can publish a candidate (set before `ready`)
+  ChunkInfo* cinfo;       // heavy rows: per 128-entry chunk of gbuf
+  unsigned* pstamp;       // per heavy-row piece: stamp of the round whose contributions are in gbuf
   SegPart* seg_part;
   int* seg_done;
   unsigned* row_stamp;
@@ -117,7 +120,9 @@ struct Problem {
   DBuf<int> srow, sr_ptr, sr_ci, sr_tile;
   DBuf<double> sr_val;
   DBuf<uint8_t> sr_own;
-  DBuf<int> long_off;
+  DBuf<int> long_off, hpiece;
+  DBuf<ChunkInfo> cinfo;
+  DBuf<unsigned> pstamp;
   DBuf<int2> piece_task, fold_task, cpiece_task;
   DBuf<int> scol, sc_ptr, sc_row, sc_tile;
   DBuf<double> sc_val;

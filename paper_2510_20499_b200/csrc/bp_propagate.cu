@@ -275,6 +275,80 @@ __device__ __forceinline__ double fold_seq(const double* src, int cnt, double ac
   return acc;
 }
 
+// Tail of a segment fold (warp-uniform inputs): combines the segment partials of multi-segment
+// rows in segment order (propagation.hpp:182-188), writes the row record, and continues with the
+// candidates (gated; inline for rows <= kCandSplit, else by publishing the row to the candidate
+// pieces).
+__device__ void fold_finish(Ctx& c, int k, int L, int seg, double smn, double smx, int imn, int imx,
+                            double gtw, double gpm, bool cand, unsigned stamp)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int lane      = c.lane;
+  const int nseg = (L + kSumSegment - 1) / kSumSegment;
+  int final_row  = 0;  // 1 if this warp holds the row's final activity
+  if (nseg == 1) {
+    final_row = 1;
+  } else {
+    if (lane == 0) {
+      const int base = __ldg(P.seg_base + k);
+      SegPart sp;
+      sp.min  = smn;
+      sp.max  = smx;
+      sp.nmin = imn;
+      sp.nmax = imx;
+      sp.tmax = gtw;
+      sp.pmax = gpm;
+      S.seg_part[base + seg] = sp;
+      __threadfence();
+      const int done = atomicAdd(&S.seg_done[k], 1);
+      if (done == nseg - 1) {
+        __threadfence();
+        double tmn = 0.0, tmx = 0.0;
+        int cmn = 0, cmx = 0;
+        for (int q = 0; q < nseg; ++q) {  // row_activity's segment fold (propagation.hpp:182-188)
+          const SegPart* sq = S.seg_part + base + q;
+          tmn = __dadd_rn(tmn, __ldcg(&sq->min));
+          tmx = __dadd_rn(tmx, __ldcg(&sq->max));
+          cmn += __ldcg(&sq->nmin);
+          cmx += __ldcg(&sq->nmax);
+          gtw = fmax(gtw, __ldcg(&sq->tmax));
+          gpm = fmax(gpm, __ldcg(&sq->pmax));
+        }
+        smn           = tmn;
+        smx           = tmx;
+        imn           = cmn;
+        imx           = cmx;
+        S.seg_done[k] = 0;
+        final_row     = 1;
+      }
+    }
+    final_row = __shfl_sync(FULL, final_row, 0);
+    smn       = __shfl_sync(FULL, smn, 0);
+    smx       = __shfl_sync(FULL, smx, 0);
+    imn       = __shfl_sync(FULL, imn, 0);
+    imx       = __shfl_sync(FULL, imx, 0);
+    gtw       = __shfl_sync(FULL, gtw, 0);
+    gpm       = __shfl_sync(FULL, gpm, 0);
+  }
+  if (!final_row) return;
+  if (lane == 0) write_rec(P, S, k, smn, smx, imn, imx);
+  if (!cand) return;
+  const double2 cb = __ldg(&P.cons[k]);
+  // row-level gating: no entry of the row can publish a candidate -> skip the candidate pass
+  const bool quiet = entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x);
+  if (L > kCandSplit) {
+    if (lane == 0) {
+      S.rquiet[k] = quiet ? 1 : 0;
+      __threadfence();
+      atomicExch(S.ready + k, stamp);
+    }
+    return;
+  }
+  if (quiet) return;
+  long_candidates(c, k, 0, L, smn, imn, smx, imx, cb.y, cb.x);
+}
+
 // F2 / P2: one 16384-entry segment of a long row, streamed in 128-entry chunks: the indices of
 // chunk j+2 and the bound gathers of chunk j+1 are in flight while lanes 0/1 run the reference's
 // sequential min/max sums over chunk j (zero contributions skipped: exact, the running sum is
@@ -361,68 +435,131 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   imx            = warp_sum(imx);
   double smn     = __shfl_sync(FULL, acc, 0);
   double smx     = __shfl_sync(FULL, acc, 1);
-  const int nseg = (L + kSumSegment - 1) / kSumSegment;
-  int final_row  = 0;  // 1 if this warp holds the row's final activity
-  if (nseg == 1) {
-    final_row = 1;
-  } else {
-    if (lane == 0) {
-      const int base = __ldg(P.seg_base + k);
-      SegPart sp;
-      sp.min  = smn;
-      sp.max  = smx;
-      sp.nmin = imn;
-      sp.nmax = imx;
-      sp.tmax = gtw;
-      sp.pmax = gpm;
-      S.seg_part[base + seg] = sp;
-      __threadfence();
-      const int done = atomicAdd(&S.seg_done[k], 1);
-      if (done == nseg - 1) {
-        __threadfence();
-        double tmn = 0.0, tmx = 0.0;
-        int cmn = 0, cmx = 0;
-        for (int q = 0; q < nseg; ++q) {  // row_activity's segment fold (propagation.hpp:182-188)
-          const SegPart* sq = S.seg_part + base + q;
-          tmn = __dadd_rn(tmn, __ldcg(&sq->min));
-          tmx = __dadd_rn(tmx, __ldcg(&sq->max));
-          cmn += __ldcg(&sq->nmin);
-          cmx += __ldcg(&sq->nmax);
-          gtw = fmax(gtw, __ldcg(&sq->tmax));
-          gpm = fmax(gpm, __ldcg(&sq->pmax));
-        }
-        smn           = tmn;
-        smx           = tmx;
-        imn           = cmn;
-        imx           = cmx;
-        S.seg_done[k] = 0;
-        final_row     = 1;
+  fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
+}
+
+// F2a (heavy rows): contributions of piece p (kPiece entries) of row k into gbuf, with the
+// per-128-chunk aggregates; the piece is published with this round's stamp.
+__device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int2 tk       = P.piece_task[pi];
+  const int k = tk.x, rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
+  const int off = __ldg(P.long_off + k);
+  const int e0 = tk.y * kPiece, e1 = min(L, e0 + kPiece);
+  for (int j0 = e0; j0 < e1; j0 += kTile) {
+    int ci[kEPL];
+    double a[kEPL];
+    double2 bd[kEPL];
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int e = j0 + h * 32 + c.lane;
+      ci[h]       = e < e1 ? __ldg(P.row_ci + rs + e) : -1;
+      a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+    int imn = 0, imx = 0;
+    double gtw = 0.0, gpm = 0.0;
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      double cm = 0.0, cx = 0.0;
+      if (ci[h] != -1) {
+        int i1, i2;
+        contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
+        imn += i1;
+        imx += i2;
+        double tw, pw;
+        entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pw);
+        gtw = fmax(gtw, tw);
+        gpm = fmax(gpm, pw);
       }
+      S.gbuf[off + j0 + h * 32 + c.lane] = make_double2(cm, cx);  // padding slots get 0.0
     }
-    final_row = __shfl_sync(FULL, final_row, 0);
-    smn       = __shfl_sync(FULL, smn, 0);
-    smx       = __shfl_sync(FULL, smx, 0);
-    imn       = __shfl_sync(FULL, imn, 0);
-    imx       = __shfl_sync(FULL, imx, 0);
-    gtw       = __shfl_sync(FULL, gtw, 0);
-    gpm       = __shfl_sync(FULL, gpm, 0);
+    imn = warp_sum(imn);
+    imx = warp_sum(imx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      gtw = fmax(gtw, __shfl_xor_sync(FULL, gtw, o));
+      gpm = fmax(gpm, __shfl_xor_sync(FULL, gpm, o));
+    }
+    if (c.lane == 0) {
+      ChunkInfo ci_{gtw, gpm, imn, imx};
+      S.cinfo[(off + j0) / kTile] = ci_;
+    }
   }
-  if (!final_row) return;
-  if (lane == 0) write_rec(P, S, k, smn, smx, imn, imx);
-  if (!cand) return;
-  const double2 cb = __ldg(&P.cons[k]);
-  // row-level gating: no entry of the row can publish a candidate -> skip the candidate pass
-  const bool quiet = entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x);
-  if (L > kCandSplit) {
+  __syncwarp();
+  if (c.lane == 0) {
+    __threadfence();
+    atomicExch(S.pstamp + pi, stamp);
+  }
+}
+
+// F2b (heavy rows): one 16384-entry segment. Waits for the segment's pieces, then streams their
+// contributions from gbuf (two chunks in flight) while lanes 0/1 run the sequential sums over
+// the order-preserving compaction of the non-zero contributions.
+__device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int lane      = c.lane;
+  const int L   = __ldg(P.row_start + k + 1) - __ldg(P.row_start + k);
+  const int off = __ldg(P.long_off + k);
+  const int e0 = seg * kSumSegment, e1 = min(L, e0 + kSumSegment);
+  {
+    const int p0 = __ldg(P.hpiece + k) + e0 / kPiece, np = (e1 - e0 + kPiece - 1) / kPiece;
+    if (lane < np)
+      while (ldv(S.pstamp + p0 + lane) != stamp) __nanosleep(100);
+    __syncwarp();
+    __threadfence();
+  }
+  const double2* gb = S.gbuf + off;
+  double2 v[kEPL], w[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    v[h] = __ldcg(gb + e0 + h * 32 + lane);
+    w[h] = e0 + kTile < e1 ? __ldcg(gb + e0 + kTile + h * 32 + lane) : make_double2(0.0, 0.0);
+  }
+  double acc = 0.0, gtw = 0.0, gpm = 0.0;
+  int imn = 0, imx = 0;
+  const unsigned lt = lanemask_lt();
+  for (int base = e0; base < e1; base += kTile) {
     if (lane == 0) {
-      S.rquiet[k] = quiet ? 1 : 0;
-      __threadfence();
-      atomicExch(S.ready + k, stamp);
+      const ChunkInfo* ch = S.cinfo + (off + base) / kTile;
+      imn += __ldcg(&ch->imn);
+      imx += __ldcg(&ch->imx);
+      gtw = fmax(gtw, __ldcg(&ch->gtw));
+      gpm = fmax(gpm, __ldcg(&ch->gpm));
     }
-    return;
+    int pm = 0, px = 0;
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const double cm = v[h].x, cx = v[h].y;  // beyond e1: padding zeros
+      const unsigned m = __ballot_sync(FULL, cm != 0.0);
+      const unsigned x = __ballot_sync(FULL, cx != 0.0);
+      if (cm != 0.0) c.w.b0[pm + __popc(m & lt)] = cm;
+      if (cx != 0.0) c.w.b1[px + __popc(x & lt)] = cx;
+      pm += __popc(m);
+      px += __popc(x);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      v[h]         = w[h];
+      const int e2 = base + 2 * kTile + h * 32 + lane;
+      w[h]         = base + 2 * kTile < e1 ? __ldcg(gb + e2) : make_double2(0.0, 0.0);
+    }
+    if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
+    __syncwarp();
   }
-  if (quiet) return;
-  long_candidates(c, k, 0, L, smn, imn, smx, imx, cb.y, cb.x);
+  imn = __shfl_sync(FULL, imn, 0);
+  imx = __shfl_sync(FULL, imx, 0);
+  gtw = __shfl_sync(FULL, gtw, 0);
+  gpm = __shfl_sync(FULL, gpm, 0);
+  const double smn = __shfl_sync(FULL, acc, 0);
+  const double smx = __shfl_sync(FULL, acc, 1);
+  fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
 }
 
 // F2 tail: candidate piece p of a row with > kCandSplit entries, once its activity is published.
@@ -448,95 +585,60 @@ __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp)
   long_candidates(c, k, p * kPiece, min(L, (p + 1) * kPiece), mnf, nmn, mxf, nmx, r.g, r.h);
 }
 
-// Loads window w0 of a packed row tile (entries p0 + w0 + [0, 128)) and gathers its bounds.
-__device__ __forceinline__ void tile_window(const Ctx& c, int p0, int p1, int w0, int* ci, double* a,
-                                            int* own, double2* bd)
-{
-  const DevProblem& P = c.P;
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    const int f = p0 + w0 + h * 32 + c.lane;
-    ci[h]       = f < p1 ? __ldg(P.sr_ci + f) : -1;
-    a[h]        = f < p1 ? __ldg(P.sr_val + f) : 0.0;
-    own[h]      = f < p1 ? __ldg(P.sr_own + f) : 0;
-  }
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) bd[h] = ci[h] != -1 ? c.S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
-}
+// One SELL-32 slice (32 rows of similar length <= kPackNnz, entries column-interleaved: entry j
+// of lane i at base + 32 j + i): thread per row. Each lane streams its row in order with 4
+// entries' loads and bound gathers in flight, runs the reference's sequential min/max sums in
+// registers (rows here are single-segment), writes the row record, then -- with `cand`, unless
+// every row of the slice is provably quiet -- streams the row again for the candidates.
+#ifndef BP_SELL_UNROLL
+#define BP_SELL_UNROLL 4
+#endif
+constexpr int kSellUnroll = BP_SELL_UNROLL;  // entries per lane in flight
 
-// Candidates of one loaded window of a packed row tile (row activities in w.ract / w.rinf).
-__device__ __forceinline__ void tile_candidates(Ctx& c, const int* ci, const double* a, const int* own,
-                                                const double2* bd)
-{
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    if (ci[h] == -1) continue;
-    const int o       = own[h];
-    const double2 rcb = c.w.vb[o];
-    double tw, pm;
-    entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pm);
-    if (entry_quiet(tw, pm, c.w.ract[o][0], c.w.rinf[o][0], c.w.ract[o][1], c.w.rinf[o][1], rcb.y,
-                    rcb.x))
-      continue;
-    double cl, cu;
-    cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], c.w.ract[o][0], c.w.rinf[o][0],
-                  c.w.ract[o][1], c.w.rinf[o][1], rcb.y, rcb.x, cl, cu);
-    publish(c.S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, c.w.rk[o]);
-  }
-}
-
-// A packed tile of <= 32 rows of <= kPackNnz entries each (<= kPackTile entries): the warp
-// streams it coalesced in 128-entry windows (bounds gathered per window), every lane folds its
-// own row in the reference's order across the windows, then (with `cand`) the candidates of every
-// entry are computed -- from the registers that still hold the window when the tile is a single
-// window, else from a second streamed pass.
-__device__ void short_tile(Ctx& c, int t, bool cand)
+__device__ void sell_slice(Ctx& c, int sl, bool cand)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  const int2 d0 = __ldg(reinterpret_cast<const int2*>(P.sr_tile) + t);      // (r0, p0)
-  const int2 d1 = __ldg(reinterpret_cast<const int2*>(P.sr_tile) + t + 1);  // (r1, p1)
-  const int r0 = d0.x, p0 = d0.y, r1 = d1.x, p1 = d1.y;
-  const int nr = r1 - r0, T = p1 - p0;
-  int ci[kEPL], own[kEPL];
-  double a[kEPL];
-  double2 bd[kEPL];
-  tile_window(c, p0, p1, 0, ci, a, own, bd);
-  int k = -1, q0 = 0, q1 = 0;
-  if (c.lane < nr) {
-    k  = __ldg(P.srow + r0 + c.lane);
-    q0 = __ldg(P.sr_ptr + r0 + c.lane) - p0;
-    q1 = __ldg(P.sr_ptr + r0 + c.lane + 1) - p0;
-  }
-  const double2 cb = k >= 0 ? __ldg(&P.cons[k]) : make_double2(0.0, 0.0);
-  double smn = 0.0, smx = 0.0;
+  const int b0 = __ldg(P.sr_tile + sl), b1 = __ldg(P.sr_tile + sl + 1);
+  const int Lm = (b1 - b0) >> 5;
+  const int k  = __ldg(P.srow + 32 * sl + c.lane);
+  const int* ciq   = P.sr_ci + b0 + c.lane;
+  const double* aq = P.sr_val + b0 + c.lane;
+  double smn = 0.0, smx = 0.0, gtw = 0.0, gpm = 0.0;
   int imn = 0, imx = 0;
-  for (int w0 = 0;;) {
+  constexpr int U = kSellUnroll;
+  for (int j = 0; j < Lm; j += U) {
+    int ci[U];
+    double a[U];
+    double2 bd[U];
 #pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      double cm = 0.0, cx = 0.0;
-      int i1 = 0, i2 = 0;
-      if (ci[h] != -1) contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
-      c.w.b0[h * 32 + c.lane] = cm;
-      c.w.b1[h * 32 + c.lane] = cx;
-      c.w.fl[h * 32 + c.lane] = (unsigned char)(i1 | (i2 << 1));
+    for (int u = 0; u < U; ++u) {
+      ci[u] = j + u < Lm ? __ldg(ciq + 32 * (j + u)) : -1;
+      a[u]  = j + u < Lm ? __ldg(aq + 32 * (j + u)) : 0.0;
     }
-    __syncwarp();
-    if (k >= 0) {
-      const int qa = max(q0, w0) - w0, qb = min(q1, w0 + kTile) - w0;
-      for (int q = qa; q < qb; ++q) {
-        smn = __dadd_rn(smn, c.w.b0[q]);
-        smx = __dadd_rn(smx, c.w.b1[q]);
-        imn += c.w.fl[q] & 1;
-        imx += c.w.fl[q] >> 1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) bd[u] = ci[u] != -1 ? S.bounds[ci[u] & ~kIntBit] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (ci[u] == -1) continue;  // padding only follows a row's last entry
+      double cm, cx;
+      int i1, i2;
+      contrib(a[u], bd[u].x, bd[u].y, cm, cx, i1, i2);
+      smn = __dadd_rn(smn, cm);
+      smx = __dadd_rn(smx, cx);
+      imn += i1;
+      imx += i2;
+      if (cand) {
+        double tw, pw;
+        entry_reach(a[u], bd[u].x, bd[u].y, ci[u] < 0, tw, pw);
+        gtw = fmax(gtw, tw);
+        gpm = fmax(gpm, pw);
       }
     }
-    __syncwarp();
-    w0 += kTile;
-    if (w0 >= T) break;
-    tile_window(c, p0, p1, w0, ci, a, own, bd);
   }
+  double2 cb = make_double2(0.0, 0.0);
   if (k >= 0) {
+    cb = __ldg(&P.cons[k]);
     RowRec r;
     r.min = imn ? box_count(imn) : smn;
     r.max = imx ? box_count(imx) : smx;
@@ -544,25 +646,32 @@ __device__ void short_tile(Ctx& c, int t, bool cand)
     r.h   = cb.x;
     st_rec(S.rec + k, r);
     if (imn | imx) S.aux[k] = make_double2(smn, smx);
-    c.w.ract[c.lane][0] = smn;
-    c.w.ract[c.lane][1] = smx;
-    c.w.rinf[c.lane][0] = imn;
-    c.w.rinf[c.lane][1] = imx;
-    c.w.rk[c.lane]      = k;
-    c.w.vb[c.lane]      = cb;
   }
-  __syncwarp();
-  if (cand) {
-    if (T <= kTile) {
-      tile_candidates(c, ci, a, own, bd);
-    } else {
-      for (int w0 = 0; w0 < T; w0 += kTile) {
-        tile_window(c, p0, p1, w0, ci, a, own, bd);
-        tile_candidates(c, ci, a, own, bd);
-      }
+  if (!cand) return;
+  const bool quiet = k < 0 || entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x);
+  if (__all_sync(FULL, quiet)) return;
+  for (int j = 0; j < Lm; j += U) {
+    int ci[U];
+    double a[U];
+    double2 bd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ci[u] = !quiet && j + u < Lm ? __ldg(ciq + 32 * (j + u)) : -1;
+      a[u]  = !quiet && j + u < Lm ? __ldg(aq + 32 * (j + u)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) bd[u] = ci[u] != -1 ? S.bounds[ci[u] & ~kIntBit] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (ci[u] == -1) continue;
+      double tw, pw;
+      entry_reach(a[u], bd[u].x, bd[u].y, ci[u] < 0, tw, pw);
+      if (entry_quiet(tw, pw, smn, imn, smx, imx, cb.y, cb.x)) continue;
+      double cl, cu;
+      cand_explicit(bd[u].x, bd[u].y, ci[u] < 0, a[u], smn, imn, smx, imx, cb.y, cb.x, cl, cu);
+      publish(S.slot + (ci[u] & ~kIntBit), cl, cu, bd[u].x, bd[u].y, k);
     }
   }
-  __syncwarp();
 }
 
 // Listed short rows (frontier rounds): flattened 128-entry windows, each lane folds its row.
@@ -622,6 +731,17 @@ __device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
   if (k >= 0) write_rec(P, c.S, k, smn, smx, imn, imx);
 }
 
+// Debug counters (BP_DEBUG=1): per task kind total / max cycles and count.
+__device__ __forceinline__ void dbg_task(Ctx& c, int kind, long long c0)
+{
+  if (c.S.dbg && c.lane == 0) {
+    const unsigned long long d = (unsigned long long)(clock64() - c0);
+    atomicAdd(c.S.dbg + 3 * kind, d);
+    atomicMax(c.S.dbg + 3 * kind + 1, d);
+    atomicAdd(c.S.dbg + 3 * kind + 2, 1ull);
+  }
+}
+
 // Phase 2 (F2 / P2): activities of all rows (full) or the dirty ones; `cand` fuses tightening.
 __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, unsigned stamp)
 {
@@ -630,31 +750,31 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
   const int nf        = full ? P.n_fold : ldv(&pc->n_dfold);
   const int2* folds   = full ? P.fold_task : S.dfold[par];
   if (full) {
-    // one cursor over [folds | short tiles | candidate pieces]: the longest chains start first
-    const int ns = P.n_srtile, nc = cand ? P.n_cpiece : 0;
-    const int total = nf + ns + nc;
-    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < total; it_t.advance()) {
-      const int t                = it_t.t;
-      const long long c0         = S.dbg ? clock64() : 0;
-      int kind;
-      if (t < nf) {
-        const int2 tk = folds[t];
-        long_fold(c, tk.x, tk.y, cand, stamp);
-        kind = 0;
-      } else if (t < nf + ns) {
-        short_tile(c, t - nf, cand);
-        kind = 1;
-      } else {
-        const int2 tk = P.cpiece_task[t - nf - ns];
-        long_cand_piece(c, tk.x, tk.y, stamp);
-        kind = 2;
-      }
-      if (S.dbg && c.lane == 0) {  // debug counters: per task kind total / max cycles, count
-        const unsigned long long d = (unsigned long long)(clock64() - c0);
-        atomicAdd(S.dbg + 3 * kind, d);
-        atomicMax(S.dbg + 3 * kind + 1, d);
-        atomicAdd(S.dbg + 3 * kind + 2, 1ull);
-      }
+    // long folds first (longest chains start first), then the SELL slices (4 per fetch: one
+    // cursor shared by the whole grid is the contended resource), then candidate pieces of rows
+    // above kCandSplit (they wait for their row's fold, all of which have been fetched by then)
+    // heavy rows' contribution pieces first: the segment folds that wait for them are fetched
+    // only after every piece has been fetched by a running warp (no deadlock)
+    for (Prefetch it_t(c, &pc->cur_p, 1); it_t.t < P.n_piece; it_t.advance()) heavy_piece(c, it_t.t, stamp);
+    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nf; it_t.advance()) {
+      const long long c0 = S.dbg ? clock64() : 0;
+      const int2 tk      = folds[it_t.t];
+      if (__ldg(P.long_off + tk.x) >= 0) heavy_fold(c, tk.x, tk.y, cand, stamp);
+      else long_fold(c, tk.x, tk.y, cand, stamp);
+      dbg_task(c, 0, c0);
+    }
+    const int ns = P.n_srtile;
+    for (Prefetch it_t(c, &pc->cur_a, 4); it_t.t < ns; it_t.advance()) {
+      const long long c0 = S.dbg ? clock64() : 0;
+      for (int q = it_t.t; q < min(ns, it_t.t + 4); ++q) sell_slice(c, q, cand);
+      dbg_task(c, 1, c0);
+    }
+    const int nc = cand ? P.n_cpiece : 0;
+    for (Prefetch it_t(c, &pc->cur_c, 1); it_t.t < nc; it_t.advance()) {
+      const long long c0 = S.dbg ? clock64() : 0;
+      const int2 tk      = P.cpiece_task[it_t.t];
+      long_cand_piece(c, tk.x, tk.y, stamp);
+      dbg_task(c, 2, c0);
     }
   } else {
     for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nf; it_t.advance()) {
@@ -1377,6 +1497,7 @@ DevProblem Problem::dev() const
   d.sr_own      = sr_own.p;
   d.sr_tile     = sr_tile.p;
   d.long_off    = long_off.p;
+  d.hpiece      = hpiece.p;
   d.n_piece     = n_piece;
   d.piece_task  = piece_task.p;
   d.n_fold      = n_fold;
@@ -1494,20 +1615,44 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
 
   // Short rows / columns: packed tiles.
   {
-    Packed r   = pack_short(m, row_start, row_col, row_val, is_integer, kPackNnz, kPackTile);
-    P.n_srow   = (int)r.ids.size();
-    P.n_srtile = (int)r.tile.size() - 1;
-    P.srow.upload(r.ids);
-    P.sr_ptr.upload(r.ptr);
-    P.sr_ci.upload(r.idx);
-    P.sr_val.upload(r.val);
-    P.sr_own.upload(r.own);
-    std::vector<int> desc(2 * r.tile.size());  // (first packed row, first packed entry) per tile
-    for (size_t t = 0; t < r.tile.size(); ++t) {
-      desc[2 * t]     = r.tile[t];
-      desc[2 * t + 1] = r.ptr[r.tile[t]];
+    // Rows with nnz <= kPackNnz as SELL-32 slices: rows sorted by length (descending, stable), 32
+    // per slice, each slice padded to its longest row, entries column-interleaved so lane i reads
+    // entry j of its row at base + 32 j + i (coalesced). Any grouping is exact: every row is
+    // summed by one thread in its own order, and candidate publication is order-independent.
+    std::vector<int> srows;
+    for (int k = 0; k < m; ++k)
+      if (row_start[k + 1] - row_start[k] <= kPackNnz) srows.push_back(k);
+    std::stable_sort(srows.begin(), srows.end(), [&](int a, int b) {
+      return row_start[a + 1] - row_start[a] > row_start[b + 1] - row_start[b];
+    });
+    const int nsl = ((int)srows.size() + 31) / 32;
+    std::vector<int> sbase(nsl + 1, 0), srow(32 * (size_t)nsl, -1);
+    long long tot = 0;
+    for (int sl = 0; sl < nsl; ++sl) {
+      sbase[sl]      = (int)tot;
+      const int Lmax = row_start[srows[32 * sl] + 1] - row_start[srows[32 * sl]];
+      tot += 32ll * Lmax;
+      if (tot > 0x7FFFFFFFll) throw std::runtime_error("SELL slices exceed int32 offsets");
     }
-    P.sr_tile.upload(desc);
+    sbase[nsl] = (int)tot;
+    std::vector<int> sci((size_t)tot, -1);
+    std::vector<double> sval((size_t)tot, 0.0);
+    for (int sl = 0; sl < nsl; ++sl)
+      for (int i = 0; i < 32 && 32 * sl + i < (int)srows.size(); ++i) {
+        const int k           = srows[32 * sl + i];
+        srow[32 * (size_t)sl + i] = k;
+        for (int e = row_start[k], j = 0; e < row_start[k + 1]; ++e, ++j) {
+          const size_t q = (size_t)sbase[sl] + 32 * (size_t)j + i;
+          sci[q]         = is_integer[row_col[e]] ? (row_col[e] | kIntBit) : row_col[e];
+          sval[q]        = row_val[e];
+        }
+      }
+    P.n_srow   = (int)srows.size();
+    P.n_srtile = nsl;
+    P.srow.upload(srow);
+    P.sr_ci.upload(sci);
+    P.sr_val.upload(sval);
+    P.sr_tile.upload(sbase);
     Packed c   = pack_short(n, col_start, col_row_in, col_val_in, nullptr, kShortNnz, kTile);
     P.n_scol   = (int)c.ids.size();
     P.n_sctile = (int)c.tile.size() - 1;
@@ -1540,12 +1685,21 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     return row_start[a + 1] - row_start[a] > row_start[b + 1] - row_start[b];
   });
-  std::vector<int2> cpiece;
+  std::vector<int2> cpiece, piece;
   std::vector<std::pair<int, int2>> folds;
+  std::vector<int> long_off(m, -1), hpiece(m, -1);
+  long long goff = 0;
   for (int k : order) {
     const int L = row_start[k + 1] - row_start[k];
     if (L > kCandSplit)
       for (int p = 0; p * kPiece < L; ++p) cpiece.push_back(make_int2(k, p));
+    if (L > kHeavyFold) {
+      long_off[k] = (int)goff;
+      goff += ((L + kTile - 1) / kTile) * (long long)kTile;
+      if (goff > 0x7FFFFFFFll) throw std::runtime_error("heavy-row entries exceed int32 offsets");
+      hpiece[k] = (int)piece.size();
+      for (int p = 0; p * kPiece < L; ++p) piece.push_back(make_int2(k, p));
+    }
     for (int s = 0; s * kSumSegment < L; ++s)
       folds.push_back({std::min(L - s * kSumSegment, kSumSegment), make_int2(k, s)});
   }
@@ -1553,8 +1707,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
                    [](const auto& a, const auto& b) { return a.first > b.first; });
   std::vector<int2> fold(folds.size());
   for (size_t j = 0; j < folds.size(); ++j) fold[j] = folds[j].second;
-  P.n_long_entries = 0;
-  P.n_piece        = 0;
+  P.n_long_entries = goff;
+  P.n_piece        = (int)piece.size();
+  P.long_off.upload(long_off);
+  P.hpiece.upload(hpiece);
+  P.piece_task.upload(piece);
   P.n_fold         = (int)fold.size();
   P.n_cpiece       = (int)cpiece.size();
   P.n_part         = slot;
@@ -1576,7 +1733,10 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.bounds.alloc(nn);
   P.rec.alloc(mm);
   P.aux.alloc(mm);
-  P.gbuf.alloc(1);  // unused since folds gather directly (kept for the DevState layout)
+  P.gbuf.alloc((size_t)std::max(P.n_long_entries, 1ll));
+  P.cinfo.alloc((size_t)std::max(P.n_long_entries / kTile, 1ll));
+  P.pstamp.alloc((size_t)std::max(P.n_piece, 1));
+  BP_CUDA(cudaMemset(P.pstamp.p, 0, sizeof(unsigned) * std::max(P.n_piece, 1)));
   P.slot.alloc(nn);
   {
     std::vector<CandSlot> empty(nn);
@@ -1616,6 +1776,8 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.slot      = P.slot.p;
   S.ready     = P.ready.p;
   S.rquiet    = P.rquiet.p;
+  S.cinfo     = P.cinfo.p;
+  S.pstamp    = P.pstamp.p;
   S.seg_part  = P.seg_part.p;
   S.seg_done  = P.seg_done.p;
   S.row_stamp = P.row_stamp.p;
@@ -1676,6 +1838,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
     BP_CUDA(cudaMemsetAsync(P.row_stamp.p, 0, sizeof(unsigned) * P.row_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.var_stamp.p, 0, sizeof(unsigned) * P.var_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.ready.p, 0, sizeof(unsigned) * P.ready.n, s));
+    BP_CUDA(cudaMemsetAsync(P.pstamp.p, 0, sizeof(unsigned) * P.pstamp.n, s));
     P.stamp_base = 1;
   }
   unsigned sb = P.stamp_base;
@@ -1721,7 +1884,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   if (P.st.dbg) {
     unsigned long long h[16];
     BP_CUDA(cudaMemcpy(h, P.st.dbg, sizeof(h), cudaMemcpyDeviceToHost));
-    const char* nm[3] = {"fold", "short_tile", "cand_piece"};
+    const char* nm[3] = {"fold", "sell_slice", "cand_piece"};
     for (int q = 0; q < 3; ++q)
       fprintf(stderr, "[bp dbg] %-10s n=%llu avg=%.1f us max=%.1f us total=%.1f warp-ms\n", nm[q],
               h[3 * q + 2], h[3 * q + 2] ? h[3 * q] / 1965.0 / h[3 * q + 2] : 0.0,

@@ -10,7 +10,7 @@ run() {  # name
   BP_DEBUG=1 timeout 300 python tools/ncu_target.py --workload C2 --reps 1 > $O/dbg_$1.log 2>&1
 }
 run default
-BP_NO_EXT_F2=1 run noext
+
 for v in $(ls paper_2510_20499_b200/variants/ | sed 's/libbp_//; s/\.so//'); do
   BP_LIB=paper_2510_20499_b200/variants/libbp_$v.so run $v
 done
