@@ -346,6 +346,7 @@ struct DevProblem {
   // Long columns (nnz > kShortNnz), nnz descending: one warp per variable.
   int n_mcol;
   const int* mcol;
+  const unsigned long long* reach;  // per var: upper bound of the frontier work a change causes
 };
 
 constexpr int kTile      = 128;   // entries per tile / per gathered chunk (4 per lane)

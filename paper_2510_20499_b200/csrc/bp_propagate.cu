@@ -108,6 +108,7 @@ struct Smem {
   int blk_crossed;
   int blk_any_rows;
   unsigned long long blk_colnnz;
+  unsigned long long blk_reach;
 };
 
 struct Ctx {
@@ -743,7 +744,10 @@ __device__ __forceinline__ void dbg_task(Ctx& c, int kind, long long c0)
 }
 
 // Phase 2 (F2 / P2): activities of all rows (full) or the dirty ones; `cand` fuses tightening.
-__device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, unsigned stamp)
+// pieces_here = false: the candidate pieces of rows above kCandSplit are left to a following
+// k_cand_pieces launch (no warp spins on an unfinished row's activity).
+__device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, unsigned stamp,
+                           bool pieces_here = true)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
@@ -769,7 +773,7 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       for (int q = it_t.t; q < min(ns, it_t.t + 4); ++q) sell_slice(c, q, cand);
       dbg_task(c, 1, c0);
     }
-    const int nc = cand ? P.n_cpiece : 0;
+    const int nc = cand && pieces_here ? P.n_cpiece : 0;
     for (Prefetch it_t(c, &pc->cur_c, 1); it_t.t < nc; it_t.advance()) {
       const long long c0 = S.dbg ? clock64() : 0;
       const int2 tk      = P.cpiece_task[it_t.t];
@@ -794,6 +798,7 @@ struct Tally {
   int crossed;
   int any_rows;
   unsigned long long colnnz;
+  unsigned long long reach;  // Σ reach[i] of the changed vars: upper bound of the next frontier's work
   int nbuf;  // warp-uniform count of staged changed vars
 };
 
@@ -830,6 +835,7 @@ __device__ __forceinline__ void tally(Ctx& c, ParCtl* pc, Tally& t, int i, int r
   if (r > 0) {
     const int nnz = __ldg(c.P.col_start + i + 1) - __ldg(c.P.col_start + i);
     t.colnnz += (unsigned long long)nnz;
+    t.reach += __ldg(c.P.reach + i);
     if (nnz > 0) t.any_rows = 1;
   }
   if (ch) {
@@ -845,19 +851,24 @@ __device__ void tally_flush_block(Ctx& c, ParCtl* pc, Tally& t)
   flush_changed(c, pc, t);
   const int cr = warp_sum(t.crossed);
   const int ar = __any_sync(FULL, t.any_rows);
-  unsigned long long cn = t.colnnz;
+  unsigned long long cn = t.colnnz, rh = t.reach;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) rh += __shfl_xor_sync(FULL, rh, o);
 #pragma unroll
   for (int o = 16; o; o >>= 1) cn += __shfl_xor_sync(FULL, cn, o);
   if (c.lane == 0) {
     if (cr) atomicAdd(&c.sm.blk_crossed, cr);
     if (ar) atomicOr(&c.sm.blk_any_rows, 1);
     if (cn) atomicAdd(&c.sm.blk_colnnz, cn);
+    if (rh) atomicAdd(&c.sm.blk_reach, rh);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     if (c.sm.blk_crossed) atomicAdd(&pc->n_crossed, c.sm.blk_crossed);
     if (c.sm.blk_any_rows) atomicOr(&pc->any_rows, 1);
     if (c.sm.blk_colnnz) atomicAdd(&pc->colnnz, c.sm.blk_colnnz);
+    if (c.sm.blk_reach) atomicAdd(&pc->reach, c.sm.blk_reach);
+    c.sm.blk_reach    = 0;
     c.sm.blk_crossed  = 0;
     c.sm.blk_any_rows = 0;
     c.sm.blk_colnnz   = 0;
@@ -870,7 +881,7 @@ __device__ void phase_finalize(Ctx& c, ParCtl* pc)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  Tally t{0, 0, 0ull, 0};
+  Tally t{0, 0, 0ull, 0ull, 0};
   for (Prefetch it_q(c, &pc->cur_vs, 32); it_q.t < P.n; it_q.advance()) {
     const int q = it_q.t;
     const int i = q + c.lane;
@@ -1061,7 +1072,7 @@ __device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  Tally t{0, 0, 0ull, 0};
+  Tally t{0, 0, 0ull, 0ull, 0};
   {
     const int n    = full ? P.n_mcol : ldv(&pc->n_dvar_m);
     const int* ids = full ? P.mcol : S.dvar_m[par];
@@ -1311,7 +1322,22 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
   Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
-  phase_rows(c, &S.ctl->par[par], par, true, true, stamp);
+  phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false);
+}
+
+// Candidate pieces of rows above kCandSplit, after k_rows_full published their activities.
+__global__ void __launch_bounds__(kThreads) k_cand_pieces(DevProblem P, DevState S, Limits lim,
+                                                          int par, unsigned stamp)
+{
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
+  const int warp = threadIdx.x >> 5;
+  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
+  const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  for (int t = gw; t < P.n_cpiece; t += nw) {
+    const int2 tk = P.cpiece_task[t];
+    long_cand_piece(c, tk.x, tk.y, stamp);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
@@ -1325,6 +1351,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     sm.blk_crossed  = 0;
     sm.blk_any_rows = 0;
     sm.blk_colnnz   = 0;
+    sm.blk_reach    = 0;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5;
@@ -1438,7 +1465,11 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     }
     if (rounds >= lim.max_rounds) break;
     if (ldv(&pc->stop)) break;       // time limit (propagation.hpp:439)
-    if (!lim.incremental || ldv(&pc->colnnz) > dense_thr) {
+    // the next frontier would span the matrix: even the upper bound of its work (Σ reach of the
+    // changed vars, duplicates counted) is checked against 4x the full-round threshold, so a
+    // "full" prediction is only taken when the frontier is certainly large or nearly so
+    if (!lim.incremental || ldv(&pc->colnnz) > dense_thr ||
+        (dense_thr != ~0ull && ldv(&pc->reach) > 4 * dense_thr)) {
       full = true;
       continue;
     }
@@ -1514,6 +1545,7 @@ DevProblem Problem::dev() const
   d.sc_own      = sc_own.p;
   d.sc_tile     = sc_tile.p;
   d.n_mcol      = n_mcol;
+  d.reach       = reach.p;
   d.mcol        = mcol.p;
   return d;
 }
@@ -1718,6 +1750,21 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.fold_task.upload(fold);
   P.cpiece_task.upload(cpiece);
   P.seg_base.upload(seg_base);
+  // reach[i] = Σ_{k in col i} (len(k) + Σ_{j in row k} collen(j)): an upper bound of the frontier
+  // work (row + column incidences) a change of var i can cause in the next round.
+  {
+    std::vector<unsigned long long> rowcol(m, 0);
+    for (int k = 0; k < m; ++k) {
+      unsigned long long acc = (unsigned long long)(row_start[k + 1] - row_start[k]);
+      for (int e = row_start[k]; e < row_start[k + 1]; ++e)
+        acc += (unsigned long long)(col_start[row_col[e] + 1] - col_start[row_col[e]]);
+      rowcol[k] = acc;
+    }
+    std::vector<unsigned long long> rc(n, 0);
+    for (int i = 0; i < n; ++i)
+      for (int e = col_start[i]; e < col_start[i + 1]; ++e) rc[i] += rowcol[col_row_in[e]];
+    P.reach.upload(rc);
+  }
   // Long columns, longest first.
   std::vector<int> mcol;
   for (int i = 0; i < n; ++i)
@@ -1818,6 +1865,8 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   int per_sm2   = 0;
   BP_CUDA(cudaFuncSetAttribute(k_rows_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)sizeof(Smem)));
+  BP_CUDA(cudaFuncSetAttribute(k_cand_pieces, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(Smem)));
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_rows_full, kThreads, sizeof(Smem)));
   P.f2_blocks = dev_sms * std::max(per_sm2, 1);
   BP_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
@@ -1864,6 +1913,12 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
     const unsigned stamp    = sb + (unsigned)h[0];
     k_rows_full<<<P.f2_blocks, kThreads, sizeof(Smem), s>>>(d, st, l, par, stamp);
     BP_CUDA(cudaGetLastError());
+    if (P.n_cpiece) {
+      k_cand_pieces<<<std::min(P.f2_blocks, (P.n_cpiece + kWarps - 1) / kWarps), kThreads, sizeof(Smem), s>>>(
+          d, st, l, par, stamp);
+      BP_CUDA(cudaGetLastError());
+      ++g_kernel_launches;
+    }
     resume = 1;
     BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
     g_kernel_launches += 2;
