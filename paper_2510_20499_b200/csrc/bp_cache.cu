@@ -322,7 +322,8 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   const int ntask = (int)tv.size();
   std::vector<int> fallback;
   if (certified && ntask) {
-    const int chunk = 1 << 18;
+    // chunks small enough for the time budget to be honoured between them
+    const int chunk = std::isfinite(budget_sec) && budget_sec < 1e6 ? (1 << 14) : (1 << 18);
     DBuf<int> dvar, dcur, dstat, dcnt;
     DBuf<double> dlo, dup;
     DBuf<long long> doff;

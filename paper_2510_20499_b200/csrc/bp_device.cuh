@@ -346,7 +346,8 @@ struct DevProblem {
   // Long columns (nnz > kShortNnz), nnz descending: one warp per variable.
   int n_mcol;
   const int* mcol;
-  const unsigned long long* reach;  // per var: upper bound of the frontier work a change causes
+  const unsigned long long* reach;  // per var: frontier work a change causes (light, heavy rows)
+  unsigned long long h_reach;       // Σ over heavy rows of their reach (caps the heavy parts)
 };
 
 constexpr int kTile      = 128;   // entries per tile / per gathered chunk (4 per lane)

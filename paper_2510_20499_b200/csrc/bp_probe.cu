@@ -35,6 +35,7 @@ constexpr int PB_VCAP    = 512;   // dirty vars per round
 constexpr int PB_SCAP    = 1024;  // dedup hash set (power of 2)
 constexpr int PB_CCAP    = 128;   // changed vars per round
 constexpr int PB_LANEROW = 64;    // rows / columns up to this length are handled by one lane
+constexpr int PB_LONGROW = 4096;  // a dirty row longer than this sends the branch to the engine
 
 struct PWarp {
   int bkey[PB_BCAP];  // var + 1, 0 = empty
@@ -312,6 +313,8 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
         if (set_insert(w, k, full)) {
           const int pos = atomicAdd(&w.n_drow, 1);
           if (pos < PB_RCAP) w.drow[pos] = k;
+          // its vars alone would exceed the overlays: overflow now instead of after the work
+          if (__ldg(c.P.row_start + k + 1) - __ldg(c.P.row_start + k) > PB_LONGROW) full = true;
         }
       }
     }

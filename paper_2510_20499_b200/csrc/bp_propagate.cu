@@ -108,7 +108,7 @@ struct Smem {
   int blk_crossed;
   int blk_any_rows;
   unsigned long long blk_colnnz;
-  unsigned long long blk_reach;
+  unsigned long long blk_reach, blk_hreach;
 };
 
 struct Ctx {
@@ -798,7 +798,7 @@ struct Tally {
   int crossed;
   int any_rows;
   unsigned long long colnnz;
-  unsigned long long reach;  // Σ reach[i] of the changed vars: upper bound of the next frontier's work
+  unsigned long long reach, hreach;  // Σ over changed vars of their light / heavy-row reach
   int nbuf;  // warp-uniform count of staged changed vars
 };
 
@@ -835,7 +835,8 @@ __device__ __forceinline__ void tally(Ctx& c, ParCtl* pc, Tally& t, int i, int r
   if (r > 0) {
     const int nnz = __ldg(c.P.col_start + i + 1) - __ldg(c.P.col_start + i);
     t.colnnz += (unsigned long long)nnz;
-    t.reach += __ldg(c.P.reach + i);
+    t.reach += __ldg(c.P.reach + 2 * i);
+    t.hreach += __ldg(c.P.reach + 2 * i + 1);
     if (nnz > 0) t.any_rows = 1;
   }
   if (ch) {
@@ -851,9 +852,12 @@ __device__ void tally_flush_block(Ctx& c, ParCtl* pc, Tally& t)
   flush_changed(c, pc, t);
   const int cr = warp_sum(t.crossed);
   const int ar = __any_sync(FULL, t.any_rows);
-  unsigned long long cn = t.colnnz, rh = t.reach;
+  unsigned long long cn = t.colnnz, rh = t.reach, hh = t.hreach;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) rh += __shfl_xor_sync(FULL, rh, o);
+  for (int o = 16; o; o >>= 1) {
+    rh += __shfl_xor_sync(FULL, rh, o);
+    hh += __shfl_xor_sync(FULL, hh, o);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) cn += __shfl_xor_sync(FULL, cn, o);
   if (c.lane == 0) {
@@ -861,6 +865,7 @@ __device__ void tally_flush_block(Ctx& c, ParCtl* pc, Tally& t)
     if (ar) atomicOr(&c.sm.blk_any_rows, 1);
     if (cn) atomicAdd(&c.sm.blk_colnnz, cn);
     if (rh) atomicAdd(&c.sm.blk_reach, rh);
+    if (hh) atomicAdd(&c.sm.blk_hreach, hh);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -868,7 +873,9 @@ __device__ void tally_flush_block(Ctx& c, ParCtl* pc, Tally& t)
     if (c.sm.blk_any_rows) atomicOr(&pc->any_rows, 1);
     if (c.sm.blk_colnnz) atomicAdd(&pc->colnnz, c.sm.blk_colnnz);
     if (c.sm.blk_reach) atomicAdd(&pc->reach, c.sm.blk_reach);
+    if (c.sm.blk_hreach) atomicAdd(&pc->hreach, c.sm.blk_hreach);
     c.sm.blk_reach    = 0;
+    c.sm.blk_hreach   = 0;
     c.sm.blk_crossed  = 0;
     c.sm.blk_any_rows = 0;
     c.sm.blk_colnnz   = 0;
@@ -881,7 +888,7 @@ __device__ void phase_finalize(Ctx& c, ParCtl* pc)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  Tally t{0, 0, 0ull, 0ull, 0};
+  Tally t{0, 0, 0ull, 0ull, 0ull, 0};
   for (Prefetch it_q(c, &pc->cur_vs, 32); it_q.t < P.n; it_q.advance()) {
     const int q = it_q.t;
     const int i = q + c.lane;
@@ -1072,7 +1079,7 @@ __device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  Tally t{0, 0, 0ull, 0ull, 0};
+  Tally t{0, 0, 0ull, 0ull, 0ull, 0};
   {
     const int n    = full ? P.n_mcol : ldv(&pc->n_dvar_m);
     const int* ids = full ? P.mcol : S.dvar_m[par];
@@ -1352,6 +1359,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     sm.blk_any_rows = 0;
     sm.blk_colnnz   = 0;
     sm.blk_reach    = 0;
+    sm.blk_hreach   = 0;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5;
@@ -1469,7 +1477,8 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     // changed vars, duplicates counted) is checked against 4x the full-round threshold, so a
     // "full" prediction is only taken when the frontier is certainly large or nearly so
     if (!lim.incremental || ldv(&pc->colnnz) > dense_thr ||
-        (dense_thr != ~0ull && ldv(&pc->reach) > 4 * dense_thr)) {
+        (dense_thr != ~0ull &&
+         ldv(&pc->reach) + min(ldv(&pc->hreach), P.h_reach) > 4 * dense_thr)) {
       full = true;
       continue;
     }
@@ -1546,6 +1555,7 @@ DevProblem Problem::dev() const
   d.sc_tile     = sc_tile.p;
   d.n_mcol      = n_mcol;
   d.reach       = reach.p;
+  d.h_reach     = h_reach;
   d.mcol        = mcol.p;
   return d;
 }
@@ -1752,18 +1762,26 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.seg_base.upload(seg_base);
   // reach[i] = Σ_{k in col i} (len(k) + Σ_{j in row k} collen(j)): an upper bound of the frontier
   // work (row + column incidences) a change of var i can cause in the next round.
+  // Rows longer than kHeavyFold are shared by many variables: their part is kept separately
+  // (reach[2i+1]) and capped, over all changed vars together, by their total h_reach.
   {
     std::vector<unsigned long long> rowcol(m, 0);
+    unsigned long long htot = 0;
     for (int k = 0; k < m; ++k) {
       unsigned long long acc = (unsigned long long)(row_start[k + 1] - row_start[k]);
       for (int e = row_start[k]; e < row_start[k + 1]; ++e)
         acc += (unsigned long long)(col_start[row_col[e] + 1] - col_start[row_col[e]]);
       rowcol[k] = acc;
+      if (row_start[k + 1] - row_start[k] > kHeavyFold) htot += acc;
     }
-    std::vector<unsigned long long> rc(n, 0);
+    std::vector<unsigned long long> rc(2 * (size_t)n, 0);
     for (int i = 0; i < n; ++i)
-      for (int e = col_start[i]; e < col_start[i + 1]; ++e) rc[i] += rowcol[col_row_in[e]];
+      for (int e = col_start[i]; e < col_start[i + 1]; ++e) {
+        const int k = col_row_in[e];
+        rc[2 * i + (row_start[k + 1] - row_start[k] > kHeavyFold ? 1 : 0)] += rowcol[k];
+      }
     P.reach.upload(rc);
+    P.h_reach = htot;
   }
   // Long columns, longest first.
   std::vector<int> mcol;

@@ -25,6 +25,8 @@
 #include <sstream>
 #include <string>
 #include <stdexcept>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/bp.h"
@@ -152,6 +154,24 @@ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? h
 
 }  // namespace
 
+// Host-side step timers of the driver (BP_ROUND_PROFILE=1 prints them at the end of a call).
+struct StepTimes {
+  double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool on = getenv("BP_ROUND_PROFILE") != nullptr;
+};
+struct StepTimer {
+  StepTimes& T;
+  int k;
+  std::chrono::steady_clock::time_point t0;
+  StepTimer(StepTimes& T_, int k_) : T(T_), k(k_), t0(std::chrono::steady_clock::now()) {}
+  ~StepTimer()
+  {
+    T.t[k] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    T.n[k]++;
+  }
+};
+
 // Persistent per-call device context of the rounding driver.
 struct RoundCtx {
   Problem& P;
@@ -164,6 +184,7 @@ struct RoundCtx {
   DBuf<unsigned long long> keys_in, keys_out;
   DBuf<double> dlo, dup;
   DBuf<unsigned char> cub_tmp;
+  StepTimes* tt = nullptr;
   int n_unset = 0;
   bool ws_infeasible = false;
   bool ws_cert       = false;
@@ -320,7 +341,7 @@ struct RoundCtx {
     bool inf          = ws_infeasible;
     bool root_changed = false;
     std::vector<int> changed;
-    std::vector<uint8_t> evm;
+    auto t_ws = std::chrono::steady_clock::now();
     if (cache) {
       // warm start on the host (sparse deltas over the cache root), meet on the device
       std::vector<int> conflicts, dv;
@@ -349,8 +370,12 @@ struct RoundCtx {
       for (size_t j = 0; j < dv.size(); ++j)
         if (ch[j]) changed.push_back(dv[j]);
     }
-    evm.assign(P.n, 0);
-    for (int v : out.evicted) evm[v] = 1;
+    if (tt) {
+      tt->t[4] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_ws).count();
+      tt->n[4]++;
+    }
+    auto t_fx = std::chrono::steady_clock::now();
+    const std::unordered_set<int> evm(out.evicted.begin(), out.evicted.end());
     // fixings (rounding.hpp:186-195) on the post-meet bounds of the bulk vars
     const std::vector<double2> cur = [&] {
       std::vector<double2> o(vars.size());
@@ -366,24 +391,27 @@ struct RoundCtx {
     int crossings = inf ? 1 : 0;
     std::vector<int> fv;
     std::vector<double2> fb;
-    std::vector<double2> now = cur;  // repeated vars: later assignments see earlier fixings
+    // repeated vars: later assignments see earlier fixings (the var's current bounds)
+    std::unordered_map<int, int> slot_of;  // var -> index in fv
+    slot_of.reserve(2 * vars.size());
     for (size_t j = 0; j < vars.size(); ++j) {
       const int v = vars[j];
-      if (evm[v]) continue;
-      double2 b = now[j];
-      for (size_t q = 0; q < j; ++q)
-        if (vars[q] == v) b = now[q];
+      if (!evm.empty() && evm.count(v)) continue;
+      const auto it   = slot_of.find(v);
+      const double2 b = it == slot_of.end() ? cur[j] : fb[it->second];
       const double val = values[j];
       if (val < b.x - 1e-9 || val > b.y + 1e-9) {
         ++crossings;
         continue;
       }
       if (b.x != val || b.y != val) changed.push_back(v);
-      now[j] = make_double2(val, val);
-      for (size_t q = 0; q < j; ++q)
-        if (vars[q] == v) now[q] = now[j];
-      fv.push_back(v);
-      fb.push_back(now[j]);
+      if (it == slot_of.end()) {
+        slot_of.emplace(v, (int)fv.size());
+        fv.push_back(v);
+        fb.push_back(make_double2(val, val));
+      } else {
+        fb[it->second] = make_double2(val, val);  // the last fixing of v wins
+      }
       out.fixed.push_back({v, val});
     }
     scatter(P.st.bounds, fv, fb);  // applied even when crossing, as in the reference's out.bounds
@@ -395,7 +423,16 @@ struct RoundCtx {
     std::sort(changed.begin(), changed.end());
     changed.erase(std::unique(changed.begin(), changed.end()), changed.end());
     const bool frontier = ws_cert && !root_changed;
-    const RunResult r   = propagate_engine(frontier, changed);
+    if (tt) {
+      tt->t[5] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_fx).count();
+      tt->n[5]++;
+    }
+    auto t_en         = std::chrono::steady_clock::now();
+    const RunResult r = propagate_engine(frontier, changed);
+    if (tt) {
+      tt->t[6] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_en).count();
+      tt->n[6]++;
+    }
     if (r.status == BP_STATUS_INFEASIBLE) {
       out.infeasible   = true;
       out.infeas_count = std::max(1, r.crossed);
@@ -522,6 +559,8 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
       return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() >= deadline_sec;
     };
     bp::RoundCtx X(P, H);
+    bp::StepTimes TT;
+    X.tt = &TT;
     std::vector<double> orig(2 * (size_t)n);
     bp_problem_root(p, orig.data());
     X.ws.upload(reinterpret_cast<const double2*>(orig.data()), n);
@@ -563,22 +602,36 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
       }
       const int bulk = bp::get_bulk_size(X.n_unset, recovery && !force, cfg.single_var_tail);
       if (!force) {
-        if (bulk > 1) X.slack_sort();
-        const std::vector<int> take = X.take_first(bulk);
-        const auto tb               = X.gather(X.ws, take);
-        bp::candidate_values(start_values, take, tb, rng, cfg.random_band, pv0, pv1);
-        auto pr0   = X.run_probe(take, pv0, hc);
+        if (bulk > 1) {
+          bp::StepTimer st(TT, 0);
+          X.slack_sort();
+        }
+        std::vector<int> take;
+        std::vector<double2> tb;
+        {
+          bp::StepTimer st(TT, 1);
+          take = X.take_first(bulk);
+          tb   = X.gather(X.ws, take);
+          bp::candidate_values(start_values, take, tb, rng, cfg.random_band, pv0, pv1);
+        }
+        bp::RoundCtx::Probe pr0;
+        {
+          bp::StepTimer st(TT, 2);
+          pr0 = X.run_probe(take, pv0, hc);
+        }
         int sel    = -1;
         bp::RoundCtx::Probe pr1;
         if (pr0.infeas_count == 0) {
           sel = 0;
         } else {
+          bp::StepTimer st(TT, 2);
           pr1 = X.run_probe(take, pv1, hc);
           if (pr1.infeas_count == 0) sel = 1;
         }
         if (sel >= 0) {
           auto& pr = sel == 0 ? pr0 : pr1;
           if (!pr.fixed.empty()) {  // commit (rounding.hpp:436-443)
+            bp::StepTimer st(TT, 3);
             BP_CUDA(cudaMemcpyAsync(X.ws.p, P.st.bounds, sizeof(double2) * n, cudaMemcpyDeviceToDevice, X.s));
             X.ws_infeasible = false;
             X.ws_cert       = pr.cert;
@@ -677,6 +730,14 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
       if (wsb[2 * i] == wsb[2 * i + 1]) out_values[i] = wsb[2 * i];
       else out_values[i] = bp::clampd(std::round(v), H.var_lower[i], H.var_upper[i]);
       if (wsb[2 * i] == wsb[2 * i + 1]) o.set_count++;
+    }
+    if (TT.on) {
+      const char* nm[7] = {"slack_sort", "take+gather+draw", "run_probe", "commit",
+                           " probe:warm+meet", " probe:fix", " probe:engine"};
+      for (int q = 0; q < 7; ++q)
+        fprintf(stderr, "[bp round] %-18s n=%lld total=%.3f s avg=%.1f us\n", nm[q], TT.n[q], TT.t[q],
+                TT.n[q] ? 1e6 * TT.t[q] / TT.n[q] : 0.0);
+      fprintf(stderr, "[bp round] engine device %.3f s over %lld calls\n", X.dev_ms * 1e-3, X.bp_calls);
     }
     o.completed       = X.n_unset == 0;
     o.bounds_feasible = o.completed && !o.rounding_infeasible && !X.ws_infeasible;
