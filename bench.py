@@ -577,7 +577,9 @@ def main():
                     "ms_per_step": e2e_s * 1e3, "api": "bp_propagate (C-ABI, host pinned bounds)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_engine", "kernel_ms": kern_ms},
+                         "kernel": "one propagate = k_engine (cooperative) + per full round "
+                                   "k_rows_full + k_cand_pieces, CUDA events around the sequence",
+                         "kernel_ms": kern_ms},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks,

@@ -10,6 +10,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 1200 python bench.py --steps 20 --warmup 3 > $O/bench.log 2>&1; echo "bench exit $?" >> $O/bench.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
    python bench.py --steps 2 --warmup 3 --no-probing --no-rounding --no-cpu-baseline --e2e-steps 1 > $O/ncu_launch_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_engine -s 2 -c 1 -o $O/k_engine_C2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rows_full -s 3 -c 1 -o $O/k_rows_full_C2 \
    python tools/ncu_target.py --workload C2 --reps 3 > $O/ncu_full.log 2>&1
 echo done > $O/DONE
