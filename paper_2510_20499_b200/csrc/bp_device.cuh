@@ -315,7 +315,7 @@ struct DevProblem {
   const uint8_t* is_int;
   // Rows with nnz <= kPackNnz in SELL-32 slices (build: problem_build): n_srtile slices, slice s
   // has 32 rows srow[32 s + i] (-1 padding) and entries sr_ci / sr_val[sr_tile[s] + 32 j + i].
-  int n_srow, n_srtile;
+  int n_srow, n_srtile, n_srow_long;  // n_srow_long: leading slices with rows > kShortNnz
   const int* srow;          // slice lane -> row id
   const int* sr_ptr;        // unused
   const int* sr_ci;         // column | integrality << 31, -1 = padding

@@ -46,6 +46,10 @@ constexpr int kWarps    = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kEPL      = kTile / 32;
 constexpr int kIntBit   = (int)0x80000000u;
+#ifndef BP_ROW_GATE
+#define BP_ROW_GATE 1
+#endif
+constexpr bool kRowGate = BP_ROW_GATE != 0;  // row-level candidate gating (maxima in the fold pass)
 
 __device__ __forceinline__ unsigned lanemask_lt()
 {
@@ -119,6 +123,17 @@ struct Ctx {
   WarpSmem& w;
   int lane, warp;
 };
+
+// Debug counters (BP_DEBUG=1): per task kind total / max cycles and count.
+__device__ __forceinline__ void dbg_task(Ctx& c, int kind, long long c0)
+{
+  if (c.S.dbg && c.lane == 0) {
+    const unsigned long long d = (unsigned long long)(clock64() - c0);
+    atomicAdd(c.S.dbg + 3 * kind, d);
+    atomicMax(c.S.dbg + 3 * kind + 1, d);
+    atomicAdd(c.S.dbg + 3 * kind + 2, 1ull);
+  }
+}
 
 // Allocates `cnt` slots per lane in a global list with one atomic per warp; returns this lane's
 // first slot.
@@ -337,7 +352,7 @@ __device__ void fold_finish(Ctx& c, int k, int L, int seg, double smn, double sm
   if (!cand) return;
   const double2 cb = __ldg(&P.cons[k]);
   // row-level gating: no entry of the row can publish a candidate -> skip the candidate pass
-  const bool quiet = entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x);
+  const bool quiet = kRowGate && entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x);
   if (L > kCandSplit) {
     if (lane == 0) {
       S.rquiet[k] = quiet ? 1 : 0;
@@ -393,7 +408,7 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
         contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
         imn += i1;
         imx += i2;
-        if (cand) {
+        if (cand && kRowGate) {
           double tw, pw;
           entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pw);
           gtw = fmax(gtw, tw);
@@ -515,7 +530,8 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
     __syncwarp();
     __threadfence();
   }
-  const double2* gb = S.gbuf + off;
+  const long long c_stream = S.dbg ? clock64() : 0;
+  const double2* gb         = S.gbuf + off;
   double2 v[kEPL], w[kEPL];
 #pragma unroll
   for (int h = 0; h < kEPL; ++h) {
@@ -525,14 +541,15 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   double acc = 0.0, gtw = 0.0, gpm = 0.0;
   int imn = 0, imx = 0;
   const unsigned lt = lanemask_lt();
+  // chunk aggregates of the segment: lanes read them strided (off the fold's critical path)
+  for (int q = (off + e0) / kTile + lane; q < (off + e1 + kTile - 1) / kTile; q += 32) {
+    const ChunkInfo* ch = S.cinfo + q;
+    imn += __ldcg(&ch->imn);
+    imx += __ldcg(&ch->imx);
+    gtw = fmax(gtw, __ldcg(&ch->gtw));
+    gpm = fmax(gpm, __ldcg(&ch->gpm));
+  }
   for (int base = e0; base < e1; base += kTile) {
-    if (lane == 0) {
-      const ChunkInfo* ch = S.cinfo + (off + base) / kTile;
-      imn += __ldcg(&ch->imn);
-      imx += __ldcg(&ch->imx);
-      gtw = fmax(gtw, __ldcg(&ch->gtw));
-      gpm = fmax(gpm, __ldcg(&ch->gpm));
-    }
     int pm = 0, px = 0;
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
@@ -554,12 +571,16 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
     if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
     __syncwarp();
   }
-  imn = __shfl_sync(FULL, imn, 0);
-  imx = __shfl_sync(FULL, imx, 0);
-  gtw = __shfl_sync(FULL, gtw, 0);
-  gpm = __shfl_sync(FULL, gpm, 0);
+  imn = warp_sum(imn);
+  imx = warp_sum(imx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    gtw = fmax(gtw, __shfl_xor_sync(FULL, gtw, o));
+    gpm = fmax(gpm, __shfl_xor_sync(FULL, gpm, o));
+  }
   const double smn = __shfl_sync(FULL, acc, 0);
   const double smx = __shfl_sync(FULL, acc, 1);
+  dbg_task(c, 3, c_stream);  // streaming part of a heavy segment (after its pieces are ready)
   fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
 }
 
@@ -629,7 +650,7 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand)
       smx = __dadd_rn(smx, cx);
       imn += i1;
       imx += i2;
-      if (cand) {
+      if (cand && kRowGate) {
         double tw, pw;
         entry_reach(a[u], bd[u].x, bd[u].y, ci[u] < 0, tw, pw);
         gtw = fmax(gtw, tw);
@@ -649,7 +670,7 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand)
     if (imn | imx) S.aux[k] = make_double2(smn, smx);
   }
   if (!cand) return;
-  const bool quiet = k < 0 || entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x);
+  const bool quiet = k < 0 || (kRowGate && entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x));
   if (__all_sync(FULL, quiet)) return;
   for (int j = 0; j < Lm; j += U) {
     int ci[U];
@@ -732,17 +753,6 @@ __device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
   if (k >= 0) write_rec(P, c.S, k, smn, smx, imn, imx);
 }
 
-// Debug counters (BP_DEBUG=1): per task kind total / max cycles and count.
-__device__ __forceinline__ void dbg_task(Ctx& c, int kind, long long c0)
-{
-  if (c.S.dbg && c.lane == 0) {
-    const unsigned long long d = (unsigned long long)(clock64() - c0);
-    atomicAdd(c.S.dbg + 3 * kind, d);
-    atomicMax(c.S.dbg + 3 * kind + 1, d);
-    atomicAdd(c.S.dbg + 3 * kind + 2, 1ull);
-  }
-}
-
 // Phase 2 (F2 / P2): activities of all rows (full) or the dirty ones; `cand` fuses tightening.
 // pieces_here = false: the candidate pieces of rows above kCandSplit are left to a following
 // k_cand_pieces launch (no warp spins on an unfinished row's activity).
@@ -767,10 +777,16 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       else long_fold(c, tk.x, tk.y, cand, stamp);
       dbg_task(c, 0, c0);
     }
-    const int ns = P.n_srtile;
-    for (Prefetch it_t(c, &pc->cur_a, 4); it_t.t < ns; it_t.advance()) {
+    // SELL slices, longest first: slices of rows > 32 entries one per fetch, the rest four
+    const int ns = P.n_srtile, nsl = P.n_srow_long;
+    for (Prefetch it_t(c, &pc->cur_s, 1); it_t.t < nsl; it_t.advance()) {
       const long long c0 = S.dbg ? clock64() : 0;
-      for (int q = it_t.t; q < min(ns, it_t.t + 4); ++q) sell_slice(c, q, cand);
+      sell_slice(c, it_t.t, cand);
+      dbg_task(c, 1, c0);
+    }
+    for (Prefetch it_t(c, &pc->cur_a, 4); nsl + it_t.t < ns; it_t.advance()) {
+      const long long c0 = S.dbg ? clock64() : 0;
+      for (int q = nsl + it_t.t; q < min(ns, nsl + it_t.t + 4); ++q) sell_slice(c, q, cand);
       dbg_task(c, 1, c0);
     }
     const int nc = cand && pieces_here ? P.n_cpiece : 0;
@@ -1530,6 +1546,7 @@ DevProblem Problem::dev() const
   d.is_int      = is_int.p;
   d.n_srow      = n_srow;
   d.n_srtile    = n_srtile;
+  d.n_srow_long = n_srow_long;
   d.srow        = srow.p;
   d.sr_ptr      = sr_ptr.p;
   d.sr_ci       = sr_ci.p;
@@ -1691,6 +1708,9 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
       }
     P.n_srow   = (int)srows.size();
     P.n_srtile = nsl;
+    P.n_srow_long = 0;  // slices whose longest row exceeds kShortNnz (fetched one at a time)
+    while (P.n_srow_long < nsl && sbase[P.n_srow_long + 1] - sbase[P.n_srow_long] > 32 * kShortNnz)
+      ++P.n_srow_long;
     P.srow.upload(srow);
     P.sr_ci.upload(sci);
     P.sr_val.upload(sval);
@@ -1914,7 +1934,10 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
       (flags & ENGINE_FORCE_FRONTIER) ? ~0ull : (unsigned long long)(P.nnz / 4);
   long long* stp = d_stats;
   static const bool no_ext = getenv("BP_NO_EXT_F2") != nullptr;
-  int ext        = (mode == MODE_PROPAGATE && !no_ext) ? 1 : 0;
+  // small problems keep the row phase inside the engine: the hand-off's host round trip would
+  // cost more than the occupancy it buys
+  static const long long ext_min = getenv("BP_EXT_MIN_NNZ") ? atoll(getenv("BP_EXT_MIN_NNZ")) : 2000000;
+  int ext        = (mode == MODE_PROPAGATE && !no_ext && P.nnz >= ext_min) ? 1 : 0;
   int resume     = 0;
   void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume};
   BP_CUDA(cudaEventRecord(P.ev0, s));
@@ -1957,8 +1980,8 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   if (P.st.dbg) {
     unsigned long long h[16];
     BP_CUDA(cudaMemcpy(h, P.st.dbg, sizeof(h), cudaMemcpyDeviceToHost));
-    const char* nm[3] = {"fold", "sell_slice", "cand_piece"};
-    for (int q = 0; q < 3; ++q)
+    const char* nm[4] = {"fold", "sell_slice", "cand_piece", "heavy_stream"};
+    for (int q = 0; q < 4; ++q)
       fprintf(stderr, "[bp dbg] %-10s n=%llu avg=%.1f us max=%.1f us total=%.1f warp-ms\n", nm[q],
               h[3 * q + 2], h[3 * q + 2] ? h[3 * q] / 1965.0 / h[3 * q + 2] : 0.0,
               h[3 * q + 1] / 1965.0, h[3 * q] / 1965.0 / 1e3);
