@@ -330,8 +330,8 @@ struct DevProblem {
   const int* hpiece;        // per heavy row: index of its first piece in piece_task
   int n_piece;
   const int2* piece_task;   // (row, piece) of heavy rows, longest rows first
-  int n_fold;
-  const int2* fold_task;    // (row, segment), longest segments first
+  int n_fold, n_fold_heavy;  // n_fold_heavy: leading tasks that are heavy-row segments
+  const int2* fold_task;    // (row, segment): heavy-row segments, then medium rows, longest first
   int n_cpiece;
   const int2* cpiece_task;  // (row, piece) candidate tasks of rows with nnz > kCandSplit
   const int* seg_base;      // per row: first partial slot if the row has > 1 segment, else -1

@@ -61,7 +61,7 @@ struct ParCtl {
   int cur_a, cur_b, cur_c, cur_vm, cur_vs;
   int cur_x1, cur_x2, n_xtask, stop;
   int n_ctask, cur_x3, cur_x4, xabort;  // xabort: a frontier expansion stopped early (full next)
-  int cur_p, cur_s;                     // full rounds: heavy-row pieces, long SELL slices
+  int cur_p, cur_s, cur_g, pad4;        // full rounds: heavy-row pieces, long SELL slices, medium-row groups
   unsigned long long colnnz, roww, colw, reach, hreach;
 };
 
@@ -132,7 +132,7 @@ struct Problem {
   unsigned long long h_reach = 0;
   int n_srow_long = 0;
   int n_srow = 0, n_srtile = 0, n_scol = 0, n_sctile = 0, n_mcol = 0, n_part = 0;
-  int n_piece = 0, n_fold = 0, n_cpiece = 0;
+  int n_piece = 0, n_fold = 0, n_cpiece = 0, n_fold_heavy = 0;
   long long n_long_entries = 0;
   // workspace
   DBuf<double2> bounds;

@@ -584,6 +584,123 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
 }
 
+// Four medium rows (kPackNnz < nnz <= kHeavyFold, single segment) per warp, eight lanes per row:
+// each group streams its row in 32-entry chunks (next chunk's indices in flight), compacts the
+// non-zero contributions into its own shared-memory slice, and its lanes 0/1 run the row's
+// sequential min/max sums -- the four rows' chains advance in the same instructions. Then the
+// candidates of the non-quiet rows.
+__device__ void group_fold(Ctx& c, int t0, int nt, bool cand)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int lane = c.lane, g = lane >> 3, gl = lane & 7;
+  const unsigned gmask = 0xFFu << (8 * g);
+  const bool act       = g < nt;
+  int k = -1, rs = 0, L = 0;
+  if (act) {
+    k  = __ldg(&P.fold_task[t0 + g].x);
+    rs = __ldg(P.row_start + k);
+    L  = __ldg(P.row_start + k + 1) - rs;
+  }
+  int Lmax = L;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) Lmax = max(Lmax, __shfl_xor_sync(FULL, Lmax, o));
+  double* gb0 = c.w.b0 + 64 * g;  // group slices of the staging buffers (32 used per chunk)
+  double* gb1 = c.w.b1 + 64 * g;
+  int ci[4], cn[4];
+  double a[4], an[4];
+  double2 bd[4];
+  auto load = [&](int base, int* ci_, double* a_) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int e = base + h * 8 + gl;
+      ci_[h]      = e < L ? __ldg(P.row_ci + rs + e) : -1;
+      a_[h]       = e < L ? __ldg(P.row_val + rs + e) : 0.0;
+    }
+  };
+  auto gather = [&]() {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+  };
+  load(0, ci, a);
+  gather();
+  load(32, cn, an);
+  const unsigned lt = lanemask_lt() & gmask;
+  double acc = 0.0, gtw = 0.0, gpm = 0.0;
+  int imn = 0, imx = 0;
+  for (int base = 0; base < Lmax; base += 32) {
+    int pm = 0, px = 0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      double cm = 0.0, cx = 0.0;
+      if (ci[h] != -1) {
+        int i1, i2;
+        contrib(a[h], bd[h].x, bd[h].y, cm, cx, i1, i2);
+        imn += i1;
+        imx += i2;
+        if (cand && kRowGate) {
+          double tw, pw;
+          entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pw);
+          gtw = fmax(gtw, tw);
+          gpm = fmax(gpm, pw);
+        }
+      }
+      const unsigned m = __ballot_sync(FULL, cm != 0.0) & gmask;
+      const unsigned x = __ballot_sync(FULL, cx != 0.0) & gmask;
+      if (cm != 0.0) gb0[pm + __popc(m & lt)] = cm;
+      if (cx != 0.0) gb1[px + __popc(x & lt)] = cx;
+      pm += __popc(m);
+      px += __popc(x);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      ci[h] = cn[h];
+      a[h]  = an[h];
+    }
+    gather();
+    load(base + 64, cn, an);
+    if (gl < 2 && act) acc = fold_seq(gl ? gb1 : gb0, gl ? px : pm, acc);
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 4; o; o >>= 1) {
+    imn += __shfl_xor_sync(FULL, imn, o);
+    imx += __shfl_xor_sync(FULL, imx, o);
+    gtw = fmax(gtw, __shfl_xor_sync(FULL, gtw, o));
+    gpm = fmax(gpm, __shfl_xor_sync(FULL, gpm, o));
+  }
+  const double smn = __shfl_sync(FULL, acc, 8 * g);
+  const double smx = __shfl_sync(FULL, acc, 8 * g + 1);
+  double2 cb       = make_double2(0.0, 0.0);
+  if (act) {
+    cb = __ldg(&P.cons[k]);
+    if (gl == 0) write_rec(P, S, k, smn, smx, imn, imx);
+  }
+  if (!cand) return;
+  const bool quiet = !act || (kRowGate && entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x));
+  if (__all_sync(FULL, quiet)) return;
+  for (int base = 0; base < Lmax; base += 32) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int e = base + h * 8 + gl;
+      ci[h]       = !quiet && e < L ? __ldg(P.row_ci + rs + e) : -1;
+      a[h]        = !quiet && e < L ? __ldg(P.row_val + rs + e) : 0.0;
+    }
+    gather();
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      if (ci[h] == -1) continue;
+      double tw, pw;
+      entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pw);
+      if (entry_quiet(tw, pw, smn, imn, smx, imx, cb.y, cb.x)) continue;
+      double cl, cu;
+      cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], smn, imn, smx, imx, cb.y, cb.x, cl, cu);
+      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
+    }
+  }
+}
+
 // F2 tail: candidate piece p of a row with > kCandSplit entries, once its activity is published.
 __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp)
 {
@@ -770,12 +887,17 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     // heavy rows' contribution pieces first: the segment folds that wait for them are fetched
     // only after every piece has been fetched by a running warp (no deadlock)
     for (Prefetch it_t(c, &pc->cur_p, 1); it_t.t < P.n_piece; it_t.advance()) heavy_piece(c, it_t.t, stamp);
-    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nf; it_t.advance()) {
+    const int nfh = P.n_fold_heavy;
+    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nfh; it_t.advance()) {
       const long long c0 = S.dbg ? clock64() : 0;
       const int2 tk      = folds[it_t.t];
-      if (__ldg(P.long_off + tk.x) >= 0) heavy_fold(c, tk.x, tk.y, cand, stamp);
-      else long_fold(c, tk.x, tk.y, cand, stamp);
+      heavy_fold(c, tk.x, tk.y, cand, stamp);
       dbg_task(c, 0, c0);
+    }
+    for (Prefetch it_t(c, &pc->cur_g, 4); nfh + it_t.t < nf; it_t.advance()) {
+      const long long c0 = S.dbg ? clock64() : 0;
+      group_fold(c, nfh + it_t.t, min(4, nf - nfh - it_t.t), cand);
+      dbg_task(c, 4, c0);
     }
     // SELL slices, longest first: slices of rows > 32 entries one per fetch, the rest four
     const int ns = P.n_srtile, nsl = P.n_srow_long;
@@ -1558,6 +1680,7 @@ DevProblem Problem::dev() const
   d.n_piece     = n_piece;
   d.piece_task  = piece_task.p;
   d.n_fold      = n_fold;
+  d.n_fold_heavy = n_fold_heavy;
   d.fold_task   = fold_task.p;
   d.n_cpiece    = n_cpiece;
   d.cpiece_task = cpiece_task.p;
@@ -1765,10 +1888,20 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
     for (int s = 0; s * kSumSegment < L; ++s)
       folds.push_back({std::min(L - s * kSumSegment, kSumSegment), make_int2(k, s)});
   }
-  std::stable_sort(folds.begin(), folds.end(),
-                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  // heavy-row segments first (longest first), then the medium rows (longest first): medium rows
+  // are folded four per warp (group_fold), so neighbours in the list have similar lengths
+  auto heavy_row = [&](int k) { return row_start[k + 1] - row_start[k] > kHeavyFold; };
+  std::stable_sort(folds.begin(), folds.end(), [&](const auto& a, const auto& b) {
+    const bool ha = heavy_row(a.second.x), hb = heavy_row(b.second.x);
+    if (ha != hb) return ha;
+    return a.first > b.first;
+  });
   std::vector<int2> fold(folds.size());
-  for (size_t j = 0; j < folds.size(); ++j) fold[j] = folds[j].second;
+  P.n_fold_heavy = 0;
+  for (size_t j = 0; j < folds.size(); ++j) {
+    fold[j] = folds[j].second;
+    if (heavy_row(fold[j].x)) P.n_fold_heavy++;
+  }
   P.n_long_entries = goff;
   P.n_piece        = (int)piece.size();
   P.long_off.upload(long_off);
@@ -1980,8 +2113,8 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   if (P.st.dbg) {
     unsigned long long h[16];
     BP_CUDA(cudaMemcpy(h, P.st.dbg, sizeof(h), cudaMemcpyDeviceToHost));
-    const char* nm[4] = {"fold", "sell_slice", "cand_piece", "heavy_stream"};
-    for (int q = 0; q < 4; ++q)
+    const char* nm[5] = {"heavy_fold", "sell_slice", "cand_piece", "heavy_stream", "group_fold"};
+    for (int q = 0; q < 5; ++q)
       fprintf(stderr, "[bp dbg] %-10s n=%llu avg=%.1f us max=%.1f us total=%.1f warp-ms\n", nm[q],
               h[3 * q + 2], h[3 * q + 2] ? h[3 * q] / 1965.0 / h[3 * q + 2] : 0.0,
               h[3 * q + 1] / 1965.0, h[3 * q] / 1965.0 / 1e3);
