@@ -111,6 +111,7 @@ struct Problem {
   long long nnz = 0;
   // host copies kept for classification of caller-supplied lists
   std::vector<int> h_row_start, h_col_start;
+  std::vector<int> h_hpiece;  // first contribution piece of each heavy row (-1 otherwise)
   // device arrays: the matrix twice
   DBuf<int> row_start, row_col, row_ci, col_start, col_row;
   DBuf<double> row_val, col_val;

@@ -919,10 +919,14 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       dbg_task(c, 2, c0);
     }
   } else {
+    // dirty heavy rows: contribution pieces first (the folds waiting for them are fetched after)
+    const int ndp = ldv(&pc->n_dpiece);
+    for (Prefetch it_t(c, &pc->cur_p, 1); it_t.t < ndp; it_t.advance())
+      heavy_piece(c, S.dpiece[par][it_t.t].x, stamp);
     for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nf; it_t.advance()) {
-    const int t = it_t.t;
-      const int2 tk = folds[t];
-      long_fold(c, tk.x, tk.y, false, stamp);
+      const int2 tk = folds[it_t.t];
+      if (__ldg(P.long_off + tk.x) >= 0) heavy_fold(c, tk.x, tk.y, false, stamp);
+      else long_fold(c, tk.x, tk.y, false, stamp);
     }
     const int n = ldv(&pc->n_drow_s);
     for (Prefetch it_t(c, &pc->cur_c, 32); it_t.t < n; it_t.advance())
@@ -1259,7 +1263,7 @@ __device__ __forceinline__ void expand_rows_window(Ctx& c, ParCtl* qc, int qpar,
     nall += nw[h];
     const bool lg = nw[h] && RL[h] > kShortNnz;
     n_s += nw[h] && !lg;
-    n_p += lg ? 1 : 0;
+    n_p += lg && RL[h] > kHeavyFold ? (RL[h] + kPiece - 1) / kPiece : 0;
     n_f += lg ? (RL[h] + kSumSegment - 1) / kSumSegment : 0;
     n_x += lg ? (RL[h] + kTile - 1) / kTile : 0;
   }
@@ -1267,12 +1271,17 @@ __device__ __forceinline__ void expand_rows_window(Ctx& c, ParCtl* qc, int qpar,
 #pragma unroll
   for (int h = 0; h < kEPL; ++h)
     if (nw[h] && RL[h] <= kShortNnz) S.drow_s[qpar][ps++] = k[h];
-  if (__any_sync(FULL, n_p > 0)) {  // rare: a long row became dirty
+  if (__any_sync(FULL, n_f > 0)) {  // rare: a long row became dirty
     int pf = warp_alloc(&qc->n_dfold, n_f, c.lane);
     int px = warp_alloc(&qc->n_xtask, n_x, c.lane);
+    int pp = warp_alloc(&qc->n_dpiece, n_p, c.lane);
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
       if (!nw[h] || RL[h] <= kShortNnz) continue;
+      if (RL[h] > kHeavyFold) {  // heavy: buffered fold, fed by contribution pieces
+        const int p0 = __ldg(P.hpiece + k[h]);
+        for (int s = 0; s * kPiece < RL[h]; ++s) S.dpiece[qpar][pp++] = make_int2(p0 + s, 0);
+      }
       for (int s = 0; s * kSumSegment < RL[h]; ++s) S.dfold[qpar][pf++] = make_int2(k[h], s);
       for (int s = 0; s * kTile < RL[h]; ++s) S.xtask[qpar][px++] = make_int2(k[h], s);
     }
@@ -1906,6 +1915,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.n_piece        = (int)piece.size();
   P.long_off.upload(long_off);
   P.hpiece.upload(hpiece);
+  P.h_hpiece = hpiece;
   P.piece_task.upload(piece);
   P.n_fold         = (int)fold.size();
   P.n_cpiece       = (int)cpiece.size();
@@ -1981,7 +1991,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   // int lists per parity: drow_s (m), dvar_s, dvar_m (n each); changed (n)
   P.lists_i.alloc(2 * (mm + 2 * nn) + nn);
   // int2 lists per parity: dpiece, dfold (all long-row tasks), xtask (N/256 + m)
-  const size_t np_cap = 1;  // gather pieces: unused
+  const size_t np_cap = (size_t)std::max(P.n_piece, 1);  // dirty heavy rows' contribution pieces
   const size_t nf_cap = (size_t)std::max(nf_front, 1ll);
   const size_t nx_cap = (size_t)(N / kTile) + mm + 1;
   P.lists_i2.alloc(2 * (np_cap + nf_cap + nx_cap) + (size_t)(N / kTile) + nn + 1);
@@ -2139,6 +2149,10 @@ void stage_rows(Problem& P, const int* rows, int nrows, cudaStream_t s)
       sr.push_back(k);
     } else {
       for (int q = 0; q * kSumSegment < L; ++q) fd.push_back(make_int2(k, q));
+      if (L > kHeavyFold) {
+        const int p0 = P.h_hpiece[k];
+        for (int q = 0; q * kPiece < L; ++q) pc.push_back(make_int2(p0 + q, 0));
+      }
     }
   }
   DevState& S = P.st;
