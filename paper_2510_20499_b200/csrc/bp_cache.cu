@@ -79,8 +79,10 @@ Limits default_limits()
 
 struct Branch {
   int feasible = 1;
-  std::vector<int> var;
+  std::vector<int> var;  // deltas of engine branches
   std::vector<double> lo, up;
+  long long pool_off = -1;  // deltas of batched branches: range of the flat host pool
+  int pool_cnt       = 0;
 };
 
 // Full-engine branch (probing.hpp:194-219 verbatim semantics, any root).
@@ -315,6 +317,8 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   }
   const int ne = (int)C.e_var.size();
   std::vector<Branch> res(2 * (size_t)ne);
+  std::vector<int> hp_var;  // batched branches' deltas (flat, by chunk)
+  std::vector<double> hp_lo, hp_up;
   std::vector<uint8_t> done(2 * (size_t)ne, 0);
   for (int e = 0; e < ne; ++e) done[2 * e] = done[2 * e + 1] = 1;
   for (int slot : tslot) done[slot] = 0;
@@ -372,21 +376,23 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
         BP_CUDA(cudaMemcpy(st.data(), dstat.p, sizeof(int) * nt, cudaMemcpyDeviceToHost));
         BP_CUDA(cudaMemcpy(cn.data(), dcnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost));
         BP_CUDA(cudaMemcpy(of.data(), doff.p, sizeof(long long) * nt, cudaMemcpyDeviceToHost));
-        std::vector<int> hv(used);
-        std::vector<double> hl(used), hu(used);
+        // the chunk's delta pool is appended to one flat host pool; branches keep (offset, count)
+        const long long hbase = (long long)hp_var.size();
+        hp_var.resize(hbase + used);
+        hp_lo.resize(hbase + used);
+        hp_up.resize(hbase + used);
         if (used) {
-          BP_CUDA(cudaMemcpy(hv.data(), pvar.p, sizeof(int) * used, cudaMemcpyDeviceToHost));
-          BP_CUDA(cudaMemcpy(hl.data(), plo.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
-          BP_CUDA(cudaMemcpy(hu.data(), pup.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
+          BP_CUDA(cudaMemcpy(hp_var.data() + hbase, pvar.p, sizeof(int) * used, cudaMemcpyDeviceToHost));
+          BP_CUDA(cudaMemcpy(hp_lo.data() + hbase, plo.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
+          BP_CUDA(cudaMemcpy(hp_up.data() + hbase, pup.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
         }
         for (int j = 0; j < nt; ++j) {
           const int t = t0 + j;
           Branch& br  = res[tslot[t]];
           if (st[j] == 0) {
-            br.feasible = 1;
-            br.var.assign(hv.begin() + of[j], hv.begin() + of[j] + cn[j]);
-            br.lo.assign(hl.begin() + of[j], hl.begin() + of[j] + cn[j]);
-            br.up.assign(hu.begin() + of[j], hu.begin() + of[j] + cn[j]);
+            br.feasible    = 1;
+            br.pool_off    = hbase + of[j];
+            br.pool_cnt    = cn[j];
             done[tslot[t]] = 1;
           } else if (st[j] == 1) {
             br.feasible    = 0;
@@ -425,7 +431,16 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   out.probe_ms  = C.probe_ms;
   out.n_fallback = C.n_fallback;
   out.entry_of.assign(n, -1);
+  out.d_off.reserve(2 * (size_t)ne + 1);
   out.d_off.push_back(0);
+  out.e_var.reserve(ne);
+  out.e_kind.reserve(ne);
+  out.e_branch.reserve(4 * (size_t)ne);
+  out.e_feas.reserve(2 * (size_t)ne);
+  out.e_force.reserve(2 * (size_t)ne);
+  out.d_var.reserve(hp_var.size());
+  out.d_lo.reserve(hp_var.size());
+  out.d_up.reserve(hp_var.size());
   for (int e = 0; e < ne; ++e) {
     if (!done[2 * e] || !done[2 * e + 1]) continue;
     const int v    = C.e_var[e];
@@ -441,9 +456,16 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
     out.e_force.push_back((uint8_t)(!upb.feasible && dn.feasible));  // forces_down
     out.e_force.push_back((uint8_t)(!dn.feasible && upb.feasible));  // forces_up
     for (const Branch* b : {&dn, &upb}) {
-      out.d_var.insert(out.d_var.end(), b->var.begin(), b->var.end());
-      out.d_lo.insert(out.d_lo.end(), b->lo.begin(), b->lo.end());
-      out.d_up.insert(out.d_up.end(), b->up.begin(), b->up.end());
+      if (b->pool_off >= 0) {
+        const long long o = b->pool_off, cnt = b->pool_cnt;
+        out.d_var.insert(out.d_var.end(), hp_var.begin() + o, hp_var.begin() + o + cnt);
+        out.d_lo.insert(out.d_lo.end(), hp_lo.begin() + o, hp_lo.begin() + o + cnt);
+        out.d_up.insert(out.d_up.end(), hp_up.begin() + o, hp_up.begin() + o + cnt);
+      } else {
+        out.d_var.insert(out.d_var.end(), b->var.begin(), b->var.end());
+        out.d_lo.insert(out.d_lo.end(), b->lo.begin(), b->lo.end());
+        out.d_up.insert(out.d_up.end(), b->up.begin(), b->up.end());
+      }
       out.d_off.push_back((long long)out.d_var.size());
     }
   }

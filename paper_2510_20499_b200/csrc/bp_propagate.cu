@@ -2073,8 +2073,12 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   }
   unsigned sb = P.stamp_base;
   P.stamp_base += (unsigned)std::max(lim.max_rounds, 1) + 1;
+  // a round is evaluated as a full sweep when its frontier (dirty-row nnz + dirty-column nnz)
+  // exceeds kFullPct % of nnz: a fused full round costs about as much as a frontier round over
+  // ~40% of the matrix (frontier work per entry is the CSC gather, ~2.5x a full round's)
+  static const int full_pct = getenv("BP_FULL_PCT") ? atoi(getenv("BP_FULL_PCT")) : 35;
   unsigned long long dense_thr =
-      (flags & ENGINE_FORCE_FRONTIER) ? ~0ull : (unsigned long long)(P.nnz / 4);
+      (flags & ENGINE_FORCE_FRONTIER) ? ~0ull : (unsigned long long)(P.nnz * full_pct / 200);
   long long* stp = d_stats;
   static const bool no_ext = getenv("BP_NO_EXT_F2") != nullptr;
   // small problems keep the row phase inside the engine: the hand-off's host round trip would
