@@ -285,10 +285,18 @@ struct RoundCtx {
   // implied_slack_sort of the unset list, in place (stable).
   void slack_sort()
   {
-    activities(ws.p);
+    // compute_activities(p, ws) (rounding.hpp:427): a certified ws already has them -- the
+    // records its last propagate ended with (no bound changed in that round), kept in ws_rec
+    const RowRec* rec  = P.st.rec;
+    const double2* aux = P.st.aux;
+    if (ws_cert && P.m && ws_rec.n >= (size_t)P.m) {
+      rec = ws_rec.p;
+      aux = ws_aux.p;
+    } else {
+      activities(ws.p);
+    }
     const int k = n_unset;
-    k_slack_keys<<<blocks_for(k), 256, 0, s>>>(P.dev(), P.st.rec, P.st.aux, unset.p, k, keys_in.p,
-                                               pos_in.p);
+    k_slack_keys<<<blocks_for(k), 256, 0, s>>>(P.dev(), rec, aux, unset.p, k, keys_in.p, pos_in.p);
     size_t need = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, need, keys_in.p, keys_out.p, pos_in.p, pos_out.p, k, 0,
                                     64, s);
