@@ -71,7 +71,8 @@ struct Ctl {
   int fixpoint;  // 1 if the loop ended at a fixpoint (no change / no dirty row): certifies the bounds
   // hand-off of a full round's row phase to k_rows_full (engine state kept across launches)
   int need_full;              // the engine exited to have round `rounds` run its F2 externally
-  int pad0, pad1;
+  unsigned stamp_base;        // stamp base of the running propagate (for the hand-off launches)
+  int pad1;
   unsigned long long t0;      // globaltimer at the start of the propagate (time limit, stats)
   int pad[4];
 };

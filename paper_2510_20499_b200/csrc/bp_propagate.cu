@@ -1469,9 +1469,15 @@ __device__ void zero_par(ParCtl* q)
 #ifndef BP_F2_MIN_BLOCKS
 #define BP_F2_MIN_BLOCKS 2
 #endif
+// The host enqueues [k_rows_full, k_cand_pieces, k_engine(resume)] speculatively, several rounds
+// ahead without waiting: each is a no-op unless the engine handed a full round over (need_full).
 __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
-    k_rows_full(DevProblem P, DevState S, Limits lim, int par, unsigned stamp)
+    k_rows_full(DevProblem P, DevState S, Limits lim)
 {
+  if (!ldv(&S.ctl->need_full)) return;
+  const int rnd         = ldv(&S.ctl->rounds);
+  const int par         = rnd & 1;
+  const unsigned stamp  = ldv(&S.ctl->stamp_base) + (unsigned)rnd;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
@@ -1480,9 +1486,10 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
 }
 
 // Candidate pieces of rows above kCandSplit, after k_rows_full published their activities.
-__global__ void __launch_bounds__(kThreads) k_cand_pieces(DevProblem P, DevState S, Limits lim,
-                                                          int par, unsigned stamp)
+__global__ void __launch_bounds__(kThreads) k_cand_pieces(DevProblem P, DevState S, Limits lim)
 {
+  if (!ldv(&S.ctl->need_full)) return;
+  const unsigned stamp = ldv(&S.ctl->stamp_base) + (unsigned)ldv(&S.ctl->rounds);
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
@@ -1522,6 +1529,11 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     return;
   }
 
+  if (resume) {  // nothing handed over: the engine already finished (speculative launch)
+    if (!ldv(&S.ctl->need_full)) return;
+    grid.sync();  // every block has read need_full before it is cleared
+    if (blockIdx.x == 0 && threadIdx.x == 0) S.ctl->need_full = 0;
+  }
   const unsigned long long t0 = resume ? ldv(&S.ctl->t0) : globaltimer();
   const bool timed            = isfinite(lim.time_limit);
   const bool lead             = blockIdx.x == 0 && threadIdx.x == 0;
@@ -1536,7 +1548,8 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     any_change = ldv(&S.ctl->any_change) != 0;
     resumed    = true;
   } else if (lead) {
-    S.ctl->t0 = t0;
+    S.ctl->t0         = t0;
+    S.ctl->stamp_base = stamp_base;
   }
   if (!resume && full_first == 2) {
     // frontier start from a certified fixpoint: rows(changed) / vars(rows) of the staged list
@@ -2090,26 +2103,24 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   BP_CUDA(cudaEventRecord(P.ev0, s));
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
   ++g_kernel_launches;
-  while (ext) {  // full rounds: the row phase runs in k_rows_full, then the engine resumes
-    int h[2];
-    BP_CUDA(cudaMemcpyAsync(h, &P.st.ctl->rounds, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BP_CUDA(cudaMemcpyAsync(h + 1, &P.st.ctl->need_full, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BP_CUDA(cudaStreamSynchronize(s));
-    if (!h[1]) break;
-    BP_CUDA(cudaMemsetAsync(&P.st.ctl->need_full, 0, sizeof(int), s));
-    const int par           = h[0] & 1;
-    const unsigned stamp    = sb + (unsigned)h[0];
-    k_rows_full<<<P.f2_blocks, kThreads, sizeof(Smem), s>>>(d, st, l, par, stamp);
-    BP_CUDA(cudaGetLastError());
-    if (P.n_cpiece) {
-      k_cand_pieces<<<std::min(P.f2_blocks, (P.n_cpiece + kWarps - 1) / kWarps), kThreads, sizeof(Smem), s>>>(
-          d, st, l, par, stamp);
-      BP_CUDA(cudaGetLastError());
-      ++g_kernel_launches;
-    }
+  // full rounds: the row phase runs in k_rows_full, then the engine resumes. Batches of such
+  // round trips are enqueued without waiting (no-ops past the engine's end); the host only reads
+  // need_full between batches (1, 2, 4, 8 rounds).
+  for (int batch = 1; ext; batch = std::min(2 * batch, 8)) {
     resume = 1;
-    BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
-    g_kernel_launches += 2;
+    for (int b = 0; b < batch; ++b) {
+      k_rows_full<<<P.f2_blocks, kThreads, sizeof(Smem), s>>>(d, st, l);
+      if (P.n_cpiece)
+        k_cand_pieces<<<std::min(P.f2_blocks, (P.n_cpiece + kWarps - 1) / kWarps), kThreads,
+                        sizeof(Smem), s>>>(d, st, l);
+      BP_CUDA(cudaGetLastError());
+      BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
+      g_kernel_launches += P.n_cpiece ? 3 : 2;
+    }
+    int h = 0;
+    BP_CUDA(cudaMemcpyAsync(&h, &P.st.ctl->need_full, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaStreamSynchronize(s));
+    if (!h) break;
   }
   BP_CUDA(cudaEventRecord(P.ev1, s));
   RunResult r{0, 0, 0, 0};

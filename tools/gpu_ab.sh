@@ -4,7 +4,7 @@
 TAG=${1:-ab}
 O=gpurun_out/$TAG
 mkdir -p $O
-#timeout 600 python -m pytest tests/test_gpu_propagation.py tests/test_gpu_probing.py tests/test_gpu_rounding.py -x -q > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
+timeout 600 python -m pytest tests/test_gpu_propagation.py tests/test_gpu_probing.py tests/test_gpu_rounding.py -x -q > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
 run() {  # name
   timeout 300 python tools/phase_profile.py --workload C2 > $O/phase_$1.log 2>&1
   BP_DEBUG=1 timeout 300 python tools/ncu_target.py --workload C2 --reps 1 > $O/dbg_$1.log 2>&1
