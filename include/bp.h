@@ -164,7 +164,7 @@ int bp_assemble_bulk_warm_start(const bp_cache* c, const int32_t* vars, const do
 typedef struct {
   double random_band;         /* 0.25 */
   int32_t single_var_tail;    /* 36 */
-  int32_t repair_enabled;     /* 0 (repair is not implemented: non-zero is rejected) */
+  int32_t repair_enabled;     /* 0 (rounding.hpp:25; on: failed single-var probes call bp_repair) */
   int32_t repair_attempt_cap; /* 16 */
   int32_t repair_shift_cap;   /* 64 */
 } bp_rounding_config;
@@ -200,6 +200,16 @@ int bp_propagation_round_rng(bp_problem* p, const double* start_values, const bp
                              char* rng_state, int64_t rng_state_bytes, double deadline_sec,
                              const bp_rounding_config* cfg, double* out_values,
                              bp_rounding_outcome* out);
+
+/* pulse::repair (rounding.hpp:234-311): shifts the fixed values (v, val) in list order, one variable
+ * per most-violated row, until propagation from the original bounds with every value fixed
+ * succeeds. *repaired = 1 on success (RepairResult present) with the shifted values in out_vals
+ * (nfixed, same order as the input) and the propagated bounds in out_bounds2n; 0 = std::nullopt
+ * (no in-bounds shift, shift cap cfg->repair_shift_cap reached, deadline expired, or propagation
+ * infeasible without violated rows). deadline_sec <= 0 = never. cfg may be NULL (defaults). */
+int bp_repair(bp_problem* p, const int32_t* fixed_vars, const double* fixed_vals, int32_t nfixed,
+              double deadline_sec, const bp_rounding_config* cfg, int32_t* repaired,
+              double* out_vals, double* out_bounds2n);
 
 /* pulse::parallel_propagate (rounding.hpp:213-224; detail::run_probe :167-207): both candidate
  * vectors v0 / v1 for `vars` from host bounds base2n (+ its infeasible flag), warm-started from

@@ -13,6 +13,7 @@
 //   pulse::build_cache                 probing.hpp:243       -> bp_build_cache
 //   pulse::assemble_bulk_warm_start    probing.hpp:292       -> bp_assemble_bulk_warm_start
 //   pulse::parallel_propagate          rounding.hpp:213      -> bp_parallel_propagate
+//   pulse::repair                      rounding.hpp:234      -> bp_repair
 //   pulse::propagation_round           rounding.hpp:393      -> bp_propagation_round_rng
 //                                                               (+ the reference's own lp_polish)
 //
@@ -446,6 +447,31 @@ inline ParallelProbeResult parallel_propagate(const ProblemDef& p, const BoundsS
     for (int j = 0; j < nfx[q]; ++j) pr.fixed.push_back({fv[k * q + j], fx[k * q + j]});
   }
   return r;
+}
+
+// rounding.hpp:234 (device activity sweeps, most-violated-row scan and propagate)
+inline std::optional<RepairResult> repair(const ProblemDef& p,
+                                          std::vector<std::pair<int, double>> fixed,
+                                          const Deadline& deadline, const RoundingConfig& cfg,
+                                          const WorkPlan& /*plan*/)
+{
+  bp_rounding_config bc;
+  bp_rounding_config_default(&bc);
+  bc.repair_shift_cap = cfg.repair_shift_cap;
+  const double rem = deadline.remaining_sec();
+  const double dl  = rem == kInf ? 0.0 : (rem > 0.0 ? rem : 1e-300);  // 0 = never in bp.h
+  std::vector<int32_t> fv(fixed.size() + 1);
+  std::vector<double> fx(fixed.size() + 1), out(fixed.size() + 1), b(2 * (size_t)p.n_vars + 1);
+  for (size_t j = 0; j < fixed.size(); ++j) {
+    fv[j] = fixed[j].first;
+    fx[j] = fixed[j].second;
+  }
+  int32_t ok = 0;
+  detail::check(bp_repair(detail::handle(p), fv.data(), fx.data(), (int32_t)fixed.size(), dl, &bc,
+                          &ok, out.data(), b.data()));
+  if (!ok) return std::nullopt;
+  for (size_t j = 0; j < fixed.size(); ++j) fixed[j].second = out[j];
+  return RepairResult{std::move(fixed), detail::from_raw(p, b.data(), false)};
 }
 
 // rounding.hpp:393. The bulk loop runs in the engine's driver with device-resident bounds and

@@ -83,6 +83,7 @@ class Ref:
                 "ref_implied_slack_sort": (None, [V, V, V, V, V, I]),
                 "ref_get_bulk_size": (I, [I, I, I]),
                 "ref_generate_candidate_values": (None, [V, V, I, V, I, V, D, V, V]),
+                "ref_repair": (I, [V, V, V, I, I, V, V]),
                 "ref_parallel_propagate": (None, [V, V, I, V, I, V, V, V, V, V, V, V, V, V, V, V, V]),
                 "ref_propagation_round": (None, [V, V, V, C.c_ulonglong, D, D, I, V, V]),
             }
@@ -349,3 +350,16 @@ def ref_propagation_round(rp, n_vars, start, cache=None, seed=0, deadline=0.0, b
     keys = ["rounding_infeasible", "timed_out", "completed", "repair_attempts", "bulks_committed",
             "set_count"]
     return vals[:n_vars], dict(zip(keys, (int(x) for x in fl)))
+
+
+def ref_repair(rp, n_vars, fixed, shift_cap=64):
+    """rounding.hpp:234 repair through oracle/_ref: None (std::nullopt) or (values, bounds2n)."""
+    k = len(fixed)
+    fv = np.ascontiguousarray([v for v, _ in fixed] or [0], dtype=np.int32)
+    fx = np.ascontiguousarray([x for _, x in fixed] or [0.0], dtype=np.float64)
+    out = np.zeros(max(k, 1))
+    b = np.zeros(max(2 * n_vars, 1))
+    ok = Ref.lib().ref_repair(rp.h, _p(fv), _p(fx), k, int(shift_cap), _p(out), _p(b))
+    if not ok:
+        return None
+    return [(int(v), float(out[j])) for j, (v, _) in enumerate(fixed)], b[: 2 * n_vars]

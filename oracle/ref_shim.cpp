@@ -472,6 +472,24 @@ void ref_parallel_propagate(const void* pv, const double* base2n, int base_infea
   }
 }
 
+// rounding.hpp:234 repair(p, fixed, Deadline::never(), cfg{shift_cap}, plan). Returns 1 when a
+// RepairResult is present (shifted values in out_vals, its bounds in out_bounds2n), else 0.
+int ref_repair(const void* pv, const int* fixed_vars, const double* fixed_vals, int nfixed,
+               int shift_cap, double* out_vals, double* out_bounds2n)
+{
+  const auto& p = *static_cast<const ProblemDef*>(pv);
+  std::vector<std::pair<int, double>> fixed(nfixed);
+  for (int j = 0; j < nfixed; ++j) fixed[j] = {fixed_vars[j], fixed_vals[j]};
+  RoundingConfig cfg;
+  cfg.repair_shift_cap = shift_cap;
+  const WorkPlan plan  = build_work_plan(p);
+  const auto r         = repair(p, fixed, Deadline::never(), cfg, plan);
+  if (!r) return 0;
+  for (int j = 0; j < nfixed; ++j) out_vals[j] = r->values[j].second;
+  bounds_to(r->bounds, out_bounds2n, nullptr);
+  return 1;
+}
+
 // rounding.hpp:393 with a cache handle (or null) and Rng(seed). lp_polish runs inside (OUT OF
 // SCOPE for parity; callers compare integer values and flags). out_values has n_vars entries.
 // flags = {rounding_infeasible, timed_out, completed, repair_attempts, bulks_committed, set_count}

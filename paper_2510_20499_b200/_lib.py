@@ -117,6 +117,9 @@ _SIGS = [
     ("bp_propagation_round_rng", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p,
                                            C.c_int64, C.c_double, C.POINTER(bp_rounding_config),
                                            C.c_void_p, C.POINTER(bp_rounding_outcome)]),
+    ("bp_repair", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
+                            C.POINTER(bp_rounding_config), C.POINTER(C.c_int32), C.c_void_p,
+                            C.c_void_p]),
     ("bp_parallel_propagate", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

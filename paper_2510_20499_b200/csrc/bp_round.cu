@@ -143,6 +143,62 @@ __global__ void k_count_violations(DevProblem P, const RowRec* rec, const double
   if (cnt) atomicAdd(out, cnt);
 }
 
+// repair's most-violated-row scan (rounding.hpp:249-266), pass 1: the largest violation above
+// kFeasTol (positive doubles order like their bit patterns).
+__device__ __forceinline__ void row_violations(const RowRec& q, const double2* aux, int k,
+                                               double& vu, double& vl)
+{
+  double mnf, mxf;
+  int nmn, nmx;
+  decode_rec(q, aux, k, mnf, nmn, mxf, nmx);
+  vu = (isfinite(q.g) && nmn == 0) ? __dsub_rn(mnf, q.g) : -INFINITY;
+  vl = (isfinite(q.h) && nmx == 0) ? __dsub_rn(q.h, mxf) : -INFINITY;
+}
+
+__global__ void k_worst_viol(DevProblem P, const RowRec* rec, const double2* aux,
+                             unsigned long long* best)
+{
+  double w = kFeasTol;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < P.m; k += gridDim.x * blockDim.x) {
+    double vu, vl;
+    row_violations(rec[k], aux, k, vu, vl);
+    if (vu > w) w = vu;
+    if (vl > w) w = vl;
+  }
+  unsigned long long b = __double_as_longlong(w);
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+    b = x > b ? x : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b > (unsigned long long)__double_as_longlong(kFeasTol))
+    atomicMax(best, b);
+}
+
+// pass 2: the first (row ascending, upper side before lower) candidate attaining it, as 2k + side
+// (the reference keeps the earlier candidate on ties: `viol > worst_viol`).
+__global__ void k_worst_pos(DevProblem P, const RowRec* rec, const double2* aux,
+                            const unsigned long long* best, int* pos)
+{
+  const unsigned long long b = *best;
+  if (b == 0) return;
+  const double w = __longlong_as_double((long long)b);
+  int first      = INT_MAX;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < P.m; k += gridDim.x * blockDim.x) {
+    double vu, vl;
+    row_violations(rec[k], aux, k, vu, vl);
+    if (vu == w) {
+      first = min(first, 2 * k);
+      break;  // later k of this thread are larger
+    }
+    if (vl == w) {
+      first = min(first, 2 * k + 1);
+      break;
+    }
+  }
+  for (int o = 16; o; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  if ((threadIdx.x & 31) == 0 && first != INT_MAX) atomicMin(pos, first);
+}
+
 struct NotFixed {
   const double2* ws;
   __device__ __forceinline__ bool operator()(const int& v) const { return ws[v].x != ws[v].y; }
@@ -177,7 +233,7 @@ struct RoundCtx {
   Problem& P;
   const bp_problem_host& H;
   cudaStream_t s;
-  DBuf<double2> ws, root, tmp2;
+  DBuf<double2> ws, root, tmp2, orig;
   DBuf<RowRec> ws_rec;   // activity records consistent with ws while ws_cert holds
   DBuf<double2> ws_aux;
   DBuf<int> unset, unset_alt, pos_in, pos_out, sel_count, flags, ivar, ichg;
@@ -449,6 +505,101 @@ struct RoundCtx {
     return out;
   }
 
+  // repair (rounding.hpp:234-311): shifts fixed values one variable per violated row until
+  // propagation from the original bounds succeeds. Per shift: original bounds + fixings built on
+  // the device, full activity sweep, most-violated-row scan (k_worst_viol / k_worst_pos), then the
+  // shift chosen on the host from that one row. On success the repaired bounds are left in
+  // P.st.bounds and *rr holds the propagate's result (its exit reason certifies the state).
+  template <class Expired>
+  bool repair(std::vector<std::pair<int, double>>& fixed, const double2* d_orig, Expired expired,
+              int shift_cap, RunResult* rr)
+  {
+    const int n = P.n;
+    std::vector<int> fixed_pos(n, -1);
+    for (size_t j = 0; j < fixed.size(); ++j) fixed_pos[fixed[j].first] = (int)j;
+    // b.fix in list order: the last fixing of a var wins, so scatter one value per var
+    std::vector<int> fv;
+    std::vector<double2> fb;
+    std::vector<int> slot(n, -1);
+    for (const auto& [v, val] : fixed) {
+      if (slot[v] < 0) {
+        slot[v] = (int)fv.size();
+        fv.push_back(v);
+        fb.push_back(make_double2(val, val));
+      } else {
+        fb[slot[v]] = make_double2(val, val);
+      }
+    }
+    DBuf<int> dfv;
+    DBuf<double2> dfb;
+    if (!fv.empty()) {
+      dfv.alloc(fv.size());
+      dfb.alloc(fv.size());
+      BP_CUDA(cudaMemcpyAsync(dfv.p, fv.data(), sizeof(int) * fv.size(), cudaMemcpyHostToDevice, s));
+      BP_CUDA(cudaMemcpyAsync(dfb.p, fb.data(), sizeof(double2) * fv.size(), cudaMemcpyHostToDevice, s));
+    }
+    DBuf<unsigned long long> best;
+    DBuf<int> bpos;
+    best.alloc(1);
+    bpos.alloc(1);
+    for (int iter = 0; iter < shift_cap; ++iter) {
+      if (expired()) return false;
+      if (n) BP_CUDA(cudaMemcpyAsync(P.st.bounds, d_orig, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+      if (!fv.empty())
+        k_scatter<<<blocks_for(fv.size()), 256, 0, s>>>(P.st.bounds, dfv.p, dfb.p, (int)fv.size());
+      BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+      run_engine(P, MODE_ACTIVITY, true, limits(), s);
+      dev_ms += P.last_kernel_ms;
+      BP_CUDA(cudaMemsetAsync(best.p, 0, sizeof(unsigned long long), s));
+      BP_CUDA(cudaMemsetAsync(bpos.p, 0x7f, sizeof(int), s));
+      k_worst_viol<<<blocks_for(P.m), 256, 0, s>>>(P.dev(), P.st.rec, P.st.aux, best.p);
+      k_worst_pos<<<blocks_for(P.m), 256, 0, s>>>(P.dev(), P.st.rec, P.st.aux, best.p, bpos.p);
+      unsigned long long hb = 0;
+      int hpos              = 0;
+      BP_CUDA(cudaMemcpyAsync(&hb, best.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
+      BP_CUDA(cudaMemcpyAsync(&hpos, bpos.p, sizeof(hpos), cudaMemcpyDeviceToHost, s));
+      sync();
+      if (hb == 0) {  // no violated row: propagate from the fixed-value state (rounding.hpp:268-274)
+        BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
+        *rr = run_engine(P, MODE_PROPAGATE, true, limits(), s);
+        bp_calls++;
+        dev_ms += P.last_kernel_ms;
+        return rr->status != BP_STATUS_INFEASIBLE;
+      }
+      double worst_viol;
+      std::memcpy(&worst_viol, &hb, sizeof(double));
+      const int row         = hpos >> 1;
+      const bool upper_side = (hpos & 1) == 0;
+      // smallest in-bounds shift of one fixed variable that restores the row (rounding.hpp:276-306)
+      int best_var    = -1;
+      double best_val = 0.0;
+      for (int e = P.h_row_start[row]; e < P.h_row_start[row + 1]; ++e) {
+        const int v = H.row_col[e];
+        if (fixed_pos[v] < 0) continue;
+        const double a_kv = H.row_val[e];
+        const double cur  = fixed[fixed_pos[v]].second;
+        double delta      = worst_viol / std::abs(a_kv);
+        if (H.is_integer[v]) delta = std::ceil(delta - 1e-9);
+        double cand;
+        if (upper_side) cand = (a_kv > 0.0) ? cur - delta : cur + delta;
+        else cand = (a_kv > 0.0) ? cur + delta : cur - delta;
+        if (cand < H.var_lower[v] - 1e-9 || cand > H.var_upper[v] + 1e-9) continue;
+        if (best_var < 0 || std::abs(cand - cur) < std::abs(best_val - fixed[fixed_pos[best_var]].second)) {
+          best_var = v;
+          best_val = cand;
+        }
+      }
+      if (best_var < 0) return false;
+      fixed[fixed_pos[best_var]].second = best_val;
+      const double2 nb                  = make_double2(best_val, best_val);
+      fb[slot[best_var]]                = nb;
+      BP_CUDA(cudaMemcpyAsync(dfb.p + slot[best_var], &fb[slot[best_var]], sizeof(double2),
+                              cudaMemcpyHostToDevice, s));
+    }
+    sync();
+    return false;
+  }
+
   // rounding.hpp:361-383
   int count_envelope_violations(const std::vector<int>& vars, const std::vector<double>& values)
   {
@@ -554,7 +705,8 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
     bp_rounding_config cfg;
     bp_rounding_config_default(&cfg);
     if (cfg_in) cfg = *cfg_in;
-    if (cfg.repair_enabled) throw std::invalid_argument("repair is not supported by this engine yet");
+    if (cfg.repair_enabled && (cfg.repair_attempt_cap < 0 || cfg.repair_shift_cap < 0))
+      throw std::invalid_argument("negative repair cap");
     bp::Problem& P                 = bp_problem_impl(p);
     const bp_problem_host& H       = bp_problem_hostdata(p);
     const bp::HostCache* hc        = cache ? bp_cache_host(cache) : nullptr;
@@ -703,7 +855,26 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
         X.scatter(X.ws.p, {v}, {make_double2(val, val)});
         X.ws_cert = false;
         X.drop_fixed();
-        force = true;  // repair disabled (rounding.hpp:505-507)
+        if (cfg.repair_enabled && o.repair_attempts < cfg.repair_attempt_cap && !expired()) {
+          o.repair_attempts++;  // rounding.hpp:492-504
+          if (!X.orig.p && n) X.orig.upload(reinterpret_cast<const double2*>(orig.data()), n);
+          std::vector<std::pair<int, double>> rep = committed;
+          bp::RunResult rr{};
+          if (X.repair(rep, X.orig.p, expired, cfg.repair_shift_cap, &rr)) {
+            committed = std::move(rep);
+            if (n) BP_CUDA(cudaMemcpyAsync(X.ws.p, P.st.bounds, sizeof(double2) * n, cudaMemcpyDeviceToDevice, X.s));
+            X.ws_infeasible       = false;  // ws.clear_infeasible()
+            X.ws_cert             = rr.fixpoint != 0;
+            if (X.ws_cert) X.snapshot_ws_activities();
+            o.rounding_infeasible = 0;
+            recovery              = false;
+            X.drop_fixed();
+          } else {
+            force = true;
+          }
+        } else {
+          force = true;
+        }
         continue;
       }
       // terminal phase (rounding.hpp:511-528)
@@ -810,6 +981,61 @@ int bp_propagation_round_rng(bp_problem* p, const double* start_values, const bp
   }
   std::memcpy(rng_state, st.c_str(), st.size() + 1);
   return BP_OK;
+}
+
+int bp_repair(bp_problem* p, const int32_t* fixed_vars, const double* fixed_vals, int32_t nfixed,
+              double deadline_sec, const bp_rounding_config* cfg_in, int32_t* repaired,
+              double* out_vals, double* out_bounds2n)
+{
+  try {
+    if (!p || !repaired || nfixed < 0 || (nfixed > 0 && (!fixed_vars || !fixed_vals || !out_vals)) ||
+        !out_bounds2n)
+      throw std::invalid_argument("null argument");
+    bp_rounding_config cfg;
+    bp_rounding_config_default(&cfg);
+    if (cfg_in) cfg = *cfg_in;
+    bp::Problem& P           = bp_problem_impl(p);
+    const bp_problem_host& H = bp_problem_hostdata(p);
+    const int n              = P.n;
+    std::vector<std::pair<int, double>> fixed(nfixed);
+    for (int j = 0; j < nfixed; ++j) {
+      if (fixed_vars[j] < 0 || fixed_vars[j] >= n) throw std::out_of_range("var out of range");
+      fixed[j] = {fixed_vars[j], fixed_vals[j]};
+    }
+    std::lock_guard<std::mutex> lk(P.mu);
+    BP_CUDA(cudaSetDevice(P.device));
+    const auto t0 = std::chrono::steady_clock::now();
+    auto expired  = [&] {
+      if (!(deadline_sec > 0.0)) return false;
+      return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() >= deadline_sec;
+    };
+    bp::RoundCtx X(P, H);
+    std::vector<double> orig(2 * (size_t)n);
+    bp_problem_root(p, orig.data());
+    X.orig.upload(reinterpret_cast<const double2*>(orig.data()), n);
+    bp::RunResult rr{};
+    const bool ok = X.repair(fixed, X.orig.p, expired, cfg.repair_shift_cap, &rr);
+    *repaired     = ok ? 1 : 0;
+    if (ok) {
+      for (int j = 0; j < nfixed; ++j) out_vals[j] = fixed[j].second;
+      if (n)
+        BP_CUDA(cudaMemcpyAsync(out_bounds2n, P.st.bounds, sizeof(double2) * n, cudaMemcpyDeviceToHost, X.s));
+      X.sync();
+    }
+    return BP_OK;
+  } catch (const std::invalid_argument& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_OUT_OF_RANGE;
+  } catch (const bp::cuda_error& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_CUDA;
+  } catch (const std::exception& e) {
+    bp_set_last_error(e.what());
+    return BP_ERR_RUNTIME;
+  }
 }
 
 int bp_parallel_propagate(bp_problem* p, const double* base2n, int32_t base_infeasible,

@@ -4,6 +4,7 @@
 * ``initial_sort`` (:35-65) and ``get_bulk_size`` (:119-123) (host helpers)
 * ``propagation_round`` (:393-558): the whole bulk loop runs in libbp's driver with device-resident
   bounds; the host RNG stream is the reference's (std::mt19937_64(seed)).
+* ``repair`` (:234-311): device activity sweeps + most-violated-row scan, host shift choice
 
 ``lp_polish`` (PDHG) is out of scope: ``propagation_round`` returns the point the reference would
 polish, and ``outcome.bounds_feasible`` tells whether it would.
@@ -71,19 +72,52 @@ def get_bulk_size(remaining: int, recovery: bool, single_var_tail: int = 36) -> 
     return int(_round_half_away(math.sqrt(float(remaining))))
 
 
-def propagation_round(p: ProblemDef, start_values, cache: ProbingCache | None, seed: int,
-                      deadline_sec: float = math.inf, cfg: RoundingConfig | None = None) -> RoundingOutcome:
-    """rounding.hpp:393 with Rng(seed) and Deadline(deadline_sec) (inf = never)."""
+def _config(cfg: RoundingConfig | None):
     cfg = cfg or RoundingConfig()
-    dp = device_problem(p)
-    L = _lib.lib()
     c = _lib.bp_rounding_config()
-    L.bp_rounding_config_default(C.byref(c))
+    _lib.lib().bp_rounding_config_default(C.byref(c))
     c.random_band = cfg.random_band
     c.single_var_tail = cfg.single_var_tail
     c.repair_enabled = 1 if cfg.repair_enabled else 0
     c.repair_attempt_cap = cfg.repair_attempt_cap
     c.repair_shift_cap = cfg.repair_shift_cap
+    return c
+
+
+@dataclass
+class RepairResult:
+    """rounding.hpp:225-228."""
+    values: list              # [(var, value)] in the input order
+    bounds: "object"          # BoundsState
+
+
+def repair(p: ProblemDef, fixed, deadline_sec: float = math.inf,
+           cfg: RoundingConfig | None = None, plan=None) -> RepairResult | None:
+    """rounding.hpp:234-311 on the engine: None where the reference returns std::nullopt. The
+    plan argument is accepted for signature parity only."""
+    from .propagation import BoundsState
+    dp = device_problem(p)
+    c = _config(cfg)
+    fv = np.ascontiguousarray([v for v, _ in fixed], dtype=np.int32)
+    fx = np.ascontiguousarray([x for _, x in fixed], dtype=np.float64)
+    out = np.zeros(max(len(fixed), 1))
+    b = np.zeros(max(2 * p.n_vars, 1))
+    ok = C.c_int32(0)
+    dl = 0.0 if not math.isfinite(deadline_sec) else float(deadline_sec)
+    _lib.check(_lib.lib().bp_repair(dp.h, _lib.ptr(fv), _lib.ptr(fx), len(fixed), dl, C.byref(c),
+                                    C.byref(ok), _lib.ptr(out), _lib.ptr(b)))
+    if not ok.value:
+        return None
+    return RepairResult([(int(v), float(out[j])) for j, (v, _) in enumerate(fixed)],
+                        BoundsState(raw=b[: 2 * p.n_vars]))
+
+
+def propagation_round(p: ProblemDef, start_values, cache: ProbingCache | None, seed: int,
+                      deadline_sec: float = math.inf, cfg: RoundingConfig | None = None) -> RoundingOutcome:
+    """rounding.hpp:393 with Rng(seed) and Deadline(deadline_sec) (inf = never)."""
+    dp = device_problem(p)
+    L = _lib.lib()
+    c = _config(cfg)
     sv = np.ascontiguousarray(start_values, dtype=np.float64)
     out = np.zeros(max(p.n_vars, 1))
     o = _lib.bp_rounding_outcome()

@@ -296,6 +296,49 @@ void rounding_mixed()
          std::to_string(runs) + " runs, " + std::to_string(bad) + " mismatches");
 }
 
+void repair_stream()
+{
+  std::mt19937_64 gen(2718);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  int bad = 0, runs = 0, present = 0, rounds_bad = 0, rounds = 0;
+  for (int t = 0; t < 200; ++t) {
+    const ProblemDef p = testkit::random_instance(gen, {});
+    std::vector<std::pair<int, double>> fixed;
+    for (int i = 0; i < p.n_vars; ++i)
+      if (p.is_integer[i] && U(gen) < 0.8)
+        fixed.push_back({i, std::min(p.var_upper[i], std::floor(p.var_lower[i] +
+                                                                (p.var_upper[i] - p.var_lower[i] + 1) * U(gen)))});
+    RoundingConfig cfg;
+    const WorkPlan plan = build_work_plan(p);
+    const auto ra       = repair(p, fixed, Deadline::never(), cfg, plan);
+    const auto rg       = pg::repair(p, fixed, Deadline::never(), cfg, plan);
+    ++runs;
+    bool same = ra.has_value() == rg.has_value();
+    if (same && ra) {
+      ++present;
+      same = ra->values == rg->values && same_state(ra->bounds, rg->bounds);
+    }
+    if (!same) ++bad;
+    // propagation_round with repair enabled (rounding.hpp:492-504)
+    SolutionVector s;
+    for (int i = 0; i < p.n_vars; ++i) s.values.push_back(p.var_lower[i] + (p.var_upper[i] - p.var_lower[i]) * U(gen));
+    RoundingConfig rc;
+    rc.repair_enabled = true;
+    Rng a(t), g(t);
+    const auto oa = propagation_round(p, s, nullptr, Deadline::never(), a, rc);
+    const auto og = pg::propagation_round(p, s, nullptr, Deadline::never(), g, rc);
+    ++rounds;
+    if (!(oa.rounding_infeasible == og.rounding_infeasible && oa.completed == og.completed &&
+          oa.repair_attempts == og.repair_attempts && oa.bulks_committed == og.bulks_committed &&
+          oa.set_count == og.set_count && same_bits(oa.point.values, og.point.values) && a == g))
+      ++rounds_bad;
+  }
+  report("repair + propagation_round with repair enabled", bad == 0 && rounds_bad == 0,
+         std::to_string(runs) + " repairs (" + std::to_string(present) + " present), " +
+             std::to_string(bad) + " mismatches; " + std::to_string(rounds) + " rounding runs, " +
+             std::to_string(rounds_bad) + " mismatches");
+}
+
 void errors()
 {
   const ProblemDef p = testkit::tiny_knapsack();
@@ -329,6 +372,7 @@ int main()
   warm_start_and_pairs();
   rounding_stream();
   rounding_mixed();
+  repair_stream();
   std::printf("%d failure(s)\n", g_failures);
   return g_failures;
 }

@@ -138,3 +138,86 @@ def test_parallel_propagate_matches_reference(oracle_built):
                 assert np.array_equal(g[q].bounds.raw().view(np.uint64), rb.view(np.uint64)), (t, q)
                 assert (g[q].bounds.infeasible(), g[q].infeas_count, g[q].evicted, g[q].fixed) == \
                     (rinf, rcnt, rev, rfx), (t, q, use_cache)
+
+
+def test_repair_known_answers():
+    """test_rounding.cpp:178-205 (repair shifts fixed values inside original bounds)."""
+    from paper_2510_20499_b200.rounding import repair
+    knap = make_problem([(0, 1, True, -1), (0, 1, True, -1)], [([(0, 1.0), (1, 1.0)], -INF, 1.0)])
+    r = repair(knap, [(0, 1.0), (1, 1.0)])
+    assert r is not None
+    vals = dict(r.values)
+    assert vals[0] + vals[1] <= 1.0
+    capped = make_problem([(0, 3, True)], [([(0, 1.0)], 5.0, INF)])
+    assert repair(capped, [(0, 3.0)]) is None
+    r = repair(knap, [(0, 1.0), (1, 0.0)])
+    assert r is not None and r.values == [(0, 1.0), (1, 0.0)]
+
+
+def test_repair_matches_reference(oracle_built):
+    """repair (rounding.hpp:234-311) on random fixings of random instances: presence, shifted
+    values and the propagated bounds identical to the reference's (bounds bitwise)."""
+    from oracle.bind import RefRng, ref_repair
+
+    from paper_2510_20499_b200.rounding import RoundingConfig, repair
+    rng = RefRng(8080)
+    gen = np.random.default_rng(17)
+    n_ok = 0
+    for t in range(150):
+        rp = rng.random_instance()
+        p = rp.to_def()
+        ints = [i for i in range(p.n_vars) if p.is_integer[i]]
+        if not ints:
+            continue
+        vars_ = [i for i in ints if gen.random() < 0.8] or ints[:1]
+        if gen.random() < 0.2:
+            vars_ = vars_ + vars_[:1]  # a repeated fixing: the last one wins
+        fixed = [(v, float(np.floor(p.var_lower[v] + (p.var_upper[v] - p.var_lower[v] + 1) * gen.random())))
+                 for v in vars_]
+        fixed = [(v, min(x, float(p.var_upper[v]))) for v, x in fixed]
+        cap = int(gen.choice([1, 2, 64]))
+        g = repair(p, fixed, cfg=RoundingConfig(repair_shift_cap=cap))
+        r = ref_repair(rp, p.n_vars, fixed, cap)
+        assert (g is None) == (r is None), t
+        if g is None:
+            continue
+        n_ok += 1
+        assert g.values == r[0], t
+        assert np.array_equal(g.bounds.raw().view(np.uint64), r[1].view(np.uint64)), t
+    assert n_ok > 10
+
+
+def test_rounding_with_repair_known_answers():
+    """test_rounding.cpp:360-390 (propagation_round drives repair when enabled)."""
+    from paper_2510_20499_b200.rounding import RoundingConfig
+    cfg = RoundingConfig(repair_enabled=True)
+    q = make_problem([(0, 1, True)], [([(0, 1.0)], 1.0, INF), ([(0, 1.0)], -INF, 0.0)])
+    out = propagation_round(q, [0.5], None, seed=9, deadline_sec=5.0, cfg=cfg)
+    assert out.repair_attempts >= 1 and out.rounding_infeasible and out.completed
+    e = make_problem([(0, 1, True), (0, 1, True)], [([(0, 1.0), (1, 1.0)], 2.0, 2.0)])
+    out = propagation_round(e, [0.2, 0.2], None, seed=4, deadline_sec=5.0, cfg=cfg)
+    assert out.completed and list(out.values) == [1.0, 1.0]
+
+
+def test_rounding_with_repair_matches_reference(oracle_built):
+    """propagation_round with repair_enabled on the acceptance-style stream: identical integer
+    outputs and flags, including repair_attempts."""
+    from oracle.bind import RefRng, ref_propagation_round
+
+    from paper_2510_20499_b200.rounding import RoundingConfig
+    rng = RefRng(6161)
+    cfg = RoundingConfig(repair_enabled=True)
+    attempts = 0
+    for t in range(300):
+        rp = rng.random_instance()
+        p = rp.to_def()
+        start = np.array([p.var_lower[i] + rng.uniform_real(0.0, 1.0) * (p.var_upper[i] - p.var_lower[i])
+                          for i in range(p.n_vars)])
+        rv, rf = ref_propagation_round(rp, p.n_vars, start, None, t, repair=True)
+        g = propagation_round(p, start, None, t, cfg=cfg)
+        keys = FLAGS + ("repair_attempts",)
+        assert {k: int(getattr(g, k)) for k in keys} == {k: rf[k] for k in keys}, t
+        isint = p.is_integer.astype(bool)
+        assert np.array_equal(g.values[isint], rv[isint]), t
+        attempts += g.repair_attempts
+    assert attempts > 0
