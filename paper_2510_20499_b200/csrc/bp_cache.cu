@@ -3,6 +3,8 @@
 //
 // References: probing.hpp:30-60 make_branch_spec, :105-190 prioritize_probe_vars,
 // :225-238 probe_variable, :243-281 build_cache, :292-352 assemble_bulk_warm_start.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -473,71 +475,97 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   return out;
 }
 
-// probing.hpp:105-190 from the original bounds' activities.
-std::vector<int> prioritize(const std::vector<int>& row_start, const std::vector<int>& col_start,
-                            const int* col_row, const double* col_val, const uint8_t* is_int,
-                            const double* var_lower, const double* var_upper,
-                            const double* cons_lower, const double* cons_upper,
-                            const std::vector<double>& act, const std::vector<int>& nmin,
-                            const std::vector<int>& nmax)
+__global__ void k_gather_u64(const unsigned long long* src, const int* idx, int k, unsigned long long* dst)
 {
-  const int n = (int)col_start.size() - 1;
-  struct Key {
-    int violated;
-    double max_violation, min_unit_slack;
-    int var;
-  };
-  std::vector<Key> keys;
-  const double kFeasTol = 1e-6;
-  for (int i = 0; i < n; ++i) {
-    if (!is_int[i]) continue;
-    Key key{0, 0.0, INFINITY, i};
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) dst[j] = src[idx[j]];
+}
+__global__ void k_gather_u32(const unsigned* src, const int* idx, int k, unsigned* dst)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) dst[j] = src[idx[j]];
+}
+__global__ void k_gather_i32(const int* src, const int* idx, int k, int* dst)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) dst[j] = src[idx[j]];
+}
+
+// probing.hpp:105-190 on the device: one warp per integer variable folds its column's keys
+// (count, max and min are order-independent here: every folded value is positive, so there are
+// no signed-zero ties), then three stable radix passes give the lexicographic stable order.
+__global__ void k_prio_keys(DevProblem P, const RowRec* rec, const double2* aux,
+                            const double2* bounds, const int* ivar, int k, unsigned* k_viol,
+                            unsigned long long* k_maxv, unsigned long long* k_slack, int* vals)
+{
+  constexpr double kFeasTol = 1e-6;  // common.hpp:20
+  const int lane  = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < k; j += warps) {
+    const int i  = ivar[j];
+    const int e0 = P.col_start[i], e1 = P.col_start[i + 1];
     bool pos = false, neg = false;
-    for (int e = col_start[i]; e < col_start[i + 1]; ++e) (col_val[e] > 0 ? pos : neg) = true;
-    const double lo = var_lower[i], up = var_upper[i];
-    for (int e = col_start[i]; e < col_start[i + 1]; ++e) {
-      const int k    = col_row[e];
-      const double a = col_val[e];
-      if (pos && neg) {
-        const double min_c = a > 0 ? a * lo : a * up;
-        const double max_c = a > 0 ? a * up : a * lo;
+    for (int e = e0 + lane; e < e1; e += 32) (P.col_val[e] > 0 ? pos : neg) = true;
+    const bool both = __any_sync(0xffffffffu, pos) && __any_sync(0xffffffffu, neg);
+    const double2 b = bounds[i];
+    const double lo = b.x, up = b.y;
+    int viol        = 0;
+    double maxv     = 0.0, slk = INFINITY;
+    for (int e = e0 + lane; e < e1; e += 32) {
+      const int r    = P.col_row[e];
+      const double a = P.col_val[e];
+      const RowRec q = rec[r];
+      double mnf, mxf;
+      int nmn, nmx;
+      decode_rec(q, aux, r, mnf, nmn, mxf, nmx);
+      if (both) {
+        const double min_c = a > 0 ? __dmul_rn(a, lo) : __dmul_rn(a, up);
+        const double max_c = a > 0 ? __dmul_rn(a, up) : __dmul_rn(a, lo);
         const bool min_inf = a > 0 ? lo == -INFINITY : up == INFINITY;
         const bool max_inf = a > 0 ? up == INFINITY : lo == -INFINITY;
-        if (std::isfinite(cons_upper[k]) && nmin[k] - (min_inf ? 1 : 0) == 0) {
-          const double fm = max_inf ? INFINITY : act[2 * k] - (min_inf ? 0.0 : min_c) + max_c;
-          if (fm > cons_upper[k] + kFeasTol) {
-            key.violated++;
-            key.max_violation = std::max(key.max_violation, fm - cons_upper[k]);
+        if (isfinite(q.g) && nmn - (min_inf ? 1 : 0) == 0) {
+          const double fm = max_inf ? INFINITY : __dadd_rn(__dsub_rn(mnf, min_inf ? 0.0 : min_c), max_c);
+          if (fm > __dadd_rn(q.g, kFeasTol)) {
+            ++viol;
+            const double d = __dsub_rn(fm, q.g);
+            maxv           = (maxv < d) ? d : maxv;
           }
         }
-        if (std::isfinite(cons_lower[k]) && nmax[k] - (max_inf ? 1 : 0) == 0) {
-          const double fx = min_inf ? -INFINITY : act[2 * k + 1] - (max_inf ? 0.0 : max_c) + min_c;
-          if (fx < cons_lower[k] - kFeasTol) {
-            key.violated++;
-            key.max_violation = std::max(key.max_violation, cons_lower[k] - fx);
+        if (isfinite(q.h) && nmx - (max_inf ? 1 : 0) == 0) {
+          const double fx = min_inf ? -INFINITY : __dadd_rn(__dsub_rn(mxf, max_inf ? 0.0 : max_c), min_c);
+          if (fx < __dsub_rn(q.h, kFeasTol)) {
+            ++viol;
+            const double d = __dsub_rn(q.h, fx);
+            maxv           = (maxv < d) ? d : maxv;
           }
         }
       }
-      if (std::isfinite(cons_upper[k]) && nmin[k] == 0) {
-        const double slack = cons_upper[k] - act[2 * k];
-        if (slack > 0.0) key.min_unit_slack = std::min(key.min_unit_slack, std::abs(a) / slack);
+      if (isfinite(q.g) && nmn == 0) {
+        const double sl = __dsub_rn(q.g, mnf);
+        if (sl > 0.0) {
+          const double u = __ddiv_rn(fabs(a), sl);
+          slk            = (u < slk) ? u : slk;
+        }
       }
-      if (std::isfinite(cons_lower[k]) && nmax[k] == 0) {
-        const double slack = act[2 * k + 1] - cons_lower[k];
-        if (slack > 0.0) key.min_unit_slack = std::min(key.min_unit_slack, std::abs(a) / slack);
+      if (isfinite(q.h) && nmx == 0) {
+        const double sl = __dsub_rn(mxf, q.h);
+        if (sl > 0.0) {
+          const double u = __ddiv_rn(fabs(a), sl);
+          slk            = (u < slk) ? u : slk;
+        }
       }
     }
-    keys.push_back(key);
+    for (int o = 16; o; o >>= 1) {
+      viol += __shfl_xor_sync(0xffffffffu, viol, o);
+      const double m = __shfl_xor_sync(0xffffffffu, maxv, o);
+      const double s = __shfl_xor_sync(0xffffffffu, slk, o);
+      maxv           = (maxv < m) ? m : maxv;
+      slk            = (s < slk) ? s : slk;
+    }
+    if (lane == 0) {
+      k_viol[j]  = (unsigned)viol;
+      k_maxv[j]  = (unsigned long long)__double_as_longlong(maxv);  // >= +0.0: bits order like values
+      k_slack[j] = (unsigned long long)__double_as_longlong(slk);   // > 0 or +inf (or +0 on underflow)
+      vals[j]    = i;
+    }
   }
-  std::stable_sort(keys.begin(), keys.end(), [](const Key& x, const Key& y) {
-    if (x.violated != y.violated) return x.violated > y.violated;
-    if (x.max_violation != y.max_violation) return x.max_violation > y.max_violation;
-    return x.min_unit_slack < y.min_unit_slack;
-  });
-  std::vector<int> order;
-  for (const auto& k : keys) order.push_back(k.var);
-  (void)row_start;
-  return order;
 }
 
 // probing.hpp:292-352 over the flat cache. Returns merged bounds; fills conflicts / evicted.
@@ -769,20 +797,77 @@ int bp_prioritize_probe_vars(bp_problem* p, int32_t* order, int32_t* n_order)
 {
   return cguard([&] {
     need(p && order && n_order, "null argument");
-    bp::Problem& P = bp_problem_impl(p);
+    bp::Problem& P           = bp_problem_impl(p);
+    const bp_problem_host& H = bp_problem_hostdata(p);
+    std::lock_guard<std::mutex> lk(P.mu);
+    BP_CUDA(cudaSetDevice(P.device));
+    cudaStream_t s = P.stream;
+    std::vector<int> ivar;
+    for (int i = 0; i < P.n; ++i)
+      if (H.is_integer[i]) ivar.push_back(i);
+    const int k = (int)ivar.size();
+    *n_order    = k;
+    if (k == 0) return;
+    // compute_activities of the original bounds (probing.hpp:107-109) into P.st.rec / aux
     std::vector<double> root(2 * (size_t)P.n);
     bp_problem_root(p, root.data());
-    std::vector<double> act(2 * (size_t)P.m);
-    std::vector<int> nmin(P.m), nmax(P.m);
-    if (int rc = bp_compute_activities(p, root.data(), nullptr, -1, act.data(), nmin.data(), nmax.data()))
-      throw std::runtime_error(bp_last_error());
-    std::lock_guard<std::mutex> lk(P.mu);
-    const bp_problem_host& H = bp_problem_hostdata(p);
-    const auto o = bp::prioritize(P.h_row_start, P.h_col_start, H.col_row.data(), H.col_val.data(),
-                                  H.is_integer.data(), H.var_lower.data(), H.var_upper.data(),
-                                  H.cons_lower.data(), H.cons_upper.data(), act, nmin, nmax);
-    std::copy(o.begin(), o.end(), order);
-    *n_order = (int32_t)o.size();
+    BP_CUDA(cudaMemcpyAsync(P.st.bounds, root.data(), sizeof(double) * root.size(), cudaMemcpyHostToDevice, s));
+    BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(bp::Ctl), s));
+    bp::Limits lim{};
+    lim.max_rounds    = 64;
+    lim.time_limit    = INFINITY;
+    lim.abs_threshold = 1e-7;
+    lim.rel_threshold = 1e-4;
+    lim.incremental   = 1;
+    bp::run_engine(P, bp::MODE_ACTIVITY, true, lim, s);
+    bp::DBuf<int> d_ivar, va, vb;
+    bp::DBuf<unsigned> kv, kv2;
+    bp::DBuf<unsigned long long> km, ks, k64;
+    d_ivar.alloc(k);
+    va.alloc(k);
+    vb.alloc(k);
+    kv.alloc(k);
+    kv2.alloc(k);
+    km.alloc(k);
+    ks.alloc(k);
+    k64.alloc(k);
+    BP_CUDA(cudaMemcpyAsync(d_ivar.p, ivar.data(), sizeof(int) * k, cudaMemcpyHostToDevice, s));
+    const int blocks = (int)std::min<long long>(148LL * 16, ((long long)k * 32 + 255) / 256);
+    bp::k_prio_keys<<<blocks, 256, 0, s>>>(P.dev(), P.st.rec, P.st.aux, P.st.bounds, d_ivar.p, k,
+                                           kv.p, km.p, ks.p, va.p);
+    BP_CUDA(cudaGetLastError());
+    // stable lexicographic sort (probing.hpp:176-180): least significant key first; each pass
+    // carries the var ids and the remaining keys' positions through a permutation.
+    bp::DBuf<int> perm, perm2;
+    perm.alloc(k);
+    perm2.alloc(k);
+    bp::DBuf<unsigned char> tmp;
+    size_t need_b = 0, have = 0;
+    auto grow = [&](size_t nb) {
+      if (nb > tmp.n) tmp.alloc(nb);
+      have = tmp.n;
+    };
+    // pass 1: min_unit_slack ascending; values = positions 0..k-1 (va holds var ids by position)
+    std::vector<int> iota(k);
+    std::iota(iota.begin(), iota.end(), 0);
+    bp::DBuf<int> pos0;
+    pos0.upload(iota);
+    cub::DeviceRadixSort::SortPairs(nullptr, need_b, ks.p, k64.p, pos0.p, perm.p, k, 0, 64, s);
+    grow(need_b);
+    cub::DeviceRadixSort::SortPairs(tmp.p, have, ks.p, k64.p, pos0.p, perm.p, k, 0, 64, s);
+    // pass 2: max_violation descending over the pass-1 order
+    bp::k_gather_u64<<<(k + 255) / 256, 256, 0, s>>>(km.p, perm.p, k, ks.p);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, need_b, ks.p, k64.p, perm.p, perm2.p, k, 0, 64, s);
+    grow(need_b);
+    cub::DeviceRadixSort::SortPairsDescending(tmp.p, have, ks.p, k64.p, perm.p, perm2.p, k, 0, 64, s);
+    // pass 3: violated count descending
+    bp::k_gather_u32<<<(k + 255) / 256, 256, 0, s>>>(kv.p, perm2.p, k, kv2.p);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, need_b, kv2.p, kv.p, perm2.p, perm.p, k, 0, 32, s);
+    grow(need_b);
+    cub::DeviceRadixSort::SortPairsDescending(tmp.p, have, kv2.p, kv.p, perm2.p, perm.p, k, 0, 32, s);
+    bp::k_gather_i32<<<(k + 255) / 256, 256, 0, s>>>(va.p, perm.p, k, vb.p);
+    BP_CUDA(cudaMemcpyAsync(order, vb.p, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -166,3 +166,19 @@ def test_pack_merge_roundtrip():
     for v in range(0, 2000, 7):
         x, y = merged.at(v), full.at(v)
         assert x == y
+
+
+def test_prioritize_on_device_matches_reference(oracle_built):
+    """prioritize_probe_vars (probing.hpp:105-190) computed on the device (warp-per-column keys +
+    three stable radix passes) equals the reference's stable order on mixed-sign instances with
+    long rows and columns, and on a knapsack/assignment instance."""
+    import ctypes as C
+
+    from oracle.bind import Ref, RefProblem
+
+    from paper_2510_20499_b200.probing import prioritize_probe_vars
+    for p in (synth.c1(seed=5, n=4000, m=3000), synth.c4(seed=6, n=6000, m=6000, n_long=4, long_len=3000)[0]):
+        rp = RefProblem.from_def(p)
+        ref = np.zeros(max(p.n_vars, 1), np.int32)
+        k = Ref.lib().ref_prioritize_probe_vars(rp.h, ref.ctypes.data_as(C.c_void_p))
+        assert prioritize_probe_vars(p) == ref[:k].tolist()
