@@ -155,6 +155,7 @@ struct Problem {
   unsigned stamp_base = 1;
   int grid_blocks = 0;
   int f2_blocks   = 0;  // k_rows_full grid (its own occupancy)
+  int sell_blocks = 0;  // k_rows_sell grid (its own occupancy)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket every engine launch on its stream
   double last_kernel_ms = 0.0;

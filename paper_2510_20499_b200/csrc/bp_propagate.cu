@@ -870,11 +870,30 @@ __device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
   if (k >= 0) write_rec(P, c.S, k, smn, smx, imn, imx);
 }
 
+// SELL slices of a full round, longest first: slices of rows > 32 entries one per fetch, the rest
+// four per fetch (one cursor shared by the whole grid is the contended resource).
+__device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int ns = P.n_srtile, nsl = P.n_srow_long;
+  for (Prefetch it_t(c, &pc->cur_s, 1); it_t.t < nsl; it_t.advance()) {
+    const long long c0 = S.dbg ? clock64() : 0;
+    sell_slice(c, it_t.t, cand);
+    dbg_task(c, 1, c0);
+  }
+  for (Prefetch it_t(c, &pc->cur_a, 4); nsl + it_t.t < ns; it_t.advance()) {
+    const long long c0 = S.dbg ? clock64() : 0;
+    for (int q = nsl + it_t.t; q < min(ns, nsl + it_t.t + 4); ++q) sell_slice(c, q, cand);
+    dbg_task(c, 1, c0);
+  }
+}
+
 // Phase 2 (F2 / P2): activities of all rows (full) or the dirty ones; `cand` fuses tightening.
 // pieces_here = false: the candidate pieces of rows above kCandSplit are left to a following
 // k_cand_pieces launch (no warp spins on an unfinished row's activity).
 __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, unsigned stamp,
-                           bool pieces_here = true)
+                           bool pieces_here = true, bool sell_here = true)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
@@ -899,18 +918,7 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       group_fold(c, nfh + it_t.t, min(4, nf - nfh - it_t.t), cand);
       dbg_task(c, 4, c0);
     }
-    // SELL slices, longest first: slices of rows > 32 entries one per fetch, the rest four
-    const int ns = P.n_srtile, nsl = P.n_srow_long;
-    for (Prefetch it_t(c, &pc->cur_s, 1); it_t.t < nsl; it_t.advance()) {
-      const long long c0 = S.dbg ? clock64() : 0;
-      sell_slice(c, it_t.t, cand);
-      dbg_task(c, 1, c0);
-    }
-    for (Prefetch it_t(c, &pc->cur_a, 4); nsl + it_t.t < ns; it_t.advance()) {
-      const long long c0 = S.dbg ? clock64() : 0;
-      for (int q = nsl + it_t.t; q < min(ns, nsl + it_t.t + 4); ++q) sell_slice(c, q, cand);
-      dbg_task(c, 1, c0);
-    }
+    if (sell_here) phase_sell(c, pc, cand);
     const int nc = cand && pieces_here ? P.n_cpiece : 0;
     for (Prefetch it_t(c, &pc->cur_c, 1); it_t.t < nc; it_t.advance()) {
       const long long c0 = S.dbg ? clock64() : 0;
@@ -1472,8 +1480,11 @@ __device__ void zero_par(ParCtl* q)
 // The host enqueues [k_rows_full, k_cand_pieces, k_engine(resume)] speculatively, several rounds
 // ahead without waiting: each is a no-op unless the engine handed a full round over (need_full).
 __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
-    k_rows_full(DevProblem P, DevState S, Limits lim)
+    k_rows_full(DevProblem P, DevState S, Limits lim, int split_sell)
 {
+  // with split_sell the SELL slices run in k_rows_sell, launched as a programmatic dependent of
+  // this grid: its blocks take over SM resources as soon as this grid's blocks retire
+  if (split_sell) asm volatile("griddepcontrol.launch_dependents;");
   if (!ldv(&S.ctl->need_full)) return;
   const int rnd         = ldv(&S.ctl->rounds);
   const int par         = rnd & 1;
@@ -1482,7 +1493,29 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
   Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
-  phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false);
+  phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell);
+}
+
+// The SELL slices of a full round (short rows, thread per row) at this kernel's own occupancy:
+// they need no shared memory and few registers, so many more warps keep gathers in flight than in
+// k_rows_full. Launched with programmatic stream serialization right behind k_rows_full; before
+// exiting, every block waits for k_rows_full to complete (griddepcontrol.wait), so this grid's
+// completion -- which the following launches are stream-ordered on -- implies that one's.
+#ifndef BP_SELL_MIN_BLOCKS
+#define BP_SELL_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, BP_SELL_MIN_BLOCKS)
+    k_rows_sell(DevProblem P, DevState S, Limits lim)
+{
+  if (ldv(&S.ctl->need_full)) {
+    const int par = ldv(&S.ctl->rounds) & 1;
+    __shared__ __align__(16) unsigned char no_smem[16];  // sell_slice never touches the warp smem
+    Smem& sm       = *reinterpret_cast<Smem*>(no_smem);
+    const int warp = threadIdx.x >> 5;
+    Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp};
+    phase_sell(c, &S.ctl->par[par], true);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Candidate pieces of rows above kCandSplit, after k_rows_full published their activities.
@@ -2063,6 +2096,9 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
                                (int)sizeof(Smem)));
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_rows_full, kThreads, sizeof(Smem)));
   P.f2_blocks = dev_sms * std::max(per_sm2, 1);
+  int per_sm3   = 0;
+  BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_rows_sell, kThreads, 0));
+  P.sell_blocks = dev_sms * std::max(per_sm3, 1);
   BP_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
   BP_CUDA(cudaEventCreate(&P.ev0));
   BP_CUDA(cudaEventCreate(&P.ev1));
@@ -2099,6 +2135,10 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   static const long long ext_min = getenv("BP_EXT_MIN_NNZ") ? atoll(getenv("BP_EXT_MIN_NNZ")) : 2000000;
   int ext        = (mode == MODE_PROPAGATE && !no_ext && P.nnz >= ext_min) ? 1 : 0;
   int resume     = 0;
+  // BP_SPLIT_SELL=1: SELL slices in k_rows_sell at their own (higher) occupancy. Measured slower on
+  // C2 (9.45 -> 11.0 ms: more warps in flight only lengthen each gather), so off.
+  static const int split_env = getenv("BP_SPLIT_SELL") ? atoi(getenv("BP_SPLIT_SELL")) : 0;
+  const int split_sell       = split_env && P.n_srtile > 0 ? 1 : 0;
   void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume};
   BP_CUDA(cudaEventRecord(P.ev0, s));
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
@@ -2109,7 +2149,21 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   for (int batch = 1; ext; batch = std::min(2 * batch, 8)) {
     resume = 1;
     for (int b = 0; b < batch; ++b) {
-      k_rows_full<<<P.f2_blocks, kThreads, sizeof(Smem), s>>>(d, st, l);
+      k_rows_full<<<P.f2_blocks, kThreads, sizeof(Smem), s>>>(d, st, l, split_sell);
+      if (split_sell) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id                                         = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.gridDim                                      = dim3(P.sell_blocks);
+        cfg.blockDim                                     = dim3(kThreads);
+        cfg.dynamicSmemBytes                             = 0;
+        cfg.stream                                       = s;
+        cfg.attrs                                        = at;
+        cfg.numAttrs                                     = 1;
+        BP_CUDA(cudaLaunchKernelEx(&cfg, k_rows_sell, d, st, l));
+        ++g_kernel_launches;
+      }
       if (P.n_cpiece)
         k_cand_pieces<<<std::min(P.f2_blocks, (P.n_cpiece + kWarps - 1) / kWarps), kThreads,
                         sizeof(Smem), s>>>(d, st, l);
