@@ -222,8 +222,9 @@ def run_probing(args, rank, world, local):
 
     log("probing: generating C3")
     p = synth.c3()
-    vars_ = list(range(200_000))  # the binaries (every one is probed: order is immaterial)
-    probe_variables(p, None, vars_[:2000])  # warm-up: kernels loaded, problem uploaded
+    vars_ = np.arange(200_000, dtype=np.int32)  # the binaries (every one is probed: order is immaterial)
+    for _ in range(2):  # warm-up: kernels loaded, problem uploaded, probing scratch sized
+        probe_variables(p, None, vars_)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -79,6 +79,25 @@ Limits default_limits()
   return l;
 }
 
+// Batched branches' deltas from the kernel's pool (allocation order) into task order: task t's
+// deltas go to [scan[t], scan[t] + cnt[t]) (scan = exclusive sum of the counts). One copy to
+// the host then yields the cache's delta arrays directly.
+__global__ void k_pack_pool(int nt, const int* cnt, const long long* off, const int* scan,
+                            const int* pvar, const double* plo, const double* pup, int* ovar,
+                            double* olo, double* oup)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    const int c = cnt[t];
+    const long long o = off[t];
+    const int d       = scan[t];
+    for (int j = 0; j < c; ++j) {
+      ovar[d + j] = pvar[o + j];
+      olo[d + j]  = plo[o + j];
+      oup[d + j]  = pup[o + j];
+    }
+  }
+}
+
 struct Branch {
   int feasible = 1;
   std::vector<int> var;  // deltas of engine branches
@@ -260,6 +279,48 @@ Branch engine_branch_cert(Problem& P, const DBuf<double2>& d_root, FallbackBufs&
 }  // namespace
 
 // Probes `vars` (both branches each) from `root`; entries follow probe_variable semantics.
+// Pinned host staging that only grows (async copies at full PCIe / C2C rate).
+struct PinBuf {
+  void* p  = nullptr;
+  size_t n = 0;
+  PinBuf() = default;
+  PinBuf(const PinBuf&) = delete;
+  PinBuf& operator=(const PinBuf&) = delete;
+  ~PinBuf()
+  {
+    if (p) cudaFreeHost(p);
+  }
+  template <class T>
+  T* get(size_t count)
+  {
+    const size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
+    if (n < bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      n = bytes + bytes / 4;
+      BP_CUDA(cudaMallocHost(&p, n));
+    }
+    return static_cast<T*>(p);
+  }
+};
+
+template <class T>
+void grow(DBuf<T>& b, size_t k)
+{
+  if (b.n < k) b.alloc(k + k / 4);
+}
+
+// Probing scratch of one problem, kept across calls (no cudaMalloc / cudaFree per batch).
+struct ProbeWs {
+  DBuf<double2> d_root;
+  DBuf<int> dvar, dcur, dstat, dcnt, dscan, qvar, pvar;
+  DBuf<double> dlo, dup, qlo, qup, plo, pup;
+  DBuf<long long> doff;
+  DBuf<unsigned long long> dpc;
+  DBuf<unsigned char> dtmp;
+  PinBuf h_var, h_lo, h_up, h_st, h_cn, h_qv, h_ql, h_qu;
+};
+
 HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vector<int>& vars,
                      double budget_sec)
 {
@@ -274,8 +335,10 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   C.n    = n;
   C.root = root;
   C.entry_of.assign(n, -1);
-  DBuf<double2> d_root;
-  d_root.alloc(std::max(n, 1));
+  if (!P.probe_ws) P.probe_ws = std::make_shared<ProbeWs>();
+  ProbeWs& W            = *static_cast<ProbeWs*>(P.probe_ws.get());
+  DBuf<double2>& d_root = W.d_root;
+  grow(d_root, (size_t)std::max(n, 1));
   if (n) BP_CUDA(cudaMemcpy(d_root.p, root.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
   // certification: one full round from the root changes nothing (fixpoint) -> frontier starts
   // are exact. Leaves the root activities in P.st.rec / aux.
@@ -293,6 +356,15 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   // tasks: down then up branch of every var with a spec (probing.hpp:228-234)
   std::vector<int> tv, tslot;
   std::vector<double> tlo, tup;
+  tv.reserve(2 * vars.size());
+  tslot.reserve(2 * vars.size());
+  tlo.reserve(2 * vars.size());
+  tup.reserve(2 * vars.size());
+  C.e_var.reserve(vars.size());
+  C.e_kind.reserve(vars.size());
+  C.e_feas.reserve(2 * vars.size());
+  C.e_force.reserve(2 * vars.size());
+  C.e_branch.reserve(4 * vars.size());
   for (int v : vars) {
     if (v < 0 || v >= n) throw std::out_of_range("probe var out of range");
     int e = C.entry_of[v];
@@ -317,8 +389,18 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
       tslot.push_back(2 * e + side);
     }
   }
+  static const bool prof = getenv("BP_PROBE_PROFILE") != nullptr;
+  const double t_tasks = elapsed();
   const int ne = (int)C.e_var.size();
-  std::vector<Branch> res(2 * (size_t)ne);
+  // per branch: kernel result (range of the flat host pool) or index of an engine branch
+  struct BrRef {
+    long long pool_off = -1;
+    int pool_cnt       = 0;
+    int feasible       = 1;
+    int eng            = -1;
+  };
+  std::vector<BrRef> res(2 * (size_t)ne);
+  std::vector<Branch> eng;
   std::vector<int> hp_var;  // batched branches' deltas (flat, by chunk)
   std::vector<double> hp_lo, hp_up;
   std::vector<uint8_t> done(2 * (size_t)ne, 0);
@@ -329,29 +411,52 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   std::vector<int> fallback;
   if (certified && ntask) {
     // chunks small enough for the time budget to be honoured between them
-    const int chunk = std::isfinite(budget_sec) && budget_sec < 1e6 ? (1 << 14) : (1 << 18);
-    DBuf<int> dvar, dcur, dstat, dcnt;
-    DBuf<double> dlo, dup;
-    DBuf<long long> doff;
-    DBuf<unsigned long long> dpc;
-    long long pool_cap = 32ll * std::min(ntask, chunk) + 4096;
-    DBuf<int> pvar;
-    DBuf<double> plo, pup;
-    pvar.alloc(pool_cap);
-    plo.alloc(pool_cap);
-    pup.alloc(pool_cap);
+    const int chunk = std::isfinite(budget_sec) && budget_sec < 1e6 ? (1 << 14) : (1 << 20);
+    auto& dvar = W.dvar;
+    auto& dcur = W.dcur;
+    auto& dstat = W.dstat;
+    auto& dcnt = W.dcnt;
+    auto& dlo = W.dlo;
+    auto& dup = W.dup;
+    auto& doff = W.doff;
+    auto& dpc = W.dpc;
+    auto& dscan = W.dscan;
+    auto& qvar = W.qvar;
+    auto& qlo = W.qlo;
+    auto& qup = W.qup;
+    auto& dtmp = W.dtmp;
+    auto& pvar = W.pvar;
+    auto& plo = W.plo;
+    auto& pup = W.pup;
+    // initial delta pool: >= 4 per branch (a chunk whose deltas overflow it reruns once, sized)
+    grow(pvar, 4ull * std::min(ntask, chunk) + 4096);
+    grow(plo, pvar.n);
+    grow(pup, pvar.n);
+    long long pool_cap = (long long)std::min(pvar.n, std::min(plo.n, pup.n));
     ProbeRoot R{d_root.p, P.st.rec, P.st.aux};
     for (int t0 = 0; t0 < ntask; t0 += chunk) {
       if (t0 > 0 && elapsed() >= budget_sec) break;
       const int nt = std::min(chunk, ntask - t0);
-      dvar.upload(tv.data() + t0, nt);
-      dlo.upload(tlo.data() + t0, nt);
-      dup.upload(tup.data() + t0, nt);
-      dcur.alloc(1);
-      dstat.alloc(nt);
-      dcnt.alloc(nt);
-      doff.alloc(nt);
-      dpc.alloc(1);
+      const double tb0 = elapsed();
+      grow(dvar, nt);
+      grow(dlo, nt);
+      grow(dup, nt);
+      grow(dcur, 1);
+      grow(dstat, nt);
+      grow(dcnt, nt);
+      grow(doff, nt);
+      grow(dpc, 1);
+      {
+        int* hv    = W.h_var.get<int>(nt);
+        double* hl = W.h_lo.get<double>(nt);
+        double* hu = W.h_up.get<double>(nt);
+        std::memcpy(hv, tv.data() + t0, sizeof(int) * nt);
+        std::memcpy(hl, tlo.data() + t0, sizeof(double) * nt);
+        std::memcpy(hu, tup.data() + t0, sizeof(double) * nt);
+        BP_CUDA(cudaMemcpyAsync(dvar.p, hv, sizeof(int) * nt, cudaMemcpyHostToDevice, s));
+        BP_CUDA(cudaMemcpyAsync(dlo.p, hl, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
+        BP_CUDA(cudaMemcpyAsync(dup.p, hu, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
+      }
       for (;;) {
         BP_CUDA(cudaMemsetAsync(dcur.p, 0, sizeof(int), s));
         BP_CUDA(cudaMemsetAsync(dpc.p, 0, sizeof(unsigned long long), s));
@@ -361,8 +466,10 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
         probe_launch(P, R, B, default_limits(), s);
         BP_CUDA(cudaEventRecord(P.ev1, s));
         unsigned long long used = 0;
+        const double tb1 = elapsed();
         BP_CUDA(cudaMemcpyAsync(&used, dpc.p, sizeof(used), cudaMemcpyDeviceToHost, s));
         BP_CUDA(cudaStreamSynchronize(s));
+        const double tb2 = elapsed();
         float ms = 0.f;
         BP_CUDA(cudaEventElapsedTime(&ms, P.ev0, P.ev1));
         C.probe_ms += ms;
@@ -373,28 +480,57 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
           pup.alloc(pool_cap);
           continue;
         }
-        std::vector<int> st(nt), cn(nt);
-        std::vector<long long> of(nt);
-        BP_CUDA(cudaMemcpy(st.data(), dstat.p, sizeof(int) * nt, cudaMemcpyDeviceToHost));
-        BP_CUDA(cudaMemcpy(cn.data(), dcnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost));
-        BP_CUDA(cudaMemcpy(of.data(), doff.p, sizeof(long long) * nt, cudaMemcpyDeviceToHost));
-        // the chunk's delta pool is appended to one flat host pool; branches keep (offset, count)
+        int* st = W.h_st.get<int>(nt);
+        int* cn = W.h_cn.get<int>(nt);
+        BP_CUDA(cudaMemcpyAsync(st, dstat.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
+        BP_CUDA(cudaMemcpyAsync(cn, dcnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
+        // the chunk's deltas in task order (device scan + pack), appended to the flat host pool
         const long long hbase = (long long)hp_var.size();
         hp_var.resize(hbase + used);
         hp_lo.resize(hbase + used);
         hp_up.resize(hbase + used);
+        int* hqv    = nullptr;
+        double* hql = nullptr;
+        double* hqu = nullptr;
         if (used) {
-          BP_CUDA(cudaMemcpy(hp_var.data() + hbase, pvar.p, sizeof(int) * used, cudaMemcpyDeviceToHost));
-          BP_CUDA(cudaMemcpy(hp_lo.data() + hbase, plo.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
-          BP_CUDA(cudaMemcpy(hp_up.data() + hbase, pup.p, sizeof(double) * used, cudaMemcpyDeviceToHost));
+          grow(dscan, nt);
+          size_t nb = 0;
+          cub::DeviceScan::ExclusiveSum(nullptr, nb, dcnt.p, dscan.p, nt, s);
+          if (nb > dtmp.n) dtmp.alloc(nb);
+          nb = dtmp.n;
+          cub::DeviceScan::ExclusiveSum(dtmp.p, nb, dcnt.p, dscan.p, nt, s);
+          grow(qvar, used);
+          grow(qlo, used);
+          grow(qup, used);
+          k_pack_pool<<<(int)std::min<long long>(4096, (nt + 255) / 256), 256, 0, s>>>(
+              nt, dcnt.p, doff.p, dscan.p, pvar.p, plo.p, pup.p, qvar.p, qlo.p, qup.p);
+          BP_CUDA(cudaGetLastError());
+          hqv = W.h_qv.get<int>(used);
+          hql = W.h_ql.get<double>(used);
+          hqu = W.h_qu.get<double>(used);
+          BP_CUDA(cudaMemcpyAsync(hqv, qvar.p, sizeof(int) * used, cudaMemcpyDeviceToHost, s));
+          BP_CUDA(cudaMemcpyAsync(hql, qlo.p, sizeof(double) * used, cudaMemcpyDeviceToHost, s));
+          BP_CUDA(cudaMemcpyAsync(hqu, qup.p, sizeof(double) * used, cudaMemcpyDeviceToHost, s));
         }
+        BP_CUDA(cudaStreamSynchronize(s));
+        if (used) {
+          std::memcpy(hp_var.data() + hbase, hqv, sizeof(int) * used);
+          std::memcpy(hp_lo.data() + hbase, hql, sizeof(double) * used);
+          std::memcpy(hp_up.data() + hbase, hqu, sizeof(double) * used);
+        }
+        const double tb3 = elapsed();
+        if (prof)
+          fprintf(stderr, "[bp probe] chunk of %d: uploads+launch %.2f ms, kernel wait %.2f ms, pack+D2H %.2f ms\n",
+                  nt, 1e3 * (tb1 - tb0), 1e3 * (tb2 - tb1), 1e3 * (tb3 - tb2));
+        long long run = hbase;
         for (int j = 0; j < nt; ++j) {
           const int t = t0 + j;
-          Branch& br  = res[tslot[t]];
+          BrRef& br   = res[tslot[t]];
           if (st[j] == 0) {
             br.feasible    = 1;
-            br.pool_off    = hbase + of[j];
+            br.pool_off    = run;
             br.pool_cnt    = cn[j];
+            run += cn[j];
             done[tslot[t]] = 1;
           } else if (st[j] == 1) {
             br.feasible    = 0;
@@ -409,6 +545,7 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   } else {
     for (int t = 0; t < ntask; ++t) fallback.push_back(t);
   }
+  const double t_batch = elapsed();
   FallbackBufs F;
   if (certified && !fallback.empty() && P.m) {
     // snapshot of the root activities (left in P.st.rec / aux by the certification round)
@@ -420,10 +557,57 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   }
   for (int t : fallback) {
     if (elapsed() >= budget_sec) break;
-    res[tslot[t]]  = certified ? engine_branch_cert(P, d_root, F, tv[t], tlo[t], tup[t], root, s)
-                               : engine_branch(P, d_root, tv[t], tlo[t], tup[t], root, s);
+    eng.push_back(certified ? engine_branch_cert(P, d_root, F, tv[t], tlo[t], tup[t], root, s)
+                            : engine_branch(P, d_root, tv[t], tlo[t], tup[t], root, s));
+    BrRef& br   = res[tslot[t]];
+    br.feasible = eng.back().feasible;
+    br.pool_off = -1;
+    br.eng      = (int)eng.size() - 1;
     done[tslot[t]] = 1;
     C.n_fallback++;
+  }
+  const double t_fallback = elapsed();
+  bool all_done = C.n_fallback == 0 && fallback.empty();
+  for (size_t t = 1; t < tslot.size() && all_done; ++t) all_done = tslot[t] > tslot[t - 1];  // no repeated vars
+  for (int e = 0; e < ne && all_done; ++e) all_done = done[2 * e] && done[2 * e + 1];
+  if (all_done) {
+    // every branch came from the batched kernel: the flat pool is already the cache's delta
+    // arrays in entry order (down, up), so only the per-entry tables are filled
+    HostCache out;
+    out.n          = n;
+    out.root       = root;
+    out.certified  = certified;
+    out.probe_ms   = C.probe_ms;
+    out.n_fallback = 0;
+    out.entry_of   = std::move(C.entry_of);
+    out.e_var      = std::move(C.e_var);
+    out.e_kind     = std::move(C.e_kind);
+    out.e_branch   = std::move(C.e_branch);
+    out.e_feas.resize(2 * (size_t)ne);
+    out.e_force.resize(2 * (size_t)ne);
+    out.d_off.resize(2 * (size_t)ne + 1);
+    long long o = 0;
+    for (int e = 0; e < ne; ++e) {
+      const BrRef& dn  = res[2 * e];
+      const BrRef& upb = res[2 * e + 1];
+      out.e_feas[2 * e]      = (uint8_t)dn.feasible;
+      out.e_feas[2 * e + 1]  = (uint8_t)upb.feasible;
+      out.e_force[2 * e]     = (uint8_t)(!upb.feasible && dn.feasible);  // forces_down
+      out.e_force[2 * e + 1] = (uint8_t)(!dn.feasible && upb.feasible);  // forces_up
+      out.d_off[2 * e]       = o;
+      o += dn.pool_off >= 0 ? dn.pool_cnt : 0;
+      out.d_off[2 * e + 1] = o;
+      o += upb.pool_off >= 0 ? upb.pool_cnt : 0;
+    }
+    out.d_off[2 * (size_t)ne] = o;
+    out.d_var = std::move(hp_var);
+    out.d_lo  = std::move(hp_lo);
+    out.d_up  = std::move(hp_up);
+    out.finalize_stats();
+    if (prof)
+      fprintf(stderr, "[bp probe] setup+cert %.2f ms, batches %.2f ms (device %.2f ms), assemble %.2f ms\n",
+              1e3 * t_tasks, 1e3 * (t_batch - t_tasks), C.probe_ms, 1e3 * (elapsed() - t_fallback));
+    return out;
   }
   // assemble (entries whose branches were not both computed within the budget are dropped)
   HostCache out;
@@ -451,27 +635,32 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
     out.e_var.push_back(v);
     out.e_kind.push_back(C.e_kind[e]);
     for (int q = 0; q < 4; ++q) out.e_branch.push_back(C.e_branch[4 * e + q]);
-    const Branch& dn = res[2 * e];
-    const Branch& upb = res[2 * e + 1];
+    const BrRef& dn  = res[2 * e];
+    const BrRef& upb = res[2 * e + 1];
     out.e_feas.push_back((uint8_t)dn.feasible);
     out.e_feas.push_back((uint8_t)upb.feasible);
     out.e_force.push_back((uint8_t)(!upb.feasible && dn.feasible));  // forces_down
     out.e_force.push_back((uint8_t)(!dn.feasible && upb.feasible));  // forces_up
-    for (const Branch* b : {&dn, &upb}) {
+    for (const BrRef* b : {&dn, &upb}) {
       if (b->pool_off >= 0) {
         const long long o = b->pool_off, cnt = b->pool_cnt;
         out.d_var.insert(out.d_var.end(), hp_var.begin() + o, hp_var.begin() + o + cnt);
         out.d_lo.insert(out.d_lo.end(), hp_lo.begin() + o, hp_lo.begin() + o + cnt);
         out.d_up.insert(out.d_up.end(), hp_up.begin() + o, hp_up.begin() + o + cnt);
-      } else {
-        out.d_var.insert(out.d_var.end(), b->var.begin(), b->var.end());
-        out.d_lo.insert(out.d_lo.end(), b->lo.begin(), b->lo.end());
-        out.d_up.insert(out.d_up.end(), b->up.begin(), b->up.end());
+      } else if (b->eng >= 0) {
+        const Branch& eb = eng[b->eng];
+        out.d_var.insert(out.d_var.end(), eb.var.begin(), eb.var.end());
+        out.d_lo.insert(out.d_lo.end(), eb.lo.begin(), eb.lo.end());
+        out.d_up.insert(out.d_up.end(), eb.up.begin(), eb.up.end());
       }
       out.d_off.push_back((long long)out.d_var.size());
     }
   }
   out.finalize_stats();
+  if (prof)
+    fprintf(stderr, "[bp probe] setup+cert %.2f ms, batches %.2f ms (device %.2f ms), fallback %.2f ms, assemble %.2f ms\n",
+            1e3 * t_tasks, 1e3 * (t_batch - t_tasks), C.probe_ms, 1e3 * (t_fallback - t_batch),
+            1e3 * (elapsed() - t_fallback));
   return out;
 }
 

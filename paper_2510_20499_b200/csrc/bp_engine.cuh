@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -156,6 +157,7 @@ struct Problem {
   int grid_blocks = 0;
   int f2_blocks   = 0;  // k_rows_full grid (its own occupancy)
   int sell_blocks = 0;  // k_rows_sell grid (its own occupancy)
+  std::shared_ptr<void> probe_ws;  // probing scratch (device + pinned host), kept across calls
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket every engine launch on its stream
   double last_kernel_ms = 0.0;

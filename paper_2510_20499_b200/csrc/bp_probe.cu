@@ -66,6 +66,32 @@ struct PCtx {
   int lane;
 };
 
+// Overlay slot of var v, or -1 (then the root value applies).
+__device__ __forceinline__ int bfind(PCtx& c, int v)
+{
+  unsigned s = hsh(v) & (PB_BCAP - 1);
+  for (int probe = 0; probe < PB_BCAP; ++probe) {
+    const int k = c.w.bkey[s];
+    if (k == v + 1) return (int)s;
+    if (k == 0) break;
+    s = (s + 1) & (PB_BCAP - 1);
+  }
+  return -1;
+}
+
+// Overlay slot of row k's activity, or -1 (then the root record applies).
+__device__ __forceinline__ int afind(PCtx& c, int k)
+{
+  unsigned s = hsh(k) & (PB_ACAP - 1);
+  for (int probe = 0; probe < PB_ACAP; ++probe) {
+    const int key = c.w.akey[s];
+    if (key == k + 1) return (int)s;
+    if (key == 0) break;
+    s = (s + 1) & (PB_ACAP - 1);
+  }
+  return -1;
+}
+
 __device__ __forceinline__ double2 bget(PCtx& c, int v)
 {
   unsigned s = hsh(v) & (PB_BCAP - 1);
@@ -155,29 +181,42 @@ __device__ __forceinline__ void set_clear(PWarp& w, int lane)
   __syncwarp();
 }
 
-// Activity of one row in reference order (sequential within 16384-entry segments).
+// Activity of one row of <= PB_LANEROW entries (a single 16384-entry segment) in reference order,
+// four entries' index loads and bound gathers in flight at a time.
+constexpr int PB_U = 4;
 __device__ void row_act_lane(PCtx& c, int k, double& smn, int& imn, double& smx, int& imx)
 {
   const int rs = __ldg(c.P.row_start + k), re = __ldg(c.P.row_start + k + 1);
-  double tmn = 0.0, tmx = 0.0, pmn = 0.0, pmx = 0.0;
+  double pmn = 0.0, pmx = 0.0;
   imn = imx = 0;
-  for (int e = rs; e < re; ++e) {
-    if (e > rs && ((e - rs) % kSumSegment) == 0) {
-      tmn = __dadd_rn(tmn, pmn);
-      tmx = __dadd_rn(tmx, pmx);
-      pmn = pmx = 0.0;
+  for (int e0 = rs; e0 < re; e0 += PB_U) {
+    int col[PB_U];
+    double a[PB_U];
+    double2 b[PB_U];
+#pragma unroll
+    for (int u = 0; u < PB_U; ++u) {
+      col[u] = e0 + u < re ? __ldg(c.P.row_col + e0 + u) : -1;
+      a[u]   = e0 + u < re ? __ldg(c.P.row_val + e0 + u) : 0.0;
     }
-    const double2 b = bget(c, __ldg(c.P.row_col + e));
-    double cm, cx;
-    int i1, i2;
-    contrib(__ldg(c.P.row_val + e), b.x, b.y, cm, cx, i1, i2);
-    pmn = __dadd_rn(pmn, cm);
-    pmx = __dadd_rn(pmx, cx);
-    imn += i1;
-    imx += i2;
+#pragma unroll
+    for (int u = 0; u < PB_U; ++u) {
+      const int sl = col[u] >= 0 ? bfind(c, col[u]) : -1;
+      b[u]         = sl >= 0 ? c.w.bval[sl] : (col[u] >= 0 ? c.R.bounds[col[u]] : make_double2(0.0, 0.0));
+    }
+#pragma unroll
+    for (int u = 0; u < PB_U; ++u) {
+      if (col[u] < 0) break;
+      double cm, cx;
+      int i1, i2;
+      contrib(a[u], b[u].x, b[u].y, cm, cx, i1, i2);
+      pmn = __dadd_rn(pmn, cm);
+      pmx = __dadd_rn(pmx, cx);
+      imn += i1;
+      imx += i2;
+    }
   }
-  smn = __dadd_rn(tmn, pmn);
-  smx = __dadd_rn(tmx, pmx);
+  smn = __dadd_rn(0.0, pmn);  // the segment total onto the row total (propagation.hpp:182-188)
+  smx = __dadd_rn(0.0, pmx);
 }
 
 // Same for a long row, warp-cooperatively (lanes gather, lanes 0/1 fold).
@@ -221,21 +260,45 @@ __device__ void row_act_warp(PCtx& c, int k, double& smn, int& imn, double& smx,
   imx = cmx;
 }
 
-// Candidate fold of variable i over its column (lane-sequential).
+// Candidate fold of variable i over its column (lane-sequential, CSC order), four entries' row
+// records in flight at a time.
 __device__ void col_fold_lane(PCtx& c, int i, double lo, double up, bool integer, double& nl,
                               double& nu)
 {
   nl = lo;
   nu = up;
   const int cs = __ldg(c.P.col_start + i), ce = __ldg(c.P.col_start + i + 1);
-  for (int e = cs; e < ce; ++e) {
-    const int k = __ldg(c.P.col_row + e);
-    double mnf, mxf, g, h, cl, cu;
-    int nmn, nmx;
-    aget(c, k, mnf, nmn, mxf, nmx, g, h);
-    cand_explicit(lo, up, integer, __ldg(c.P.col_val + e), mnf, nmn, mxf, nmx, g, h, cl, cu);
-    if (cu < nu) nu = cu;
-    if (nl < cl) nl = cl;
+  for (int e0 = cs; e0 < ce; e0 += PB_U) {
+    int k[PB_U], sl[PB_U];
+    double a[PB_U];
+    RowRec r[PB_U];
+#pragma unroll
+    for (int u = 0; u < PB_U; ++u) {
+      k[u] = e0 + u < ce ? __ldg(c.P.col_row + e0 + u) : -1;
+      a[u] = e0 + u < ce ? __ldg(c.P.col_val + e0 + u) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PB_U; ++u) {
+      sl[u] = k[u] >= 0 ? afind(c, k[u]) : -1;
+      if (k[u] >= 0) r[u] = ld_rec(c.R.rec + k[u]);  // g / h, and the root activity if no overlay
+    }
+#pragma unroll
+    for (int u = 0; u < PB_U; ++u) {
+      if (k[u] < 0) break;
+      double mnf, mxf, cl, cu;
+      int nmn, nmx;
+      if (sl[u] >= 0) {
+        mnf = c.w.amn[sl[u]];
+        mxf = c.w.amx[sl[u]];
+        nmn = c.w.ainf[sl[u]][0];
+        nmx = c.w.ainf[sl[u]][1];
+      } else {
+        decode_rec(r[u], c.R.aux, k[u], mnf, nmn, mxf, nmx);
+      }
+      cand_explicit(lo, up, integer, a[u], mnf, nmn, mxf, nmx, r[u].g, r[u].h, cl, cu);
+      if (cu < nu) nu = cu;
+      if (nl < cl) nl = cl;
+    }
   }
 }
 

@@ -16,6 +16,8 @@ import numpy as np
 
 def shard(items, rank: int, world: int):
     """Strided interleave of a priority-ordered candidate list (balances skewed probe costs)."""
+    if isinstance(items, np.ndarray):
+        return np.ascontiguousarray(items[rank::world])
     return list(items[rank::world])
 
 

@@ -6,6 +6,7 @@
 // rows. Everything is compared bit for bit. One PASS/FAIL line per criterion, like acceptance.cpp;
 // exit status = number of failures.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <random>
@@ -365,14 +366,17 @@ int main()
     std::printf("FAIL  no CUDA device (%s)\n", bp_last_error());
     return 1;
   }
-  errors();
-  propagation_stream();
-  propagation_mixed();
-  probing_stream();
-  warm_start_and_pairs();
-  rounding_stream();
-  rounding_mixed();
-  repair_stream();
+  // DROPIN_ONLY=<criterion name> runs one criterion (debugging)
+  const char* only = std::getenv("DROPIN_ONLY");
+  auto want = [&](const char* name) { return !only || std::strcmp(only, name) == 0; };
+  if (want("errors")) errors();
+  if (want("propagation_stream")) propagation_stream();
+  if (want("propagation_mixed")) propagation_mixed();
+  if (want("probing_stream")) probing_stream();
+  if (want("warm_start_and_pairs")) warm_start_and_pairs();
+  if (want("rounding_stream")) rounding_stream();
+  if (want("rounding_mixed")) rounding_mixed();
+  if (want("repair_stream")) repair_stream();
   std::printf("%d failure(s)\n", g_failures);
   return g_failures;
 }
