@@ -30,9 +30,18 @@ constexpr unsigned FULL  = 0xffffffffu;
 constexpr int PB_WARPS   = 4;     // warps per block
 constexpr int PB_BCAP    = 128;   // bounds overlay slots (power of 2)
 constexpr int PB_ACAP    = 128;   // activity overlay slots (power of 2)
-constexpr int PB_RCAP    = 256;   // dirty rows per round
-constexpr int PB_VCAP    = 512;   // dirty vars per round
-constexpr int PB_SCAP    = 1024;  // dedup hash set (power of 2)
+#ifndef PB_RCAP_V
+#define PB_RCAP_V 256
+#endif
+constexpr int PB_RCAP    = PB_RCAP_V;   // dirty rows per round
+#ifndef PB_VCAP_V
+#define PB_VCAP_V 512
+#endif
+constexpr int PB_VCAP    = PB_VCAP_V;   // dirty vars per round
+#ifndef PB_SCAP_V
+#define PB_SCAP_V 1024
+#endif
+constexpr int PB_SCAP    = PB_SCAP_V;  // dedup hash set (power of 2)
 constexpr int PB_CCAP    = 128;   // changed vars per round
 constexpr int PB_LANEROW = 64;    // rows / columns up to this length are handled by one lane
 constexpr int PB_LONGROW = 4096;  // a dirty row longer than this sends the branch to the engine
@@ -183,7 +192,10 @@ __device__ __forceinline__ void set_clear(PWarp& w, int lane)
 
 // Activity of one row of <= PB_LANEROW entries (a single 16384-entry segment) in reference order,
 // four entries' index loads and bound gathers in flight at a time.
-constexpr int PB_U = 4;
+#ifndef PB_U_V
+#define PB_U_V 4
+#endif
+constexpr int PB_U = PB_U_V;
 __device__ void row_act_lane(PCtx& c, int k, double& smn, int& imn, double& smx, int& imx)
 {
   const int rs = __ldg(c.P.row_start + k), re = __ldg(c.P.row_start + k + 1);
