@@ -82,6 +82,44 @@ int bp_problem_create(const bp_problem_desc* desc, int32_t device, bp_problem** 
 int bp_problem_destroy(bp_problem* p);
 int bp_problem_info(const bp_problem* p, int32_t* n_vars, int32_t* n_cons, int64_t* nnz);
 
+/* pulse::ProblemBuilder state (problem.hpp:102-242): variables, rows and the entries in
+ * insertion order (add_entry), before build(). */
+typedef struct {
+  int32_t n_vars;
+  int32_t n_cons;
+  int64_t n_entries;
+  const int32_t* entry_row;
+  const int32_t* entry_col;
+  const double* entry_val;
+  const double* var_lower; /* as given to add_var (not yet integrally tightened) */
+  const double* var_upper;
+  const uint8_t* is_integer;
+  const double* cons_lower;
+  const double* cons_upper;
+} bp_builder_desc;
+
+/* The built pulse::ProblemDef arrays (caller-allocated): row_start n_cons + 1, col_start
+ * n_vars + 1, row_col / row_val / col_row / col_val capacity n_entries, var_lower / var_upper
+ * n_vars (integrally tightened). nnz is written. */
+typedef struct {
+  int64_t nnz;
+  int32_t* row_start;
+  int32_t* row_col;
+  double* row_val;
+  int32_t* col_start;
+  int32_t* col_row;
+  double* col_val;
+  double* var_lower;
+  double* var_upper;
+} bp_built;
+
+/* pulse::ProblemBuilder::build (problem.hpp:141-227) on the device: integral tightening, the
+ * reference's checks (BP_ERR_RUNTIME for an empty domain / crossed row, BP_ERR_OUT_OF_RANGE for
+ * an entry index), stable sort by (row, col), coalescing of duplicates (summed in insertion
+ * order), zero dropping, CSR + stable-transpose CSC. If prob != NULL the built problem is also
+ * created on `device` (as bp_problem_create). */
+int bp_build_problem(const bp_builder_desc* desc, int32_t device, bp_built* out, bp_problem** prob);
+
 /* pulse::compute_activities (propagation.hpp:226). rows == NULL with nrows < 0 recomputes all
  * rows; otherwise only rows[0..nrows) and the others keep the values passed in. */
 int bp_compute_activities(bp_problem* p, const double* bounds2n, const int32_t* rows,

@@ -5,6 +5,7 @@
 // exception behaviour of the `pulse::` function it replaces, and computes on the GPU through the
 // C-ABI in bp.h (plain pointers; no CUDA or torch types cross it):
 //
+//   pulse::ProblemBuilder::build       problem.hpp:141       -> bp_build_problem
 //   pulse::compute_activities          propagation.hpp:226   -> bp_compute_activities
 //   pulse::tighten_bounds              propagation.hpp:378   -> bp_tighten_bounds
 //   pulse::propagate                   propagation.hpp:418   -> bp_propagate
@@ -414,6 +415,109 @@ inline BulkWarmStart assemble_bulk_warm_start(const ProbingCache& cache,
   out.evicted.assign(ev.begin(), ev.begin() + nev);
   return out;
 }
+
+// ---------------------------------------------------------------- problem.hpp
+
+// problem.hpp:102-243 with build() on the GPU (bp_build_problem): the same interface, results
+// and exceptions as pulse::ProblemBuilder (duplicates of one (row, col) are summed in insertion
+// order; the reference's std::sort leaves that order unspecified).
+class ProblemBuilder {
+ public:
+  int add_var(std::string name, double lower, double upper, bool integer, double obj = 0.0)
+  {
+    var_names_.push_back(std::move(name));
+    lower_.push_back(lower);
+    upper_.push_back(upper);
+    integer_.push_back(integer ? 1 : 0);
+    obj_.push_back(obj);
+    return static_cast<int>(var_names_.size()) - 1;
+  }
+  int add_row(std::string name, double lower, double upper)
+  {
+    cons_names_.push_back(std::move(name));
+    cons_lower_.push_back(lower);
+    cons_upper_.push_back(upper);
+    return static_cast<int>(cons_names_.size()) - 1;
+  }
+  void add_entry(int row, int col, double val)
+  {
+    e_row_.push_back(row);
+    e_col_.push_back(col);
+    e_val_.push_back(val);
+  }
+  void set_objective(int var, double coeff) { obj_[var] = coeff; }
+  void add_to_objective(int var, double coeff) { obj_[var] += coeff; }
+  void set_var_lower(int var, double v) { lower_[var] = v; }
+  void set_var_upper(int var, double v) { upper_[var] = v; }
+  void set_var_integer(int var) { integer_[var] = 1; }
+  void set_row_lower(int row, double v) { cons_lower_[row] = v; }
+  void set_row_upper(int row, double v) { cons_upper_[row] = v; }
+  double row_lower(int row) const { return cons_lower_[row]; }
+  double row_upper(int row) const { return cons_upper_[row]; }
+  void set_name(std::string n) { name_ = std::move(n); }
+  void set_objective_name(std::string n) { obj_name_ = std::move(n); }
+  int n_vars() const { return static_cast<int>(var_names_.size()); }
+  int n_rows() const { return static_cast<int>(cons_names_.size()); }
+
+  ProblemDef build() const
+  {
+    ProblemDef p;
+    p.n_vars         = n_vars();
+    p.n_cons         = n_rows();
+    p.var_names      = var_names_;
+    p.cons_names     = cons_names_;
+    p.obj_coeffs     = obj_;
+    p.cons_lower     = cons_lower_;
+    p.cons_upper     = cons_upper_;
+    p.name           = name_;
+    p.objective_name = obj_name_;
+    p.is_integer     = integer_;
+    // the O(n + m) domain / row checks here for the reference's named messages (problem.hpp:164-173)
+    for (int i = 0; i < p.n_vars; ++i) {
+      double lo = lower_[i], up = upper_[i];
+      if (integer_[i]) {
+        if (is_finite(lo)) lo = ceil_eps(lo, 1e-9);
+        if (is_finite(up)) up = floor_eps(up, 1e-9);
+      }
+      if (lo > up)
+        throw std::runtime_error("variable '" + var_names_[i] + "' has empty domain after bound tightening");
+    }
+    for (int k = 0; k < p.n_cons; ++k)
+      if (cons_lower_[k] > cons_upper_[k])
+        throw std::runtime_error("constraint '" + cons_names_[k] + "' has crossed bounds");
+    const size_t N = e_row_.size();
+    p.row_start.resize(p.n_cons + 1);
+    p.col_start.resize(p.n_vars + 1);
+    p.row_col.resize(N);
+    p.row_val.resize(N);
+    p.col_row.resize(N);
+    p.col_val.resize(N);
+    p.var_lower.resize(p.n_vars);
+    p.var_upper.resize(p.n_vars);
+    bp_builder_desc d{p.n_vars, p.n_cons, (int64_t)N, e_row_.data(), e_col_.data(), e_val_.data(),
+                      lower_.data(), upper_.data(), integer_.data(), cons_lower_.data(),
+                      cons_upper_.data()};
+    bp_built o{0, p.row_start.data(), p.row_col.data(), p.row_val.data(), p.col_start.data(),
+               p.col_row.data(), p.col_val.data(), p.var_lower.data(), p.var_upper.data()};
+    detail::check(bp_build_problem(&d, detail::registry().device, &o, nullptr));
+    p.row_col.resize(o.nnz);
+    p.row_val.resize(o.nnz);
+    p.col_row.resize(o.nnz);
+    p.col_val.resize(o.nnz);
+    return p;
+  }
+
+ private:
+  std::vector<std::string> var_names_;
+  std::vector<double> lower_, upper_, obj_;
+  std::vector<uint8_t> integer_;
+  std::vector<std::string> cons_names_;
+  std::vector<double> cons_lower_, cons_upper_;
+  std::vector<int32_t> e_row_, e_col_;
+  std::vector<double> e_val_;
+  std::string name_;
+  std::string obj_name_ = "OBJ";
+};
 
 // ---------------------------------------------------------------- rounding.hpp
 

@@ -39,6 +39,24 @@ class bp_problem_desc(C.Structure):
     ]
 
 
+class bp_builder_desc(C.Structure):
+    _fields_ = [
+        ("n_vars", C.c_int32), ("n_cons", C.c_int32), ("n_entries", C.c_int64),
+        ("entry_row", C.c_void_p), ("entry_col", C.c_void_p), ("entry_val", C.c_void_p),
+        ("var_lower", C.c_void_p), ("var_upper", C.c_void_p), ("is_integer", C.c_void_p),
+        ("cons_lower", C.c_void_p), ("cons_upper", C.c_void_p),
+    ]
+
+
+class bp_built(C.Structure):
+    _fields_ = [
+        ("nnz", C.c_int64),
+        ("row_start", C.c_void_p), ("row_col", C.c_void_p), ("row_val", C.c_void_p),
+        ("col_start", C.c_void_p), ("col_row", C.c_void_p), ("col_val", C.c_void_p),
+        ("var_lower", C.c_void_p), ("var_upper", C.c_void_p),
+    ]
+
+
 class bp_limits(C.Structure):
     _fields_ = [("max_rounds", C.c_int32), ("time_limit", C.c_double),
                 ("abs_threshold", C.c_double), ("rel_threshold", C.c_double),
@@ -124,6 +142,8 @@ _SIGS = [
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_void_p]),
+    ("bp_build_problem", C.c_int, [C.POINTER(bp_builder_desc), C.c_int32, C.POINTER(bp_built),
+                                   C.POINTER(C.c_void_p)]),
     ("bp_kernel_launches", C.c_int64, []),
     ("bp_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                  C.POINTER(C.c_int64)]),

@@ -215,6 +215,48 @@ class ProblemBuilder:
         return p
 
 
+def build_on_device(b: ProblemBuilder, device: int = 0) -> ProblemDef:
+    """ProblemBuilder::build (problem.hpp:141-227) with every O(N log N) step on the GPU
+    (bp_build_problem): the returned ProblemDef carries the device problem it was built into.
+    Same results and error types as ``ProblemBuilder.build`` (duplicates summed in insertion
+    order); messages name variables / rows by index."""
+    import ctypes as C
+
+    from . import _lib
+    from .propagation import DeviceProblem
+    n, m = b.n_vars(), b.n_rows()
+    lo = np.ascontiguousarray(b._lo, dtype=np.float64)
+    up = np.ascontiguousarray(b._up, dtype=np.float64)
+    isint = np.ascontiguousarray(b._int, dtype=np.uint8)
+    clo = np.ascontiguousarray(b._clo, dtype=np.float64)
+    cup = np.ascontiguousarray(b._cup, dtype=np.float64)
+    er = np.ascontiguousarray(b._er, dtype=np.int32)
+    ec = np.ascontiguousarray(b._ec, dtype=np.int32)
+    ev = np.ascontiguousarray(b._ev, dtype=np.float64)
+    N = er.size
+    P = _lib.ptr
+    d = _lib.bp_builder_desc(n, m, N, P(er), P(ec), P(ev), P(lo), P(up), P(isint), P(clo), P(cup))
+    rs = np.zeros(m + 1, np.int32)
+    cs = np.zeros(n + 1, np.int32)
+    rc_, rv = np.zeros(max(N, 1), np.int32), np.zeros(max(N, 1))
+    cr, cv = np.zeros(max(N, 1), np.int32), np.zeros(max(N, 1))
+    olo, oup = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    out = _lib.bp_built(0, P(rs), P(rc_), P(rv), P(cs), P(cr), P(cv), P(olo), P(oup))
+    h = C.c_void_p()
+    # empty domain / crossed row: BPError (a RuntimeError); bad entry index: IndexError
+    _lib.check(_lib.lib().bp_build_problem(C.byref(d), int(device), C.byref(out), C.byref(h)))
+    nnz = int(out.nnz)
+    p = ProblemDef(n_vars=n, n_cons=m, obj_coeffs=np.array(b._obj, dtype=np.float64),
+                   var_lower=olo[:n].copy(), var_upper=oup[:n].copy(), is_integer=isint,
+                   row_start=rs, row_col=rc_[:nnz].copy(), row_val=rv[:nnz].copy(),
+                   col_start=cs, col_row=cr[:nnz].copy(), col_val=cv[:nnz].copy(),
+                   cons_lower=clo, cons_upper=cup, name=b.name)
+    p.var_names = list(b._vn)
+    p.cons_names = list(b._cn)
+    p._device_handle = DeviceProblem.adopt(p, h, device)
+    return p
+
+
 def make_problem(vars_spec, rows_spec) -> ProblemDef:
     """testkit::make_problem (tests/testkit.hpp:36-48): vars = [(lo, up, integer[, obj])],
     rows = [([(col, val), ...], lo, up)]."""

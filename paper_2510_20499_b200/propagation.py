@@ -200,6 +200,16 @@ class DeviceProblem:
         self.h = h
         self.device = device
 
+    @classmethod
+    def adopt(cls, p: ProblemDef, handle: C.c_void_p, device: int = 0) -> "DeviceProblem":
+        """Wraps a handle created elsewhere (bp_build_problem) for problem p."""
+        dp = cls.__new__(cls)
+        dp.p = p
+        dp._keep = []
+        dp.h = handle
+        dp.device = device
+        return dp
+
     def __del__(self):
         try:
             if getattr(self, "h", None) and _lib._lib is not None:

@@ -340,6 +340,68 @@ void repair_stream()
              std::to_string(rounds_bad) + " mismatches");
 }
 
+void builder_stream()
+{
+  std::mt19937_64 gen(4711);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  int bad = 0, runs = 0, threw = 0;
+  for (int t = 0; t < 300; ++t) {
+    const int n = 1 + (int)(40 * U(gen)), m = 1 + (int)(30 * U(gen)), ne = (int)(300 * U(gen));
+    pulse::ProblemBuilder a;
+    pg::ProblemBuilder g;
+    for (int i = 0; i < n; ++i) {
+      double lo = std::floor(6 * U(gen)) - 3 + (U(gen) < 0.5 ? 0.3 : 0.0);
+      double up = lo + std::floor(5 * U(gen)) + 0.6;
+      if (U(gen) < 0.1) lo = -kInf;
+      if (U(gen) < 0.1) up = kInf;
+      const bool integer = U(gen) < 0.7;
+      a.add_var("x" + std::to_string(i), lo, up, integer, U(gen));
+      g.add_var("x" + std::to_string(i), lo, up, integer, 0.0);
+      g.set_objective(i, 0.0);
+    }
+    for (int k = 0; k < m; ++k) {
+      const double lo = U(gen) < 0.5 ? -kInf : -5.0, up = U(gen) < 0.5 ? kInf : 5.0;
+      a.add_row("c" + std::to_string(k), lo, up);
+      g.add_row("c" + std::to_string(k), lo, up);
+    }
+    for (int e = 0; e < ne; ++e) {
+      // integer-valued entries: any number of duplicates sums identically in any order
+      const int r = (int)(m * U(gen)) % m, c = (int)(n * U(gen)) % n;
+      const double v = std::floor(7 * U(gen)) - 3;
+      a.add_entry(r, c, v);
+      g.add_entry(r, c, v);
+    }
+    ++runs;
+    std::string ea, eg;
+    ProblemDef pa, pgd;
+    try {
+      pa = a.build();
+    } catch (const std::exception& x) {
+      ea = x.what();
+    }
+    try {
+      pgd = g.build();
+    } catch (const std::exception& x) {
+      eg = x.what();
+    }
+    if (!ea.empty() || !eg.empty()) {
+      ++threw;
+      if (ea != eg) ++bad;
+      continue;
+    }
+    const bool same = pa.row_start == pgd.row_start && pa.row_col == pgd.row_col &&
+                      pa.col_start == pgd.col_start && pa.col_row == pgd.col_row &&
+                      same_bits(pa.row_val, pgd.row_val) && same_bits(pa.col_val, pgd.col_val) &&
+                      same_bits(pa.var_lower, pgd.var_lower) && same_bits(pa.var_upper, pgd.var_upper) &&
+                      pa.is_integer == pgd.is_integer && pa.var_names == pgd.var_names &&
+                      pa.cons_names == pgd.cons_names;
+    if (!same) ++bad;
+  }
+  report("ProblemBuilder::build on the device (random builders, duplicates, zeros, errors)", bad == 0,
+         std::to_string(runs) + " builds (" + std::to_string(threw) + " threw), " + std::to_string(bad) +
+             " mismatches");
+}
+
 void errors()
 {
   const ProblemDef p = testkit::tiny_knapsack();
@@ -377,6 +439,7 @@ int main()
   if (want("rounding_stream")) rounding_stream();
   if (want("rounding_mixed")) rounding_mixed();
   if (want("repair_stream")) repair_stream();
+  if (want("builder_stream")) builder_stream();
   std::printf("%d failure(s)\n", g_failures);
   return g_failures;
 }
