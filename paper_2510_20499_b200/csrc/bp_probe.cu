@@ -58,6 +58,7 @@ struct PWarp {
   int cvar[PB_CCAP];
   double2 cval[PB_CCAP];
   double stage[64];
+  int off[33], st[32];  // flattened entry windows: exclusive offsets / first entry of 32 items
   int n_drow, n_dvar, n_chg, crossed, overflow;
 };
 
@@ -351,6 +352,49 @@ __device__ __forceinline__ int decide(double lo, double up, double nl, double nu
   return r;
 }
 
+__device__ __forceinline__ int warp_incl_scan_p(int v, int lane)
+{
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Calls f(e) for every entry e of the ranges [start[it], start[it + 1]) of items[0..cnt), the
+// (item, entry) pairs flattened across the warp 32 items at a time: two dependent loads per
+// window instead of two per item.
+template <class F>
+__device__ __forceinline__ void for_each_entry(PCtx& c, const int* items, int cnt, const int* start,
+                                               F f)
+{
+  const int lane = c.lane;
+  for (int w0 = 0; w0 < cnt; w0 += 32) {
+    const int j = w0 + lane;
+    int s0 = 0, len = 0;
+    if (j < cnt) {
+      const int it = items[j];
+      s0  = __ldg(start + it);
+      len = __ldg(start + it + 1) - s0;
+    }
+    const int incl  = warp_incl_scan_p(len, lane);
+    const int total = __shfl_sync(FULL, incl, 31);
+    c.w.off[lane]   = incl - len;
+    c.w.st[lane]    = s0;
+    if (lane == 0) c.w.off[32] = total;
+    __syncwarp();
+    for (int f0 = lane; f0 < total; f0 += 32) {
+      int o = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1)
+        if (c.w.off[o + step] <= f0) o += step;
+      f(c.w.st[o] + (f0 - c.w.off[o]));
+    }
+    __syncwarp();
+  }
+}
+
 // One probe branch (probing.hpp:194-219 + propagate) on this warp. Returns 0 feasible,
 // 1 infeasible, 2 overflow (caller re-runs on the full engine).
 __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
@@ -380,19 +424,15 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
     bool full = false;
     if (lane == 0) w.n_drow = 0;
     __syncwarp();
-    for (int j = 0; j < w.n_chg; ++j) {
-      const int i  = w.cvar[j];
-      const int cs = __ldg(c.P.col_start + i), ce = __ldg(c.P.col_start + i + 1);
-      for (int e = cs + lane; e < ce; e += 32) {
-        const int k = __ldg(c.P.col_row + e);
-        if (set_insert(w, k, full)) {
-          const int pos = atomicAdd(&w.n_drow, 1);
-          if (pos < PB_RCAP) w.drow[pos] = k;
-          // its vars alone would exceed the overlays: overflow now instead of after the work
-          if (__ldg(c.P.row_start + k + 1) - __ldg(c.P.row_start + k) > PB_LONGROW) full = true;
-        }
+    for_each_entry(c, w.cvar, w.n_chg, c.P.col_start, [&](int e) {
+      const int k = __ldg(c.P.col_row + e);
+      if (set_insert(w, k, full)) {
+        const int pos = atomicAdd(&w.n_drow, 1);
+        if (pos < PB_RCAP) w.drow[pos] = k;
+        // its vars alone would exceed the overlays: overflow now instead of after the work
+        if (__ldg(c.P.row_start + k + 1) - __ldg(c.P.row_start + k) > PB_LONGROW) full = true;
       }
-    }
+    });
     __syncwarp();
     if (__any_sync(FULL, full) || w.n_drow > PB_RCAP) return 2;
     const int nr = w.n_drow;
@@ -401,37 +441,36 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
     set_clear(w, lane);
     if (lane == 0) w.n_dvar = 0;
     __syncwarp();
-    for (int j = 0; j < nr; ++j) {
-      const int k  = w.drow[j];
-      const int rs = __ldg(c.P.row_start + k), re = __ldg(c.P.row_start + k + 1);
-      for (int e = rs + lane; e < re; e += 32) {
-        const int i = __ldg(c.P.row_col + e);
-        if (set_insert(w, i, full)) {
-          const int pos = atomicAdd(&w.n_dvar, 1);
-          if (pos < PB_VCAP) w.dvar[pos] = i;
-        }
+    for_each_entry(c, w.drow, nr, c.P.row_start, [&](int e) {
+      const int i = __ldg(c.P.row_col + e);
+      if (set_insert(w, i, full)) {
+        const int pos = atomicAdd(&w.n_dvar, 1);
+        if (pos < PB_VCAP) w.dvar[pos] = i;
       }
-    }
+    });
     __syncwarp();
     if (__any_sync(FULL, full) || w.n_dvar > PB_VCAP) return 2;
     ++rounds;
     // ---- activities of the dirty rows
+    // short rows one per lane; the long ones of each 32-row window warp-cooperatively
     bool ovf = false;
-    for (int j = lane; j < nr; j += 32) {
-      const int k = w.drow[j];
-      if (__ldg(c.P.row_start + k + 1) - __ldg(c.P.row_start + k) > PB_LANEROW) continue;
-      double smn, smx;
-      int imn, imx;
-      row_act_lane(c, k, smn, imn, smx, imx);
-      if (!aset(c, k, smn, imn, smx, imx)) ovf = true;
-    }
-    for (int j = 0; j < nr; ++j) {
-      const int k = w.drow[j];
-      if (__ldg(c.P.row_start + k + 1) - __ldg(c.P.row_start + k) <= PB_LANEROW) continue;
-      double smn, smx;
-      int imn, imx;
-      row_act_warp(c, k, smn, imn, smx, imx);
-      if (lane == 0 && !aset(c, k, smn, imn, smx, imx)) ovf = true;
+    for (int w0 = 0; w0 < nr; w0 += 32) {
+      const int j  = w0 + lane;
+      const int k  = j < nr ? w.drow[j] : -1;
+      const bool lng = k >= 0 && __ldg(c.P.row_start + k + 1) - __ldg(c.P.row_start + k) > PB_LANEROW;
+      if (k >= 0 && !lng) {
+        double smn, smx;
+        int imn, imx;
+        row_act_lane(c, k, smn, imn, smx, imx);
+        if (!aset(c, k, smn, imn, smx, imx)) ovf = true;
+      }
+      for (unsigned m = __ballot_sync(FULL, lng); m; m &= m - 1) {
+        const int kk = __shfl_sync(FULL, k, __ffs(m) - 1);
+        double smn, smx;
+        int imn, imx;
+        row_act_warp(c, kk, smn, imn, smx, imx);
+        if (lane == 0 && !aset(c, kk, smn, imn, smx, imx)) ovf = true;
+      }
     }
     __syncwarp();
     if (__any_sync(FULL, ovf)) return 2;
@@ -440,15 +479,7 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
     if (lane == 0) w.n_chg = 0;
     __syncwarp();
     int crossed = 0;
-    for (int j = lane; j < nv; j += 32) {
-      const int i = w.dvar[j];
-      if (__ldg(c.P.col_start + i + 1) - __ldg(c.P.col_start + i) > PB_LANEROW) continue;
-      const double2 b    = bget(c, i);
-      const bool integer = __ldg(c.P.is_int + i) != 0;
-      double nl, nu;
-      col_fold_lane(c, i, b.x, b.y, integer, nl, nu);
-      double2 out;
-      const int r = decide(b.x, b.y, nl, nu, integer, c.lim, out);
+    auto record = [&](int i, int r, const double2& out) {
       if (r < 0) crossed++;
       if (r > 0) {
         const int pos = atomicAdd(&w.n_chg, 1);
@@ -457,24 +488,29 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
           w.cval[pos] = out;
         }
       }
-    }
-    for (int j = 0; j < nv; ++j) {
-      const int i = w.dvar[j];
-      if (__ldg(c.P.col_start + i + 1) - __ldg(c.P.col_start + i) <= PB_LANEROW) continue;
-      const double2 b    = bget(c, i);
-      const bool integer = __ldg(c.P.is_int + i) != 0;
-      double nl, nu;
-      col_fold_warp(c, i, b.x, b.y, integer, nl, nu);
-      if (lane == 0) {
+    };
+    // short columns one per lane; the long ones of each 32-var window warp-cooperatively
+    for (int w0 = 0; w0 < nv; w0 += 32) {
+      const int j = w0 + lane;
+      const int i = j < nv ? w.dvar[j] : -1;
+      const bool lng = i >= 0 && __ldg(c.P.col_start + i + 1) - __ldg(c.P.col_start + i) > PB_LANEROW;
+      if (i >= 0 && !lng) {
+        const double2 b    = bget(c, i);
+        const bool integer = __ldg(c.P.is_int + i) != 0;
+        double nl, nu;
+        col_fold_lane(c, i, b.x, b.y, integer, nl, nu);
         double2 out;
-        const int r = decide(b.x, b.y, nl, nu, integer, c.lim, out);
-        if (r < 0) crossed++;
-        if (r > 0) {
-          const int pos = atomicAdd(&w.n_chg, 1);
-          if (pos < PB_CCAP) {
-            w.cvar[pos] = i;
-            w.cval[pos] = out;
-          }
+        record(i, decide(b.x, b.y, nl, nu, integer, c.lim, out), out);
+      }
+      for (unsigned m = __ballot_sync(FULL, lng); m; m &= m - 1) {
+        const int ii       = __shfl_sync(FULL, i, __ffs(m) - 1);
+        const double2 b    = bget(c, ii);
+        const bool integer = __ldg(c.P.is_int + ii) != 0;
+        double nl, nu;
+        col_fold_warp(c, ii, b.x, b.y, integer, nl, nu);
+        if (lane == 0) {
+          double2 out;
+          record(ii, decide(b.x, b.y, nl, nu, integer, c.lim, out), out);
         }
       }
     }
