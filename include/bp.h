@@ -260,6 +260,40 @@ int bp_parallel_propagate(bp_problem* p, const double* base2n, int32_t base_infe
                           int32_t* infeas_count, int32_t* evicted, int32_t* n_evicted,
                           int32_t* fixed_vars, double* fixed_vals, int32_t* n_fixed);
 
+/* ---------------------------------------------------------------- PDHG (lp.hpp)
+ * pulse::LpInstance (lp.hpp:17-47) on the device: the sparse products of the PDHG solver and its
+ * inner iteration, bit-identical to the reference (16384-entry segment summation, no FMA). */
+typedef struct bp_lp bp_lp;
+typedef struct {
+  int32_t n_vars;
+  int32_t n_rows;
+  const int32_t* row_start; /* CSR, n_rows + 1 */
+  const int32_t* row_col;
+  const double* row_val;
+  const int32_t* col_start; /* CSC, n_vars + 1 */
+  const int32_t* col_row;
+  const double* col_val;
+  const double* obj;        /* n_vars, may be NULL (then bp_lp_pdhg_iterate is unavailable) */
+  const double* row_lower;  /* n_rows */
+  const double* row_upper;
+  const double* var_lower;  /* n_vars */
+  const double* var_upper;
+} bp_lp_desc;
+
+int bp_lp_create(const bp_lp_desc* desc, int32_t device, bp_lp** out);
+int bp_lp_destroy(bp_lp* lp);
+/* lpdetail::spmv_rows (lp.hpp:74-87): ax[k] = sum_e row_val[e] * x[row_col[e]]. */
+int bp_lp_spmv_rows(bp_lp* lp, const double* x, double* ax);
+/* lpdetail::spmv_cols (lp.hpp:89-102): aty[i] = sum_e col_val[e] * y[col_row[e]]. */
+int bp_lp_spmv_cols(bp_lp* lp, const double* y, double* aty);
+/* `iters` PDHG iterations of pulse::lp::solve's inner loop (lp.hpp:315-340) with fixed step sizes:
+ * dual ascent y <- prox(y + sigma A x_bar), primal descent x <- clamp(x - tau (c + A'y)),
+ * x_bar <- 2 x_new - x, x_sum += x, y_sum += y. All five vectors are read and written back. */
+int bp_lp_pdhg_iterate(bp_lp* lp, double* x, double* y, double* x_bar, double* x_sum, double* y_sum,
+                       double tau, double sigma, int32_t iters);
+/* Device time (CUDA events on the LP's stream) of the last spmv / iterate call. */
+int bp_lp_last_ms(const bp_lp* lp, double* ms);
+
 /* Number of engine kernels launched by this process. */
 int64_t bp_kernel_launches(void);
 

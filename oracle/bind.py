@@ -84,6 +84,10 @@ class Ref:
                 "ref_get_bulk_size": (I, [I, I, I]),
                 "ref_generate_candidate_values": (None, [V, V, I, V, I, V, D, V, V]),
                 "ref_repair": (I, [V, V, V, I, I, V, V]),
+                "ref_problem_set_obj": (None, [V, V]),
+                "ref_lp_spmv_rows": (None, [V, V, V]),
+                "ref_lp_spmv_cols": (None, [V, V, V]),
+                "ref_lp_pdhg_iterate": (None, [V, V, V, V, V, V, D, D, I]),
                 "ref_parallel_propagate": (None, [V, V, I, V, I, V, V, V, V, V, V, V, V, V, V, V, V]),
                 "ref_propagation_round": (None, [V, V, V, C.c_ulonglong, D, D, I, V, V]),
             }

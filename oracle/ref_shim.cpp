@@ -19,6 +19,7 @@
 #include "pulse/probing.hpp"
 #include "pulse/propagation.hpp"
 #include "pulse/rounding.hpp"
+#include "pulse/lp.hpp"
 #include "testkit.hpp"
 
 using namespace pulse;
@@ -121,6 +122,11 @@ void* ref_problem_from_csr(int n_vars, int n_cons, const int* row_start, const i
 }
 
 void ref_problem_free(void* p) { delete static_cast<ProblemDef*>(p); }
+void ref_problem_set_obj(void* pv, const double* obj)
+{
+  auto* p = static_cast<ProblemDef*>(pv);
+  p->obj_coeffs.assign(obj, obj + p->n_vars);
+}
 
 void ref_problem_dims(const void* pv, int* n_vars, int* n_cons, int* nnz)
 {
@@ -488,6 +494,55 @@ int ref_repair(const void* pv, const int* fixed_vars, const double* fixed_vals, 
   for (int j = 0; j < nfixed; ++j) out_vals[j] = r->values[j].second;
   bounds_to(r->bounds, out_bounds2n, nullptr);
   return 1;
+}
+
+// lp.hpp:74-102 on LpInstance::relax(p) (the products only read the CSR / CSC).
+void ref_lp_spmv_rows(const void* pv, const double* x, double* out)
+{
+  const auto s = LpInstance::relax(*static_cast<const ProblemDef*>(pv));
+  std::vector<double> xv(x, x + s.n_vars), o(s.n_rows);
+  lpdetail::spmv_rows(s, xv, o);
+  std::copy(o.begin(), o.end(), out);
+}
+void ref_lp_spmv_cols(const void* pv, const double* y, double* out)
+{
+  const auto s = LpInstance::relax(*static_cast<const ProblemDef*>(pv));
+  std::vector<double> yv(y, y + s.n_rows), o(s.n_vars);
+  lpdetail::spmv_cols(s, yv, o);
+  std::copy(o.begin(), o.end(), out);
+}
+
+// The inner PDHG iteration of lp::solve (lp.hpp:315-340) restated verbatim around the reference's
+// own lpdetail::spmv_rows / spmv_cols and pulse::clamp, `iters` times with fixed tau / sigma.
+void ref_lp_pdhg_iterate(const void* pv, double* x, double* y, double* x_bar, double* x_sum,
+                         double* y_sum, double tau, double sigma, int iters)
+{
+  const auto s = LpInstance::relax(*static_cast<const ProblemDef*>(pv));
+  const int n = s.n_vars, m = s.n_rows;
+  std::vector<double> X(x, x + n), Y(y, y + m), XB(x_bar, x_bar + n), XS(x_sum, x_sum + n),
+      YS(y_sum, y_sum + m), xn(n), ax(m), aty(n);
+  for (int it = 0; it < iters; ++it) {
+    lpdetail::spmv_rows(s, XB, ax);
+    for (int k = 0; k < m; ++k) {
+      const double v    = Y[k] + sigma * ax[k];
+      const double proj = clamp(v / sigma, s.row_lower[k], s.row_upper[k]);
+      Y[k]              = v - sigma * proj;
+    }
+    lpdetail::spmv_cols(s, Y, aty);
+    for (int i = 0; i < n; ++i) {
+      const double v = X[i] - tau * (s.obj[i] + aty[i]);
+      xn[i]          = clamp(v, s.var_lower[i], s.var_upper[i]);
+      XB[i]          = 2.0 * xn[i] - X[i];
+    }
+    std::swap(X, xn);
+    for (int i = 0; i < n; ++i) XS[i] += X[i];
+    for (int k = 0; k < m; ++k) YS[k] += Y[k];
+  }
+  std::copy(X.begin(), X.end(), x);
+  std::copy(Y.begin(), Y.end(), y);
+  std::copy(XB.begin(), XB.end(), x_bar);
+  std::copy(XS.begin(), XS.end(), x_sum);
+  std::copy(YS.begin(), YS.end(), y_sum);
 }
 
 // rounding.hpp:393 with a cache handle (or null) and Rng(seed). lp_polish runs inside (OUT OF

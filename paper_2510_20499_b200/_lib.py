@@ -57,6 +57,16 @@ class bp_built(C.Structure):
     ]
 
 
+class bp_lp_desc(C.Structure):
+    _fields_ = [
+        ("n_vars", C.c_int32), ("n_rows", C.c_int32),
+        ("row_start", C.c_void_p), ("row_col", C.c_void_p), ("row_val", C.c_void_p),
+        ("col_start", C.c_void_p), ("col_row", C.c_void_p), ("col_val", C.c_void_p),
+        ("obj", C.c_void_p), ("row_lower", C.c_void_p), ("row_upper", C.c_void_p),
+        ("var_lower", C.c_void_p), ("var_upper", C.c_void_p),
+    ]
+
+
 class bp_limits(C.Structure):
     _fields_ = [("max_rounds", C.c_int32), ("time_limit", C.c_double),
                 ("abs_threshold", C.c_double), ("rel_threshold", C.c_double),
@@ -144,6 +154,13 @@ _SIGS = [
                                         C.c_void_p]),
     ("bp_build_problem", C.c_int, [C.POINTER(bp_builder_desc), C.c_int32, C.POINTER(bp_built),
                                    C.POINTER(C.c_void_p)]),
+    ("bp_lp_create", C.c_int, [C.POINTER(bp_lp_desc), C.c_int32, C.POINTER(C.c_void_p)]),
+    ("bp_lp_destroy", C.c_int, [C.c_void_p]),
+    ("bp_lp_spmv_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("bp_lp_spmv_cols", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("bp_lp_pdhg_iterate", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_double, C.c_double, C.c_int32]),
+    ("bp_lp_last_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("bp_kernel_launches", C.c_int64, []),
     ("bp_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                  C.POINTER(C.c_int64)]),
