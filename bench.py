@@ -316,6 +316,57 @@ def run_rounding(args, rank, world, local):
     return res
 
 
+def run_lp(args, rank, world, local, p):
+    """the PDHG inner iteration (lp.hpp:315-340: spmv_rows + dual prox +
+    spmv_cols + primal step + running sums) on the C2 matrix, device-resident; CUDA-event time of
+    `iters` iterations per call. Algorithmic bytes per iteration: both matrix views streamed once
+    (24 B per nnz), one 8-B gather per nnz in each product, and the elementwise vectors (dual step
+    40 B / row, primal step 72 B / var + 16 B / row for the running sums)."""
+    from paper_2510_20499_b200.lp import DeviceLp, LpInstance
+    if rank != 0:
+        return None
+    n, m, N = p.n_vars, p.n_cons, p.nnz()
+    s = LpInstance.relax(p)
+    s.obj = np.random.default_rng(7).normal(size=n)
+    lp = DeviceLp(s)
+    x = np.clip(np.zeros(n), p.var_lower, p.var_upper)
+    st = [x, np.zeros(m), x.copy(), np.zeros(n), np.zeros(m)]
+    iters = 20
+    lp.pdhg_iterate(*st, 1e-3, 1e-3, 3)  # warm-up
+    ms = []
+    for _ in range(3):
+        st = list(lp.pdhg_iterate(*st, 1e-3, 1e-3, iters))
+        ms.append(lp.last_ms() / iters)
+    it_ms = float(np.median(ms))
+    alg = 24 * N + 16 * N + 40 * m + 72 * n + 16 * m
+    peak, peak_kind = peaks()
+    out = {"workload": "PDHG inner iteration on the C2 matrix (1M x 1M, %d nnz)" % N,
+           "ms_per_iteration": it_ms, "iterations_per_s": 1e3 / it_ms,
+           "roofline": {"bound": "hbm", "achieved": alg / (it_ms * 1e-3) / 1e9, "peak": peak,
+                        "unit": "GB/s", "frac": alg / (it_ms * 1e-3) / 1e9 / peak,
+                        "algorithmic_bytes_per_iteration": alg, "peak_kind": peak_kind},
+           "parity": "bitwise vs lpdetail::spmv_rows / spmv_cols (tests/test_gpu_lp.py)"}
+    if world == 1 and not args.no_cpu_baseline:
+        import ctypes as C
+
+        from oracle.bind import Ref, RefProblem
+        if Ref.available():
+            rp = RefProblem.from_def(p)
+            o = np.ascontiguousarray(s.obj)
+            Ref.lib().ref_problem_set_obj(rp.h, o.ctypes.data_as(C.c_void_p))
+            r = [np.ascontiguousarray(a, dtype=np.float64).copy() for a in st]
+            P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+            k = 5
+            t0 = time.perf_counter()
+            Ref.lib().ref_lp_pdhg_iterate(rp.h, *[P(a) for a in r], 1e-3, 1e-3, k)
+            el = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": k / el, "unit": "iterations/s",
+                                   "cores": int(Ref.lib().ref_max_threads()), "kind": "reference",
+                                   "sample": f"{k} iterations of the reference's products (parallel_for) + "
+                                             f"the restated elementwise steps ({el:.2f} s)"}
+    return out
+
+
 def run_batch(args, rank, world, local):
     """configs[4]: 64 heterogeneous MIPLIB-shaped instances (10k-5M nnz), LPT-partitioned by size
     over the ranks; each rank uploads its instances and propagates them one after another on its
@@ -419,6 +470,7 @@ def main():
     ap.add_argument("--no-rounding", action="store_true")
     ap.add_argument("--cpu-sample-sec", type=float, default=20.0)
     ap.add_argument("--no-batch", action="store_true")
+    ap.add_argument("--no-lp", action="store_true")
     ap.add_argument("--round-deadline", type=float, default=30.0,
                     help="C4 propagation_round deadline (s), as the reference's Deadline")
     ap.add_argument("--cache-budget", type=float, default=5.0,
@@ -540,6 +592,8 @@ def main():
     log("rounding done")
     batch = None if args.no_batch else run_batch(args, rank, world, local)
     log("batch done")
+    lp = None if args.no_lp or args.workload != "C2" else run_lp(args, rank, world, local, p)
+    log("lp done")
 
     if rank == 0:
         peak, peak_kind = peaks()
@@ -587,6 +641,7 @@ def main():
             "probing": probing,
             "rounding": rounding,
             "batch": batch,
+            "lp": lp,
         }
         print(json.dumps(line))
     if world > 1:
