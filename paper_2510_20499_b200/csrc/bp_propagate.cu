@@ -788,6 +788,13 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand)
   }
   if (!cand) return;
   const bool quiet = k < 0 || (kRowGate && entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x));
+  if (S.dbg) {  // gate statistics (BP_DEBUG=1)
+    const unsigned nr = __popc(__ballot_sync(FULL, k >= 0)), nq = __popc(__ballot_sync(FULL, !quiet));
+    if (c.lane == 0) {
+      atomicAdd(S.dbg + 16, (unsigned long long)nr);
+      atomicAdd(S.dbg + 17, (unsigned long long)nq);
+    }
+  }
   if (__all_sync(FULL, quiet)) return;
   for (int j = 0; j < Lm; j += U) {
     int ci[U];
@@ -805,7 +812,9 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand)
       if (ci[u] == -1) continue;
       double tw, pw;
       entry_reach(a[u], bd[u].x, bd[u].y, ci[u] < 0, tw, pw);
+      if (S.dbg) atomicAdd(S.dbg + 18, 1ull);
       if (entry_quiet(tw, pw, smn, imn, smx, imx, cb.y, cb.x)) continue;
+      if (S.dbg) atomicAdd(S.dbg + 19, 1ull);
       double cl, cu;
       cand_explicit(bd[u].x, bd[u].y, ci[u] < 0, a[u], smn, imn, smx, imx, cb.y, cb.x, cl, cu);
       publish(S.slot + (ci[u] & ~kIntBit), cl, cu, bd[u].x, bd[u].y, k);
@@ -2077,8 +2086,8 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.ctl     = P.ctl.p;
   S.dbg     = nullptr;
   if (getenv("BP_DEBUG")) {
-    P.dbg.alloc(16);
-    BP_CUDA(cudaMemset(P.dbg.p, 0, 16 * sizeof(unsigned long long)));
+    P.dbg.alloc(24);
+    BP_CUDA(cudaMemset(P.dbg.p, 0, 24 * sizeof(unsigned long long)));
     S.dbg = P.dbg.p;
   }
 
@@ -2190,13 +2199,15 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
     BP_CUDA(cudaStreamSynchronize(s));
   }
   if (P.st.dbg) {
-    unsigned long long h[16];
+    unsigned long long h[24];
     BP_CUDA(cudaMemcpy(h, P.st.dbg, sizeof(h), cudaMemcpyDeviceToHost));
     const char* nm[5] = {"heavy_fold", "sell_slice", "cand_piece", "heavy_stream", "group_fold"};
     for (int q = 0; q < 5; ++q)
       fprintf(stderr, "[bp dbg] %-10s n=%llu avg=%.1f us max=%.1f us total=%.1f warp-ms\n", nm[q],
               h[3 * q + 2], h[3 * q + 2] ? h[3 * q] / 1965.0 / h[3 * q + 2] : 0.0,
               h[3 * q + 1] / 1965.0, h[3 * q] / 1965.0 / 1e3);
+    fprintf(stderr, "[bp dbg] sell rows %llu, past the row gate %llu, pass-2 entries %llu, past the entry gate %llu\n",
+            h[16], h[17], h[18], h[19]);
     BP_CUDA(cudaMemset(P.st.dbg, 0, sizeof(h)));
   }
   float ms = 0.f;
