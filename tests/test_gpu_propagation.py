@@ -237,3 +237,20 @@ def test_c5_small_instances_bitwise(oracle_built):
         kinds.add(sp[2])
         _compare_with_oracle(p, lims=(Lim(),))
     assert len(kinds) >= 3
+
+
+@pytest.mark.parametrize("config", ["C2", "C4"])
+def test_full_size_bitwise_vs_reference(oracle_built, config):
+    """BASELINE.json's full sizes: one propagate from the original bounds of C2 (1M x 1M,
+    19.6M nnz, 24 rounds) and of C4 (2M x 2M, 25.7M nnz) equals the reference's own propagate
+    (oracle/_ref, all host threads) bit for bit: bounds, status, rounds, crossed."""
+    from oracle.bind import Ref, RefProblem, ref_propagate
+    if not Ref.available():
+        pytest.skip("reference library missing")
+    p = synth.c2() if config == "C2" else synth.c4()[0]
+    rp = RefProblem.from_def(p)
+    ob, oinf, ost, orr, ocr = ref_propagate(rp, p.root_bounds())
+    b = BoundsState(p)
+    r = propagate(p, b)
+    assert (b.infeasible(), int(r.status), r.rounds, r.crossed_vars) == (oinf, ost, orr, ocr)
+    assert_bitwise(b.raw(), ob, f"{config} bounds")
