@@ -605,8 +605,8 @@ __device__ void group_fold(Ctx& c, int t0, int nt, bool cand)
   int Lmax = L;
 #pragma unroll
   for (int o = 16; o; o >>= 1) Lmax = max(Lmax, __shfl_xor_sync(FULL, Lmax, o));
-  double* gb0 = c.w.b0 + 64 * g;  // group slices of the staging buffers (32 used per chunk)
-  double* gb1 = c.w.b1 + 64 * g;
+  double* gb0 = c.w.b0 + 32 * g;  // group slices of the staging buffers (<= 32 per chunk)
+  double* gb1 = c.w.b1 + 32 * g;
   int ci[4], cn[4];
   double a[4], an[4];
   double2 bd[4];
@@ -1486,6 +1486,16 @@ __device__ void zero_par(ParCtl* q)
 #ifndef BP_F2_MIN_BLOCKS
 #define BP_F2_MIN_BLOCKS 2
 #endif
+// Shared memory of k_rows_full: its row tasks stage at most 128 values per chain (heavy folds)
+// or 4 x 32 (grouped medium rows) in b0 / b1, so each warp gets a 3 KB region (b0 at 0, b1 at
+// 2 KB) instead of a full WarpSmem: 24 KB per block, which lets the SM keep the larger L1 split
+// (the bound gathers are L1 hits as often as the L1 is large).
+#ifndef BP_ROWS_COMPACT_SMEM
+#define BP_ROWS_COMPACT_SMEM 1
+#endif
+constexpr int kRowsWarpBytes = 3072;
+static_assert(offsetof(WarpSmem, b1) == 2048 && 2048 + 128 * 8 <= kRowsWarpBytes, "row-task smem layout");
+constexpr size_t kRowsSmem = BP_ROWS_COMPACT_SMEM ? (size_t)kWarps * kRowsWarpBytes : sizeof(Smem);
 // The host enqueues [k_rows_full, k_cand_pieces, k_engine(resume)] speculatively, several rounds
 // ahead without waiting: each is a no-op unless the engine handed a full round over (need_full).
 __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
@@ -1501,7 +1511,13 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
-  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
+#if BP_ROWS_COMPACT_SMEM
+  // compact warp regions: only b0[0..128) and b1[0..128) are used by the full round's row tasks
+  WarpSmem& w = *reinterpret_cast<WarpSmem*>(dyn_smem + warp * kRowsWarpBytes);
+#else
+  WarpSmem& w = sm.w[warp];
+#endif
+  Ctx c{P, S, lim, sm, w, (int)(threadIdx.x & 31), warp};
   phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell);
 }
 
@@ -2103,7 +2119,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
                                (int)sizeof(Smem)));
   BP_CUDA(cudaFuncSetAttribute(k_cand_pieces, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)sizeof(Smem)));
-  BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_rows_full, kThreads, sizeof(Smem)));
+  BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_rows_full, kThreads, kRowsSmem));
   P.f2_blocks = dev_sms * std::max(per_sm2, 1);
   int per_sm3   = 0;
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_rows_sell, kThreads, 0));
@@ -2158,7 +2174,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   for (int batch = 1; ext; batch = std::min(2 * batch, 8)) {
     resume = 1;
     for (int b = 0; b < batch; ++b) {
-      k_rows_full<<<P.f2_blocks, kThreads, sizeof(Smem), s>>>(d, st, l, split_sell);
+      k_rows_full<<<P.f2_blocks, kThreads, kRowsSmem, s>>>(d, st, l, split_sell);
       if (split_sell) {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
