@@ -4,16 +4,16 @@
 // spmv_rows: out[k] = sum over the row's entries of a * x[col], summed like the reference: within
 // each 16384-entry segment left to right from 0.0 (`part += a * x`, separately rounded product, no
 // FMA), segment partials added in order onto 0.0 (`total += part`). spmv_cols is the same over the
-// CSC. Rows (columns) of <= kLpLane entries are one per thread with four entries' loads and gathers
-// in flight; longer ones are split into 16384-entry segments, one warp per segment: the lanes
-// gather 256 products into shared memory while lane 0 runs the sequential sum over the previous
-// 256 (double buffered), then the segment partials are combined in order by a finalize pass.
+// CSC. Rows (columns) of <= kLpLane entries sit in SELL-32 slices (thread per item, coalesced
+// index / value loads, four entries' gathers in flight); longer ones are split into 16384-entry
+// segments, one warp per segment: the lanes gather 256 products into shared memory while lane 0
+// runs the sequential sum over the previous 256 (double buffered), then the segment partials are
+// combined in order.
 //
-// The PDHG step kernels fuse the elementwise updates into the SpMV epilogues: the dual update
-// (y = v - sigma * clamp(v / sigma, row bounds), v = y + sigma * A x_bar) into spmv_rows, and the
-// primal update (x_next = clamp(x - tau (c + A'y)), x_bar = 2 x_next - x) plus the running sums
-// x_sum += x, y_sum += y into spmv_cols / its finalize — each vector is read and written once per
-// half-step.
+// The PDHG iteration adds one elementwise kernel after each product: the dual step
+// (y = v - sigma * clamp(v / sigma, row bounds), v = y + sigma * A x_bar) and the primal step
+// (x_next = clamp(x - tau (c + A'y)), x_bar = 2 x_next - x) fused with the running sums
+// x_sum += x, y_sum += y -- each vector is read and written once per half-step.
 #include <algorithm>
 #include <cmath>
 #include <stdexcept>
@@ -37,64 +37,75 @@ __device__ __forceinline__ double lp_clamp(double v, double lo, double hi)
   return v < lo ? lo : (v > hi ? hi : v);  // common.hpp clamp: std::max(lo, std::min(v, hi))
 }
 
-// One short row / column per thread (single segment): total = 0.0 + (sequential partial).
-__global__ void k_spmv_short(int nitem, const int* start, const int* idx, const double* val,
-                             const double* x, const int* items, int nshort, double* out)
+// Short rows / columns in SELL-32 slices (sorted by length, 32 per slice, entry j of lane i at
+// base + 32 j + i): thread per item, coalesced index / value loads, four entries' gathers in
+// flight, the sequential single-segment sum in registers.
+__global__ void k_spmv_sell(int nslice, const int* sbase, const int* sitem, const int* sidx,
+                            const double* sval, const double* x, double* out)
 {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nshort; j += gridDim.x * blockDim.x) {
-    const int it = items[j];
-    const int s0 = __ldg(start + it), s1 = __ldg(start + it + 1);
-    double part  = 0.0;
-    for (int e0 = s0; e0 < s1; e0 += 4) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int sl = gw; sl < nslice; sl += nw) {
+    const int b0 = __ldg(sbase + sl), Lm = (__ldg(sbase + sl + 1) - b0) >> 5;
+    const int it = __ldg(sitem + 32 * sl + lane);
+    const int* ip    = sidx + b0 + lane;
+    const double* vp = sval + b0 + lane;
+    double part = 0.0;
+    for (int j = 0; j < Lm; j += 4) {
       int c[4];
       double a[4], xv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        c[u] = e0 + u < s1 ? __ldg(idx + e0 + u) : -1;
-        a[u] = e0 + u < s1 ? __ldg(val + e0 + u) : 0.0;
+        c[u] = j + u < Lm ? __ldg(ip + 32 * (j + u)) : -1;
+        a[u] = j + u < Lm ? __ldg(vp + 32 * (j + u)) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (c[u] >= 0) part = __dadd_rn(part, __dmul_rn(a[u], xv[u]));
+        if (c[u] >= 0) part = __dadd_rn(part, __dmul_rn(a[u], xv[u]));  // padding follows the row
     }
-    out[it] = __dadd_rn(0.0, part);
+    if (it >= 0) out[it] = __dadd_rn(0.0, part);
   }
-  (void)nitem;
 }
 
-// One 16384-entry segment of a long row / column per warp: partial sum into seg_out[task].
+// One 16384-entry segment of a long row / column per warp: partial sum into seg_out[task]. The
+// products of chunk j + 1 are loaded into registers while lane 0 runs the sequential sum over
+// chunk j from shared memory, then staged (the loads overlap the DADD chain).
 __global__ void __launch_bounds__(kLpThreads)
     k_spmv_segments(const int* start, const int* idx, const double* val, const double* x,
-                    const int2* tasks, int ntask, double* seg_out)
+                    const int2* tasks, const int* slot, int ntask, double* seg_out)
 {
-  __shared__ double buf[kLpThreads / 32][2][kLpChunk];
+  __shared__ double buf[kLpThreads / 32][kLpChunk];
+  constexpr int PL = kLpChunk / 32;  // products per lane per chunk
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = blockIdx.x * (kLpThreads / 32) + wib, nw = gridDim.x * (kLpThreads / 32);
   for (int t = gw; t < ntask; t += nw) {
-    const int2 tk = tasks[t];  // (item, segment)
+    const int2 tk = tasks[t];  // (item, segment), longest first
     const int s0  = __ldg(start + tk.x) + tk.y * kLpSeg;
     const int s1  = min(__ldg(start + tk.x + 1), s0 + kLpSeg);
     double part   = 0.0;
-    int cur       = 0;
-    int prev_n    = 0;
-    for (int b0 = s0; b0 < s1 + kLpChunk; b0 += kLpChunk) {
-      // stage the products of chunk b0 (if any) while lane 0 folds the previous chunk
-      const int n = max(0, min(kLpChunk, s1 - b0));
+    double pr[PL];
+    auto load = [&](int b0) {
 #pragma unroll
-      for (int h = 0; h < kLpChunk / 32; ++h) {
+      for (int h = 0; h < PL; ++h) {
         const int e = b0 + h * 32 + lane;
-        if (h * 32 + lane < n) buf[wib][cur][h * 32 + lane] = __dmul_rn(__ldg(val + e), x[__ldg(idx + e)]);
+        pr[h]       = e < s1 ? __dmul_rn(__ldg(val + e), x[__ldg(idx + e)]) : 0.0;
       }
-      if (lane == 0)
-        for (int q = 0; q < prev_n; ++q) part = __dadd_rn(part, buf[wib][cur ^ 1][q]);
+    };
+    load(s0);
+    for (int b0 = s0; b0 < s1; b0 += kLpChunk) {
+#pragma unroll
+      for (int h = 0; h < PL; ++h) buf[wib][h * 32 + lane] = pr[h];
       __syncwarp();
-      prev_n = n;
-      cur ^= 1;
+      load(b0 + kLpChunk);  // in flight during the fold below
+      if (lane == 0) {
+        const int n = min(kLpChunk, s1 - b0);
+        for (int q = 0; q < n; ++q) part = __dadd_rn(part, buf[wib][q]);
+      }
+      __syncwarp();
     }
-    if (lane == 0) seg_out[t] = part;
-    __syncwarp();
+    if (lane == 0) seg_out[slot[t]] = part;
   }
 }
 
@@ -148,7 +159,11 @@ struct LpView {
   DBuf<int> start, idx;
   DBuf<double> val;
   DBuf<int> short_items, long_items, seg_first;
+  DBuf<int> sl_base, sl_item, sl_idx;
+  DBuf<double> sl_val;
+  int n_slice = 0;
   DBuf<int2> tasks;
+  DBuf<int> task_slot;
   DBuf<double> seg_out;
   int n_short = 0, n_long = 0, n_task = 0;
 
@@ -168,31 +183,72 @@ struct LpView {
       } else {
         lg.push_back(i);
         for (int q = 0; q * kLpSeg < L; ++q) tk.push_back(make_int2(i, q));
-        sf.push_back((int)tk.size());
+        sf.push_back((int)tk.size());  // segment outputs of item lg[j]: seg_out[sf[j] .. sf[j+1])
       }
+    }
+    // SELL-32 slices of the short items, longest first
+    {
+      std::vector<int> ord(sh);
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+        return h_start[a + 1] - h_start[a] > h_start[b + 1] - h_start[b];
+      });
+      std::vector<int> base{0}, item, sidx;
+      std::vector<double> sval;
+      for (size_t s0 = 0; s0 < ord.size(); s0 += 32) {
+        const size_t cnt = std::min<size_t>(32, ord.size() - s0);
+        const int Lm     = h_start[ord[s0] + 1] - h_start[ord[s0]];
+        const size_t off = sidx.size();
+        sidx.resize(off + 32 * (size_t)Lm, -1);
+        sval.resize(off + 32 * (size_t)Lm, 0.0);
+        for (size_t i = 0; i < 32; ++i) {
+          item.push_back(i < cnt ? ord[s0 + i] : -1);
+          if (i >= cnt) continue;
+          const int it = ord[s0 + i];
+          for (int e = h_start[it], j = 0; e < h_start[it + 1]; ++e, ++j) {
+            sidx[off + 32 * (size_t)j + i] = h_idx[e];
+            sval[off + 32 * (size_t)j + i] = h_val[e];
+          }
+        }
+        base.push_back((int)sidx.size());
+      }
+      n_slice = (int)(base.size() - 1);
+      sl_base.upload(base);
+      sl_item.upload(item);
+      sl_idx.upload(sidx);
+      sl_val.upload(sval);
     }
     n_short = (int)sh.size();
     n_long  = (int)lg.size();
     n_task  = (int)tk.size();
+    // launch order: longest segments first (the sequential sums are the critical path)
+    std::vector<int> ord(tk.size());
+    for (size_t t = 0; t < tk.size(); ++t) ord[t] = (int)t;
+    auto seglen = [&](const int2& q) {
+      return std::min(h_start[q.x + 1] - h_start[q.x] - q.y * kLpSeg, kLpSeg);
+    };
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return seglen(tk[a]) > seglen(tk[b]); });
+    std::vector<int2> tks(tk.size());
+    for (size_t t = 0; t < tk.size(); ++t) tks[t] = tk[ord[t]];
+    task_slot.upload(ord);
     short_items.upload(sh);
     long_items.upload(lg);
     seg_first.upload(sf);
-    tasks.upload(tk);
+    tasks.upload(tks);
     seg_out.alloc(std::max(n_task, 1));
   }
 
   void spmv(const double* x, double* out, cudaStream_t s)
   {
-    if (n_short)
-      k_spmv_short<<<nblk(n_short), 256, 0, s>>>(n_item, start.p, idx.p, val.p, x, short_items.p,
-                                                 n_short, out);
+    if (n_slice)
+      k_spmv_sell<<<nblk(32ll * n_slice), 256, 0, s>>>(n_slice, sl_base.p, sl_item.p, sl_idx.p,
+                                                       sl_val.p, x, out);
     if (n_task) {
       k_spmv_segments<<<std::min(148 * 8, (n_task + kLpThreads / 32 - 1) / (kLpThreads / 32)), kLpThreads,
-                        0, s>>>(start.p, idx.p, val.p, x, tasks.p, n_task, seg_out.p);
+                        0, s>>>(start.p, idx.p, val.p, x, tasks.p, task_slot.p, n_task, seg_out.p);
       k_spmv_combine<<<nblk(n_long), 256, 0, s>>>(long_items.p, seg_first.p, n_long, seg_out.p, out);
     }
     BP_CUDA(cudaGetLastError());
-    g_kernel_launches += (n_short ? 1 : 0) + (n_task ? 2 : 0);
+    g_kernel_launches += (n_slice ? 1 : 0) + (n_task ? 2 : 0);
   }
 };
 
