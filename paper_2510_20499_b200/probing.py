@@ -100,10 +100,17 @@ class ProbingCache:
         self.n_fallback = nfb.value
         self.certified = bool(cert.value)
         self.probe_ms = ms.value
-        r = np.zeros(2 * self.n_vars)
-        _lib.check(_lib.lib().bp_cache_root(self.h, _lib.ptr(r)))
-        self.root = BoundsState(raw=r)
+        self._root = None
         self._memo = {}
+
+    @property
+    def root(self) -> BoundsState:
+        """probing.hpp:96 (materialised on first access: a 16n-byte copy)."""
+        if self._root is None:
+            r = np.zeros(2 * self.n_vars)
+            _lib.check(_lib.lib().bp_cache_root(self.h, _lib.ptr(r)))
+            self._root = BoundsState(raw=r)
+        return self._root
 
     def __del__(self):
         try:
