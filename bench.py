@@ -493,6 +493,8 @@ def main():
     from paper_2510_20499_b200.propagation import FORCE_FRONTIER, device_problem, propagate_device
 
     torch.cuda.set_device(local)
+    from paper_2510_20499_b200 import set_device
+    set_device(local)  # every problem / LP this rank uploads lives on its own GPU
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     log(f"generating {args.workload}")

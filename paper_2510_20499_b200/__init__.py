@@ -8,11 +8,11 @@ from .problem import (K_INF, ProblemBuilder, ProblemDef, make_problem, problem_f
                       round_integer_bounds)
 from .propagation import (ActivityState, BoundsState, PropagationLimits, PropagationResult,
                           PropagationStatus, WorkPlan, build_work_plan, compute_activities,
-                          propagate, propagate_device, size_class_of, tighten_bounds)
+                          propagate, propagate_device, set_device, size_class_of, tighten_bounds)
 
 __all__ = [
     "K_INF", "ProblemBuilder", "ProblemDef", "make_problem", "problem_from_csr",
     "round_integer_bounds", "ActivityState", "BoundsState", "PropagationLimits",
     "PropagationResult", "PropagationStatus", "WorkPlan", "build_work_plan", "compute_activities",
-    "propagate", "propagate_device", "size_class_of", "tighten_bounds",
+    "propagate", "propagate_device", "set_device", "size_class_of", "tighten_bounds",
 ]

@@ -39,7 +39,9 @@ class LpInstance:
 class DeviceLp:
     """Owning handle of a device LP instance (bp_lp_create)."""
 
-    def __init__(self, s: LpInstance, device: int = 0):
+    def __init__(self, s: LpInstance, device: int | None = None):
+        from .propagation import default_device
+        device = default_device() if device is None else device
         f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
         i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)  # noqa: E731
         self._keep = [i32(s.row_start), i32(s.row_col), f64(s.row_val), i32(s.col_start),

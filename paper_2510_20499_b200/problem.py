@@ -215,7 +215,7 @@ class ProblemBuilder:
         return p
 
 
-def build_on_device(b: ProblemBuilder, device: int = 0) -> ProblemDef:
+def build_on_device(b: ProblemBuilder, device: int | None = None) -> ProblemDef:
     """ProblemBuilder::build (problem.hpp:141-227) with every O(N log N) step on the GPU
     (bp_build_problem): the returned ProblemDef carries the device problem it was built into.
     Same results and error types as ``ProblemBuilder.build`` (duplicates summed in insertion
@@ -223,7 +223,8 @@ def build_on_device(b: ProblemBuilder, device: int = 0) -> ProblemDef:
     import ctypes as C
 
     from . import _lib
-    from .propagation import DeviceProblem
+    from .propagation import DeviceProblem, default_device
+    device = default_device() if device is None else device
     n, m = b.n_vars(), b.n_rows()
     lo = np.ascontiguousarray(b._lo, dtype=np.float64)
     up = np.ascontiguousarray(b._up, dtype=np.float64)

@@ -219,8 +219,28 @@ class DeviceProblem:
             pass
 
 
-def device_problem(p: ProblemDef, device: int = 0) -> DeviceProblem:
+_DEFAULT_DEVICE = 0
+
+
+def set_device(device: int) -> None:
+    """GPU for problems uploaded from now on (pulse_gpu.hpp's set_device): one process per GPU
+    calls it with its local rank."""
+    global _DEFAULT_DEVICE
+    _DEFAULT_DEVICE = int(device)
+
+
+def default_device() -> int:
+    return _DEFAULT_DEVICE
+
+
+def device_problem(p: ProblemDef, device: int | None = None) -> DeviceProblem:
+    """The device copy of p: the one already attached when no device is named, else uploaded to
+    `device` (default: set_device's)."""
     dp = getattr(p, "_device_handle", None)
+    if device is None:
+        if dp is not None:
+            return dp
+        device = _DEFAULT_DEVICE
     if dp is None or dp.device != device:
         dp = DeviceProblem(p, device)
         p._device_handle = dp
