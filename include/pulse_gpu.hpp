@@ -6,6 +6,8 @@
 // C-ABI in bp.h (plain pointers; no CUDA or torch types cross it):
 //
 //   pulse::ProblemBuilder::build       problem.hpp:141       -> bp_build_problem
+//   pulse::lpdetail::spmv_rows / cols  lp.hpp:74, :89        -> bp_lp_spmv_rows / bp_lp_spmv_cols
+//   (PDHG inner iteration, lp.hpp:315-340)                   -> bp_lp_pdhg_iterate
 //   pulse::compute_activities          propagation.hpp:226   -> bp_compute_activities
 //   pulse::tighten_bounds              propagation.hpp:378   -> bp_tighten_bounds
 //   pulse::propagate                   propagation.hpp:418   -> bp_propagate
@@ -43,6 +45,7 @@
 #include "bp.h"
 #include "pulse/probing.hpp"
 #include "pulse/propagation.hpp"
+#include "pulse/lp.hpp"
 #include "pulse/rounding.hpp"
 
 namespace pulse::gpu {
@@ -518,6 +521,63 @@ class ProblemBuilder {
   std::string name_;
   std::string obj_name_ = "OBJ";
 };
+
+// ---------------------------------------------------------------- lp.hpp
+
+// Device copy of a pulse::LpInstance (lp.hpp:17-47) for repeated PDHG products; results are
+// bit-identical to lpdetail::spmv_rows / spmv_cols.
+class LpProducts {
+ public:
+  explicit LpProducts(const LpInstance& s) : n_(s.n_vars), m_(s.n_rows)
+  {
+    bp_lp_desc d{s.n_vars,        s.n_rows,           s.row_start.data(), s.row_col.data(),
+                 s.row_val.data(), s.col_start.data(), s.col_row.data(),   s.col_val.data(),
+                 s.obj.empty() ? nullptr : s.obj.data(), s.row_lower.data(), s.row_upper.data(),
+                 s.var_lower.data(), s.var_upper.data()};
+    detail::check(bp_lp_create(&d, detail::registry().device, &h_));
+  }
+  ~LpProducts()
+  {
+    if (h_) bp_lp_destroy(h_);
+  }
+  LpProducts(const LpProducts&) = delete;
+  LpProducts& operator=(const LpProducts&) = delete;
+
+  // lp.hpp:74-87
+  void spmv_rows(const std::vector<double>& x, std::vector<double>& out)
+  {
+    out.resize(m_);
+    detail::check(bp_lp_spmv_rows(h_, x.data(), out.data()));
+  }
+  // lp.hpp:89-102
+  void spmv_cols(const std::vector<double>& y, std::vector<double>& out)
+  {
+    out.resize(n_);
+    detail::check(bp_lp_spmv_cols(h_, y.data(), out.data()));
+  }
+  // `iters` iterations of lp::solve's inner loop (lp.hpp:315-340) with fixed tau / sigma
+  void pdhg_iterate(std::vector<double>& x, std::vector<double>& y, std::vector<double>& x_bar,
+                    std::vector<double>& x_sum, std::vector<double>& y_sum, double tau, double sigma,
+                    int iters)
+  {
+    detail::check(bp_lp_pdhg_iterate(h_, x.data(), y.data(), x_bar.data(), x_sum.data(),
+                                     y_sum.data(), tau, sigma, iters));
+  }
+
+ private:
+  int n_, m_;
+  bp_lp* h_ = nullptr;
+};
+
+// lp.hpp:74 / :89 one-shot (uploads the instance; keep an LpProducts for repeated products)
+inline void spmv_rows(const LpInstance& s, const std::vector<double>& x, std::vector<double>& out)
+{
+  LpProducts(s).spmv_rows(x, out);
+}
+inline void spmv_cols(const LpInstance& s, const std::vector<double>& y, std::vector<double>& out)
+{
+  LpProducts(s).spmv_cols(y, out);
+}
 
 // ---------------------------------------------------------------- rounding.hpp
 

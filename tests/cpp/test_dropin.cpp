@@ -402,6 +402,29 @@ void builder_stream()
              " mismatches");
 }
 
+void lp_products()
+{
+  int bad = 0, runs = 0;
+  for (uint64_t sd = 0; sd < 3; ++sd) {
+    const ProblemDef p = mixed_instance(700 + sd, sd == 2 ? 40000 : 3000, 2500, sd == 2 ? 2 : 0, 20000);
+    const LpInstance s = LpInstance::relax(p);
+    std::mt19937_64 g(sd);
+    std::normal_distribution<double> N01(0.0, 1.0);
+    std::vector<double> x(s.n_vars), y(s.n_rows), ra(s.n_rows), rc(s.n_vars), ga, gc;
+    for (auto& v : x) v = N01(g);
+    for (auto& v : y) v = N01(g);
+    lpdetail::spmv_rows(s, x, ra);
+    lpdetail::spmv_cols(s, y, rc);
+    pg::LpProducts dev(s);
+    dev.spmv_rows(x, ga);
+    dev.spmv_cols(y, gc);
+    ++runs;
+    if (!same_bits(ra, ga) || !same_bits(rc, gc)) ++bad;
+  }
+  report("lpdetail::spmv_rows / spmv_cols (PDHG products, incl. rows > 16384 entries)", bad == 0,
+         std::to_string(runs) + " instances, " + std::to_string(bad) + " mismatches");
+}
+
 void errors()
 {
   const ProblemDef p = testkit::tiny_knapsack();
@@ -440,6 +463,7 @@ int main()
   if (want("rounding_mixed")) rounding_mixed();
   if (want("repair_stream")) repair_stream();
   if (want("builder_stream")) builder_stream();
+  if (want("lp_products")) lp_products();
   std::printf("%d failure(s)\n", g_failures);
   return g_failures;
 }
