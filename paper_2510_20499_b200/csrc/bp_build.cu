@@ -7,7 +7,8 @@
 //   1. integral tightening of integer-variable bounds, ceil(l - 1e-9) / floor(u + 1e-9)
 //      (problem.hpp:157-163; an integer lower bound in (-1, 0] becomes -0.0, as there), and the
 //      reference's error checks in its order (empty domains, crossed rows, entry indices);
-//   2. (row, col) keys sorted by a stable LSD radix sort (CUB), so duplicates keep insertion order;
+//   2. packed (row, col) keys sorted by a stable LSD radix sort (CUB) over their used bits only, so
+//      duplicates keep insertion order;
 //   3. duplicates coalesced by one thread per (row, col) run, summing left to right from the first
 //      value like the reference's `merged.back() += t` pass, then explicit zeros dropped;
 //   4. CSR offsets by histogram + scan; the CSC by a stable radix sort of the CSR positions on
@@ -55,15 +56,20 @@ __global__ void k_crossed_rows(int m, const double* lo, const double* up, int* f
     if (lo[k] > up[k]) atomicMin(first_bad, k);
 }
 
-// problem.hpp:178-181: first entry (insertion order) with a bad row or col; keys (row << 32 | col).
-__global__ void k_entry_keys(long long N, int n, int m, const int* row, const int* col,
+// problem.hpp:178-181: first entry (insertion order) with a bad row or col; keys
+// (row << cbits | col), cbits = bits of n, so the sort touches only rbits + cbits bits.
+__global__ void k_entry_keys(long long N, int n, int m, int cbits, const int* row, const int* col,
                              unsigned long long* key, unsigned long long* first_bad)
 {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < N;
        e += (long long)gridDim.x * blockDim.x) {
     const int r = row[e], c = col[e];
-    if (r < 0 || r >= m || c < 0 || c >= n) atomicMin(first_bad, (unsigned long long)e);
-    key[e] = ((unsigned long long)(unsigned)r << 32) | (unsigned)c;
+    if (r < 0 || r >= m || c < 0 || c >= n) {
+      atomicMin(first_bad, (unsigned long long)e);
+      key[e] = 0;
+      continue;
+    }
+    key[e] = ((unsigned long long)(unsigned)r << cbits) | (unsigned)c;
   }
 }
 
@@ -92,12 +98,13 @@ __global__ void k_coalesce(long long R, long long N, const long long* start,
 }
 
 // CSR split of the final keys + per-row / per-column counts.
-__global__ void k_split(long long nnz, const unsigned long long* key, int* row, int* col,
+__global__ void k_split(long long nnz, int cbits, const unsigned long long* key, int* row, int* col,
                         unsigned* col_key, int* rcount, int* ccount)
 {
+  const unsigned long long cmask = (1ull << cbits) - 1;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
        e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(key[e] >> 32), c = (int)(key[e] & 0xffffffffu);
+    const int r = (int)(key[e] >> cbits), c = (int)(key[e] & cmask);
     row[e]     = r;
     col[e]     = c;
     col_key[e] = (unsigned)c;
@@ -200,7 +207,13 @@ extern "C" int bp_build_problem(const bp_builder_desc* d, int32_t device, bp_bui
     key2.alloc(std::max(N, 1ll));
     badE.alloc(1);
     BP_CUDA(cudaMemsetAsync(badE.p, 0xff, sizeof(unsigned long long), s));
-    if (N) k_entry_keys<<<nblk(N), 256, 0, s>>>(N, n, m, erow.p, ecol.p, key.p, badE.p);
+    auto bits = [](long long x) {
+      int b = 1;
+      while ((1ll << b) < x) ++b;
+      return b;
+    };
+    const int cbits = bits(std::max(n, 1)), rbits = bits(std::max(m, 1));
+    if (N) k_entry_keys<<<nblk(N), 256, 0, s>>>(N, n, m, cbits, erow.p, ecol.p, key.p, badE.p);
     int hbad[2];
     unsigned long long hbadE = 0;
     BP_CUDA(cudaMemcpyAsync(hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, s));
@@ -214,24 +227,16 @@ extern "C" int bp_build_problem(const bp_builder_desc* d, int32_t device, bp_bui
       const int r = d->entry_row[hbadE];
       throw std::out_of_range(r < 0 || r >= m ? "entry row out of range" : "entry col out of range");
     }
-    // row and col need ceil(log2) bits each: sort only those (LSD radix, stable)
-    auto bits = [](long long x) {
-      int b = 1;
-      while ((1ll << b) < x) ++b;
-      return b;
-    };
-    const int cbits = bits(std::max(n, 1)), rbits = bits(std::max(m, 1));
+    // stable LSD radix sort over the rbits + cbits key bits only
     DBuf<double> val2;
     val2.alloc(std::max(N, 1ll));
     if (N) {
       size_t nb = 0;
-      // keys: row in bits [32, 32 + rbits), col in [0, cbits): sort bits [0, 32 + rbits) but the
-      // gap [cbits, 32) is all zero, so two passes over the used ranges are equivalent to one
-      cub::DeviceRadixSort::SortPairs(nullptr, nb, key.p, key2.p, eval.p, val2.p, (int)N, 0, 32 + rbits, s);
+      cub::DeviceRadixSort::SortPairs(nullptr, nb, key.p, key2.p, eval.p, val2.p, (int)N, 0,
+                                      rbits + cbits, s);
       size_t have = nb;
       cub::DeviceRadixSort::SortPairs(tmp.get(nb), have, key.p, key2.p, eval.p, val2.p, (int)N, 0,
-                                      32 + rbits, s);
-      (void)cbits;
+                                      rbits + cbits, s);
     }
     // 3. coalesce runs of equal keys, drop zeros
     DBuf<unsigned char> head, keep;
@@ -295,7 +300,7 @@ extern "C" int bp_build_problem(const bp_builder_desc* d, int32_t device, bp_bui
     cstart.alloc(n + 1);
     BP_CUDA(cudaMemsetAsync(rcount.p, 0, sizeof(int) * (m + 1), s));
     BP_CUDA(cudaMemsetAsync(ccount.p, 0, sizeof(int) * (n + 1), s));
-    if (nnz) k_split<<<nblk(nnz), 256, 0, s>>>(nnz, fkey.p, row.p, col.p, ckey.p, rcount.p, ccount.p);
+    if (nnz) k_split<<<nblk(nnz), 256, 0, s>>>(nnz, cbits, fkey.p, row.p, col.p, ckey.p, rcount.p, ccount.p);
     {
       size_t nb = 0;
       cub::DeviceScan::ExclusiveSum(nullptr, nb, rcount.p, rstart.p, m + 1, s);

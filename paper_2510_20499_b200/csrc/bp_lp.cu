@@ -158,14 +158,14 @@ struct LpView {
   int n_item = 0;
   DBuf<int> start, idx;
   DBuf<double> val;
-  DBuf<int> short_items, long_items, seg_first;
+  DBuf<int> long_items, seg_first;
   DBuf<int> sl_base, sl_item, sl_idx;
   DBuf<double> sl_val;
   int n_slice = 0;
   DBuf<int2> tasks;
   DBuf<int> task_slot;
   DBuf<double> seg_out;
-  int n_short = 0, n_long = 0, n_task = 0;
+  int n_long = 0, n_task = 0;
 
   void build(int n, const int* h_start, const int* h_idx, const double* h_val)
   {
@@ -217,7 +217,6 @@ struct LpView {
       sl_idx.upload(sidx);
       sl_val.upload(sval);
     }
-    n_short = (int)sh.size();
     n_long  = (int)lg.size();
     n_task  = (int)tk.size();
     // launch order: longest segments first (the sequential sums are the critical path)
@@ -230,7 +229,6 @@ struct LpView {
     std::vector<int2> tks(tk.size());
     for (size_t t = 0; t < tk.size(); ++t) tks[t] = tk[ord[t]];
     task_slot.upload(ord);
-    short_items.upload(sh);
     long_items.upload(lg);
     seg_first.upload(sf);
     tasks.upload(tks);
