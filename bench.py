@@ -367,6 +367,53 @@ def run_lp(args, rank, world, local, p):
     return out
 
 
+def run_build(args, rank, world, local, p):
+    """SURVEY §8f row 3: ProblemBuilder::build (problem.hpp:141-227) of the C2 problem from its
+    entries in shuffled insertion order, on the device (bp_build_problem: bounds, checks, sort,
+    coalesce, CSR + CSC) from host arrays to host arrays, against the reference's own builder on the
+    host (oracle/_ref). Wall time of the C-ABI call (host -> device -> host copies included)."""
+    import ctypes as C
+
+    from paper_2510_20499_b200 import _lib
+    if rank != 0:
+        return None
+    n, m, N = p.n_vars, p.n_cons, p.nnz()
+    rows = np.repeat(np.arange(m, dtype=np.int32), np.diff(p.row_start))
+    perm = np.random.default_rng(11).permutation(N)
+    er, ec, ev = (np.ascontiguousarray(a[perm]) for a in (rows, p.row_col, p.row_val))
+    P = _lib.ptr
+    ins = [np.ascontiguousarray(a) for a in (p.var_lower, p.var_upper, p.is_integer, p.cons_lower, p.cons_upper)]
+    d = _lib.bp_builder_desc(n, m, N, P(er), P(ec), P(ev), *[P(a) for a in ins])
+    outs = [np.zeros(m + 1, np.int32), np.zeros(N, np.int32), np.zeros(N), np.zeros(n + 1, np.int32),
+            np.zeros(N, np.int32), np.zeros(N), np.zeros(n), np.zeros(n)]
+    o = _lib.bp_built(0, *[P(a) for a in outs])
+    L = _lib.lib()
+    times = []
+    for _ in range(4):  # first call warms up (allocations, module load)
+        t0 = time.perf_counter()
+        _lib.check(L.bp_build_problem(C.byref(d), int(local), C.byref(o), None))
+        times.append(time.perf_counter() - t0)
+    assert int(o.nnz) == N and np.array_equal(outs[1], p.row_col) and np.array_equal(outs[4], p.col_row)
+    el = float(np.median(times[1:]))
+    out = {"workload": "ProblemBuilder::build of C2 (1M x 1M, %d entries, shuffled)" % N,
+           "build_ms": el * 1e3, "entries_per_s": N / el,
+           "api": "bp_build_problem (C-ABI, host arrays in and out)",
+           "parity": "bitwise vs the reference builder (tests/test_gpu_build.py, drop-in criterion)"}
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.bind import Ref
+        if Ref.available():
+            Q = lambda a: np.ascontiguousarray(a).ctypes.data_as(C.c_void_p)  # noqa: E731
+            t0 = time.perf_counter()
+            h = Ref.lib().ref_problem_build(n, m, Q(p.var_lower), Q(p.var_upper), Q(p.is_integer), None,
+                                            Q(p.cons_lower), Q(p.cons_upper), N, Q(er), Q(ec), Q(ev))
+            el_cpu = time.perf_counter() - t0
+            Ref.lib().ref_problem_free(h)
+            out["cpu_baseline"] = {"value": N / el_cpu, "unit": "entries/s", "cores": 1,
+                                   "kind": "reference",
+                                   "sample": f"pulse::ProblemBuilder::build of the same entries ({el_cpu:.2f} s)"}
+    return out
+
+
 def run_batch(args, rank, world, local):
     """configs[4]: 64 heterogeneous MIPLIB-shaped instances (10k-5M nnz), LPT-partitioned by size
     over the ranks; each rank uploads its instances and propagates them one after another on its
@@ -471,6 +518,7 @@ def main():
     ap.add_argument("--cpu-sample-sec", type=float, default=20.0)
     ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--no-lp", action="store_true")
+    ap.add_argument("--no-build", action="store_true")
     ap.add_argument("--round-deadline", type=float, default=30.0,
                     help="C4 propagation_round deadline (s), as the reference's Deadline")
     ap.add_argument("--cache-budget", type=float, default=5.0,
@@ -596,6 +644,8 @@ def main():
     log("batch done")
     lp = None if args.no_lp or args.workload != "C2" else run_lp(args, rank, world, local, p)
     log("lp done")
+    build = None if args.no_build or args.workload != "C2" else run_build(args, rank, world, local, p)
+    log("build done")
 
     if rank == 0:
         peak, peak_kind = peaks()
@@ -644,6 +694,7 @@ def main():
             "rounding": rounding,
             "batch": batch,
             "lp": lp,
+            "build": build,
         }
         print(json.dumps(line))
     if world > 1:
