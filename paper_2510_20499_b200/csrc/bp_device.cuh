@@ -368,9 +368,10 @@ struct ChunkInfo {
 #define BP_PACK_TILE 128
 #endif
 constexpr int kPackNnz   = BP_PACK_NNZ;   // full rounds: rows up to this length go to packed tiles
-// Only the validated split is allowed: with BP_PACK_NNZ=16 a C2 propagate ended after 23 rounds
-// instead of the reference's 24 (rows of 17-32 entries in the medium-row path), so the SELL / medium
-// boundary must coincide with the one-lane-per-row boundary of the frontier paths.
+// The full-round task lists assume the SELL / medium boundary is the short-row boundary
+// (problem_build skips rows <= kShortNnz before listing rows > kPackNnz as fold tasks): with
+// BP_PACK_NNZ=16, rows of 17-32 entries were in no list and a C2 propagate ended after 23 rounds
+// instead of 24. Pinned at compile time.
 static_assert(kPackNnz == kShortNnz, "BP_PACK_NNZ must equal kShortNnz (the validated configuration)");
 constexpr int kPackTile  = BP_PACK_TILE;  // packed row tiles: <= 32 rows and <= this many entries
 
