@@ -2114,6 +2114,13 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine, kThreads, sizeof(Smem)));
   if (per_sm < 1) throw cuda_error("engine kernel cannot be resident (occupancy 0)");
   P.grid_blocks = dev_sms * std::min(per_sm, 4);
+  // small problems get a grid sized to their work (>= one block per 8192 nonzeros): cheaper grid
+  // barriers, and independent instances on their own streams can run side by side (a cooperative
+  // grid only launches when all its blocks fit)
+  static const int grid_div = getenv("BP_GRID_NNZ") ? atoi(getenv("BP_GRID_NNZ")) : 8192;
+  if (grid_div > 0)
+    P.grid_blocks = (int)std::max<long long>(std::min<long long>(P.grid_blocks, 16),
+                                             std::min<long long>(P.grid_blocks, (P.nnz + grid_div - 1) / grid_div));
   int per_sm2   = 0;
   BP_CUDA(cudaFuncSetAttribute(k_rows_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)sizeof(Smem)));
