@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -195,6 +196,6 @@ void stage_vars(Problem& P, const int* vars, int nvars, cudaStream_t s);
 // Stage the changed-variable list of a frontier start (ENGINE_START_FRONTIER).
 void stage_changed(Problem& P, const int* vars, int nvars, cudaStream_t s);
 
-extern long long g_kernel_launches;
+extern std::atomic<long long> g_kernel_launches;  // host threads may drive problems concurrently
 
 }  // namespace bp

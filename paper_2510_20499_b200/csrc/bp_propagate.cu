@@ -37,7 +37,7 @@ namespace cg = cooperative_groups;
 
 namespace bp {
 
-long long g_kernel_launches = 0;
+std::atomic<long long> g_kernel_launches{0};
 
 namespace {
 
