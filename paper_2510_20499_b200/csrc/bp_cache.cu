@@ -319,6 +319,8 @@ struct ProbeWs {
   DBuf<unsigned long long> dpc;
   DBuf<unsigned char> dtmp;
   PinBuf h_var, h_lo, h_up, h_st, h_cn, h_qv, h_ql, h_qu, h_root;
+  std::vector<int> tv, tslot;  // task lists, reused across calls (no first-touch page faults)
+  std::vector<double> tlo, tup;
 };
 
 HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vector<int>& vars,
@@ -360,8 +362,14 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   const double t_cert = elapsed();
 
   // tasks: down then up branch of every var with a spec (probing.hpp:228-234)
-  std::vector<int> tv, tslot;
-  std::vector<double> tlo, tup;
+  std::vector<int>& tv    = W.tv;
+  std::vector<int>& tslot = W.tslot;
+  std::vector<double>& tlo = W.tlo;
+  std::vector<double>& tup = W.tup;
+  tv.clear();
+  tslot.clear();
+  tlo.clear();
+  tup.clear();
   tv.reserve(2 * vars.size());
   tslot.reserve(2 * vars.size());
   tlo.reserve(2 * vars.size());
