@@ -27,7 +27,10 @@ namespace bp {
 namespace {
 
 constexpr unsigned FULL  = 0xffffffffu;
-constexpr int PB_WARPS   = 4;     // warps per block
+#ifndef PB_WARPS_V
+#define PB_WARPS_V 4
+#endif
+constexpr int PB_WARPS   = PB_WARPS_V;  // warps per block
 constexpr int PB_BCAP    = 128;   // bounds overlay slots (power of 2)
 constexpr int PB_ACAP    = 128;   // activity overlay slots (power of 2)
 #ifndef PB_RCAP_V
