@@ -69,6 +69,31 @@ __global__ void k_spmv_sell(int nslice, const int* sbase, const int* sitem, cons
   }
 }
 
+// Sequential left-to-right sum of src[0..cnt) onto acc with the next eight shared-memory values
+// loaded while the current eight are added (the chain runs at the DADD latency, not the load's).
+__device__ __forceinline__ double lp_fold_seq(const double* src, int cnt, double acc)
+{
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  int j             = 0;
+  if (cnt >= 8) {
+    double2 v0 = s2[0], v1 = s2[1], v2 = s2[2], v3 = s2[3];
+    for (j = 8; j + 8 <= cnt; j += 8) {
+      const double2 w0 = s2[j / 2], w1 = s2[j / 2 + 1], w2 = s2[j / 2 + 2], w3 = s2[j / 2 + 3];
+      acc = __dadd_rn(acc, v0.x); acc = __dadd_rn(acc, v0.y);
+      acc = __dadd_rn(acc, v1.x); acc = __dadd_rn(acc, v1.y);
+      acc = __dadd_rn(acc, v2.x); acc = __dadd_rn(acc, v2.y);
+      acc = __dadd_rn(acc, v3.x); acc = __dadd_rn(acc, v3.y);
+      v0 = w0; v1 = w1; v2 = w2; v3 = w3;
+    }
+    acc = __dadd_rn(acc, v0.x); acc = __dadd_rn(acc, v0.y);
+    acc = __dadd_rn(acc, v1.x); acc = __dadd_rn(acc, v1.y);
+    acc = __dadd_rn(acc, v2.x); acc = __dadd_rn(acc, v2.y);
+    acc = __dadd_rn(acc, v3.x); acc = __dadd_rn(acc, v3.y);
+  }
+  for (; j < cnt; ++j) acc = __dadd_rn(acc, src[j]);
+  return acc;
+}
+
 // One 16384-entry segment of a long row / column per warp: partial sum into seg_out[task]. The
 // products of chunk j + 1 are loaded into registers while lane 0 runs the sequential sum over
 // chunk j from shared memory, then staged (the loads overlap the DADD chain).
@@ -76,7 +101,7 @@ __global__ void __launch_bounds__(kLpThreads)
     k_spmv_segments(const int* start, const int* idx, const double* val, const double* x,
                     const int2* tasks, const int* slot, int ntask, double* seg_out)
 {
-  __shared__ double buf[kLpThreads / 32][kLpChunk];
+  __shared__ __align__(16) double buf[kLpThreads / 32][kLpChunk];
   constexpr int PL = kLpChunk / 32;  // products per lane per chunk
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = blockIdx.x * (kLpThreads / 32) + wib, nw = gridDim.x * (kLpThreads / 32);
@@ -99,10 +124,7 @@ __global__ void __launch_bounds__(kLpThreads)
       for (int h = 0; h < PL; ++h) buf[wib][h * 32 + lane] = pr[h];
       __syncwarp();
       load(b0 + kLpChunk);  // in flight during the fold below
-      if (lane == 0) {
-        const int n = min(kLpChunk, s1 - b0);
-        for (int q = 0; q < n; ++q) part = __dadd_rn(part, buf[wib][q]);
-      }
+      if (lane == 0) part = lp_fold_seq(buf[wib], min(kLpChunk, s1 - b0), part);
       __syncwarp();
     }
     if (lane == 0) seg_out[slot[t]] = part;
