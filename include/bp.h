@@ -291,7 +291,12 @@ int bp_lp_spmv_cols(bp_lp* lp, const double* y, double* aty);
  * x_bar <- 2 x_new - x, x_sum += x, y_sum += y. All five vectors are read and written back. */
 int bp_lp_pdhg_iterate(bp_lp* lp, double* x, double* y, double* x_bar, double* x_sum, double* y_sum,
                        double tau, double sigma, int32_t iters);
-/* Device time (CUDA events on the LP's stream) of the last spmv / iterate call. */
+/* lpdetail::evaluate_kkt (lp.hpp:134-206) at (x, y): out7 = {primal_res, dual_res, gap,
+ * primal_obj, dual_obj, x_norm, score}. The residual maxima are exact; the objective sums are
+ * compensated (double-double, fixed order) where the reference uses a sequential Neumaier sum, so
+ * primal_obj / dual_obj (and gap / score) agree with it to a few ulps, not bitwise. */
+int bp_lp_evaluate_kkt(bp_lp* lp, const double* x, const double* y, double* out7);
+/* Device time (CUDA events on the LP's stream) of the last spmv / iterate / KKT call. */
 int bp_lp_last_ms(const bp_lp* lp, double* ms);
 
 /* Number of engine kernels launched by this process. */

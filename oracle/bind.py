@@ -86,6 +86,7 @@ class Ref:
                 "ref_repair": (I, [V, V, V, I, I, V, V]),
                 "ref_problem_set_obj": (None, [V, V]),
                 "ref_lp_spmv_rows": (None, [V, V, V]),
+                "ref_lp_evaluate_kkt": (None, [V, V, V, V]),
                 "ref_lp_spmv_cols": (None, [V, V, V]),
                 "ref_lp_pdhg_iterate": (None, [V, V, V, V, V, V, D, D, I]),
                 "ref_parallel_propagate": (None, [V, V, I, V, I, V, V, V, V, V, V, V, V, V, V, V, V]),

@@ -512,6 +512,17 @@ void ref_lp_spmv_cols(const void* pv, const double* y, double* out)
   std::copy(o.begin(), o.end(), out);
 }
 
+// lpdetail::evaluate_kkt (lp.hpp:134) at (x, y): out7 = {primal_res, dual_res, gap, primal_obj,
+// dual_obj, x_norm, score}.
+void ref_lp_evaluate_kkt(const void* pv, const double* x, const double* y, double* out7)
+{
+  const auto s = LpInstance::relax(*static_cast<const ProblemDef*>(pv));
+  std::vector<double> X(x, x + s.n_vars), Y(y, y + s.n_rows), ax(s.n_rows), aty(s.n_vars);
+  const auto k = lpdetail::evaluate_kkt(s, X, Y, ax, aty);
+  const double v[7] = {k.primal_res, k.dual_res, k.gap, k.primal_obj, k.dual_obj, k.x_norm, k.score};
+  std::copy(v, v + 7, out7);
+}
+
 // The inner PDHG iteration of lp::solve (lp.hpp:315-340) restated verbatim around the reference's
 // own lpdetail::spmv_rows / spmv_cols and pulse::clamp, `iters` times with fixed tau / sigma.
 void ref_lp_pdhg_iterate(const void* pv, double* x, double* y, double* x_bar, double* x_sum,

@@ -160,6 +160,7 @@ _SIGS = [
     ("bp_lp_spmv_cols", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("bp_lp_pdhg_iterate", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_double, C.c_double, C.c_int32]),
+    ("bp_lp_evaluate_kkt", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("bp_lp_last_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("bp_kernel_launches", C.c_int64, []),
     ("bp_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),

@@ -16,6 +16,7 @@
 // x_sum += x, y_sum += y -- each vector is read and written once per half-step.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -169,6 +170,112 @@ __global__ void k_pdhg_primal(int n, int m, const double* aty, const double* c, 
   }
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += stride)
     y_sum[k] = __dadd_rn(y_sum[k], y[k]);
+}
+
+// ---- KKT scoring (lp.hpp:134-200) ------------------------------------------------------------
+// The maxima are order-independent (exact); the two objective sums are compensated: each thread
+// and block accumulates a double-double (TwoSum), blocks are combined in a fixed order, so the
+// result is the exact sum rounded once -- the reference's Neumaier sum agrees with it to a few ulps.
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ void dd_add(DD& a, double x)
+{
+  const double s = __dadd_rn(a.hi, x);
+  const double bb = __dsub_rn(s, a.hi);
+  const double err = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, bb)), __dsub_rn(x, bb));
+  a.hi = s;
+  a.lo = __dadd_rn(a.lo, err);
+}
+__device__ __forceinline__ void dd_merge(DD& a, const DD& b)
+{
+  dd_add(a, b.hi);
+  a.lo = __dadd_rn(a.lo, b.lo);
+}
+__device__ __forceinline__ void max_u64(unsigned long long* p, double v)  // v >= +0.0
+{
+  atomicMax(p, (unsigned long long)__double_as_longlong(v));
+}
+
+constexpr int kKktThreads = 256;
+// stats: [0] primal_res, [1] rhs_scale, [2] obj_scale, [3] x_norm, [4] dual_res (u64 bit patterns)
+__global__ void __launch_bounds__(kKktThreads)
+    k_kkt(int n, int m, const double* x, const double* y, const double* ax, const double* aty,
+          const double* obj, const double* rlo, const double* rup, const double* vlo,
+          const double* vup, unsigned long long* stats, DD* part)
+{
+  __shared__ DD sp[kKktThreads], sd[kKktThreads];
+  double pres = 0.0, rsc = 0.0, osc = 0.0, xn = 0.0, dres = 0.0;
+  DD po{0.0, 0.0}, dobj{0.0, 0.0};
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int k = tid; k < m; k += nt) {  // lp.hpp:143-155
+    double v = 0.0;
+    if (isfinite(rup[k])) {
+      const double d = __dsub_rn(ax[k], rup[k]);
+      v              = (v < d) ? d : v;
+      rsc            = fmax(rsc, fabs(rup[k]));
+    }
+    if (isfinite(rlo[k])) {
+      const double d = __dsub_rn(rlo[k], ax[k]);
+      v              = (v < d) ? d : v;
+      rsc            = fmax(rsc, fabs(rlo[k]));
+    }
+    pres = fmax(pres, v);
+    const double yk = y[k];  // lp.hpp:181-196
+    if (yk > 0.0) {
+      if (isfinite(rup[k])) dd_add(dobj, __dmul_rn(-yk, rup[k]));
+      else dres = fmax(dres, yk);
+    } else if (yk < 0.0) {
+      if (isfinite(rlo[k])) dd_add(dobj, __dmul_rn(-yk, rlo[k]));
+      else dres = fmax(dres, -yk);
+    }
+  }
+  for (int i = tid; i < n; i += nt) {  // lp.hpp:157-176
+    dd_add(po, __dmul_rn(obj[i], x[i]));
+    osc = fmax(osc, fabs(obj[i]));
+    xn  = fmax(xn, fabs(x[i]));
+    const double r = __dadd_rn(obj[i], aty[i]);
+    double viol = 0.0, term = 0.0;
+    if (r > 0.0) {
+      if (isfinite(vlo[i])) term = __dmul_rn(r, vlo[i]);
+      else viol = r;
+    } else if (r < 0.0) {
+      if (isfinite(vup[i])) term = __dmul_rn(r, vup[i]);
+      else viol = -r;
+    }
+    dres = fmax(dres, viol);
+    dd_add(dobj, term);
+  }
+  // maxima of non-negative values (+0.0 at least): bit patterns order like the values
+  max_u64(stats + 0, pres);
+  max_u64(stats + 1, rsc);
+  max_u64(stats + 2, osc);
+  max_u64(stats + 3, xn);
+  max_u64(stats + 4, dres);
+  sp[threadIdx.x] = po;
+  sd[threadIdx.x] = dobj;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // fixed-order block combine
+    DD a = sp[0], b = sd[0];
+    for (int t = 1; t < blockDim.x; ++t) {
+      dd_merge(a, sp[t]);
+      dd_merge(b, sd[t]);
+    }
+    part[2 * blockIdx.x]     = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void k_kkt_final(int nblocks, const DD* part, double* sums)
+{
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  DD a = part[0], b = part[1];
+  for (int q = 1; q < nblocks; ++q) {
+    dd_merge(a, part[2 * q]);
+    dd_merge(b, part[2 * q + 1]);
+  }
+  sums[0] = __dadd_rn(a.hi, a.lo);
+  sums[1] = __dadd_rn(b.hi, b.lo);
 }
 
 inline int nblk(long long n) { return (int)std::max(1ll, std::min(148ll * 16, (n + 255) / 256)); }
@@ -438,6 +545,59 @@ int bp_lp_pdhg_iterate(bp_lp* L, double* x, double* y, double* x_bar, double* x_
     down(y, L->y, m);
     down(y_sum, L->ysum, m);
     BP_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    BP_CUDA(cudaEventElapsedTime(&ms, L->e0, L->e1));
+    L->last_ms = ms;
+  });
+}
+
+int bp_lp_evaluate_kkt(bp_lp* L, const double* x, const double* y, double* out7)
+{
+  return lguard([&] {
+    need(L && x && y && out7, "null argument");
+    need(L->obj.p && L->rlo.p && L->rup.p && L->vlo.p && L->vup.p, "KKT needs obj and bounds");
+    BP_CUDA(cudaSetDevice(L->device));
+    const int n = L->n, m = L->m;
+    cudaStream_t s = L->s;
+    if (n) BP_CUDA(cudaMemcpyAsync(L->x.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    if (m) BP_CUDA(cudaMemcpyAsync(L->y.p, y, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+    BP_CUDA(cudaEventRecord(L->e0, s));
+    L->rows.spmv(L->x.p, L->ax.p, s);  // lp.hpp:139-140
+    L->cols.spmv(L->y.p, L->aty.p, s);
+    const int nb = std::max(1, std::min(148 * 4, (std::max(n, m) + bp::kKktThreads - 1) / bp::kKktThreads));
+    bp::DBuf<unsigned long long> st;
+    bp::DBuf<bp::DD> part;
+    bp::DBuf<double> sums;
+    st.alloc(5);
+    part.alloc(2 * nb);
+    sums.alloc(2);
+    BP_CUDA(cudaMemsetAsync(st.p, 0, 5 * sizeof(unsigned long long), s));
+    bp::k_kkt<<<nb, bp::kKktThreads, 0, s>>>(n, m, L->x.p, L->y.p, L->ax.p, L->aty.p, L->obj.p, L->rlo.p,
+                                             L->rup.p, L->vlo.p, L->vup.p, st.p, part.p);
+    bp::k_kkt_final<<<1, 32, 0, s>>>(nb, part.p, sums.p);
+    BP_CUDA(cudaGetLastError());
+    bp::g_kernel_launches += 2;
+    BP_CUDA(cudaEventRecord(L->e1, s));
+    unsigned long long h[5];
+    double sm[2];
+    BP_CUDA(cudaMemcpyAsync(h, st.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaMemcpyAsync(sm, sums.p, sizeof(sm), cudaMemcpyDeviceToHost, s));
+    BP_CUDA(cudaStreamSynchronize(s));
+    double v[5];
+    std::memcpy(v, h, sizeof(v));
+    const double primal_res = v[0], rhs_scale = v[1], obj_scale = v[2], x_norm = v[3], dual_res = v[4];
+    const double pobj = sm[0], dobj = sm[1];
+    // lp.hpp:198-205, on the host in the reference's expression order
+    const double gap = std::abs(pobj - dobj) / (1.0 + std::abs(pobj) + std::abs(dobj));
+    const double pr  = primal_res / (1.0 + rhs_scale);
+    const double dr  = dual_res / (1.0 + obj_scale);
+    out7[0] = primal_res;
+    out7[1] = dual_res;
+    out7[2] = gap;
+    out7[3] = pobj;
+    out7[4] = dobj;
+    out7[5] = x_norm;
+    out7[6] = std::max({pr, dr, gap});
     float ms = 0.f;
     BP_CUDA(cudaEventElapsedTime(&ms, L->e0, L->e1));
     L->last_ms = ms;

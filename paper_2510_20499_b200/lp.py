@@ -83,6 +83,16 @@ class DeviceLp:
                                                  float(sigma), int(iters)))
         return tuple(v)
 
+    def evaluate_kkt(self, x, y) -> dict:
+        """lp.hpp:134-206: residual maxima exact, objectives compensated (a few ulps from the
+        reference's Neumaier sums)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        out = np.zeros(7)
+        _lib.check(_lib.lib().bp_lp_evaluate_kkt(self.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(out)))
+        keys = ("primal_res", "dual_res", "gap", "primal_obj", "dual_obj", "x_norm", "score")
+        return dict(zip(keys, (float(v) for v in out)))
+
     def last_ms(self) -> float:
         ms = C.c_double()
         _lib.check(_lib.lib().bp_lp_last_ms(self.h, C.byref(ms)))

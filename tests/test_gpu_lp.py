@@ -84,3 +84,30 @@ def test_pdhg_iterations_match_reference(oracle_built):
     Ref.lib().ref_lp_pdhg_iterate(rp.h, *[P(a) for a in r], tau, sigma, 37)
     for a, b in zip(g, r):
         assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.parametrize("case", ["c1", "heavy"])
+def test_kkt_matches_reference(oracle_built, case):
+    """lpdetail::evaluate_kkt (lp.hpp:134-206): residual maxima and x_norm bit for bit; the
+    objectives (the reference's sequential Neumaier sums vs a compensated device sum), the gap and
+    the score within 1e-12 relative."""
+    from oracle.bind import Ref, RefProblem
+    p = synth.c1(n=5000, m=4000) if case == "c1" else _heavy_instance()
+    p.obj_coeffs = np.random.default_rng(9).normal(size=p.n_vars)
+    rp = RefProblem.from_def(p)
+    Ref_set_obj(rp, p.obj_coeffs)
+    lp = DeviceLp(LpInstance.relax(p))
+    rng = np.random.default_rng(1)
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    for _ in range(3):
+        x = np.clip(rng.normal(size=p.n_vars) * 3, p.var_lower, p.var_upper)
+        y = rng.normal(size=p.n_cons) * rng.choice([0.0, 1.0], p.n_cons)
+        ref = np.zeros(7)
+        Ref.lib().ref_lp_evaluate_kkt(rp.h, P(x), P(y), P(ref))
+        g = lp.evaluate_kkt(x, y)
+        got = np.array([g[k] for k in ("primal_res", "dual_res", "gap", "primal_obj", "dual_obj",
+                                       "x_norm", "score")])
+        for j in (0, 1, 5):
+            assert bits(got[j:j + 1])[0] == bits(ref[j:j + 1])[0], j
+        for j in (2, 3, 4, 6):
+            assert abs(got[j] - ref[j]) <= 1e-12 * max(1.0, abs(ref[j])), (j, got[j], ref[j])
