@@ -555,6 +555,21 @@ class LpProducts {
     out.resize(n_);
     detail::check(bp_lp_spmv_cols(h_, y.data(), out.data()));
   }
+  // lp.hpp:134-206 (residual maxima exact; objectives a few ulps from the reference's Neumaier sums)
+  lpdetail::KktInfo evaluate_kkt(const std::vector<double>& x, const std::vector<double>& y)
+  {
+    double o[7];
+    detail::check(bp_lp_evaluate_kkt(h_, x.data(), y.data(), o));
+    lpdetail::KktInfo k;
+    k.primal_res = o[0];
+    k.dual_res   = o[1];
+    k.gap        = o[2];
+    k.primal_obj = o[3];
+    k.dual_obj   = o[4];
+    k.x_norm     = o[5];
+    k.score      = o[6];
+    return k;
+  }
   // `iters` iterations of lp::solve's inner loop (lp.hpp:315-340) with fixed tau / sigma
   void pdhg_iterate(std::vector<double>& x, std::vector<double>& y, std::vector<double>& x_bar,
                     std::vector<double>& x_sum, std::vector<double>& y_sum, double tau, double sigma,

@@ -420,8 +420,22 @@ void lp_products()
     dev.spmv_cols(y, gc);
     ++runs;
     if (!same_bits(ra, ga) || !same_bits(rc, gc)) ++bad;
+    // evaluate_kkt: maxima bitwise, objective-based fields within 1e-12 relative
+    LpInstance sk = s;
+    sk.obj.resize(sk.n_vars);
+    for (auto& c : sk.obj) c = N01(g);
+    std::vector<double> xk(sk.n_vars), yk(sk.n_rows), axk(sk.n_rows), atyk(sk.n_vars);
+    for (int i = 0; i < sk.n_vars; ++i) xk[i] = clamp(3 * N01(g), sk.var_lower[i], sk.var_upper[i]);
+    for (auto& v : yk) v = N01(g);
+    const auto kr = lpdetail::evaluate_kkt(sk, xk, yk, axk, atyk);
+    const auto kg = pg::LpProducts(sk).evaluate_kkt(xk, yk);
+    auto near = [](double a, double b) { return std::abs(a - b) <= 1e-12 * std::max(1.0, std::abs(b)); };
+    if (kr.primal_res != kg.primal_res || kr.dual_res != kg.dual_res || kr.x_norm != kg.x_norm ||
+        !near(kg.primal_obj, kr.primal_obj) || !near(kg.dual_obj, kr.dual_obj) ||
+        !near(kg.gap, kr.gap) || !near(kg.score, kr.score))
+      ++bad;
   }
-  report("lpdetail::spmv_rows / spmv_cols (PDHG products, incl. rows > 16384 entries)", bad == 0,
+  report("lpdetail::spmv_rows / spmv_cols / evaluate_kkt (PDHG, incl. rows > 16384 entries)", bad == 0,
          std::to_string(runs) + " instances, " + std::to_string(bad) + " mismatches");
 }
 
