@@ -197,7 +197,7 @@ __device__ __forceinline__ void set_clear(PWarp& w, int lane)
 // Activity of one row of <= PB_LANEROW entries (a single 16384-entry segment) in reference order,
 // four entries' index loads and bound gathers in flight at a time.
 #ifndef PB_U_V
-#define PB_U_V 4
+#define PB_U_V 3
 #endif
 constexpr int PB_U = PB_U_V;
 __device__ void row_act_lane(PCtx& c, int k, double& smn, int& imn, double& smx, int& imx)
