@@ -30,7 +30,14 @@ namespace {
 
 constexpr int kLpLane    = 64;      // rows / columns up to this length: one thread each
 constexpr int kLpSeg     = 16384;   // problem.hpp:274 kSumSegment
-constexpr int kLpChunk   = 256;     // products staged per warp step
+#ifndef LP_CHUNK
+#define LP_CHUNK 512
+#endif
+#ifndef LP_SELL_U
+#define LP_SELL_U 4
+#endif
+constexpr int kLpChunk   = LP_CHUNK;  // products staged per warp step
+constexpr int kLpSellU   = LP_SELL_U; // SELL entries in flight per lane
 constexpr int kLpThreads = 256;
 
 __device__ __forceinline__ double lp_clamp(double v, double lo, double hi)
@@ -52,18 +59,18 @@ __global__ void k_spmv_sell(int nslice, const int* sbase, const int* sitem, cons
     const int* ip    = sidx + b0 + lane;
     const double* vp = sval + b0 + lane;
     double part = 0.0;
-    for (int j = 0; j < Lm; j += 4) {
-      int c[4];
-      double a[4], xv[4];
+    for (int j = 0; j < Lm; j += kLpSellU) {
+      int c[kLpSellU];
+      double a[kLpSellU], xv[kLpSellU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kLpSellU; ++u) {
         c[u] = j + u < Lm ? __ldg(ip + 32 * (j + u)) : -1;
         a[u] = j + u < Lm ? __ldg(vp + 32 * (j + u)) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : 0.0;
+      for (int u = 0; u < kLpSellU; ++u) xv[u] = c[u] >= 0 ? x[c[u]] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kLpSellU; ++u)
         if (c[u] >= 0) part = __dadd_rn(part, __dmul_rn(a[u], xv[u]));  // padding follows the row
     }
     if (it >= 0) out[it] = __dadd_rn(0.0, part);
