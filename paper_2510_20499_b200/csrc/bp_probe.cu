@@ -46,7 +46,10 @@ constexpr int PB_VCAP    = PB_VCAP_V;   // dirty vars per round
 #endif
 constexpr int PB_SCAP    = PB_SCAP_V;  // dedup hash set (power of 2)
 constexpr int PB_CCAP    = 128;   // changed vars per round
-constexpr int PB_LANEROW = 64;    // rows / columns up to this length are handled by one lane
+#ifndef PB_LANEROW_V
+#define PB_LANEROW_V 64
+#endif
+constexpr int PB_LANEROW = PB_LANEROW_V;  // rows / columns up to this length are handled by one lane
 constexpr int PB_LONGROW = 4096;  // a dirty row longer than this sends the branch to the engine
 
 struct PWarp {
