@@ -192,7 +192,8 @@ int bp_cache_pack_size(const bp_cache* c, int64_t* bytes);
 int bp_cache_pack(const bp_cache* c, void* buf, int64_t bytes);
 int bp_cache_merge_packed(bp_cache* dst, const void* buf, int64_t bytes);
 /* pulse::assemble_bulk_warm_start (probing.hpp:292-352): merged bounds (2n), conflicts as
- * (kept, evicted) pairs (capacity 2 * n), evicted vars (capacity n). */
+ * (kept, evicted) pairs (capacity 2 * nvars ints: each assignment adds at most one pair, repeated
+ * variables included), evicted vars (capacity nvars). */
 int bp_assemble_bulk_warm_start(const bp_cache* c, const int32_t* vars, const double* vals,
                                 int32_t n, double* bounds2n, int32_t* conflicts,
                                 int32_t* n_conflicts, int32_t* evicted, int32_t* n_evicted);

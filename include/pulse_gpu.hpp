@@ -407,7 +407,10 @@ inline BulkWarmStart assemble_bulk_warm_start(const ProbingCache& cache,
     vals.push_back(x);
   }
   std::vector<double> raw(2 * (size_t)n);
-  std::vector<int32_t> conf(2 * (size_t)n + 2), ev((size_t)n + 1);
+  // capacities per bp.h: one conflict pair and at most one eviction per assignment
+  (void)n;
+  const size_t na = std::max<size_t>(assignments.size(), 1);
+  std::vector<int32_t> conf(2 * na), ev(na);
   int32_t nconf = 0, nev = 0;
   detail::check(bp_assemble_bulk_warm_start(c.get(), vars.data(), vals.data(), (int32_t)vars.size(),
                                             raw.data(), conf.data(), &nconf, ev.data(), &nev));
@@ -546,18 +549,25 @@ class LpProducts {
   // lp.hpp:74-87
   void spmv_rows(const std::vector<double>& x, std::vector<double>& out)
   {
+    if ((int)x.size() != n_) throw std::invalid_argument("spmv_rows: x has the wrong size");
     out.resize(m_);
     detail::check(bp_lp_spmv_rows(h_, x.data(), out.data()));
   }
   // lp.hpp:89-102
   void spmv_cols(const std::vector<double>& y, std::vector<double>& out)
   {
+    if ((int)y.size() != m_) throw std::invalid_argument("spmv_cols: y has the wrong size");
     out.resize(n_);
     detail::check(bp_lp_spmv_cols(h_, y.data(), out.data()));
   }
-  // lp.hpp:134-206 (residual maxima exact; objectives a few ulps from the reference's Neumaier sums)
+  // lp.hpp:134-206. NOT bit-identical: the residual maxima are exact, but primal_obj / dual_obj
+  // (and so gap and score) are compensated parallel sums, a few ulps from the reference's
+  // sequential Neumaier sums; ax / aty are not returned. Callers that need the reference's exact
+  // solve trajectory keep lpdetail::evaluate_kkt.
   lpdetail::KktInfo evaluate_kkt(const std::vector<double>& x, const std::vector<double>& y)
   {
+    if ((int)x.size() != n_ || (int)y.size() != m_)
+      throw std::invalid_argument("evaluate_kkt: x / y have the wrong size");
     double o[7];
     detail::check(bp_lp_evaluate_kkt(h_, x.data(), y.data(), o));
     lpdetail::KktInfo k;
@@ -575,6 +585,10 @@ class LpProducts {
                     std::vector<double>& x_sum, std::vector<double>& y_sum, double tau, double sigma,
                     int iters)
   {
+    for (const auto* v : {&x, &x_bar, &x_sum})
+      if ((int)v->size() != n_) throw std::invalid_argument("pdhg_iterate: primal vector size");
+    for (const auto* v : {&y, &y_sum})
+      if ((int)v->size() != m_) throw std::invalid_argument("pdhg_iterate: dual vector size");
     detail::check(bp_lp_pdhg_iterate(h_, x.data(), y.data(), x_bar.data(), x_sum.data(),
                                      y_sum.data(), tau, sigma, iters));
   }

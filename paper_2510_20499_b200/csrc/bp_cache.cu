@@ -1274,6 +1274,10 @@ int bp_cache_merge_packed(bp_cache* dst, const void* buf, int64_t bytes)
     int64_t hdr[4];
     get(hdr, sizeof(hdr));
     const int64_t ne = hdr[0], nd = hdr[1];
+    // the slice arrives from another rank: validate its header against the buffer before reading
+    need(ne >= 0 && nd >= 0 && ne <= (bytes - 32) / 60 && nd <= (bytes - 32) / 20 &&
+             bytes >= 32 + ne * 60 + nd * 20,
+         "packed cache slice: header does not match the buffer size");
     struct E {
       int var, kind;
       uint8_t feas[2], force[2];
@@ -1288,6 +1292,15 @@ int bp_cache_merge_packed(bp_cache* dst, const void* buf, int64_t bytes)
       get(e.force, 2);
       get(e.br, 32);
       get(e.cnt, 16);
+    }
+    {
+      int64_t tot = 0;
+      for (const auto& e : es) {
+        need(e.cnt[0] >= 0 && e.cnt[1] >= 0 && e.cnt[0] <= nd && e.cnt[1] <= nd,
+             "packed cache slice: negative or oversized delta count");
+        tot += e.cnt[0] + e.cnt[1];
+      }
+      need(tot == nd, "packed cache slice: delta counts do not sum to the delta total");
     }
     std::vector<int> dv(nd);
     std::vector<double> dl(nd), du(nd);

@@ -347,6 +347,7 @@ struct DevProblem {
   int n_mcol;
   const int* mcol;
   const unsigned long long* reach;  // per var: frontier work a change causes (light, heavy rows)
+  const int* col_mark;              // per CSC entry: row task holding it (see problem_build)
   unsigned long long h_reach;       // Σ over heavy rows of their reach (caps the heavy parts)
 };
 

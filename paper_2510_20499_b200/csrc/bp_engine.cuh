@@ -74,9 +74,14 @@ struct Ctl {
   // hand-off of a full round's row phase to k_rows_full (engine state kept across launches)
   int need_full;              // the engine exited to have round `rounds` run its F2 externally
   unsigned stamp_base;        // stamp base of the running propagate (for the hand-off launches)
+  // Dirty-filtered full rounds: 0 = the handed-over round is a true full round;
+  // otherwise only rows with row_stamp == df_stamp (rows of the vars changed last round) are
+  // recomputed and publish candidates, the candidate slots of unchanged vars persisting.
+  unsigned df_stamp;
+  int df_cnt[3];  // dirty lists of a dirty-filtered round: slices, medium-row groups, heavy pieces
   int pad1;
   unsigned long long t0;      // globaltimer at the start of the propagate (time limit, stats)
-  int pad[4];
+  int pad[2];
 };
 
 // Mutable per-problem workspace (one propagate at a time per problem; calls serialized).
@@ -86,10 +91,22 @@ struct DevState {
   double2* aux;
   double2* gbuf;      // gathered bounds of long rows' entries (DevProblem::long_off)
   CandSlot* slot;     // fused full round: per-var candidate slots
+  // Candidate-slot state, kept across calls (outside Ctl, which callers zero per call): 0 = all
+  // empty, 1 = valid for the current bounds (left by a full or dirty-filtered round's finalize:
+  // every unchanged var's slot holds its exact fold), 2 = stale (cleared before the next true full
+  // round).
+  int* slot_state;
   unsigned* ready;    // per row: stamp of the round whose activity is published
   unsigned char* rquiet;  // per row: 1 if no entry can publish a candidate (set before `ready`)
   ChunkInfo* cinfo;       // heavy rows: per 128-entry chunk of gbuf
   unsigned* pstamp;       // per heavy-row piece: stamp of the round whose contributions are in gbuf
+  unsigned* piece_dirty;  // per heavy-row piece: stamp of the dirty-filtered round that recomputes it
+  double2* ckpt;          // per heavy-row piece: (min, max) running sums of its segment before it
+  unsigned* task_stamp;   // per SELL slice / medium-row group: stamp of the dirty-filtered round
+  int n_task;             // SELL slices + medium-row groups
+  int* df_slice;          // dirty lists (phase_df_lists)
+  int* df_group;
+  int* df_piece;
   SegPart* seg_part;
   int* seg_done;
   unsigned* row_stamp;
@@ -126,7 +143,12 @@ struct Problem {
   DBuf<uint8_t> sr_own;
   DBuf<int> long_off, hpiece;
   DBuf<ChunkInfo> cinfo;
-  DBuf<unsigned> pstamp;
+  DBuf<unsigned> pstamp, piece_dirty;
+  DBuf<double2> ckpt;
+  DBuf<int> col_mark;
+  DBuf<unsigned> task_stamp;
+  DBuf<int> df_lists;
+  int n_task = 0;
   DBuf<int2> piece_task, fold_task, cpiece_task;
   DBuf<int> scol, sc_ptr, sc_row, sc_tile;
   DBuf<double> sc_val;
@@ -144,6 +166,7 @@ struct Problem {
   DBuf<double2> aux;
   DBuf<double2> gbuf;
   DBuf<CandSlot> slot;
+  DBuf<int> slot_state;
   DBuf<unsigned> ready;
   DBuf<unsigned char> rquiet;
   DBuf<SegPart> seg_part;

@@ -517,7 +517,8 @@ int bp_lp_pdhg_iterate(bp_lp* L, double* x, double* y, double* x_bar, double* x_
   return lguard([&] {
     need(L && x && y && x_bar && x_sum && y_sum, "null argument");
     need(iters >= 0, "negative iteration count");
-    need(L->obj.p && L->rlo.p && L->rup.p && L->vlo.p && L->vup.p,
+    // empty dimensions upload nothing (null device arrays): only non-empty ones must be present
+    need((L->n == 0 || (L->obj.p && L->vlo.p && L->vup.p)) && (L->m == 0 || (L->rlo.p && L->rup.p)),
          "PDHG needs obj and row / variable bounds");
     BP_CUDA(cudaSetDevice(L->device));
     const int n = L->n, m = L->m;
@@ -562,7 +563,8 @@ int bp_lp_evaluate_kkt(bp_lp* L, const double* x, const double* y, double* out7)
 {
   return lguard([&] {
     need(L && x && y && out7, "null argument");
-    need(L->obj.p && L->rlo.p && L->rup.p && L->vlo.p && L->vup.p, "KKT needs obj and bounds");
+    need((L->n == 0 || (L->obj.p && L->vlo.p && L->vup.p)) && (L->m == 0 || (L->rlo.p && L->rup.p)),
+         "KKT needs obj and bounds");
     BP_CUDA(cudaSetDevice(L->device));
     const int n = L->n, m = L->m;
     cudaStream_t s = L->s;

@@ -602,12 +602,9 @@ __global__ void __launch_bounds__(PB_WARPS * 32)
 
 void probe_launch(Problem& Pr, const ProbeRoot& R, ProbeBatch& B, const Limits& lim, cudaStream_t s)
 {
-  static bool attr = false;
-  if (!attr) {
-    BP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(PSmem)));
-    attr = true;
-  }
+  // the attribute is per device (problems may live on several GPUs): set it on every launch's
+  // device, next to the occupancy query (a cheap driver call)
+  BP_CUDA(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PSmem)));
   int dev_sms = 0, per_sm = 0;
   BP_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, Pr.device));
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_probe, PB_WARPS * 32, sizeof(PSmem)));

@@ -166,25 +166,40 @@ __device__ __forceinline__ int warp_fetch(Ctx& c, int* cursor, int step)
   return __shfl_sync(FULL, t, 0);
 }
 
-// Dynamic work cursor with the next fetch in flight while the current task runs.
+// Work cursor over `lim` items in chunks of `step`. When the whole range fits one chunk per warp
+// of the grid, warps take chunks statically (no atomics: an empty or small list costs nothing);
+// otherwise a grid-wide atomic cursor with the next fetch in flight while the current chunk runs
+// (and no fetch past the end).
 struct Prefetch {
   Ctx& c;
   int* cur;
-  int step, t, nx;
-  __device__ Prefetch(Ctx& c_, int* cur_, int step_) : c(c_), cur(cur_), step(step_)
+  int step, t, nx, lim;
+  bool stat;
+  __device__ Prefetch(Ctx& c_, int* cur_, int step_, int lim_ = 0x3FFFFFFF)
+      : c(c_), cur(cur_), step(step_), lim(lim_)
   {
-    t = warp_fetch(c, cur, step);
-    issue();
+    const int nw = gridDim.x * kWarps;
+    stat         = lim <= 0 || (long long)lim <= (long long)step * nw;
+    if (stat) {
+      t = lim <= 0 ? 0x3FFFFFFF : (blockIdx.x * kWarps + c.warp) * step;
+    } else {
+      t = warp_fetch(c, cur, step);
+      issue();
+    }
   }
   __device__ __forceinline__ void issue()
   {
-    nx = 0;
-    if (c.lane == 0) nx = atomicAdd(cur, step);
+    nx = 0x3FFFFFFF;
+    if (c.lane == 0 && t < lim) nx = atomicAdd(cur, step);
   }
   __device__ __forceinline__ void advance()
   {
-    t = __shfl_sync(FULL, nx, 0);
-    issue();
+    if (stat) {
+      t = 0x3FFFFFFF;
+    } else {
+      t = __shfl_sync(FULL, nx, 0);
+      issue();
+    }
   }
 };
 
@@ -202,6 +217,20 @@ __device__ __forceinline__ int list_tile_setup(Ctx& c, int first, int len, int& 
 
 // ------------------------------------------------------------------ candidate publication
 
+// Records a zero candidate of row k in a slot's zero-tie word: the smallest row wins (the first CSC
+// position, i.e. the reference's fold keeps it), and a row replaces its own earlier record -- with
+// persistent slots (dirty-filtered rounds) a dirty row republishes, and its zero may change sign.
+__device__ __forceinline__ void publish_zero(unsigned* z, int k, bool neg)
+{
+  const unsigned nv = ((unsigned)k << 1) | (neg ? 1u : 0u);
+  unsigned cur      = *(volatile unsigned*)z;
+  while (cur != nv && (cur >> 1) >= (unsigned)k) {  // kZeroEmpty >> 1 exceeds every row id
+    const unsigned prev = atomicCAS(z, cur, nv);
+    if (prev == cur) break;
+    cur = prev;
+  }
+}
+
 // Publishes the candidates of one (row k, variable) entry that strictly improve the round-start
 // bounds (lo, up) into the variable's slot.
 __device__ __forceinline__ void publish(CandSlot* s, double cl, double cu, double lo, double up,
@@ -209,12 +238,19 @@ __device__ __forceinline__ void publish(CandSlot* s, double cl, double cu, doubl
 {
   if (cu < up) {
     atomicMin(&s->up_key, okey(cu == 0.0 ? 0.0 : cu));
-    if (cu == 0.0) atomicMin(&s->up_zero, ((unsigned)k << 1) | (signbit(cu) ? 1u : 0u));
+    if (cu == 0.0) publish_zero(&s->up_zero, k, signbit(cu));
   }
   if (lo < cl) {
     atomicMax(&s->lo_key, okey(cl == 0.0 ? 0.0 : cl));
-    if (cl == 0.0) atomicMin(&s->lo_zero, ((unsigned)k << 1) | (signbit(cl) ? 1u : 0u));
+    if (cl == 0.0) publish_zero(&s->lo_zero, k, signbit(cl));
   }
+}
+
+// Dirty filter of a full round's row tasks: ds = 0 (true full round) or the stamp the previous
+// round's finalize wrote into row_stamp for the rows of its changed vars.
+__device__ __forceinline__ bool row_live(const DevState& S, int k, unsigned ds)
+{
+  return ds == 0 || __ldcg(S.row_stamp + k) == ds;
 }
 
 // ------------------------------------------------------------------ row activities
@@ -461,6 +497,8 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   const int2 tk       = P.piece_task[pi];
+  // (dirty-filtered rounds call only the pieces holding a variable changed last round: the others'
+  // contributions, chunk aggregates and checkpoints are current)
   const int k = tk.x, rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
   const int off = __ldg(P.long_off + k);
   const int e0 = tk.y * kPiece, e1 = min(L, e0 + kPiece);
@@ -515,7 +553,7 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
 // F2b (heavy rows): one 16384-entry segment. Waits for the segment's pieces, then streams their
 // contributions from gbuf (two chunks in flight) while lanes 0/1 run the sequential sums over
 // the order-preserving compaction of the non-zero contributions.
-__device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
+__device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
@@ -523,22 +561,41 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   const int L   = __ldg(P.row_start + k + 1) - __ldg(P.row_start + k);
   const int off = __ldg(P.long_off + k);
   const int e0 = seg * kSumSegment, e1 = min(L, e0 + kSumSegment);
-  {
-    const int p0 = __ldg(P.hpiece + k) + e0 / kPiece, np = (e1 - e0 + kPiece - 1) / kPiece;
-    if (lane < np)
-      while (ldv(S.pstamp + p0 + lane) != stamp) __nanosleep(100);
-    __syncwarp();
-    __threadfence();
+  const int p0 = __ldg(P.hpiece + k) + e0 / kPiece, np = (e1 - e0 + kPiece - 1) / kPiece;
+  // dirty-filtered round: the segment's sum is replayed from the checkpoint of its first recomputed
+  // piece (the prefix before it is unchanged); a segment without one keeps its partial
+  const bool mine = lane < np && (ds == 0 || __ldcg(S.piece_dirty + p0 + lane) == ds);
+  const unsigned dm = __ballot_sync(FULL, mine);
+  if (dm == 0) {
+    double smn = 0.0, smx = 0.0, gtw = 0.0, gpm = 0.0;
+    int imn = 0, imx = 0;
+    if (lane == 0) {
+      const SegPart* sq = S.seg_part + __ldg(P.seg_base + k) + seg;
+      smn = __ldcg(&sq->min);
+      smx = __ldcg(&sq->max);
+      imn = __ldcg(&sq->nmin);
+      imx = __ldcg(&sq->nmax);
+      gtw = __ldcg(&sq->tmax);
+      gpm = __ldcg(&sq->pmax);
+    }
+    fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
+    return;
   }
+  if (mine)
+    while (ldv(S.pstamp + p0 + lane) != stamp) __nanosleep(100);
+  __syncwarp();
+  __threadfence();
+  const int es              = e0 + (__ffs(dm) - 1) * kPiece;  // first recomputed piece
   const long long c_stream = S.dbg ? clock64() : 0;
   const double2* gb         = S.gbuf + off;
   double2 v[kEPL], w[kEPL];
 #pragma unroll
   for (int h = 0; h < kEPL; ++h) {
-    v[h] = __ldcg(gb + e0 + h * 32 + lane);
-    w[h] = e0 + kTile < e1 ? __ldcg(gb + e0 + kTile + h * 32 + lane) : make_double2(0.0, 0.0);
+    v[h] = __ldcg(gb + es + h * 32 + lane);
+    w[h] = es + kTile < e1 ? __ldcg(gb + es + kTile + h * 32 + lane) : make_double2(0.0, 0.0);
   }
   double acc = 0.0, gtw = 0.0, gpm = 0.0;
+  if (es > e0 && lane < 2) acc = __ldcg(reinterpret_cast<const double*>(S.ckpt + p0 + (es - e0) / kPiece) + lane);
   int imn = 0, imx = 0;
   const unsigned lt = lanemask_lt();
   // chunk aggregates of the segment: lanes read them strided (off the fold's critical path)
@@ -549,7 +606,9 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
     gtw = fmax(gtw, __ldcg(&ch->gtw));
     gpm = fmax(gpm, __ldcg(&ch->gpm));
   }
-  for (int base = e0; base < e1; base += kTile) {
+  for (int base = es; base < e1; base += kTile) {
+    if (lane < 2 && ((base - e0) & (kPiece - 1)) == 0)  // checkpoint: the sums before this piece
+      reinterpret_cast<double*>(S.ckpt + p0 + (base - e0) / kPiece)[lane] = acc;
     int pm = 0, px = 0;
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
@@ -595,10 +654,10 @@ __device__ void group_fold(Ctx& c, int t0, int nt, bool cand)
   const DevState& S   = c.S;
   const int lane = c.lane, g = lane >> 3, gl = lane & 7;
   const unsigned gmask = 0xFFu << (8 * g);
-  const bool act       = g < nt;
-  int k = -1, rs = 0, L = 0;
+  const int k          = g < nt ? __ldg(&P.fold_task[t0 + g].x) : -1;
+  const bool act       = k >= 0;
+  int rs = 0, L = 0;
   if (act) {
-    k  = __ldg(&P.fold_task[t0 + g].x);
     rs = __ldg(P.row_start + k);
     L  = __ldg(P.row_start + k + 1) - rs;
   }
@@ -702,10 +761,11 @@ __device__ void group_fold(Ctx& c, int t0, int nt, bool cand)
 }
 
 // F2 tail: candidate piece p of a row with > kCandSplit entries, once its activity is published.
-__device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp)
+__device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
+  if (!row_live(S, k, ds)) return;  // clean row: no activity published this round
   if (c.lane == 0)
     while (ldv(S.ready + k) != stamp) __nanosleep(200);
   __syncwarp();
@@ -738,9 +798,11 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
+  // (dirty-filtered rounds select whole slices: recomputing a clean row is exact and republishes
+  // candidates its variables' persistent slots already hold)
+  const int k = __ldg(P.srow + 32 * sl + c.lane);
   const int b0 = __ldg(P.sr_tile + sl), b1 = __ldg(P.sr_tile + sl + 1);
   const int Lm = (b1 - b0) >> 5;
-  const int k  = __ldg(P.srow + 32 * sl + c.lane);
   const int* ciq   = P.sr_ci + b0 + c.lane;
   const double* aq = P.sr_val + b0 + c.lane;
   double smn = 0.0, smx = 0.0, gtw = 0.0, gpm = 0.0;
@@ -752,8 +814,8 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand)
     double2 bd[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ci[u] = j + u < Lm ? __ldg(ciq + 32 * (j + u)) : -1;
-      a[u]  = j + u < Lm ? __ldg(aq + 32 * (j + u)) : 0.0;
+      ci[u] = k >= 0 && j + u < Lm ? __ldg(ciq + 32 * (j + u)) : -1;
+      a[u]  = k >= 0 && j + u < Lm ? __ldg(aq + 32 * (j + u)) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) bd[u] = ci[u] != -1 ? S.bounds[ci[u] & ~kIntBit] : make_double2(0.0, 0.0);
@@ -881,17 +943,23 @@ __device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
 
 // SELL slices of a full round, longest first: slices of rows > 32 entries one per fetch, the rest
 // four per fetch (one cursor shared by the whole grid is the contended resource).
-__device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand)
+__device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   const int ns = P.n_srtile, nsl = P.n_srow_long;
-  for (Prefetch it_t(c, &pc->cur_s, 1); it_t.t < nsl; it_t.advance()) {
+  if (ds != 0) {  // dirty-filtered round: the engine's list of dirty slices, 4 per fetch
+    const int nd = ldv(&S.ctl->df_cnt[0]);
+    for (Prefetch it_t(c, &pc->cur_a, 4, nd); it_t.t < nd; it_t.advance())
+      for (int q = it_t.t; q < min(nd, it_t.t + 4); ++q) sell_slice(c, __ldcg(S.df_slice + q), cand);
+    return;
+  }
+  for (Prefetch it_t(c, &pc->cur_s, 1, nsl); it_t.t < nsl; it_t.advance()) {
     const long long c0 = S.dbg ? clock64() : 0;
     sell_slice(c, it_t.t, cand);
     dbg_task(c, 1, c0);
   }
-  for (Prefetch it_t(c, &pc->cur_a, 4); nsl + it_t.t < ns; it_t.advance()) {
+  for (Prefetch it_t(c, &pc->cur_a, 4, ns - nsl); nsl + it_t.t < ns; it_t.advance()) {
     const long long c0 = S.dbg ? clock64() : 0;
     for (int q = nsl + it_t.t; q < min(ns, nsl + it_t.t + 4); ++q) sell_slice(c, q, cand);
     dbg_task(c, 1, c0);
@@ -902,7 +970,7 @@ __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand)
 // pieces_here = false: the candidate pieces of rows above kCandSplit are left to a following
 // k_cand_pieces launch (no warp spins on an unfinished row's activity).
 __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, unsigned stamp,
-                           bool pieces_here = true, bool sell_here = true)
+                           bool pieces_here = true, bool sell_here = true, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
@@ -914,39 +982,52 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     // above kCandSplit (they wait for their row's fold, all of which have been fetched by then)
     // heavy rows' contribution pieces first: the segment folds that wait for them are fetched
     // only after every piece has been fetched by a running warp (no deadlock)
-    for (Prefetch it_t(c, &pc->cur_p, 1); it_t.t < P.n_piece; it_t.advance()) heavy_piece(c, it_t.t, stamp);
+    if (ds == 0) {
+      for (Prefetch it_t(c, &pc->cur_p, 1, P.n_piece); it_t.t < P.n_piece; it_t.advance()) heavy_piece(c, it_t.t, stamp);
+    } else {  // dirty-filtered round: the engine's list of dirty pieces
+      const int nd = ldv(&S.ctl->df_cnt[2]);
+      for (Prefetch it_t(c, &pc->cur_p, 1, nd); it_t.t < nd; it_t.advance()) heavy_piece(c, __ldcg(S.df_piece + it_t.t), stamp);
+    }
     const int nfh = P.n_fold_heavy;
-    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nfh; it_t.advance()) {
+    for (Prefetch it_t(c, &pc->cur_b, 1, nfh); it_t.t < nfh; it_t.advance()) {
       const long long c0 = S.dbg ? clock64() : 0;
       const int2 tk      = folds[it_t.t];
-      heavy_fold(c, tk.x, tk.y, cand, stamp);
+      if (row_live(S, tk.x, ds)) heavy_fold(c, tk.x, tk.y, cand, stamp, ds);
       dbg_task(c, 0, c0);
     }
-    for (Prefetch it_t(c, &pc->cur_g, 4); nfh + it_t.t < nf; it_t.advance()) {
-      const long long c0 = S.dbg ? clock64() : 0;
-      group_fold(c, nfh + it_t.t, min(4, nf - nfh - it_t.t), cand);
-      dbg_task(c, 4, c0);
+    if (ds == 0) {
+      for (Prefetch it_t(c, &pc->cur_g, 4, nf - nfh); nfh + it_t.t < nf; it_t.advance()) {
+        const long long c0 = S.dbg ? clock64() : 0;
+        group_fold(c, nfh + it_t.t, min(4, nf - nfh - it_t.t), cand);
+        dbg_task(c, 4, c0);
+      }
+    } else {  // dirty-filtered round: the engine's list of dirty groups of four medium rows
+      const int nd = ldv(&S.ctl->df_cnt[1]);
+      for (Prefetch it_t(c, &pc->cur_g, 1, nd); it_t.t < nd; it_t.advance()) {
+        const int t0 = 4 * __ldcg(S.df_group + it_t.t);
+        group_fold(c, nfh + t0, min(4, nf - nfh - t0), cand);
+      }
     }
-    if (sell_here) phase_sell(c, pc, cand);
+    if (sell_here) phase_sell(c, pc, cand, ds);
     const int nc = cand && pieces_here ? P.n_cpiece : 0;
-    for (Prefetch it_t(c, &pc->cur_c, 1); it_t.t < nc; it_t.advance()) {
+    for (Prefetch it_t(c, &pc->cur_c, 1, nc); it_t.t < nc; it_t.advance()) {
       const long long c0 = S.dbg ? clock64() : 0;
       const int2 tk      = P.cpiece_task[it_t.t];
-      long_cand_piece(c, tk.x, tk.y, stamp);
+      long_cand_piece(c, tk.x, tk.y, stamp, ds);
       dbg_task(c, 2, c0);
     }
   } else {
     // dirty heavy rows: contribution pieces first (the folds waiting for them are fetched after)
     const int ndp = ldv(&pc->n_dpiece);
-    for (Prefetch it_t(c, &pc->cur_p, 1); it_t.t < ndp; it_t.advance())
+    for (Prefetch it_t(c, &pc->cur_p, 1, ndp); it_t.t < ndp; it_t.advance())
       heavy_piece(c, S.dpiece[par][it_t.t].x, stamp);
-    for (Prefetch it_t(c, &pc->cur_b, 1); it_t.t < nf; it_t.advance()) {
+    for (Prefetch it_t(c, &pc->cur_b, 1, nf); it_t.t < nf; it_t.advance()) {
       const int2 tk = folds[it_t.t];
       if (__ldg(P.long_off + tk.x) >= 0) heavy_fold(c, tk.x, tk.y, false, stamp);
       else long_fold(c, tk.x, tk.y, false, stamp);
     }
     const int n = ldv(&pc->n_drow_s);
-    for (Prefetch it_t(c, &pc->cur_c, 32); it_t.t < n; it_t.advance())
+    for (Prefetch it_t(c, &pc->cur_c, 32, n); it_t.t < n; it_t.advance())
       short_list_tile(c, S.drow_s[par], it_t.t, n);
   }
 }
@@ -1048,15 +1129,16 @@ __device__ void phase_finalize(Ctx& c, ParCtl* pc)
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   Tally t{0, 0, 0ull, 0ull, 0ull, 0};
-  for (Prefetch it_q(c, &pc->cur_vs, 32); it_q.t < P.n; it_q.advance()) {
-    const int q = it_q.t;
+  // uniform per-variable work: a static grid-stride sweep (no shared work cursor)
+  const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
+  for (int q = 32 * gw; q < P.n; q += 32 * nw) {
     const int i = q + c.lane;
     int res     = 0;
     if (i < P.n) {
       CandSlot* s                 = S.slot + i;
       const unsigned long long uk = s->up_key, lk = s->lo_key;
       if (uk != kUpEmpty || lk != kLoEmpty) {
-        const double2 b = S.bounds[i];
+        const double2 b = __ldcg(S.bounds + i);
         double nl = b.x, nu = b.y;
         if (uk != kUpEmpty) {
           nu = dekey(uk);
@@ -1066,11 +1148,16 @@ __device__ void phase_finalize(Ctx& c, ParCtl* pc)
           nl = dekey(lk);
           if (nl == 0.0) nl = (s->lo_zero & 1u) ? -0.0 : 0.0;
         }
-        s->up_key  = kUpEmpty;
-        s->lo_key  = kLoEmpty;
-        s->up_zero = kZeroEmpty;
-        s->lo_zero = kZeroEmpty;
         res = finish_var(S.bounds + i, b.x, b.y, nl, nu, __ldg(P.is_int + i) != 0, c.lim);
+        // the slot of an unchanged variable persists: next round only its dirty rows republish,
+        // and (candidates being monotone in the bounds of the other variables) the
+        // kept values never undercut a fresh one, so the slot stays the exact fold
+        if (res != 0) {
+          s->up_key  = kUpEmpty;
+          s->lo_key  = kLoEmpty;
+          s->up_zero = kZeroEmpty;
+          s->lo_zero = kZeroEmpty;
+        }
       }
     }
     tally(c, pc, t, i < P.n ? i : -1, res);
@@ -1242,7 +1329,7 @@ __device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
   {
     const int n    = full ? P.n_mcol : ldv(&pc->n_dvar_m);
     const int* ids = full ? P.mcol : S.dvar_m[par];
-    for (Prefetch it_q(c, &pc->cur_vm, 1); it_q.t < n; it_q.advance()) {
+    for (Prefetch it_q(c, &pc->cur_vm, 1, n); it_q.t < n; it_q.advance()) {
     const int q = it_q.t;
       const int i = ids[q];
       const int r = tighten_warp(c, i);
@@ -1250,11 +1337,11 @@ __device__ void phase_tighten(Ctx& c, ParCtl* pc, int par, bool full)
     }
   }
   if (full) {
-    for (Prefetch it_q(c, &pc->cur_vs, 1); it_q.t < P.n_sctile; it_q.advance())
+    for (Prefetch it_q(c, &pc->cur_vs, 1, P.n_sctile); it_q.t < P.n_sctile; it_q.advance())
       tighten_tile_packed(c, it_q.t, pc, t);
   } else {
     const int n = ldv(&pc->n_dvar_s);
-    for (Prefetch it_q(c, &pc->cur_vs, 32); it_q.t < n; it_q.advance())
+    for (Prefetch it_q(c, &pc->cur_vs, 32, n); it_q.t < n; it_q.advance())
       tighten_list_tile(c, S.dvar_s[par], it_q.t, n, pc, t);
   }
   tally_flush_block(c, pc, t);
@@ -1471,6 +1558,106 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
   flush_work(c, colw, &qc->colw, &qc->xabort, ~0ull);
 }
 
+// Dirty marks for a dirty-filtered full round: row_stamp[k] = stamp for every row of a variable
+// that changed this round (the reference's dirty_rows, propagation.hpp:474-476). Changed vars with
+// short columns go 32 per warp (flattened 128-entry windows); longer columns by their chunk tasks.
+__device__ __forceinline__ void mark_entry(const DevProblem& P, const DevState& S, int e, unsigned stamp)
+{
+  const int mk = __ldg(P.col_mark + e);
+  if (mk >= 0) {
+    S.task_stamp[mk] = stamp;  // SELL slice / medium-row group
+  } else {                     // heavy row: its piece, and the row for its segment folds
+    S.piece_dirty[-mk - 2] = stamp;
+    S.row_stamp[__ldg(P.col_row + e)] = stamp;
+  }
+}
+
+// Dirty marks for a dirty-filtered full round: every row task (SELL slice, group of four medium rows,
+// heavy-row piece + row) holding a variable that changed this round gets `stamp` (a superset of the
+// reference's dirty_rows, propagation.hpp:474-476: recomputing a clean row is exact). One lane per
+// changed var (columns <= kTile; longer ones by their chunk tasks).
+__device__ void phase_mark_rows(Ctx& c, ParCtl* pc, unsigned stamp)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int nch       = ldv(&pc->n_changed);
+  const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
+  for (int j = gw * 32 + c.lane; j < nch; j += nw * 32) {
+    const int i  = S.changed[j];
+    const int cs = __ldg(P.col_start + i), ce = __ldg(P.col_start + i + 1);
+    if (ce - cs > kTile) continue;
+    for (int e = cs; e < ce; ++e) mark_entry(P, S, e, stamp);
+  }
+  const int ntask = ldv(&pc->n_ctask);
+  for (int t = gw; t < ntask; t += nw) {
+    const int2 tk = S.ctask[t];
+    const int ce  = __ldg(P.col_start + tk.x + 1);
+    const int e0  = __ldg(P.col_start + tk.x) + tk.y * kTile, e1 = min(ce, e0 + kTile);
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const int e = e0 + h * 32 + c.lane;
+      if (e < e1) mark_entry(P, S, e, stamp);
+    }
+  }
+}
+
+// Compacts the task stamps of this round's marks into the dirty lists the next (dirty-filtered)
+// round's row phase fetches from: SELL slices, medium-row groups, heavy-row pieces.
+__device__ void phase_df_lists(Ctx& c, unsigned stamp)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
+  const int n_all = S.n_task + P.n_piece;
+  // contiguous spans of >= 8 x 32 tasks per warp: one list append (atomic) per warp and kind
+  const int span = max(256, ((n_all + nw - 1) / nw + 31) / 32 * 32);
+  const int t_lo = gw * span, t_hi = min(n_all, t_lo + span);
+  if (t_lo >= t_hi) return;
+  int cnt[3] = {0, 0, 0};
+  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {  // pass 1: counts
+    const int t = t0 + c.lane;
+    const unsigned* st = t < S.n_task ? S.task_stamp + t : S.piece_dirty + (t - S.n_task);
+    const bool d       = t < t_hi && __ldcg(st) == stamp;
+    const int kind     = t < P.n_srtile ? 0 : t < S.n_task ? 1 : 2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) cnt[q] += __popc(__ballot_sync(FULL, d && kind == q));
+  }
+  int base[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    base[q] = 0;
+    if (c.lane == 0 && cnt[q]) base[q] = atomicAdd(&S.ctl->df_cnt[q], cnt[q]);
+    base[q] = __shfl_sync(FULL, base[q], 0);
+  }
+  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {  // pass 2: ids (the stamps are L2 hits now)
+    const int t = t0 + c.lane;
+    const unsigned* st = t < S.n_task ? S.task_stamp + t : S.piece_dirty + (t - S.n_task);
+    const bool d       = t < t_hi && __ldcg(st) == stamp;
+    const int kind     = t < P.n_srtile ? 0 : t < S.n_task ? 1 : 2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const unsigned m = __ballot_sync(FULL, d && kind == q);
+      if (d && kind == q) {
+        const int id = q == 0 ? t : q == 1 ? t - P.n_srtile : t - S.n_task;
+        (q == 0 ? S.df_slice : q == 1 ? S.df_group : S.df_piece)[base[q] + __popc(m & lanemask_lt())] = id;
+      }
+      base[q] += __popc(m);
+    }
+  }
+}
+
+// Empties every candidate slot (before a true full round when a previous round left data in them).
+__device__ void clear_slots(const DevProblem& P, const DevState& S)
+{
+  CandSlot e;
+  e.lo_key  = kLoEmpty;
+  e.up_key  = kUpEmpty;
+  e.lo_zero = kZeroEmpty;
+  e.up_zero = kZeroEmpty;
+  e.pad0 = e.pad1 = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) S.slot[i] = e;
+}
+
 __device__ void zero_par(ParCtl* q)
 {
   int* w = reinterpret_cast<int*>(q);
@@ -1518,7 +1705,7 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
   WarpSmem& w = sm.w[warp];
 #endif
   Ctx c{P, S, lim, sm, w, (int)(threadIdx.x & 31), warp};
-  phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell);
+  phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell, ldv(&S.ctl->df_stamp));
 }
 
 // The SELL slices of a full round (short rows, thread per row) at this kernel's own occupancy:
@@ -1538,7 +1725,7 @@ __global__ void __launch_bounds__(kThreads, BP_SELL_MIN_BLOCKS)
     Smem& sm       = *reinterpret_cast<Smem*>(no_smem);
     const int warp = threadIdx.x >> 5;
     Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp};
-    phase_sell(c, &S.ctl->par[par], true);
+    phase_sell(c, &S.ctl->par[par], true, ldv(&S.ctl->df_stamp));
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -1548,6 +1735,7 @@ __global__ void __launch_bounds__(kThreads) k_cand_pieces(DevProblem P, DevState
 {
   if (!ldv(&S.ctl->need_full)) return;
   const unsigned stamp = ldv(&S.ctl->stamp_base) + (unsigned)ldv(&S.ctl->rounds);
+  const unsigned ds    = ldv(&S.ctl->df_stamp);
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
@@ -1555,13 +1743,14 @@ __global__ void __launch_bounds__(kThreads) k_cand_pieces(DevProblem P, DevState
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   for (int t = gw; t < P.n_cpiece; t += nw) {
     const int2 tk = P.cpiece_task[t];
-    long_cand_piece(c, tk.x, tk.y, stamp);
+    long_cand_piece(c, tk.x, tk.y, stamp, ds);
   }
 }
 
 __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     k_engine(DevProblem P, DevState S, Limits lim, int mode, int full_first, unsigned stamp_base,
-             unsigned long long dense_thr, long long* stats, int ext_f2, int resume)
+             unsigned long long dense_thr, long long* stats, int ext_f2, int resume,
+             unsigned long long mark_max)
 {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm            = *reinterpret_cast<Smem*>(dyn_smem);
@@ -1587,6 +1776,9 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     return;
   }
 
+  // slot state of the previous launch / call (read by every thread before any lead write: the
+  // lead writes it only after a grid barrier of this launch)
+  int slot_state = ldv(S.slot_state);
   if (resume) {  // nothing handed over: the engine already finished (speculative launch)
     if (!ldv(&S.ctl->need_full)) return;
     grid.sync();  // every block has read need_full before it is cleared
@@ -1601,13 +1793,17 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   int status = BP_STATUS_UNSET, crossed_out = 0;
   int rounds = 0;
   bool resumed = false;  // first iteration after k_rows_full ran this round's F2
+  unsigned df_next = 0;  // dirty stamp marked for the next round (0: the next full round is a true one)
   if (resume) {
     rounds     = ldv(&S.ctl->rounds);
     any_change = ldv(&S.ctl->any_change) != 0;
     resumed    = true;
-  } else if (lead) {
-    S.ctl->t0         = t0;
-    S.ctl->stamp_base = stamp_base;
+  } else {
+    if (lead) {
+      S.ctl->t0         = t0;
+      S.ctl->stamp_base = stamp_base;
+    }
+    if (slot_state == 1) slot_state = 2;  // valid for the previous call's bounds only
   }
   if (!resume && full_first == 2) {
     // frontier start from a certified fixpoint: rows(changed) / vars(rows) of the staged list
@@ -1639,6 +1835,21 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     long long* st        = stats ? stats + (long long)(rounds - 1) * kStatCols : nullptr;
     const bool fr        = full || !lim.incremental;
     const unsigned stamp = stamp_base + (unsigned)rounds;
+    // A full round right after a full / dirty-filtered one whose changed vars' rows were marked is
+    // dirty-filtered: only the marked rows are recomputed and republish; any other
+    // full round is a true one and starts from empty candidate slots.
+    // (ds = 0 with valid slots: every row is recomputed and republishes into the persistent slots --
+    // equally exact; chosen when marking would cost more than it saves)
+    unsigned ds = 0;
+    if (fr && !resumed) {
+      ds = slot_state == 1 ? df_next : 0u;
+      if (slot_state == 2) {
+        clear_slots(P, S);
+        grid.sync();
+        slot_state = 0;
+      }
+    }
+    df_next = 0;
     if (resumed) {
       resumed = false;  // this round's F2 (fused rows + candidates) ran in k_rows_full
     } else if (fr && ext_f2) {
@@ -1647,12 +1858,14 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
         if (st) st[10] = (long long)(globaltimer() - t0);
         S.ctl->rounds     = rounds;
         S.ctl->any_change = any_change ? 1 : 0;
+        S.ctl->df_stamp   = ds;
+        *S.slot_state     = slot_state;
         S.ctl->need_full  = 1;
       }
       return;
     } else {
       if (st && lead) st[10] = (long long)(globaltimer() - t0);
-      phase_rows(c, pc, ppar, fr, fr, stamp);
+      phase_rows(c, pc, ppar, fr, fr, stamp, true, true, ds);
       grid.sync();
     }
     if (st && lead) st[6] = (long long)(globaltimer() - t0);
@@ -1663,6 +1876,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     if (fr) phase_finalize(c, pc);
     else phase_tighten(c, pc, ppar, false);
     grid.sync();
+    slot_state   = fr ? 1 : (slot_state == 0 ? 0 : 2);  // a frontier round leaves the slots stale
     const int cr = ldv(&pc->n_crossed);
     const int nc = ldv(&pc->n_changed);
     if (st && lead) {
@@ -1694,10 +1908,26 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     // the next frontier would span the matrix: even the upper bound of its work (Σ reach of the
     // changed vars, duplicates counted) is checked against 4x the full-round threshold, so a
     // "full" prediction is only taken when the frontier is certainly large or nearly so
-    if (!lim.incremental || ldv(&pc->colnnz) > dense_thr ||
+    // the next round is a full one: with valid slots, mark the rows of this round's changed vars
+    // (complete even when a frontier expansion below stopped early) and filter by them
+    auto go_full = [&]() {
+      if (slot_state == 1 && ldv(&pc->colnnz) <= mark_max) {
+        if (lead) S.ctl->df_cnt[0] = S.ctl->df_cnt[1] = S.ctl->df_cnt[2] = 0;
+        phase_mark_rows(c, pc, stamp);
+        grid.sync();  // marks (and the zeroed counts) visible grid-wide
+        phase_df_lists(c, stamp);
+        df_next = stamp;
+        if (!ext_f2 || st) grid.sync();  // in-engine row phase: lists complete first
+        if (st && lead) st[11] = (long long)(globaltimer() - t0);
+      }
+      full = true;
+    };
+    // with valid slots a dirty-filtered round (the dirty rows only, no CSC pass, no expansion) is
+    // never more work than the frontier round it replaces
+    if (!lim.incremental || (slot_state == 1 && dense_thr != ~0ull) || ldv(&pc->colnnz) > dense_thr ||
         (dense_thr != ~0ull &&
          ldv(&pc->reach) + min(ldv(&pc->hreach), P.h_reach) > 4 * dense_thr)) {
-      full = true;
+      go_full();
       continue;
     }
     // both expansions stop early once the next round is known to be a full round
@@ -1705,7 +1935,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     grid.sync();
     if (st && lead) st[8] = st[9] = (long long)(globaltimer() - t0);
     if (ldv(&qc->roww) > dense_thr) {
-      full = true;
+      go_full();
       continue;
     }
     phase_expand_vars(c, pc, qc, qpar, stamp,
@@ -1715,6 +1945,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     // a frontier round costs ~ its gathers (row nnz + col nnz); a fused full round ~ N = 4 dense_thr
     // gathers but with far better memory-level parallelism
     full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 2 * dense_thr;
+    if (full) go_full();
   }
   }
   if (lead) {
@@ -1724,6 +1955,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     S.ctl->crossed    = crossed_out;
     S.ctl->any_change = any_change ? 1 : 0;
     S.ctl->fixpoint   = fixpoint ? 1 : 0;
+    *S.slot_state     = slot_state;
   }
 }
 
@@ -1777,6 +2009,7 @@ DevProblem Problem::dev() const
   d.reach       = reach.p;
   d.h_reach     = h_reach;
   d.mcol        = mcol.p;
+  d.col_mark    = col_mark.p;
   return d;
 }
 
@@ -1876,6 +2109,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.is_int.upload(is_integer, n);
 
   // Short rows / columns: packed tiles.
+  std::vector<int> srow_h;  // SELL slice lane -> row (host copy for the task map)
   {
     // Rows with nnz <= kPackNnz as SELL-32 slices: rows sorted by length (descending, stable), 32
     // per slice, each slice padded to its longest row, entries column-interleaved so lane i reads
@@ -1915,6 +2149,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
     while (P.n_srow_long < nsl && sbase[P.n_srow_long + 1] - sbase[P.n_srow_long] > 32 * kShortNnz)
       ++P.n_srow_long;
     P.srow.upload(srow);
+    srow_h = srow;
     P.sr_ci.upload(sci);
     P.sr_val.upload(sval);
     P.sr_tile.upload(sbase);
@@ -1987,6 +2222,26 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.long_off.upload(long_off);
   P.hpiece.upload(hpiece);
   P.h_hpiece = hpiece;
+  {
+    // per CSC entry: the row task holding it, for the marks of dirty-filtered rounds -- the SELL
+    // slice (0 .. n_srtile), the group of four medium rows (n_srtile + (fold index - n_fold_heavy) / 4,
+    // as phase_rows fetches them) or, for heavy rows, -(piece + 2). CSC positions follow the same
+    // stable transpose as the CSC itself.
+    std::vector<int> row_task(m, -1);
+    for (size_t q = 0; q < srow_h.size(); ++q)
+      if (srow_h[q] >= 0) row_task[srow_h[q]] = (int)(q / 32);
+    for (size_t j = P.n_fold_heavy; j < fold.size(); ++j)
+      row_task[fold[j].x] = P.n_srtile + (int)((j - P.n_fold_heavy) / 4);
+    std::vector<int> cmk((size_t)N, 0), cur(col_start, col_start + n);
+    for (int k = 0; k < m; ++k)
+      for (int e = row_start[k]; e < row_start[k + 1]; ++e) {
+        const int d = cur[row_col[e]]++;
+        cmk[d]      = hpiece[k] >= 0 ? -(hpiece[k] + (e - row_start[k]) / kPiece) - 2 : row_task[k];
+        if (cmk[d] == -1) throw std::runtime_error("row without a full-round task");
+      }
+    P.col_mark.upload(cmk);
+    P.n_task = P.n_srtile + (int)((fold.size() - P.n_fold_heavy + 3) / 4);
+  }
   P.piece_task.upload(piece);
   P.n_fold         = (int)fold.size();
   P.n_cpiece       = (int)cpiece.size();
@@ -2035,6 +2290,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.gbuf.alloc((size_t)std::max(P.n_long_entries, 1ll));
   P.cinfo.alloc((size_t)std::max(P.n_long_entries / kTile, 1ll));
   P.pstamp.alloc((size_t)std::max(P.n_piece, 1));
+  P.piece_dirty.alloc((size_t)std::max(P.n_piece, 1));
+  BP_CUDA(cudaMemset(P.piece_dirty.p, 0, sizeof(unsigned) * std::max(P.n_piece, 1)));
+  P.task_stamp.alloc((size_t)std::max(P.n_task, 1));
+  BP_CUDA(cudaMemset(P.task_stamp.p, 0, sizeof(unsigned) * std::max(P.n_task, 1)));
+  P.ckpt.alloc((size_t)std::max(P.n_piece, 1));
   BP_CUDA(cudaMemset(P.pstamp.p, 0, sizeof(unsigned) * std::max(P.n_piece, 1)));
   P.slot.alloc(nn);
   {
@@ -2067,16 +2327,28 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   const size_t nx_cap = (size_t)(N / kTile) + mm + 1;
   P.lists_i2.alloc(2 * (np_cap + nf_cap + nx_cap) + (size_t)(N / kTile) + nn + 1);
   P.ctl.alloc(1);
+  BP_CUDA(cudaMemset(P.ctl.p, 0, sizeof(Ctl)));
   DevState& S = P.st;
   S.bounds    = P.bounds.p;
   S.rec       = P.rec.p;
   S.aux       = P.aux.p;
   S.gbuf      = P.gbuf.p;
   S.slot      = P.slot.p;
+  P.slot_state.alloc(1);
+  BP_CUDA(cudaMemset(P.slot_state.p, 0, sizeof(int)));  // the slots start empty
+  S.slot_state = P.slot_state.p;
   S.ready     = P.ready.p;
   S.rquiet    = P.rquiet.p;
   S.cinfo     = P.cinfo.p;
   S.pstamp    = P.pstamp.p;
+  S.piece_dirty = P.piece_dirty.p;
+  S.task_stamp  = P.task_stamp.p;
+  S.n_task      = P.n_task;
+  P.df_lists.alloc((size_t)std::max(P.n_task + P.n_piece, 1));
+  S.df_slice = P.df_lists.p;
+  S.df_group = P.df_lists.p + P.n_srtile;
+  S.df_piece = P.df_lists.p + P.n_task;
+  S.ckpt      = P.ckpt.p;
   S.seg_part  = P.seg_part.p;
   S.seg_done  = P.seg_done.p;
   S.row_stamp = P.row_stamp.p;
@@ -2150,6 +2422,8 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
     BP_CUDA(cudaMemsetAsync(P.var_stamp.p, 0, sizeof(unsigned) * P.var_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.ready.p, 0, sizeof(unsigned) * P.ready.n, s));
     BP_CUDA(cudaMemsetAsync(P.pstamp.p, 0, sizeof(unsigned) * P.pstamp.n, s));
+    BP_CUDA(cudaMemsetAsync(P.piece_dirty.p, 0, sizeof(unsigned) * P.piece_dirty.n, s));
+    BP_CUDA(cudaMemsetAsync(P.task_stamp.p, 0, sizeof(unsigned) * P.task_stamp.n, s));
     P.stamp_base = 1;
   }
   unsigned sb = P.stamp_base;
@@ -2171,7 +2445,11 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   // C2 (9.45 -> 11.0 ms: more warps in flight only lengthen each gather), so off.
   static const int split_env = getenv("BP_SPLIT_SELL") ? atoi(getenv("BP_SPLIT_SELL")) : 0;
   const int split_sell       = split_env && P.n_srtile > 0 ? 1 : 0;
-  void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume};
+  // dirty-filtered rounds when the changed vars' columns hold at most BP_DF_MARK_PCT % of the nnz:
+  // beyond that nearly every row task is dirty and the marks cost more than they save (C2)
+  static const int mark_pct = getenv("BP_DF_MARK_PCT") ? atoi(getenv("BP_DF_MARK_PCT")) : 3;
+  unsigned long long mark_max = (unsigned long long)(P.nnz * mark_pct / 100);
+  void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume, &mark_max};
   BP_CUDA(cudaEventRecord(P.ev0, s));
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
   ++g_kernel_launches;

@@ -25,10 +25,11 @@ for flags, name in ((0, "fast"), (FORCE_FRONTIER, "exact-frontier")):
     t = metrics.trim(st.cpu().numpy(), r.rounds)
     print(f"== {a.workload} {name}: rounds={r.rounds} total={t[-1, 7] / 1e3:.1f} us")
     prev = 0
-    print(" r full      |R|        A      |V|        B    |C|  gath_us   act_us  tight_us  xrow_us  xvar_us")
+    print(" r full      |R|        A      |V|        B    |C|  gath_us   act_us  tight_us  xrow_us  xvar_us  mark_us")
     for i, row in enumerate(t):
         tg = row[10] - prev
         ta, tt, tx1, tx2 = row[6] - row[10], row[7] - row[6], row[8] - row[7], row[9] - row[8]
         prev = row[9]
         print(f"{i+1:2d} {row[0]:4d} {row[1]:8d} {row[2]:8d} {row[3]:8d} {row[4]:8d} {row[5]:6d} "
-              f"{tg/1e3:8.1f} {ta/1e3:8.1f} {tt/1e3:9.1f} {tx1/1e3:8.1f} {tx2/1e3:8.1f}")
+              f"{tg/1e3:8.1f} {ta/1e3:8.1f} {tt/1e3:9.1f} {tx1/1e3:8.1f} {tx2/1e3:8.1f} "
+              f"{(row[11] - row[7]) / 1e3 if row[11] else 0.0:8.1f}")
