@@ -144,6 +144,21 @@ def cpu_reference_propagate(p, reps=1):
     return times, out, int(Ref.lib().ref_max_threads())
 
 
+def cpu_reference_single_thread(workload):
+    """Seconds of one reference propagate of `workload` with PULSE_THREADS=1 (the reference's pool
+    size is fixed at first use, so this runs in a child process)."""
+    code = ("import sys, time; sys.path.insert(0, %r); import bench; "
+            "from oracle.bind import RefProblem, ref_propagate; p, _ = bench.make_workload(%r); "
+            "rp = RefProblem.from_def(p); r = p.root_bounds(); t = time.perf_counter(); "
+            "ref_propagate(rp, r); print(time.perf_counter() - t)") % (str(ROOT), workload)
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PULSE_THREADS="1"),
+                             capture_output=True, text=True, timeout=600)
+        return float(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference CPU implementation on this box's host cores."""
     if rank != 0:
@@ -248,22 +263,27 @@ def run_probing(args, rank, world, local):
            "probe_kernel_ms_max_rank": dev_ms, "n_gpus": world,
            "parallelism": f"candidates sharded x{world}, NCCL gather to rank 0"}
     if world == 1 and not args.no_cpu_baseline:
-        from oracle.bind import Ref, RefCache, RefProblem
+        from oracle.bind import Ref, RefCache, RefProblem, cache_mismatches
         if Ref.available():
             rp = RefProblem.from_def(p)
             L = Ref.lib()
             t0 = time.perf_counter()
-            h = L.ref_build_cache(rp.h, args.cpu_sample_sec)
+            rc = RefCache(L.ref_build_cache(rp.h, args.cpu_sample_sec))
             el_cpu = time.perf_counter() - t0
             import ctypes as C
             npb, ninf = C.c_int(), C.c_int()
-            L.ref_cache_stats(h, C.byref(npb), C.byref(ninf))
-            L.ref_cache_free(h)
+            L.ref_cache_stats(rc.h, C.byref(npb), C.byref(ninf))
             out["cpu_baseline"] = {"value": npb.value / args.cpu_sample_sec, "unit": "probes/s",
                                    "cores": int(L.ref_max_threads()), "kind": "reference",
                                    "sample": f"build_cache(p, {args.cpu_sample_sec:g} s): "
                                              f"{npb.value} vars probed ({el_cpu:.1f} s incl. "
                                              "prioritization)"}
+            # parity: every entry the reference's build_cache produced equals the GPU cache's, bitwise
+            checked, bad = cache_mismatches(cache, rc, range(p.n_vars))
+            out["parity"] = {"reference_entries_checked": checked, "mismatches": len(bad),
+                             "against": "pulse::build_cache (oracle/_ref) entries, bitwise"}
+            assert checked == npb.value and not bad, f"C3 cache differs from the reference at {bad[:5]}"
+
     return out
 
 
@@ -319,9 +339,9 @@ def run_rounding(args, rank, world, local):
 def run_lp(args, rank, world, local, p):
     """the PDHG inner iteration (lp.hpp:315-340: spmv_rows + dual prox +
     spmv_cols + primal step + running sums) on the C2 matrix, device-resident; CUDA-event time of
-    `iters` iterations per call. Algorithmic bytes per iteration: both matrix views streamed once
-    (24 B per nnz), one 8-B gather per nnz in each product, and the elementwise vectors (dual step
-    40 B / row, primal step 72 B / var + 16 B / row for the running sums)."""
+    `iters` iterations per call. Algorithmic (compulsory) bytes per iteration: both matrix views
+    streamed once (24 B per nnz) and the elementwise vectors (dual step 40 B / row, primal step
+    72 B / var + 16 B / row for the running sums)."""
     from paper_2510_20499_b200.lp import DeviceLp, LpInstance
     if rank != 0:
         return None
@@ -338,7 +358,9 @@ def run_lp(args, rank, world, local, p):
         st = list(lp.pdhg_iterate(*st, 1e-3, 1e-3, iters))
         ms.append(lp.last_ms() / iters)
     it_ms = float(np.median(ms))
-    alg = 24 * N + 16 * N + 40 * m + 72 * n + 16 * m
+    # compulsory unique traffic: both matrix views streamed once (24 B per nnz) + the elementwise
+    # vectors; the x / y gathers of the products are L2 hits (16 MB vectors), not compulsory
+    alg = 24 * N + 40 * m + 72 * n + 16 * m
     peak, peak_kind = peaks()
     out = {"workload": "PDHG inner iteration on the C2 matrix (1M x 1M, %d nnz)" % N,
            "ms_per_iteration": it_ms, "iterations_per_s": 1e3 / it_ms,
@@ -504,21 +526,25 @@ def run_batch(args, rank, world, local):
     if world == 1 and not args.no_cpu_baseline:
         from oracle.bind import Ref, RefProblem, ref_propagate
         if Ref.available():
-            done, v_cpu, el = 0, 0, 0.0
-            for p, _, _, v in sorted(work, key=lambda x: x[0].nnz()):
-                if el > args.cpu_sample_sec / 2:  # bounded sample: smallest instances first
-                    break
+            done, v_cpu, el, bad = 0, 0, 0.0, []
+            for p, _, w, v in sorted(work, key=lambda x: x[0].nnz()):
                 rp = RefProblem.from_def(p)
                 root = p.root_bounds()
                 t1 = time.perf_counter()
-                ref_propagate(rp, root)
+                ob, oinf, ost, orr, ocr = ref_propagate(rp, root)
                 el += time.perf_counter() - t1
                 v_cpu += v
                 done += 1
                 del rp
+                # parity: the device result of the timed sweeps (w) == the reference, bitwise
+                if not np.array_equal(w.cpu().numpy().view(np.uint64), ob.view(np.uint64)):
+                    bad.append(p.name)
             out["cpu_baseline"] = {"value": v_cpu / el, "unit": "nnz/s", "cores": int(Ref.lib().ref_max_threads()),
                                    "kind": "reference", "sample": f"reference propagate on {done} of "
                                                                   f"{len(work)} instances ({el:.1f} s)"}
+            out["parity"] = {"instances_checked": done, "bound_mismatches": len(bad),
+                             "against": "pulse::propagate (oracle/_ref), bounds bitwise"}
+            assert not bad, f"C5 instances differ from the reference: {bad[:5]}"
     return out
 
 
@@ -557,6 +583,24 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
+    if args.gpus != world:
+        # one process per GPU: `python bench.py --gpus N` re-executes itself under torchrun; a
+        # launcher whose WORLD_SIZE disagrees with --gpus, or too few GPUs, is an error (no
+        # silent single-rank run)
+        if "WORLD_SIZE" in os.environ:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        import torch
+        ndev = torch.cuda.device_count() if args.impl == "ours" else args.gpus
+        if ndev < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} requested, {ndev} GPU(s) visible")
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                   "--master-port", str(port), str(Path(__file__).resolve())]
+                  + sys.argv[1:])
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
@@ -679,13 +723,9 @@ def main():
     if rank == 0:
         peak, peak_kind = peaks()
         achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
-        prof = ROOT / "profiles" / "ncu_k_engine_summary.json"
+        # DRAM traffic needs a profiler pass (ncu): not measured inside this run; the committed
+        # capture of the same code is profiles/r02/ 
         traffic = None
-        if prof.exists():
-            try:
-                traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch", {}).get(args.workload)
-            except Exception:
-                traffic = None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             res = cpu_reference_propagate(p, reps=1)
@@ -696,6 +736,12 @@ def main():
                        "sample": f"1 full propagate of {args.workload} ({out[3]} rounds, "
                                  f"{times[0]:.2f} s), reference compiled from /root/reference"}
                 assert out[3] == r.rounds and out[2] == int(r.status), "reference trajectory differs"
+                assert np.array_equal(out[0].view(np.uint64), ref_bits), "C2 bounds differ from the reference"
+                one = cpu_reference_single_thread(args.workload)
+                if one is not None:
+                    cpu["single_thread"] = {"value": visits / one, "unit": "nnz/s", "cores": 1,
+                                            "sample": f"1 propagate of {args.workload} with PULSE_THREADS=1 "
+                                                      f"({one:.2f} s)"}
         value = world * visits * args.steps / (ms * 1e-3)
         line = {
             "metric": "BP nnz/s", "value": value, "unit": "nnz/s", "n_gpus": world,

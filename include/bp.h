@@ -187,6 +187,17 @@ int bp_cache_set_entry(bp_cache* c, int32_t v, const int32_t* hdr5, const double
                        int32_t n_down, const int32_t* down_vars, const double* down_lo,
                        const double* down_up, int32_t n_up, const int32_t* up_vars,
                        const double* up_lo, const double* up_up);
+/* pulse::build_cache over several GPUs of one process (probing.hpp:243-281, the worker pool of
+ * :256-272 with GPUs as workers). probs[d] is the same problem uploaded on a distinct
+ * device. Candidates: `vars` (nvars >= 0, all probed) or, with vars == NULL, build_cache's own
+ * (priority order minus root-fixed variables, each device's share under `budget_sec`). Device d
+ * probes positions d, d + nprob, ... of the candidate list; the packed slices are gathered to
+ * probs[0]'s device with NCCL send/recv (libnccl.so.2 resolved at run time) and merged there.
+ * probe_ms_per_device (nprob, may be NULL) receives each device's probe-kernel time. The result
+ * equals the single-GPU cache of the same candidates. */
+int bp_build_cache_multi(bp_problem* const* probs, int32_t nprob, double budget_sec,
+                         const int32_t* vars, int32_t nvars, bp_cache** out,
+                         double* probe_ms_per_device);
 /* Serialisation of a cache slice for the multi-GPU gather (NCCL) and merge on rank 0. */
 int bp_cache_pack_size(const bp_cache* c, int64_t* bytes);
 int bp_cache_pack(const bp_cache* c, void* buf, int64_t bytes);

@@ -24,11 +24,12 @@
 // was called (INTEGRATION.md shows the switch for fp.hpp). Results are bit-identical to the
 // reference's (tests/cpp/test_dropin.cpp runs both side by side).
 //
-// Device problems: one bp_problem per ProblemDef, uploaded on first use and kept in a side table
-// keyed by the ProblemDef's address and validated by its array addresses, sizes and a content
-// fingerprint (every word of small problems, a strided sample of large ones): fp.hpp:253 rebuilds
-// problems, often at the same addresses, and a stale entry is re-uploaded.
-// Call pulse::gpu::release(p) before destroying a ProblemDef to free its device copy early.
+// Device problems: one bp_problem per (ProblemDef, device), uploaded on first use and kept in a side
+// table keyed by the ProblemDef's address and validated by its array addresses, sizes and an O(1)
+// content sample (16 words per array): fp.hpp:253 rebuilds problems, often at the same addresses,
+// and a stale entry is re-uploaded. An in-place edit of a problem's arrays must be announced with
+// pulse::gpu::invalidate(p). Call pulse::gpu::release(p) before destroying a ProblemDef to free its
+// device copies early.
 #pragma once
 
 #include <cstdint>
@@ -64,58 +65,55 @@ inline void check(int rc)
   }
 }
 
-// Content fingerprint of an array: every 8-byte word when small, else a strided sample of
-// ~64k words plus both ends (a rebuilt ProblemDef often reuses the old one's addresses).
+// Cheap content sample of an array: its size and up to 16 evenly spaced 8-byte words (O(1) per
+// call -- the per-call cost of the side table must stay far below a propagate). Together with the
+// array addresses and sizes it detects a rebuilt ProblemDef (fp.hpp:253) even at a reused
+// address; an IN-PLACE edit of a problem array must be announced with pulse::gpu::invalidate(p).
 template <class T>
-inline uint64_t fingerprint(uint64_t h, const std::vector<T>& v)
+inline uint64_t sample(uint64_t h, const std::vector<T>& v)
 {
   const size_t bytes = v.size() * sizeof(T), words = bytes / 8;
   const unsigned char* c = reinterpret_cast<const unsigned char*>(v.data());
   auto mix = [&](uint64_t w) { h = (h ^ w) * 0x100000001b3ull; h ^= h >> 29; };
   mix(bytes);
-  const size_t step = words <= (1u << 20) ? 1 : words / (1u << 16);
-  for (size_t i = 0; i < words; i += step) {
+  for (size_t j = 0; words && j < 16; ++j) {
     uint64_t w;
-    std::memcpy(&w, c + 8 * i, 8);
+    std::memcpy(&w, c + 8 * (j * (words - 1) / 15), 8);
     mix(w);
   }
-  for (size_t i = (words > 4096 ? words - 4096 : 0); step > 1 && i < words; ++i) {
-    uint64_t w;
-    std::memcpy(&w, c + 8 * i, 8);
-    mix(w);
-  }
-  for (size_t i = 8 * words; i < bytes; ++i) mix(c[i]);
   return h;
 }
 
 struct Key {
   const ProblemDef* p;
+  int device;
   const void* arrays[8];
   size_t sizes[3];
   uint64_t content;
   bool operator==(const Key& o) const
   {
-    return p == o.p && std::memcmp(arrays, o.arrays, sizeof(arrays)) == 0 &&
+    return p == o.p && device == o.device && std::memcmp(arrays, o.arrays, sizeof(arrays)) == 0 &&
            std::memcmp(sizes, o.sizes, sizeof(sizes)) == 0 && content == o.content;
   }
 };
 
-inline Key key_of(const ProblemDef& p)
+inline Key key_of(const ProblemDef& p, int device)
 {
   Key k{&p,
+        device,
         {p.row_start.data(), p.row_col.data(), p.row_val.data(), p.var_lower.data(),
          p.var_upper.data(), p.is_integer.data(), p.cons_lower.data(), p.cons_upper.data()},
         {(size_t)p.n_vars, (size_t)p.n_cons, p.row_col.size()},
         1469598103934665603ull};
   uint64_t& h = k.content;
-  h = fingerprint(h, p.var_lower);
-  h = fingerprint(h, p.var_upper);
-  h = fingerprint(h, p.cons_lower);
-  h = fingerprint(h, p.cons_upper);
-  h = fingerprint(h, p.is_integer);
-  h = fingerprint(h, p.row_start);
-  h = fingerprint(h, p.row_col);
-  h = fingerprint(h, p.row_val);
+  h = sample(h, p.var_lower);
+  h = sample(h, p.var_upper);
+  h = sample(h, p.cons_lower);
+  h = sample(h, p.cons_upper);
+  h = sample(h, p.is_integer);
+  h = sample(h, p.row_start);
+  h = sample(h, p.row_col);
+  h = sample(h, p.row_val);
   return k;
 }
 
@@ -140,14 +138,16 @@ inline Registry& registry()
   return r;
 }
 
-// The device copy of p (uploaded on first use, re-uploaded when p changed).
-inline bp_problem* handle(const ProblemDef& p)
+// The device copy of p on `device` (default: set_device's), uploaded on first use and re-uploaded
+// when p changed (key mismatch) or after invalidate(p).
+inline bp_problem* handle(const ProblemDef& p, int device = -1)
 {
   Registry& R = registry();
-  const Key k = key_of(p);
+  if (device < 0) device = R.device;
+  const Key k = key_of(p, device);
   std::lock_guard<std::mutex> lk(R.mu);
   for (auto it = R.items.begin(); it != R.items.end(); ++it) {
-    if ((*it)->key.p != &p) continue;
+    if ((*it)->key.p != &p || (*it)->key.device != device) continue;
     if ((*it)->key == k) return (*it)->h;
     R.items.erase(it);  // stale: the ProblemDef at this address changed
     break;
@@ -168,7 +168,7 @@ inline bp_problem* handle(const ProblemDef& p)
   d.cons_upper = p.cons_upper.data();
   auto ph      = std::make_unique<ProblemHandle>();
   ph->key      = k;
-  check(bp_problem_create(&d, R.device, &ph->h));
+  check(bp_problem_create(&d, device, &ph->h));
   R.items.push_back(std::move(ph));
   return R.items.back()->h;
 }
@@ -290,12 +290,13 @@ inline void release(const ProblemDef& p)
 {
   auto& R = detail::registry();
   std::lock_guard<std::mutex> lk(R.mu);
-  for (auto it = R.items.begin(); it != R.items.end(); ++it)
-    if ((*it)->key.p == &p) {
-      R.items.erase(it);
-      return;
-    }
+  for (auto it = R.items.begin(); it != R.items.end();)
+    it = (*it)->key.p == &p ? R.items.erase(it) : it + 1;
 }
+
+// Announces an in-place edit of p's arrays: its device copies are dropped and re-uploaded on the
+// next call (the side table samples array contents only sparsely).
+inline void invalidate(const ProblemDef& p) { release(p); }
 
 // Device used for problems uploaded from now on (default 0).
 inline void set_device(int device) { detail::registry().device = device; }
@@ -319,19 +320,15 @@ inline std::vector<int> tighten_bounds(const ProblemDef& p, BoundsState& b, cons
                                        const std::vector<int>* vars, const PropagationLimits& lim,
                                        int* crossed_out = nullptr, const WorkPlan* /*plan*/ = nullptr)
 {
-  std::vector<double> raw = b.raw();
+  double* raw = const_cast<double*>(b.raw().data());  // in place on b's storage (b is non-const)
   std::vector<int32_t> changed(p.n_vars);
   int32_t inf = 0, nch = 0, crossed = 0;
   const bp_limits l = detail::limits(lim);
-  detail::check(bp_tighten_bounds(detail::handle(p), raw.data(), &inf, a.act.data(),
+  detail::check(bp_tighten_bounds(detail::handle(p), raw, &inf, a.act.data(),
                                   a.n_inf_min.data(), a.n_inf_max.data(),
                                   vars ? vars->data() : nullptr, vars ? (int32_t)vars->size() : -1, &l,
                                   changed.data(), &nch, &crossed));
   changed.resize(nch);
-  for (int i : changed) {
-    b.set_lower(i, raw[2 * i]);
-    b.set_upper(i, raw[2 * i + 1]);
-  }
   if (crossed > 0) b.mark_infeasible();
   if (crossed_out) *crossed_out = crossed;
   return std::vector<int>(changed.begin(), changed.end());
@@ -347,12 +344,12 @@ inline PropagationResult propagate(const ProblemDef& p, BoundsState& b,
     r.status = PropagationStatus::Infeasible;
     return r;
   }
-  std::vector<double> raw = b.raw();
+  // in place on b's own storage (raw() is the state's vector; b is non-const): no 16n-byte copies
+  double* raw = const_cast<double*>(b.raw().data());
   int32_t inf = 0;
   bp_result res{};
   const bp_limits l = detail::limits(lim);
-  detail::check(bp_propagate(detail::handle(p), raw.data(), &inf, &l, &res));
-  detail::store(b, raw);
+  detail::check(bp_propagate(detail::handle(p), raw, &inf, &l, &res));
   if (inf) b.mark_infeasible();
   r.status       = static_cast<PropagationStatus>(res.status);
   r.rounds       = res.rounds;
@@ -390,6 +387,20 @@ inline ProbingCache build_cache(const ProblemDef& p, double budget_sec)
 {
   bp_cache* c = nullptr;
   detail::check(bp_build_cache(detail::handle(p), budget_sec, &c));
+  detail::CachePtr hold(c);
+  return detail::to_pulse(p, c);
+}
+
+// probing.hpp:243 over several GPUs of this process (bp_build_cache_multi): the problem is
+// replicated on each device of `devices`, candidates are interleaved over them, and the slices are
+// gathered to devices[0] with NCCL and merged -- the same cache as build_cache(p, budget_sec).
+inline ProbingCache build_cache(const ProblemDef& p, double budget_sec, const std::vector<int>& devices)
+{
+  if (devices.empty()) return pulse::gpu::build_cache(p, budget_sec);
+  std::vector<bp_problem*> hs;
+  for (int d : devices) hs.push_back(detail::handle(p, d));
+  bp_cache* c = nullptr;
+  detail::check(bp_build_cache_multi(hs.data(), (int32_t)hs.size(), budget_sec, nullptr, -1, &c, nullptr));
   detail::CachePtr hold(c);
   return detail::to_pulse(p, c);
 }

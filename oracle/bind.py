@@ -344,6 +344,65 @@ class RefCache:
         return c
 
 
+    def entry(self, v):
+        """(hdr7, br4, [(vars, lo, up) down, up]) of the reference entry of v, or None."""
+        L = Ref.lib()
+        hdr = np.zeros(7, np.int32)
+        br = np.zeros(4)
+        if not L.ref_cache_entry(self.h, int(v), _p(hdr), _p(br)):
+            return None
+        sides = []
+        for side in range(2):
+            cnt = int(hdr[5 + side])
+            vv = np.zeros(max(cnt, 1), np.int32)
+            lo = np.zeros(max(cnt, 1))
+            up = np.zeros(max(cnt, 1))
+            L.ref_cache_deltas(self.h, int(v), side, _p(vv), _p(lo), _p(up))
+            sides.append((vv[:cnt], lo[:cnt], up[:cnt]))
+        return hdr, br, sides
+
+    @classmethod
+    def probe_into(cls, rp, n_vars, root, vars_, threads=None):
+        """The reference's probe_variable (probing.hpp:225) of each var in ``vars_`` from ``root``,
+        stored in a fresh cache handle; host threads run independent probes (ctypes releases the
+        GIL; each call writes its own entry)."""
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        c = cls(Ref.lib().ref_cache_new_empty(rp.h))
+        r = np.ascontiguousarray(root, dtype=np.float64)
+        with ThreadPoolExecutor(threads or os.cpu_count() or 4) as ex:
+            list(ex.map(lambda v: Ref.lib().ref_cache_probe_into(c.h, rp.h, _p(r), int(v), 0), vars_))
+        return c
+
+
+def cache_mismatches(gpu_cache, ref_cache, vars_):
+    """Entries of ``vars_`` present in the reference cache that differ from the GPU cache in any
+    bit (kind, forcing flags, feasibility, branch bounds, delta vars and values). Returns
+    (checked, [mismatching vars])."""
+    bad, checked = [], 0
+    for v in vars_:
+        r = ref_cache.entry(v)
+        if r is None:
+            continue
+        checked += 1
+        g = gpu_cache._entry_raw(v)
+        if g is None:
+            bad.append(int(v))
+            continue
+        rh, rb, rs = r
+        gh, gb = g
+        same = np.array_equal(np.asarray(gh[:7]), rh) and np.array_equal(np.asarray(gb).view(np.uint64), rb.view(np.uint64))
+        if same:
+            for side in range(2):
+                gv, gl, gu = gpu_cache.deltas(v, side)
+                rv, rl, ru = rs[side]
+                same = same and np.array_equal(gv, rv) and np.array_equal(gl.view(np.uint64), rl.view(np.uint64)) \
+                    and np.array_equal(gu.view(np.uint64), ru.view(np.uint64))
+        if not same:
+            bad.append(int(v))
+    return checked, bad
+
+
 def ref_propagation_round(rp, n_vars, start, cache=None, seed=0, deadline=0.0, band=0.25,
                           repair=False):
     """rounding.hpp:393 with Rng(seed); returns (values, flags dict). lp_polish runs inside."""

@@ -947,6 +947,12 @@ struct bp_cache {
 };
 
 const bp::HostCache* bp_cache_host(const bp_cache* c) { return &c->c; }
+bp_cache* bp_cache_adopt(bp::HostCache&& c)
+{
+  auto* h = new bp_cache();
+  h->c    = std::move(c);
+  return h;
+}
 
 namespace {
 

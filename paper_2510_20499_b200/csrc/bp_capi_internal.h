@@ -27,3 +27,5 @@ void warm_start_sparse(const HostCache& C, const int* vars, const double* vals, 
                        std::vector<int>& conflicts, std::vector<int>& evicted);
 }  // namespace bp
 const bp::HostCache* bp_cache_host(const bp_cache* c);
+// A new cache handle owning `c` (moved in).
+bp_cache* bp_cache_adopt(bp::HostCache&& c);

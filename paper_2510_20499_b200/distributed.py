@@ -1,13 +1,15 @@
-"""Multi-GPU probing-cache construction: candidates are sharded across ranks with no
-data-path collective; each rank probes its slice on its own GPU (problem replicated per GPU),
-packs it (bp_cache_pack) and the slices are gathered to rank 0 with one collective pair over
+"""Multi-GPU probing-cache construction, one process per GPU: candidates are sharded
+across ranks with no data-path collective; each rank probes its slice on its own GPU (problem
+replicated per GPU), packs it (bp_cache_pack), and the slices are gathered to rank 0 over
 torch.distributed (NCCL over NVLink on GPUs; gloo in the CPU tests):
 
-  1. all_gather of the per-rank packed byte counts (int64)
-  2. all_gather_into_tensor of the byte slices padded to the largest count
+  1. all_gather of the per-rank packed byte counts (int64, 8 bytes per rank)
+  2. one batch of point-to-point sends to rank 0 (ncclGroupStart / ncclSend / ncclRecv under
+     batch_isend_irecv) -- a gather: only rank 0 receives the slices
 
 Rank 0 merges the slices (bp_cache_merge_packed). Entries are deterministic per variable, so any
-partition gives the same cache.
+partition gives the same cache. The single-process variant over several GPUs is the C-ABI
+bp_build_cache_multi (probing.build_cache_multi).
 """
 from __future__ import annotations
 
@@ -22,7 +24,7 @@ def shard(items, rank: int, world: int):
 
 
 def gather_packed(buf: np.ndarray, device=None, group=None) -> list | None:
-    """Gathers every rank's packed slice; returns the list of slices on rank 0, None elsewhere."""
+    """Gathers every rank's packed slice to rank 0; returns the list of slices there, None elsewhere."""
     import torch
     import torch.distributed as dist
 
@@ -33,16 +35,23 @@ def gather_packed(buf: np.ndarray, device=None, group=None) -> list | None:
     sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
     sizes = [int(s.item()) for s in sizes]
-    mx = max(max(sizes), 1)
-    send = torch.zeros(mx, dtype=torch.uint8, device=dev)
-    if buf.size:
-        send[: buf.size] = torch.from_numpy(np.ascontiguousarray(buf, dtype=np.uint8)).to(dev)
-    recv = torch.zeros(world * mx, dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(recv, send, group=group)
+    mine = torch.from_numpy(np.ascontiguousarray(buf, dtype=np.uint8)).to(dev)
     if rank != 0:
+        if sizes[rank]:
+            ops = [dist.P2POp(dist.isend, mine, dist.get_global_rank(group, 0) if group else 0, group)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
         return None
-    host = recv.cpu().numpy()
-    return [host[r * mx: r * mx + sizes[r]] for r in range(world)]
+    recv = {r: torch.empty(sizes[r], dtype=torch.uint8, device=dev) for r in range(1, world) if sizes[r]}
+    ops = [dist.P2POp(dist.irecv, t, dist.get_global_rank(group, r) if group else r, group)
+           for r, t in recv.items()]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    out = [np.ascontiguousarray(buf, dtype=np.uint8)]
+    for r in range(1, world):
+        out.append(recv[r].cpu().numpy() if r in recv else np.zeros(0, np.uint8))
+    return out
 
 
 def build_cache_sharded(p, vars_, root=None, device=None, group=None):

@@ -219,6 +219,25 @@ def build_cache(p: ProblemDef, budget_sec: float) -> ProbingCache:
     return ProbingCache(h)
 
 
+def build_cache_multi(p: ProblemDef, devices, vars_=None, budget_sec: float = 1e9):
+    """pulse::build_cache (probing.hpp:243-281) over several GPUs of this process
+    (bp_build_cache_multi): the problem is replicated on every device, device d probes positions
+    d, d + G, ... of the candidate list (``vars_``, or build_cache's priority order under
+    ``budget_sec``), and the packed slices are gathered to ``devices[0]`` with NCCL send/recv and
+    merged there. Returns (ProbingCache, per-device probe-kernel ms)."""
+    from .propagation import DeviceProblem
+    devices = [int(d) for d in devices]
+    reps = [device_problem(p, devices[0])] + [DeviceProblem(p, d) for d in devices[1:]]
+    hs = (C.c_void_p * len(reps))(*[r.h for r in reps])
+    v = None if vars_ is None else np.ascontiguousarray(vars_, dtype=np.int32)
+    ms = np.zeros(len(reps))
+    h = C.c_void_p()
+    _lib.check(_lib.lib().bp_build_cache_multi(hs, len(reps), float(budget_sec), _lib.ptr(v),
+                                               -1 if v is None else int(v.size), C.byref(h),
+                                               _lib.ptr(ms)))
+    return ProbingCache(h), ms.tolist()
+
+
 @dataclass
 class BulkWarmStart:
     bounds: BoundsState

@@ -5,6 +5,7 @@
 // seeds of acceptance.cpp:40 / :89 and test_rounding.cpp), plus larger mixed instances with heavy
 // rows. Everything is compared bit for bit. One PASS/FAIL line per criterion, like acceptance.cpp;
 // exit status = number of failures.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -439,6 +440,78 @@ void lp_products()
          std::to_string(runs) + " instances, " + std::to_string(bad) + " mismatches");
 }
 
+// Host overhead of the drop-in per call: pg::propagate (side-table lookup, BoundsState
+// marshalling, C-ABI) against bp_propagate on the same device problem with the same host bounds; the
+// difference must stay <= 50 us per call, on a 10k x 10k and a 300k x 300k instance (heavy rows).
+void host_overhead()
+{
+  bool ok = true;
+  std::string detail;
+  for (const auto& [n, heavy] : {std::pair<int, int>{10000, 0}, std::pair<int, int>{300000, 8}}) {
+    const ProblemDef p = mixed_instance(77 + n, n, n, heavy, 40000);
+    bp_problem* h      = pg::detail::handle(p);
+    const int reps     = n > 100000 ? 20 : 200;
+    BoundsState warm(p);
+    pg::propagate(p, warm);  // upload + warm-up
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    double t_abi = 0.0, t_pg = 0.0;
+    const bp_limits l = pg::detail::limits(PropagationLimits{});
+    for (int r = 0; r < reps; ++r) {
+      std::vector<double> raw = BoundsState(p).raw();
+      int32_t inf             = 0;
+      bp_result res{};
+      const auto t0 = now();
+      pg::detail::check(bp_propagate(h, raw.data(), &inf, &l, &res));
+      const auto t1 = now();
+      BoundsState b(p);
+      const auto t2 = now();
+      pg::propagate(p, b);
+      const auto t3 = now();
+      t_abi += std::chrono::duration<double>(t1 - t0).count();
+      t_pg += std::chrono::duration<double>(t3 - t2).count();
+    }
+    const double over_us = 1e6 * (t_pg - t_abi) / reps;
+    ok = ok && over_us <= 50.0;
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "%s%dx%d: bp_propagate %.1f us, pulse::gpu::propagate %.1f us, overhead %.1f us",
+                  detail.empty() ? "" : "; ", n, n, 1e6 * t_abi / reps, 1e6 * t_pg / reps, over_us);
+    detail += buf;
+  }
+  report("drop-in host overhead per propagate <= 50 us", ok, detail);
+}
+
+// pulse::gpu::build_cache over every GPU (bp_build_cache_multi: NCCL gather to device 0) equals the
+// reference's build_cache(p, 1e9) (probing.hpp:243) entry for entry.
+void build_cache_multi()
+{
+  int32_t ndev = 0;
+  bp_device_count(&ndev);
+  std::vector<int> devs;
+  for (int d = 0; d < ndev; ++d) devs.push_back(d);
+  int bad = 0, vars = 0;
+  for (uint64_t s = 0; s < 3; ++s) {
+    const ProblemDef p   = mixed_instance(500 + s, 1500, 1200, s == 2 ? 2 : 0, 3000);
+    const ProbingCache a = build_cache(p, 1e9);
+    const ProbingCache g = pg::build_cache(p, 1e9, devs);
+    if (a.n_probed != g.n_probed || a.n_infeasible_branches != g.n_infeasible_branches) ++bad;
+    for (int v = 0; v < p.n_vars; ++v) {
+      if (a.has(v) != g.has(v)) {
+        ++bad;
+        continue;
+      }
+      if (!a.has(v)) continue;
+      ++vars;
+      const auto& x = a.at(v);
+      const auto& y = g.at(v);
+      if (x.kind != y.kind || x.forces_down != y.forces_down || x.forces_up != y.forces_up ||
+          !same_branch(x.down, y.down) || !same_branch(x.up, y.up))
+        ++bad;
+    }
+  }
+  report("build_cache over " + std::to_string(devs.size()) + " GPU(s) (NCCL gather) == reference build_cache",
+         bad == 0, std::to_string(vars) + " entries, " + std::to_string(bad) + " mismatches");
+}
+
 void errors()
 {
   const ProblemDef p = testkit::tiny_knapsack();
@@ -478,6 +551,8 @@ int main()
   if (want("repair_stream")) repair_stream();
   if (want("builder_stream")) builder_stream();
   if (want("lp_products")) lp_products();
+  if (want("host_overhead")) host_overhead();
+  if (want("build_cache_multi")) build_cache_multi();
   std::printf("%d failure(s)\n", g_failures);
   return g_failures;
 }

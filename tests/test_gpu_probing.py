@@ -182,3 +182,20 @@ def test_prioritize_on_device_matches_reference(oracle_built):
         ref = np.zeros(max(p.n_vars, 1), np.int32)
         k = Ref.lib().ref_prioritize_probe_vars(rp.h, ref.ctypes.data_as(C.c_void_p))
         assert prioritize_probe_vars(p) == ref[:k].tolist()
+
+
+def test_c3_full_size_vs_reference(oracle_built):
+    """configs[2] at full size (500k x 500k, 200k binaries): every binary is probed on the batched
+    kernel from the original bounds (a certified fixpoint), and 512 of them, spread over the whole
+    range, equal the reference's own probe_variable (probing.hpp:225, oracle/_ref) bit for bit:
+    kind, forcing flags, feasibility, branch bounds, delta vars and values."""
+    from oracle.bind import Ref, RefCache, RefProblem, cache_mismatches
+    if not Ref.available():
+        pytest.skip("reference library missing")
+    p = synth.c3()
+    cache = probe_variables(p, None, np.arange(200_000, dtype=np.int32))
+    assert cache.certified and cache.n_probed == 200_000 and cache.n_fallback == 0
+    vars_ = np.sort(np.random.default_rng(33).choice(200_000, size=512, replace=False))
+    rc = RefCache.probe_into(RefProblem.from_def(p), p.n_vars, p.root_bounds(), vars_)
+    checked, bad = cache_mismatches(cache, rc, vars_)
+    assert checked == 512 and bad == [], bad[:10]

@@ -254,3 +254,21 @@ def test_full_size_bitwise_vs_reference(oracle_built, config):
     r = propagate(p, b)
     assert (b.infeasible(), int(r.status), r.rounds, r.crossed_vars) == (oinf, ost, orr, ocr)
     assert_bitwise(b.raw(), ob, f"{config} bounds")
+
+
+def test_c5_all_instances_vs_reference(oracle_built):
+    """configs[4] (C5): all 64 heterogeneous instances (10k-5M nnz, C1-C4 generators), one
+    propagate each on the engine, equal the reference's own propagate (oracle/_ref) bit for bit:
+    bounds, status, rounds, crossed."""
+    from oracle.bind import Ref, RefProblem, ref_propagate
+    if not Ref.available():
+        pytest.skip("reference library missing")
+    for sp in synth.c5_specs():
+        p = synth.c5_instance(sp)
+        rp = RefProblem.from_def(p)
+        ob, oinf, ost, orr, ocr = ref_propagate(rp, p.root_bounds())
+        del rp
+        b = BoundsState(p)
+        r = propagate(p, b)
+        assert (b.infeasible(), int(r.status), r.rounds, r.crossed_vars) == (oinf, ost, orr, ocr), sp
+        assert_bitwise(b.raw(), ob, f"C5 instance {sp[0]}")

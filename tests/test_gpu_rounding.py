@@ -221,3 +221,33 @@ def test_rounding_with_repair_matches_reference(oracle_built):
         assert np.array_equal(g.values[isint], rv[isint]), t
         attempts += g.repair_attempts
     assert attempts > 0
+
+
+def test_c4_scaled_full_cache_vs_reference(oracle_built):
+    """SURVEY §8d C4 parity run, scaled: a 20k x 20k knapsack/assignment instance (configs[3]'s
+    generator, long rows included) presolved to its fixpoint; a FULL-coverage cache built on the
+    GPU (sample-verified against the reference's own probe_variable), handed to both drivers;
+    propagation_round with Deadline::never and Rng(4): identical integer outputs and every
+    RoundingOutcome flag (rounding.hpp:393-558)."""
+    from oracle.bind import Ref, RefCache, RefProblem, cache_mismatches, ref_propagation_round
+    if not Ref.available():
+        pytest.skip("reference library missing")
+    from paper_2510_20499_b200 import BoundsState, propagate
+    p0, start = synth.c4(n=20_000, m=20_000, n_long=10, long_len=2000)
+    b = BoundsState(p0)
+    propagate(p0, b)
+    p = synth.with_bounds(p0, b.raw())
+    rp = RefProblem.from_def(p)
+    gcache = build_cache(p, 1e9)
+    free_int = [v for v in range(p.n_vars) if p.is_integer[v] and p.var_lower[v] != p.var_upper[v]]
+    assert gcache.n_probed >= len(free_int) > 10_000
+    sample = np.random.default_rng(4).choice(free_int, size=64, replace=False)
+    checked, bad = cache_mismatches(gcache, RefCache.probe_into(rp, p.n_vars, p.root_bounds(), sample), sample)
+    assert checked == 64 and bad == []
+    rcache = RefCache.from_gpu(rp, gcache)
+    rv, rf = ref_propagation_round(rp, p.n_vars, start, rcache, 4)
+    g = propagation_round(p, start, gcache, 4)
+    assert {k: int(getattr(g, k)) for k in FLAGS} == {k: rf[k] for k in FLAGS}
+    assert g.completed and rf["completed"]
+    isint = p.is_integer.astype(bool)
+    assert np.array_equal(g.values[isint], rv[isint])
