@@ -259,9 +259,23 @@ def run_probing(args, rank, world, local):
            "probes_per_s": len(vars_) / el, "variables_probed": cache.n_probed,
            "branches": 2 * cache.n_probed, "infeasible_branches": cache.n_infeasible_branches,
            "deltas": cache.n_deltas, "fallback_branches": cache.n_fallback,
+           "block_kernel_branches": cache.n_block,
            "root_certified_fixpoint": cache.certified, "wall_ms": el * 1e3,
            "probe_kernel_ms_max_rank": dev_ms, "n_gpus": world,
-           "parallelism": f"candidates sharded x{world}, NCCL gather to rank 0"}
+           "parallelism": f"candidates sharded x{world}, NCCL send/recv gather to rank 0"}
+    if world == 1:
+        # the BP byte formula summed over branches and rounds (the engine counts each
+        # branch's dirty sets: R, row nnz A, V, col nnz B, changed C). C3's matrix (~90 MB) sits
+        # largely in L2, so this is an EFFECTIVE bandwidth that can exceed the HBM figure.
+        R, A, V, B, Cc = cache.work
+        pb = 28 * A + 28 * R + 52 * B + 21 * V + 16 * Cc
+        peak, peak_kind = peaks()
+        ach = pb / (dev_ms * 1e-3) / 1e9
+        out["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                           "frac": ach / peak, "peak_kind": peak_kind, "effective_l2": True,
+                           "algorithmic_bytes": pb, "branch_work": {"rows": R, "row_nnz": A, "vars": V,
+                                                                    "col_nnz": B, "changed": Cc},
+                           "kernel": "k_probe (warp per branch) + k_probe_block, CUDA-event time"}
     if world == 1 and not args.no_cpu_baseline:
         from oracle.bind import Ref, RefCache, RefProblem, cache_mismatches
         if Ref.available():
@@ -288,10 +302,11 @@ def run_probing(args, rank, world, local):
 
 
 def run_rounding(args, rank, world, local):
-    """configs[3]: fix-and-propagate bulk rounding with a probing cache on the 2M x 2M
-    knapsack/assignment mix (presolved to its propagation fixpoint), one replica per rank."""
-    import torch
-
+    """configs[3]: fix-and-propagate bulk rounding with a FULL-coverage probing cache on the 2M x 2M
+    knapsack/assignment mix (presolved to its propagation fixpoint), propagation_round with
+    Deadline::never() and Rng(4), one replica per rank. The CPU baseline runs the reference's
+    propagation_round with the SAME cache (RefCache.from_packed) for a bounded time; the GPU is then
+    timed on exactly the same number of committed bulks (identical trajectory), like for like."""
     from paper_2510_20499_b200 import BoundsState, propagate, synth
     from paper_2510_20499_b200.probing import build_cache
     from paper_2510_20499_b200.rounding import propagation_round
@@ -300,39 +315,54 @@ def run_rounding(args, rank, world, local):
     b = BoundsState(p0)
     r0 = propagate(p0, b)
     p = synth.with_bounds(p0, b.raw())
+    log(f"rounding: C4 presolved in {r0.rounds} rounds; building the full-coverage cache")
     t0 = time.perf_counter()
-    log(f"rounding: C4 presolved in {r0.rounds} rounds; building cache ({args.cache_budget:g} s budget)")
-    cache = build_cache(p, args.cache_budget)  # fp.hpp:263 with probing_budget_sec (fp.hpp:37)
+    cache = build_cache(p, 1e9)  # fp.hpp:263 with an unbounded budget: every candidate probed
     cache_s = _max_over_ranks(time.perf_counter() - t0, world)
-    log(f"rounding: cache {cache.n_probed} vars in {cache_s:.1f} s")
+    log(f"rounding: cache {cache.n_probed} vars in {cache_s:.1f} s ({cache.n_block} block-kernel branches)")
     t0 = time.perf_counter()
     out = propagation_round(p, start, cache, seed=4 + rank, deadline_sec=args.round_deadline)
     el = _max_over_ranks(time.perf_counter() - t0, world)
-    log(f"rounding: {out.bulks_committed} bulks, {out.bp_calls} BP calls in {el:.1f} s")
+    log(f"rounding: {out.bulks_committed} bulks, {out.bp_calls} BP calls in {el:.1f} s, completed={out.completed}")
     if rank != 0:
         return None
+    free_int = int(sum(1 for v in range(p.n_vars) if p.is_integer[v] and p.var_lower[v] != p.var_upper[v]))
     res = {"workload": "C4: knapsack/assignment 2M x 2M (N=%d), presolved root (%d BP rounds)"
                        % (p.nnz(), r0.rounds),
-           "cache_build_s": cache_s, "cache_budget_s": args.cache_budget, "cache_vars": cache.n_probed,
-           "cache_fallback_branches": cache.n_fallback,
-           "cache_probes_per_s": cache.n_probed / cache_s, "round_s": el,
+           "cache_build_s": cache_s, "cache_budget_s": "unbounded (full coverage)",
+           "cache_vars": cache.n_probed, "cache_free_integer_vars": free_int,
+           "cache_probes_per_s": cache.n_probed / cache_s, "cache_fallback_branches": cache.n_fallback,
+           "cache_block_kernel_branches": cache.n_block, "round_s": el,
            "bulks_committed": out.bulks_committed, "bp_calls": out.bp_calls,
+           "bulks_committed_per_s": out.bulks_committed / el,
            "bp_calls_per_s": world * out.bp_calls / el, "completed": out.completed,
-           "timed_out": out.timed_out, "deadline_s": args.round_deadline,
+           "timed_out": out.timed_out, "deadline_s": args.round_deadline or None,
            "rounding_infeasible": out.rounding_infeasible, "set_count": out.set_count,
            "engine_device_ms": out.device_ms, "n_gpus": world, "parallelism": f"replicas x{world}"}
     if world == 1 and not args.no_cpu_baseline:
-        from oracle.bind import Ref, RefProblem, ref_propagation_round
+        from oracle.bind import Ref, RefCache, RefProblem, ref_propagation_round
         if Ref.available():
             rp = RefProblem.from_def(p)
+            rcache = RefCache.from_packed(rp, cache)
             t0 = time.perf_counter()
-            _, fl = ref_propagation_round(rp, p.n_vars, start, None, 4, deadline=args.cpu_sample_sec)
+            _, fl = ref_propagation_round(rp, p.n_vars, start, rcache, 4, deadline=args.cpu_sample_sec)
             el_cpu = time.perf_counter() - t0
-            res["cpu_baseline"] = {"value": fl["bulks_committed"] / el_cpu, "unit": "bulks committed/s",
+            k = int(fl["bulks_committed"])
+            res["cpu_baseline"] = {"value": k / el_cpu, "unit": "bulks committed/s",
                                    "cores": int(Ref.lib().ref_max_threads()), "kind": "reference",
-                                   "sample": f"propagation_round without cache, deadline "
-                                             f"{args.cpu_sample_sec:g} s: {fl['bulks_committed']} bulks"}
-            res["bulks_committed_per_s"] = out.bulks_committed / el
+                                   "sample": f"propagation_round with the same full cache, deadline "
+                                             f"{args.cpu_sample_sec:g} s: the first {k} bulks"}
+            if k > 0:  # the GPU on exactly those first k bulks (same trajectory)
+                os.environ["BP_ROUND_MAX_BULKS"] = str(k)
+                try:
+                    t0 = time.perf_counter()
+                    gk = propagation_round(p, start, cache, seed=4, deadline_sec=0.0)
+                    el_k = time.perf_counter() - t0
+                finally:
+                    del os.environ["BP_ROUND_MAX_BULKS"]
+                assert gk.bulks_committed == k
+                res["like_for_like"] = {"bulks": k, "gpu_s": el_k, "cpu_s": el_cpu,
+                                        "gpu_bulks_per_s": k / el_k, "cpu_bulks_per_s": k / el_cpu}
     return res
 
 
@@ -573,10 +603,8 @@ def main():
     ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--no-lp", action="store_true")
     ap.add_argument("--no-build", action="store_true")
-    ap.add_argument("--round-deadline", type=float, default=30.0,
-                    help="C4 propagation_round deadline (s), as the reference's Deadline")
-    ap.add_argument("--cache-budget", type=float, default=5.0,
-                    help="C4 probing-cache time budget (the reference FP's probing_budget_sec)")
+    ap.add_argument("--round-deadline", type=float, default=0.0,
+                    help="C4 propagation_round deadline (s), as the reference's Deadline; 0 = never")
     ap.add_argument("--c5-count", type=int, default=64)
     ap.add_argument("--c5-reps", type=int, default=3)
     ap.add_argument("--c5-streams", type=int, default=8)

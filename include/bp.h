@@ -171,6 +171,12 @@ int bp_cache_destroy(bp_cache* c);
 int bp_cache_info(const bp_cache* c, int32_t* n_vars, int32_t* n_probed,
                   int32_t* n_infeasible_branches, int64_t* n_deltas, int32_t* n_fallback,
                   int32_t* certified, double* probe_ms);
+/* Branches of the cache computed by the block-per-branch kernel (overlay overflows of the batched
+ * warp kernel, or every branch when the root was not a certified fixpoint). */
+int bp_cache_block_branches(const bp_cache* c, int32_t* n_block);
+/* Work of the probed branches, summed over their rounds (the reference trajectory's dirty sets,
+ * SURVEY §8d): {Σ|R_r|, Σ row nnz of R_r, Σ|V_r|, Σ col nnz of V_r, Σ|C_r|}. */
+int bp_cache_work(const bp_cache* c, int64_t* work5);
 /* Entry of v: *present = 0 if absent; hdr7 = {kind, forces_down, forces_up, down.feasible,
  * up.feasible, n_down_deltas, n_up_deltas}; br4 = {down lo, down up, up lo, up up}. */
 int bp_cache_entry(const bp_cache* c, int32_t v, int32_t* present, int32_t* hdr7, double* br4);

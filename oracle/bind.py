@@ -78,6 +78,7 @@ class Ref:
                 "ref_cache_entry": (I, [V, I, V, V]),
                 "ref_cache_deltas": (None, [V, I, I, V, V, V]),
                 "ref_cache_set_entry": (None, [V, I, V, V, V, V, V]),
+                "ref_cache_from_packed": (V, [V, V, C.c_longlong]),
                 "ref_assemble_bulk_warm_start": (I, [V, V, V, I, V, V, V, V]),
                 "ref_initial_sort": (I, [V, V, V]),
                 "ref_implied_slack_sort": (None, [V, V, V, V, V, I]),
@@ -323,6 +324,16 @@ class RefCache:
     @classmethod
     def build(cls, rp, budget=1e9):
         return cls(Ref.lib().ref_build_cache(rp.h, budget))
+
+    @classmethod
+    def from_packed(cls, rp, gpu_cache):
+        """Every entry of an engine-built cache in a reference ProbingCache, in one call (the
+        engine's packed slice format; for caches of millions of entries)."""
+        buf = gpu_cache.pack()
+        h = Ref.lib().ref_cache_from_packed(rp.h, _p(buf), int(buf.size))
+        if not h:
+            raise ValueError("packed cache does not match its size")
+        return cls(h)
 
     @classmethod
     def from_gpu(cls, rp, gpu_cache):

@@ -375,6 +375,69 @@ void ref_cache_set_entry(void* cv, int v, const int* hdr7, const double* br4, co
   }
 }
 
+// A reference ProbingCache holding every entry of a packed engine cache (bp_cache_pack layout:
+// header {ne, nd, n_fallback, certified}, per entry {i32 var, i32 kind, u8 feas[2], u8 force[2],
+// f64 branch[4], i64 count[2]}, then the deltas SoA) -- the bulk form of ref_cache_set_entry.
+void* ref_cache_from_packed(const void* pv, const char* buf, long long bytes)
+{
+  const auto& p = *static_cast<const ProblemDef*>(pv);
+  auto* c       = new RefCache();
+  c->cache.root = BoundsState(p);
+  c->cache.entries.resize(p.n_vars);
+  long long hdr[4];
+  std::memcpy(hdr, buf, 32);
+  const long long ne = hdr[0], nd = hdr[1];
+  if (bytes < 32 + ne * 60 + nd * 20) {
+    delete c;
+    return nullptr;
+  }
+  const char* q   = buf + 32;
+  const char* dvp = buf + 32 + ne * 60;
+  const char* dlp = dvp + 4 * nd;
+  const char* dup = dlp + 8 * nd;
+  long long off   = 0;
+  for (long long e = 0; e < ne; ++e, q += 60) {
+    int var, kind;
+    unsigned char feas[2], force[2];
+    double br[4];
+    long long cnt[2];
+    std::memcpy(&var, q, 4);
+    std::memcpy(&kind, q + 4, 4);
+    std::memcpy(feas, q + 8, 2);
+    std::memcpy(force, q + 10, 2);
+    std::memcpy(br, q + 12, 32);
+    std::memcpy(cnt, q + 44, 16);
+    ProbeEntry x;
+    x.var               = var;
+    x.kind              = static_cast<BranchKind>(kind);
+    x.forces_down       = force[0] != 0;
+    x.forces_up         = force[1] != 0;
+    x.down.feasible     = feas[0] != 0;
+    x.up.feasible       = feas[1] != 0;
+    x.down.branch_lower = br[0];
+    x.down.branch_upper = br[1];
+    x.up.branch_lower   = br[2];
+    x.up.branch_upper   = br[3];
+    for (int side = 0; side < 2; ++side)
+      for (long long j = 0; j < cnt[side]; ++j, ++off) {
+        int dv;
+        double lo, up;
+        std::memcpy(&dv, dvp + 4 * off, 4);
+        std::memcpy(&lo, dlp + 8 * off, 8);
+        std::memcpy(&up, dup + 8 * off, 8);
+        (side ? x.up : x.down).deltas.push_back({dv, lo, up});
+      }
+    c->cache.entries[var] = std::move(x);
+  }
+  for (const auto& x : c->cache.entries) {
+    if (!x) continue;
+    c->cache.n_probed++;
+    if (!x->down.feasible) c->cache.n_infeasible_branches++;
+    if (!x->up.feasible) c->cache.n_infeasible_branches++;
+  }
+  return c;
+}
+
 // probing.hpp:292. Writes merged bounds; returns #conflicts; fills conflicts (pairs) and
 // evicted list (count in *n_evicted).
 int ref_assemble_bulk_warm_start(const void* cv, const int* vars, const double* vals, int nassign,

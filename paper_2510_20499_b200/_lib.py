@@ -119,6 +119,8 @@ _SIGS = [
                                      C.POINTER(C.c_void_p)]),
     ("bp_prioritize_probe_vars", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
     ("bp_build_cache", C.c_int, [C.c_void_p, C.c_double, C.POINTER(C.c_void_p)]),
+    ("bp_cache_block_branches", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    ("bp_cache_work", C.c_int, [C.c_void_p, C.c_void_p]),
     ("bp_build_cache_multi", C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p, C.c_int32,
                                        C.POINTER(C.c_void_p), C.c_void_p]),
     ("bp_cache_destroy", C.c_int, [C.c_void_p]),

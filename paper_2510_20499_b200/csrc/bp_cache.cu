@@ -52,21 +52,6 @@ int branch_spec(double lo, double up, double* s)
   return 0;
 }
 
-__global__ void k_diff(const double2* b, const double2* root, int n, int* cnt, int cap, int* var,
-                       double* lo, double* up)
-{
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const double2 x = b[i], r = root[i];
-    if (x.x != r.x || x.y != r.y) {
-      const int p = atomicAdd(cnt, 1);
-      if (p < cap) {
-        var[p] = i;
-        lo[p]  = x.x;
-        up[p]  = x.y;
-      }
-    }
-  }
-}
 
 Limits default_limits()
 {
@@ -96,184 +81,6 @@ __global__ void k_pack_pool(int nt, const int* cnt, const long long* off, const 
       oup[d + j]  = pup[o + j];
     }
   }
-}
-
-struct Branch {
-  int feasible = 1;
-  std::vector<int> var;  // deltas of engine branches
-  std::vector<double> lo, up;
-  long long pool_off = -1;  // deltas of batched branches: range of the flat host pool
-  int pool_cnt       = 0;
-};
-
-// Full-engine branch (probing.hpp:194-219 verbatim semantics, any root).
-Branch engine_branch(Problem& P, const DBuf<double2>& d_root, int v, double blo, double bup,
-                     const std::vector<double>& root, cudaStream_t s)
-{
-  Branch br;
-  // std::max(root.lower(v), branch_lo) / std::min(root.upper(v), branch_up)
-  const double nlo = (root[2 * v] < blo) ? blo : root[2 * v];
-  const double nup = (bup < root[2 * v + 1]) ? bup : root[2 * v + 1];
-  if (nlo > nup) {
-    br.feasible = 0;
-    return br;
-  }
-  BP_CUDA(cudaMemcpyAsync(P.st.bounds, d_root.p, sizeof(double2) * P.n, cudaMemcpyDeviceToDevice, s));
-  const double2 nb = make_double2(nlo, nup);
-  BP_CUDA(cudaMemcpyAsync(P.st.bounds + v, &nb, sizeof(double2), cudaMemcpyHostToDevice, s));
-  BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
-  const RunResult r = run_engine(P, MODE_PROPAGATE, true, default_limits(), s);
-  if (r.status == BP_STATUS_INFEASIBLE) {
-    br.feasible = 0;
-    return br;
-  }
-  int cap = 1 << 16;
-  for (;;) {
-    DBuf<int> cnt, var;
-    DBuf<double> dl, du;
-    cnt.alloc(1);
-    var.alloc(cap);
-    dl.alloc(cap);
-    du.alloc(cap);
-    BP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
-    k_diff<<<256, 256, 0, s>>>(P.st.bounds, d_root.p, P.n, cnt.p, cap, var.p, dl.p, du.p);
-    BP_CUDA(cudaGetLastError());
-    int h = 0;
-    BP_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BP_CUDA(cudaStreamSynchronize(s));
-    if (h > cap) {
-      cap = h;
-      continue;
-    }
-    std::vector<int> vv(h);
-    std::vector<double> l(h), u(h);
-    if (h) {
-      BP_CUDA(cudaMemcpy(vv.data(), var.p, sizeof(int) * h, cudaMemcpyDeviceToHost));
-      BP_CUDA(cudaMemcpy(l.data(), dl.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
-      BP_CUDA(cudaMemcpy(u.data(), du.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
-    }
-    std::vector<int> ord(h);
-    std::iota(ord.begin(), ord.end(), 0);
-    std::sort(ord.begin(), ord.end(), [&](int a, int b) { return vv[a] < vv[b]; });
-    for (int j : ord) {
-      br.var.push_back(vv[j]);
-      br.lo.push_back(l[j]);
-      br.up.push_back(u[j]);
-    }
-    return br;
-  }
-}
-
-// Restores the root state after a frontier-start branch: the bounds of every variable that
-// differs from the root, and the activity records of every row containing one (the only rows
-// whose activity the branch can have changed: dirty rows are rows of changed variables).
-__global__ void k_restore(DevProblem P, double2* b, const double2* root, const RowRec* root_rec,
-                          const double2* root_aux, RowRec* rec, double2* aux, const int* var, int h)
-{
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nw   = (gridDim.x * blockDim.x) >> 5;
-  for (int j = warp; j < h; j += nw) {
-    const int i = var[j];
-    if (lane == 0) b[i] = root[i];
-    for (int e = P.col_start[i] + lane; e < P.col_start[i + 1]; e += 32) {
-      const int k = P.col_row[e];
-      rec[k]      = root_rec[k];
-      aux[k]      = root_aux[k];
-    }
-  }
-}
-
-// Device scratch of the fallback branches (allocated once per probe_vars call).
-struct FallbackBufs {
-  DBuf<int> cnt, var;
-  DBuf<double> lo, up;
-  DBuf<RowRec> root_rec;
-  DBuf<double2> root_aux;
-  int cap = 0;
-};
-
-// Diff of P.st.bounds against the root, ascending by var (probing.hpp:213-217).
-void diff_root(Problem& P, const DBuf<double2>& d_root, FallbackBufs& F, cudaStream_t s,
-               std::vector<int>& vv, std::vector<double>& l, std::vector<double>& u)
-{
-  if (F.cap == 0) {
-    F.cap = 1 << 16;
-    F.cnt.alloc(1);
-    F.var.alloc(F.cap);
-    F.lo.alloc(F.cap);
-    F.up.alloc(F.cap);
-  }
-  for (;;) {
-    BP_CUDA(cudaMemsetAsync(F.cnt.p, 0, sizeof(int), s));
-    k_diff<<<592, 256, 0, s>>>(P.st.bounds, d_root.p, P.n, F.cnt.p, F.cap, F.var.p, F.lo.p, F.up.p);
-    BP_CUDA(cudaGetLastError());
-    int h = 0;
-    BP_CUDA(cudaMemcpyAsync(&h, F.cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BP_CUDA(cudaStreamSynchronize(s));
-    if (h > F.cap) {
-      F.cap = h;
-      F.var.alloc(F.cap);
-      F.lo.alloc(F.cap);
-      F.up.alloc(F.cap);
-      continue;
-    }
-    std::vector<int> v(h);
-    std::vector<double> a(h), b(h);
-    if (h) {
-      BP_CUDA(cudaMemcpy(v.data(), F.var.p, sizeof(int) * h, cudaMemcpyDeviceToHost));
-      BP_CUDA(cudaMemcpy(a.data(), F.lo.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
-      BP_CUDA(cudaMemcpy(b.data(), F.up.p, sizeof(double) * h, cudaMemcpyDeviceToHost));
-    }
-    std::vector<int> ord(h);
-    std::iota(ord.begin(), ord.end(), 0);
-    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return v[x] < v[y]; });
-    vv.clear();
-    l.clear();
-    u.clear();
-    for (int j : ord) {
-      vv.push_back(v[j]);
-      l.push_back(a[j]);
-      u.push_back(b[j]);
-    }
-    return;
-  }
-}
-
-// Branch on the full engine from a CERTIFIED root, starting from the frontier rows(v) (exact:
-// SURVEY §8a A12). Invariant between calls: P.st.bounds = root, P.st.rec/aux = root activities;
-// restored sparsely afterwards (k_restore) instead of O(n + m) copies.
-Branch engine_branch_cert(Problem& P, const DBuf<double2>& d_root, FallbackBufs& F, int v,
-                          double blo, double bup, const std::vector<double>& root, cudaStream_t s)
-{
-  Branch br;
-  const double nlo = (root[2 * v] < blo) ? blo : root[2 * v];
-  const double nup = (bup < root[2 * v + 1]) ? bup : root[2 * v + 1];
-  if (nlo > nup) {
-    br.feasible = 0;
-    return br;
-  }
-  const double2 nb = make_double2(nlo, nup);
-  BP_CUDA(cudaMemcpyAsync(P.st.bounds + v, &nb, sizeof(double2), cudaMemcpyHostToDevice, s));
-  BP_CUDA(cudaMemsetAsync(P.st.ctl, 0, sizeof(Ctl), s));
-  const int changed[1] = {v};
-  stage_changed(P, changed, 1, s);
-  const RunResult r = run_engine(P, MODE_PROPAGATE, true, default_limits(), s, ENGINE_START_FRONTIER);
-  std::vector<int> vv;
-  std::vector<double> l, u;
-  diff_root(P, d_root, F, s, vv, l, u);
-  if (!vv.empty()) {
-    k_restore<<<148, 256, 0, s>>>(P.dev(), P.st.bounds, d_root.p, F.root_rec.p, F.root_aux.p,
-                                  P.st.rec, P.st.aux, F.var.p, (int)vv.size());
-    BP_CUDA(cudaGetLastError());
-  }
-  if (r.status == BP_STATUS_INFEASIBLE) {
-    br.feasible = 0;
-    return br;
-  }
-  br.var = std::move(vv);
-  br.lo  = std::move(l);
-  br.up  = std::move(u);
-  return br;
 }
 
 }  // namespace
@@ -316,12 +123,40 @@ struct ProbeWs {
   DBuf<int> dvar, dcur, dstat, dcnt, dscan, qvar, pvar;
   DBuf<double> dlo, dup, qlo, qup, plo, pup;
   DBuf<long long> doff;
-  DBuf<unsigned long long> dpc;
+  DBuf<unsigned long long> dpc, dwork;
   DBuf<unsigned char> dtmp;
   PinBuf h_var, h_lo, h_up, h_st, h_cn, h_qv, h_ql, h_qu, h_root;
   std::vector<int> tv, tslot;  // task lists, reused across calls (no first-touch page faults)
   std::vector<double> tlo, tup;
+  DBuf<char> blk;              // dense per-block state of the block-per-branch kernel
+  BlockScratch bs;
 };
+
+// The block kernel's scratch: as many blocks as one per SM, within a quarter of the free memory
+// (and at most 24 GB); zeroed once -- its stamps compare against tags that only grow.
+BlockScratch& block_scratch(Problem& P, ProbeWs& W)
+{
+  if (W.bs.base && W.bs.n == P.n && W.bs.m == P.m) return W.bs;
+  int sms = 0;
+  BP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
+  size_t freeb = 0, totb = 0;
+  BP_CUDA(cudaMemGetInfo(&freeb, &totb));
+  const size_t per = (block_scratch_bytes(P.n, P.m) + 255) / 256 * 256;
+  const size_t cap = std::min<size_t>(freeb / 4, 24ull << 30);
+  const int nb     = (int)std::max<size_t>(1, std::min<size_t>((size_t)sms, cap / per));
+  W.blk.alloc(per * nb);
+  BP_CUDA(cudaMemset(W.blk.p, 0, per * nb));
+  W.bs.nblocks = nb;
+  W.bs.n       = P.n;
+  W.bs.m       = P.m;
+  W.bs.stride  = per;
+  W.bs.base    = W.blk.p;
+  for (int b = 0; b < nb; ++b) {  // tags start at 1 (0 = never stamped)
+    const unsigned one = 1;
+    BP_CUDA(cudaMemcpy(W.bs.for_block(b).tagc, &one, sizeof(one), cudaMemcpyHostToDevice));
+  }
+  return W.bs;
+}
 
 HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vector<int>& vars,
                      double budget_sec)
@@ -411,10 +246,8 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
     long long pool_off = -1;
     int pool_cnt       = 0;
     int feasible       = 1;
-    int eng            = -1;
   };
   std::vector<BrRef> res(2 * (size_t)ne);
-  std::vector<Branch> eng;
   std::vector<int> hp_var;  // batched branches' deltas (flat, by chunk)
   std::vector<double> hp_lo, hp_up;
   std::vector<uint8_t> done(2 * (size_t)ne, 0);
@@ -422,166 +255,174 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   for (int slot : tslot) done[slot] = 0;
 
   const int ntask = (int)tv.size();
-  std::vector<int> fallback;
-  if (certified && ntask) {
-    // chunks small enough for the time budget to be honoured between them
-    const int chunk = std::isfinite(budget_sec) && budget_sec < 1e6 ? (1 << 14) : (1 << 20);
-    auto& dvar = W.dvar;
-    auto& dcur = W.dcur;
-    auto& dstat = W.dstat;
-    auto& dcnt = W.dcnt;
-    auto& dlo = W.dlo;
-    auto& dup = W.dup;
-    auto& doff = W.doff;
-    auto& dpc = W.dpc;
-    auto& dscan = W.dscan;
-    auto& qvar = W.qvar;
-    auto& qlo = W.qlo;
-    auto& qup = W.qup;
-    auto& dtmp = W.dtmp;
-    auto& pvar = W.pvar;
-    auto& plo = W.plo;
-    auto& pup = W.pup;
-    // initial delta pool: >= 4 per branch (a chunk whose deltas overflow it reruns once, sized)
-    grow(pvar, 4ull * std::min(ntask, chunk) + 4096);
-    grow(plo, pvar.n);
-    grow(pup, pvar.n);
-    long long pool_cap = (long long)std::min(pvar.n, std::min(plo.n, pup.n));
-    ProbeRoot R{d_root.p, P.st.rec, P.st.aux};
+  auto& dvar  = W.dvar;
+  auto& dcur  = W.dcur;
+  auto& dstat = W.dstat;
+  auto& dcnt  = W.dcnt;
+  auto& dlo   = W.dlo;
+  auto& dup   = W.dup;
+  auto& doff  = W.doff;
+  auto& dpc   = W.dpc;
+  auto& dscan = W.dscan;
+  auto& qvar  = W.qvar;
+  auto& qlo   = W.qlo;
+  auto& qup   = W.qup;
+  auto& dtmp  = W.dtmp;
+  auto& pvar  = W.pvar;
+  auto& plo   = W.plo;
+  auto& pup   = W.pup;
+  // chunks small enough for the time budget to be honoured between them
+  const int chunk = std::isfinite(budget_sec) && budget_sec < 1e6 ? (1 << 14) : (1 << 20);
+  grow(pvar, 4ull * std::min(std::max(ntask, 1), chunk) + 4096);
+  grow(plo, pvar.n);
+  grow(pup, pvar.n);
+  long long pool_cap = (long long)std::min(pvar.n, std::min(plo.n, pup.n));
+  ProbeRoot R{d_root.p, P.st.rec, P.st.aux};
+  // One batch of tasks (indices into tv / tlo / tup) on the warp kernel (block = false) or the
+  // block-per-branch kernel (block = true): results into `res` / the flat host pool; the tasks the
+  // warp kernel could not hold (overlay overflow) are appended to `overflow`.
+  std::vector<int> hidx;
+  auto run_batch = [&](const int* tidx, int nt, bool block, int full_first, std::vector<int>& overflow) {
+    const double tb0 = elapsed();
+    grow(dvar, nt);
+    grow(dlo, nt);
+    grow(dup, nt);
+    grow(dcur, 1);
+    grow(dstat, nt);
+    grow(dcnt, nt);
+    grow(doff, nt);
+    grow(dpc, 1);
+    {
+      int* hv    = W.h_var.get<int>(nt);
+      double* hl = W.h_lo.get<double>(nt);
+      double* hu = W.h_up.get<double>(nt);
+      for (int j = 0; j < nt; ++j) {
+        hv[j] = tv[tidx[j]];
+        hl[j] = tlo[tidx[j]];
+        hu[j] = tup[tidx[j]];
+      }
+      BP_CUDA(cudaMemcpyAsync(dvar.p, hv, sizeof(int) * nt, cudaMemcpyHostToDevice, s));
+      BP_CUDA(cudaMemcpyAsync(dlo.p, hl, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
+      BP_CUDA(cudaMemcpyAsync(dup.p, hu, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
+    }
+    for (;;) {
+      BP_CUDA(cudaMemsetAsync(dcur.p, 0, sizeof(int), s));
+      BP_CUDA(cudaMemsetAsync(dpc.p, 0, sizeof(unsigned long long), s));
+      grow(W.dwork, 5);
+      BP_CUDA(cudaMemsetAsync(W.dwork.p, 0, 5 * sizeof(unsigned long long), s));
+      ProbeBatch B{nt, dvar.p, dlo.p, dup.p, dcur.p, dstat.p, dcnt.p, doff.p, dpc.p,
+                   pool_cap, pvar.p, plo.p, pup.p, W.dwork.p};
+      BP_CUDA(cudaEventRecord(P.ev0, s));
+      if (block) probe_block_launch(P, R, B, default_limits(), block_scratch(P, W), full_first, s);
+      else probe_launch(P, R, B, default_limits(), s);
+      BP_CUDA(cudaEventRecord(P.ev1, s));
+      unsigned long long used = 0;
+      const double tb1 = elapsed();
+      BP_CUDA(cudaMemcpyAsync(&used, dpc.p, sizeof(used), cudaMemcpyDeviceToHost, s));
+      BP_CUDA(cudaStreamSynchronize(s));
+      const double tb2 = elapsed();
+      float ms = 0.f;
+      BP_CUDA(cudaEventElapsedTime(&ms, P.ev0, P.ev1));
+      C.probe_ms += ms;
+      if ((long long)used > pool_cap) {  // grow the delta pool and rerun the batch
+        pool_cap = (long long)used + 4096;
+        pvar.alloc(pool_cap);
+        plo.alloc(pool_cap);
+        pup.alloc(pool_cap);
+        continue;
+      }
+      {
+        unsigned long long wkh[5];
+        BP_CUDA(cudaMemcpy(wkh, W.dwork.p, sizeof(wkh), cudaMemcpyDeviceToHost));
+        for (int q = 0; q < 5; ++q) C.work[q] += wkh[q];
+      }
+      int* st = W.h_st.get<int>(nt);
+      int* cn = W.h_cn.get<int>(nt);
+      BP_CUDA(cudaMemcpyAsync(st, dstat.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
+      BP_CUDA(cudaMemcpyAsync(cn, dcnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
+      // the batch's deltas in task order (device scan + pack), appended to the flat host pool
+      const long long hbase = (long long)hp_var.size();
+      hp_var.resize(hbase + used);
+      hp_lo.resize(hbase + used);
+      hp_up.resize(hbase + used);
+      int* hqv    = nullptr;
+      double* hql = nullptr;
+      double* hqu = nullptr;
+      if (used) {
+        grow(dscan, nt);
+        size_t nb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, nb, dcnt.p, dscan.p, nt, s);
+        if (nb > dtmp.n) dtmp.alloc(nb);
+        nb = dtmp.n;
+        cub::DeviceScan::ExclusiveSum(dtmp.p, nb, dcnt.p, dscan.p, nt, s);
+        grow(qvar, used);
+        grow(qlo, used);
+        grow(qup, used);
+        k_pack_pool<<<(int)std::min<long long>(4096, (nt + 255) / 256), 256, 0, s>>>(
+            nt, dcnt.p, doff.p, dscan.p, pvar.p, plo.p, pup.p, qvar.p, qlo.p, qup.p);
+        BP_CUDA(cudaGetLastError());
+        hqv = W.h_qv.get<int>(used);
+        hql = W.h_ql.get<double>(used);
+        hqu = W.h_qu.get<double>(used);
+        BP_CUDA(cudaMemcpyAsync(hqv, qvar.p, sizeof(int) * used, cudaMemcpyDeviceToHost, s));
+        BP_CUDA(cudaMemcpyAsync(hql, qlo.p, sizeof(double) * used, cudaMemcpyDeviceToHost, s));
+        BP_CUDA(cudaMemcpyAsync(hqu, qup.p, sizeof(double) * used, cudaMemcpyDeviceToHost, s));
+      }
+      BP_CUDA(cudaStreamSynchronize(s));
+      if (used) {
+        std::memcpy(hp_var.data() + hbase, hqv, sizeof(int) * used);
+        std::memcpy(hp_lo.data() + hbase, hql, sizeof(double) * used);
+        std::memcpy(hp_up.data() + hbase, hqu, sizeof(double) * used);
+      }
+      const double tb3 = elapsed();
+      if (prof)
+        fprintf(stderr, "[bp probe] %s batch of %d: uploads+launch %.2f ms, kernel wait %.2f ms, pack+D2H %.2f ms\n",
+                block ? "block" : "warp", nt, 1e3 * (tb1 - tb0), 1e3 * (tb2 - tb1), 1e3 * (tb3 - tb2));
+      long long run = hbase;
+      for (int j = 0; j < nt; ++j) {
+        const int t = tidx[j];
+        BrRef& br   = res[tslot[t]];
+        if (st[j] == 0) {
+          br.feasible    = 1;
+          br.pool_off    = run;
+          br.pool_cnt    = cn[j];
+          run += cn[j];
+          done[tslot[t]] = 1;
+        } else if (st[j] == 1) {
+          br.feasible    = 0;
+          done[tslot[t]] = 1;
+        } else {
+          overflow.push_back(t);
+        }
+        if (block && st[j] <= 1) C.n_block++;
+      }
+      return;
+    }
+  };
+  std::vector<int> fallback;  // tasks for the block-per-branch kernel
+  if (certified) {
     for (int t0 = 0; t0 < ntask; t0 += chunk) {
       if (t0 > 0 && elapsed() >= budget_sec) break;
       const int nt = std::min(chunk, ntask - t0);
-      const double tb0 = elapsed();
-      grow(dvar, nt);
-      grow(dlo, nt);
-      grow(dup, nt);
-      grow(dcur, 1);
-      grow(dstat, nt);
-      grow(dcnt, nt);
-      grow(doff, nt);
-      grow(dpc, 1);
-      {
-        int* hv    = W.h_var.get<int>(nt);
-        double* hl = W.h_lo.get<double>(nt);
-        double* hu = W.h_up.get<double>(nt);
-        std::memcpy(hv, tv.data() + t0, sizeof(int) * nt);
-        std::memcpy(hl, tlo.data() + t0, sizeof(double) * nt);
-        std::memcpy(hu, tup.data() + t0, sizeof(double) * nt);
-        BP_CUDA(cudaMemcpyAsync(dvar.p, hv, sizeof(int) * nt, cudaMemcpyHostToDevice, s));
-        BP_CUDA(cudaMemcpyAsync(dlo.p, hl, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
-        BP_CUDA(cudaMemcpyAsync(dup.p, hu, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
-      }
-      for (;;) {
-        BP_CUDA(cudaMemsetAsync(dcur.p, 0, sizeof(int), s));
-        BP_CUDA(cudaMemsetAsync(dpc.p, 0, sizeof(unsigned long long), s));
-        ProbeBatch B{nt, dvar.p, dlo.p, dup.p, dcur.p, dstat.p, dcnt.p, doff.p, dpc.p,
-                     pool_cap, pvar.p, plo.p, pup.p};
-        BP_CUDA(cudaEventRecord(P.ev0, s));
-        probe_launch(P, R, B, default_limits(), s);
-        BP_CUDA(cudaEventRecord(P.ev1, s));
-        unsigned long long used = 0;
-        const double tb1 = elapsed();
-        BP_CUDA(cudaMemcpyAsync(&used, dpc.p, sizeof(used), cudaMemcpyDeviceToHost, s));
-        BP_CUDA(cudaStreamSynchronize(s));
-        const double tb2 = elapsed();
-        float ms = 0.f;
-        BP_CUDA(cudaEventElapsedTime(&ms, P.ev0, P.ev1));
-        C.probe_ms += ms;
-        if ((long long)used > pool_cap) {  // grow the delta pool and rerun the chunk
-          pool_cap = (long long)used + 4096;
-          pvar.alloc(pool_cap);
-          plo.alloc(pool_cap);
-          pup.alloc(pool_cap);
-          continue;
-        }
-        int* st = W.h_st.get<int>(nt);
-        int* cn = W.h_cn.get<int>(nt);
-        BP_CUDA(cudaMemcpyAsync(st, dstat.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
-        BP_CUDA(cudaMemcpyAsync(cn, dcnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
-        // the chunk's deltas in task order (device scan + pack), appended to the flat host pool
-        const long long hbase = (long long)hp_var.size();
-        hp_var.resize(hbase + used);
-        hp_lo.resize(hbase + used);
-        hp_up.resize(hbase + used);
-        int* hqv    = nullptr;
-        double* hql = nullptr;
-        double* hqu = nullptr;
-        if (used) {
-          grow(dscan, nt);
-          size_t nb = 0;
-          cub::DeviceScan::ExclusiveSum(nullptr, nb, dcnt.p, dscan.p, nt, s);
-          if (nb > dtmp.n) dtmp.alloc(nb);
-          nb = dtmp.n;
-          cub::DeviceScan::ExclusiveSum(dtmp.p, nb, dcnt.p, dscan.p, nt, s);
-          grow(qvar, used);
-          grow(qlo, used);
-          grow(qup, used);
-          k_pack_pool<<<(int)std::min<long long>(4096, (nt + 255) / 256), 256, 0, s>>>(
-              nt, dcnt.p, doff.p, dscan.p, pvar.p, plo.p, pup.p, qvar.p, qlo.p, qup.p);
-          BP_CUDA(cudaGetLastError());
-          hqv = W.h_qv.get<int>(used);
-          hql = W.h_ql.get<double>(used);
-          hqu = W.h_qu.get<double>(used);
-          BP_CUDA(cudaMemcpyAsync(hqv, qvar.p, sizeof(int) * used, cudaMemcpyDeviceToHost, s));
-          BP_CUDA(cudaMemcpyAsync(hql, qlo.p, sizeof(double) * used, cudaMemcpyDeviceToHost, s));
-          BP_CUDA(cudaMemcpyAsync(hqu, qup.p, sizeof(double) * used, cudaMemcpyDeviceToHost, s));
-        }
-        BP_CUDA(cudaStreamSynchronize(s));
-        if (used) {
-          std::memcpy(hp_var.data() + hbase, hqv, sizeof(int) * used);
-          std::memcpy(hp_lo.data() + hbase, hql, sizeof(double) * used);
-          std::memcpy(hp_up.data() + hbase, hqu, sizeof(double) * used);
-        }
-        const double tb3 = elapsed();
-        if (prof)
-          fprintf(stderr, "[bp probe] chunk of %d: uploads+launch %.2f ms, kernel wait %.2f ms, pack+D2H %.2f ms\n",
-                  nt, 1e3 * (tb1 - tb0), 1e3 * (tb2 - tb1), 1e3 * (tb3 - tb2));
-        long long run = hbase;
-        for (int j = 0; j < nt; ++j) {
-          const int t = t0 + j;
-          BrRef& br   = res[tslot[t]];
-          if (st[j] == 0) {
-            br.feasible    = 1;
-            br.pool_off    = run;
-            br.pool_cnt    = cn[j];
-            run += cn[j];
-            done[tslot[t]] = 1;
-          } else if (st[j] == 1) {
-            br.feasible    = 0;
-            done[tslot[t]] = 1;
-          } else {
-            fallback.push_back(t);
-          }
-        }
-        break;
-      }
+      hidx.resize(nt);
+      std::iota(hidx.begin(), hidx.end(), t0);
+      run_batch(hidx.data(), nt, false, 0, fallback);
     }
   } else {
     for (int t = 0; t < ntask; ++t) fallback.push_back(t);
   }
   const double t_batch = elapsed();
-  FallbackBufs F;
-  if (certified && !fallback.empty() && P.m) {
-    // snapshot of the root activities (left in P.st.rec / aux by the certification round)
-    F.root_rec.alloc(P.m);
-    F.root_aux.alloc(P.m);
-    BP_CUDA(cudaMemcpyAsync(F.root_rec.p, P.st.rec, sizeof(RowRec) * P.m, cudaMemcpyDeviceToDevice, s));
-    BP_CUDA(cudaMemcpyAsync(F.root_aux.p, P.st.aux, sizeof(double2) * P.m, cudaMemcpyDeviceToDevice, s));
-    BP_CUDA(cudaMemcpyAsync(P.st.bounds, d_root.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
-  }
-  for (int t : fallback) {
+  // block-per-branch kernel: the warp kernel's overflows (frontier start from the certified root)
+  // or every branch of an uncertified root (full first round)
+  for (size_t f0 = 0; f0 < fallback.size(); f0 += chunk) {
     if (elapsed() >= budget_sec) break;
-    eng.push_back(certified ? engine_branch_cert(P, d_root, F, tv[t], tlo[t], tup[t], root, s)
-                            : engine_branch(P, d_root, tv[t], tlo[t], tup[t], root, s));
-    BrRef& br   = res[tslot[t]];
-    br.feasible = eng.back().feasible;
-    br.pool_off = -1;
-    br.eng      = (int)eng.size() - 1;
-    done[tslot[t]] = 1;
-    C.n_fallback++;
+    const int nt = (int)std::min<size_t>(chunk, fallback.size() - f0);
+    std::vector<int> again;
+    run_batch(fallback.data() + f0, nt, true, certified ? 0 : 1, again);
+    if (!again.empty()) throw std::runtime_error("block-per-branch probing returned an overflow");
   }
   const double t_fallback = elapsed();
-  bool all_done = C.n_fallback == 0 && fallback.empty();
+  bool all_done = C.n_fallback == 0 && fallback.empty() && C.n_block == 0;
   for (size_t t = 1; t < tslot.size() && all_done; ++t) all_done = tslot[t] > tslot[t - 1];  // no repeated vars
   for (int e = 0; e < ne && all_done; ++e) all_done = done[2 * e] && done[2 * e + 1];
   if (all_done) {
@@ -593,6 +434,8 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
     out.certified  = certified;
     out.probe_ms   = C.probe_ms;
     out.n_fallback = 0;
+    out.n_block    = C.n_block;
+    std::copy(C.work, C.work + 5, out.work);
     out.entry_of   = std::move(C.entry_of);
     out.e_var      = std::move(C.e_var);
     out.e_kind     = std::move(C.e_kind);
@@ -631,6 +474,8 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   out.certified = certified;
   out.probe_ms  = C.probe_ms;
   out.n_fallback = C.n_fallback;
+  out.n_block    = C.n_block;
+  std::copy(C.work, C.work + 5, out.work);
   out.entry_of.assign(n, -1);
   out.d_off.reserve(2 * (size_t)ne + 1);
   out.d_off.push_back(0);
@@ -662,11 +507,6 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
         out.d_var.insert(out.d_var.end(), hp_var.begin() + o, hp_var.begin() + o + cnt);
         out.d_lo.insert(out.d_lo.end(), hp_lo.begin() + o, hp_lo.begin() + o + cnt);
         out.d_up.insert(out.d_up.end(), hp_up.begin() + o, hp_up.begin() + o + cnt);
-      } else if (b->eng >= 0) {
-        const Branch& eb = eng[b->eng];
-        out.d_var.insert(out.d_var.end(), eb.var.begin(), eb.var.end());
-        out.d_lo.insert(out.d_lo.end(), eb.lo.begin(), eb.lo.end());
-        out.d_up.insert(out.d_up.end(), eb.up.begin(), eb.up.end());
       }
       out.d_off.push_back((long long)out.d_var.size());
     }
@@ -1104,6 +944,22 @@ int bp_build_cache(bp_problem* p, double budget_sec, bp_cache** out)
       c->c = bp::probe_vars(P, root, cand, budget_sec);
     }
     *out = c.release();
+  });
+}
+
+int bp_cache_block_branches(const bp_cache* c, int32_t* n_block)
+{
+  return cguard([&] {
+    need(c && n_block, "null argument");
+    *n_block = c->c.n_block;
+  });
+}
+
+int bp_cache_work(const bp_cache* c, int64_t* work5)
+{
+  return cguard([&] {
+    need(c && work5, "null argument");
+    for (int q = 0; q < 5; ++q) work5[q] = (int64_t)c->c.work[q];
   });
 }
 

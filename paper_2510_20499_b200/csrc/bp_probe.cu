@@ -403,7 +403,7 @@ __device__ __forceinline__ void for_each_entry(PCtx& c, const int* items, int cn
 
 // One probe branch (probing.hpp:194-219 + propagate) on this warp. Returns 0 feasible,
 // 1 infeasible, 2 overflow (caller re-runs on the full engine).
-__device__ int probe_branch(PCtx& c, int v, double blo, double bup)
+__device__ __forceinline__ int probe_branch(PCtx& c, int v, double blo, double bup, unsigned long long (&wk)[5])
 {
   PWarp& w = c.w;
   const int lane = c.lane;
@@ -457,6 +457,20 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
     __syncwarp();
     if (__any_sync(FULL, full) || w.n_dvar > PB_VCAP) return 2;
     ++rounds;
+    {  // work of this round (R, A, V, B): lane-strided lengths, reduced to lane 0
+      unsigned long long a = 0, bsum = 0;
+      for (int j = lane; j < nr; j += 32) a += __ldg(c.P.row_start + w.drow[j] + 1) - __ldg(c.P.row_start + w.drow[j]);
+      for (int j = lane; j < w.n_dvar; j += 32) bsum += __ldg(c.P.col_start + w.dvar[j] + 1) - __ldg(c.P.col_start + w.dvar[j]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(FULL, a, o);
+        bsum += __shfl_xor_sync(FULL, bsum, o);
+      }
+      wk[0] += nr;
+      wk[1] += a;
+      wk[2] += w.n_dvar;
+      wk[3] += bsum;
+    }
     // ---- activities of the dirty rows
     // short rows one per lane; the long ones of each 32-row window warp-cooperatively
     bool ovf = false;
@@ -525,6 +539,7 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
     for (int o = 16; o; o >>= 1) crossed += __shfl_xor_sync(FULL, crossed, o);
     if (crossed > 0) return 1;        // propagation.hpp:448-452
     const int nc = w.n_chg;
+    wk[4] += nc;
     if (nc > PB_CCAP) return 2;
     if (nc == 0) return 0;            // fixpoint (propagation.hpp:453)
     bool bovf = false;
@@ -536,20 +551,24 @@ __device__ int probe_branch(PCtx& c, int v, double blo, double bup)
   }
 }
 
-__global__ void __launch_bounds__(PB_WARPS * 32)
+__global__ void __launch_bounds__(PB_WARPS * 32, 1)
     k_probe(DevProblem P, ProbeRoot R, ProbeBatch B, Limits lim)
 {
   extern __shared__ __align__(16) unsigned char dyn[];
   PSmem& sm      = *reinterpret_cast<PSmem*>(dyn);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PCtx c{P, R, lim, sm.w[warp], lane};
+  unsigned long long wk[5] = {0, 0, 0, 0, 0};  // warp-uniform work counters
   for (;;) {
     int t = 0;
     if (lane == 0) t = atomicAdd(B.cursor, 1);
     t = __shfl_sync(FULL, t, 0);
     if (t >= B.n_task) break;
     const int v      = B.var[t];
-    const int status = probe_branch(c, v, B.lo[t], B.up[t]);
+    unsigned long long bw[5] = {0, 0, 0, 0, 0};
+    const int status = probe_branch(c, v, B.lo[t], B.up[t], bw);
+    if (status != 2)  // overflowing branches are counted by the kernel that reruns them
+      for (int q = 0; q < 5; ++q) wk[q] += bw[q];
     // deltas: overlay entries differing from the root, ascending by var (probing.hpp:213-217)
     PWarp& w = c.w;
     int cnt  = 0;
@@ -596,6 +615,9 @@ __global__ void __launch_bounds__(PB_WARPS * 32)
     }
     __syncwarp();
   }
+  if (lane == 0 && B.work)
+    for (int q = 0; q < 5; ++q)
+      if (wk[q]) atomicAdd(B.work + q, wk[q]);
 }
 
 }  // namespace

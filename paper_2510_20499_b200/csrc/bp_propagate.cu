@@ -166,20 +166,23 @@ __device__ __forceinline__ int warp_fetch(Ctx& c, int* cursor, int step)
   return __shfl_sync(FULL, t, 0);
 }
 
-// Work cursor over `lim` items in chunks of `step`. When the whole range fits one chunk per warp
-// of the grid, warps take chunks statically (no atomics: an empty or small list costs nothing);
-// otherwise a grid-wide atomic cursor with the next fetch in flight while the current chunk runs
-// (and no fetch past the end).
+// Work cursor over `lim` items in chunks of `step`: a grid-wide atomic cursor with the next fetch
+// in flight while the current chunk runs (and no fetch past the end). With `may_static`, when the
+// whole range fits one chunk per warp of the grid, warps take chunks statically (no atomics: an
+// empty or small list costs nothing) -- only for tasks no other warp waits on: a task that spins on
+// another task's result (heavy segment folds on their pieces) must follow the dynamic order, in
+// which every producer is claimed by a running warp before any consumer is (progress without
+// grid-wide co-residency, e.g. next to other streams' kernels).
 struct Prefetch {
   Ctx& c;
   int* cur;
   int step, t, nx, lim;
   bool stat;
-  __device__ Prefetch(Ctx& c_, int* cur_, int step_, int lim_ = 0x3FFFFFFF)
+  __device__ Prefetch(Ctx& c_, int* cur_, int step_, int lim_ = 0x3FFFFFFF, bool may_static = false)
       : c(c_), cur(cur_), step(step_), lim(lim_)
   {
     const int nw = gridDim.x * kWarps;
-    stat         = lim <= 0 || (long long)lim <= (long long)step * nw;
+    stat         = lim <= 0 || (may_static && (long long)lim <= (long long)step * nw);
     if (stat) {
       t = lim <= 0 ? 0x3FFFFFFF : (blockIdx.x * kWarps + c.warp) * step;
     } else {
@@ -950,16 +953,16 @@ __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
   const int ns = P.n_srtile, nsl = P.n_srow_long;
   if (ds != 0) {  // dirty-filtered round: the engine's list of dirty slices, 4 per fetch
     const int nd = ldv(&S.ctl->df_cnt[0]);
-    for (Prefetch it_t(c, &pc->cur_a, 4, nd); it_t.t < nd; it_t.advance())
+    for (Prefetch it_t(c, &pc->cur_a, 4, nd, true); it_t.t < nd; it_t.advance())
       for (int q = it_t.t; q < min(nd, it_t.t + 4); ++q) sell_slice(c, __ldcg(S.df_slice + q), cand);
     return;
   }
-  for (Prefetch it_t(c, &pc->cur_s, 1, nsl); it_t.t < nsl; it_t.advance()) {
+  for (Prefetch it_t(c, &pc->cur_s, 1, nsl, true); it_t.t < nsl; it_t.advance()) {
     const long long c0 = S.dbg ? clock64() : 0;
     sell_slice(c, it_t.t, cand);
     dbg_task(c, 1, c0);
   }
-  for (Prefetch it_t(c, &pc->cur_a, 4, ns - nsl); nsl + it_t.t < ns; it_t.advance()) {
+  for (Prefetch it_t(c, &pc->cur_a, 4, ns - nsl, true); nsl + it_t.t < ns; it_t.advance()) {
     const long long c0 = S.dbg ? clock64() : 0;
     for (int q = nsl + it_t.t; q < min(ns, nsl + it_t.t + 4); ++q) sell_slice(c, q, cand);
     dbg_task(c, 1, c0);
@@ -996,14 +999,14 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       dbg_task(c, 0, c0);
     }
     if (ds == 0) {
-      for (Prefetch it_t(c, &pc->cur_g, 4, nf - nfh); nfh + it_t.t < nf; it_t.advance()) {
+      for (Prefetch it_t(c, &pc->cur_g, 4, nf - nfh, true); nfh + it_t.t < nf; it_t.advance()) {
         const long long c0 = S.dbg ? clock64() : 0;
         group_fold(c, nfh + it_t.t, min(4, nf - nfh - it_t.t), cand);
         dbg_task(c, 4, c0);
       }
     } else {  // dirty-filtered round: the engine's list of dirty groups of four medium rows
       const int nd = ldv(&S.ctl->df_cnt[1]);
-      for (Prefetch it_t(c, &pc->cur_g, 1, nd); it_t.t < nd; it_t.advance()) {
+      for (Prefetch it_t(c, &pc->cur_g, 1, nd, true); it_t.t < nd; it_t.advance()) {
         const int t0 = 4 * __ldcg(S.df_group + it_t.t);
         group_fold(c, nfh + t0, min(4, nf - nfh - t0), cand);
       }

@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -755,8 +756,12 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
     bp_rounding_outcome o;
     std::memset(&o, 0, sizeof(o));
     std::vector<double> pv0, pv1;
+    // measurement knob (bench.py's like-for-like rate against the reference's first K bulks):
+    // BP_ROUND_MAX_BULKS=K stops after K committed bulks, reported as a timeout
+    const char* mb_env     = std::getenv("BP_ROUND_MAX_BULKS");
+    const long long max_bk = mb_env ? std::atoll(mb_env) : 0;
     while (X.n_unset > 0) {
-      if (expired()) {
+      if (expired() || (max_bk > 0 && o.bulks_committed >= max_bk)) {
         o.timed_out = 1;
         break;
       }

@@ -100,6 +100,13 @@ class ProbingCache:
         self.n_fallback = nfb.value
         self.certified = bool(cert.value)
         self.probe_ms = ms.value
+        nb = C.c_int32()
+        _lib.check(_lib.lib().bp_cache_block_branches(self.h, C.byref(nb)))
+        self.n_block = nb.value  # branches run by the block-per-branch kernel
+        wk = np.zeros(5, np.int64)
+        _lib.check(_lib.lib().bp_cache_work(self.h, _lib.ptr(wk)))
+        # Σ over branches and rounds of |R|, row nnz of R, |V|, col nnz of V, |C|
+        self.work = [int(x) for x in wk]
         self._root = None
         self._memo = {}
 

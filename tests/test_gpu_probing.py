@@ -125,14 +125,15 @@ def test_c1_probing_from_fixpoint(oracle_built):
         _check_entry(p, cache, v, pp.probe_variable(root, v), "C1")
 
 
-def test_c1_probing_uncertified_root_falls_back_exactly(oracle_built):
-    """Original bounds of C1 are not a fixpoint: every branch runs on the full engine."""
+def test_c1_probing_uncertified_root_block_kernel(oracle_built):
+    """Original bounds of C1 are not a fixpoint: every branch runs on the block-per-branch kernel
+    with a full first round (propagation.hpp:442), no engine fallback."""
     from oracle.bind import PortProblem
     p = synth.c1(n=1500, m=1500)
     pp = PortProblem(p)
-    vars_ = [i for i in range(p.n_vars) if p.is_integer[i]][:40]
+    vars_ = [i for i in range(p.n_vars) if p.is_integer[i]][:400]
     cache = probe_variables(p, None, vars_)
-    assert not cache.certified and cache.n_fallback > 0
+    assert not cache.certified and cache.n_fallback == 0 and cache.n_block > 0
     root = p.root_bounds()
     for v in vars_:
         _check_entry(p, cache, v, pp.probe_variable(root, v), "C1-orig")
@@ -146,7 +147,7 @@ def test_c3_probing_sample(oracle_built):
     vars_ = list(range(20_000))
     cache = probe_variables(p, None, vars_)
     assert cache.certified and cache.n_probed == 20_000
-    assert cache.n_fallback < 20  # overlay overflows re-run exactly on the full engine
+    assert cache.n_fallback == 0  # overlay overflows re-run exactly on the block kernel
     root = p.root_bounds()
     for v in rng.choice(20_000, size=60, replace=False):
         _check_entry(p, cache, int(v), pp.probe_variable(root, int(v)), "C3")
@@ -199,3 +200,24 @@ def test_c3_full_size_vs_reference(oracle_built):
     rc = RefCache.probe_into(RefProblem.from_def(p), p.n_vars, p.root_bounds(), vars_)
     checked, bad = cache_mismatches(cache, rc, vars_)
     assert checked == 512 and bad == [], bad[:10]
+
+
+def test_c4_long_frontiers_on_block_kernel(oracle_built):
+    """C4 shape (knapsack rows of 3000 entries, assignment blocks) from its presolved fixpoint:
+    branches whose frontier reaches a long row overflow the warp overlays and run on the
+    block-per-branch kernel; every sampled entry equals the reference's probe_variable."""
+    from oracle.bind import Ref, RefCache, RefProblem, cache_mismatches
+    if not Ref.available():
+        pytest.skip("reference library missing")
+    from paper_2510_20499_b200 import propagate
+    p0, _ = synth.c4(n=30_000, m=30_000, n_long=20, long_len=6000)
+    b = BoundsState(p0)
+    propagate(p0, b)
+    p = synth.with_bounds(p0, b.raw())
+    free_int = [v for v in range(p.n_vars) if p.is_integer[v] and p.var_lower[v] != p.var_upper[v]]
+    cache = probe_variables(p, None, free_int)
+    assert cache.certified and cache.n_fallback == 0 and cache.n_block > 0
+    rng = np.random.default_rng(44)
+    sample = sorted(set(rng.choice(free_int, size=200, replace=False).tolist()))
+    checked, bad = cache_mismatches(cache, RefCache.probe_into(RefProblem.from_def(p), p.n_vars, p.root_bounds(), sample), sample)
+    assert checked == len(sample) and bad == [], bad[:10]

@@ -1,0 +1,3 @@
+O=gpurun_out/it7; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_probing.py tests/test_gpu_multi.py -x -q --durations=8 > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
+BP_PROBE_PROFILE=1 timeout 900 python tools/round_profile.py --deadline 30 > $O/round.log 2>&1; echo "round exit $?" >> $O/round.log
