@@ -373,16 +373,16 @@ class RefCache:
         return hdr, br, sides
 
     @classmethod
-    def probe_into(cls, rp, n_vars, root, vars_, threads=None):
+    def probe_into(cls, rp, n_vars, root, vars_):
         """The reference's probe_variable (probing.hpp:225) of each var in ``vars_`` from ``root``,
-        stored in a fresh cache handle; host threads run independent probes (ctypes releases the
-        GIL; each call writes its own entry)."""
-        from concurrent.futures import ThreadPoolExecutor
-        import os
+        stored in a fresh cache handle. One call at a time: each probe already runs on the
+        reference's pool, and concurrent external callers widen a use-after-scope race in its
+        parallel_for (parallel.hpp:117-129: the waiter can return and destroy its mutex /
+        condition variable while the last worker is about to lock them)."""
         c = cls(Ref.lib().ref_cache_new_empty(rp.h))
         r = np.ascontiguousarray(root, dtype=np.float64)
-        with ThreadPoolExecutor(threads or os.cpu_count() or 4) as ex:
-            list(ex.map(lambda v: Ref.lib().ref_cache_probe_into(c.h, rp.h, _p(r), int(v), 0), vars_))
+        for v in vars_:
+            Ref.lib().ref_cache_probe_into(c.h, rp.h, _p(r), int(v), 0)
         return c
 
 

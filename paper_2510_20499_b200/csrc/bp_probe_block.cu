@@ -422,6 +422,7 @@ __device__ int block_branch(const DevProblem& P, const ProbeRoot& R, const Block
       if (bs) atomicAdd(&sm.wb, bs);
     }
     // Jacobi tightening of the dirty vars: new values to the changed list, written afterwards
+    __syncthreads();  // every thread has read nv = n_a
     if (tid == 0) sm.n_a = 0;
     __syncthreads();
     block_items(sm, vl, nv, P.col_start, [&](int i, int mode, int idx, int stride) {

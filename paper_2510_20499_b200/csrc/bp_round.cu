@@ -78,6 +78,16 @@ __global__ void k_gather(const double2* b, const int* var, int k, double2* out)
     out[j] = b[var[j]];
 }
 
+// The first k vars of the current order and their bounds in one pass (take_first + gather).
+__global__ void k_take_gather(const int* order, const double2* b, int k, int* var_out, double2* b_out)
+{
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    const int v = order[j];
+    var_out[j]  = v;
+    b_out[j]    = b[v];
+  }
+}
+
 __global__ void k_scatter(double2* b, const int* var, const double2* val, int k)
 {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
@@ -354,6 +364,9 @@ struct RoundCtx {
     }
     const int k = n_unset;
     k_slack_keys<<<blocks_for(k), 256, 0, s>>>(P.dev(), rec, aux, unset.p, k, keys_in.p, pos_in.p);
+    // stable LSD radix sort of (key, position): std::stable_sort's order (rounding.hpp:81-104).
+    // (An incremental variant -- merging the vars whose key did not change with the re-sorted
+    // rest -- measured slower on C4: nearly every key changes every bulk.)
     size_t need = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, need, keys_in.p, keys_out.p, pos_in.p, pos_out.p, k, 0,
                                     64, s);
@@ -379,6 +392,22 @@ struct RoundCtx {
     std::swap(unset.n, unset_alt.n);
     BP_CUDA(cudaMemcpyAsync(&n_unset, sel_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     sync();
+  }
+
+  // take_first(k) + gather(ws, ...) with one kernel and one synchronisation.
+  std::vector<int> take_gather(int k, std::vector<double2>& tb)
+  {
+    std::vector<int> t(k);
+    tb.resize(k);
+    if (k) {
+      reserve(ivar, k);
+      reserve(tmp2, k);
+      k_take_gather<<<blocks_for(k), 256, 0, s>>>(unset.p, ws.p, k, ivar.p, tmp2.p);
+      BP_CUDA(cudaMemcpyAsync(t.data(), ivar.p, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
+      BP_CUDA(cudaMemcpyAsync(tb.data(), tmp2.p, sizeof(double2) * k, cudaMemcpyDeviceToHost, s));
+      sync();
+    }
+    return t;
   }
 
   std::vector<int> take_first(int k)
@@ -775,8 +804,7 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
         std::vector<double2> tb;
         {
           bp::StepTimer st(TT, 1);
-          take = X.take_first(bulk);
-          tb   = X.gather(X.ws, take);
+          take = X.take_gather(bulk, tb);
           bp::candidate_values(start_values, take, tb, rng, cfg.random_band, pv0, pv1);
         }
         bp::RoundCtx::Probe pr0;
