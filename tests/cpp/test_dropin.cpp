@@ -5,6 +5,7 @@
 // seeds of acceptance.cpp:40 / :89 and test_rounding.cpp), plus larger mixed instances with heavy
 // rows. Everything is compared bit for bit. One PASS/FAIL line per criterion, like acceptance.cpp;
 // exit status = number of failures.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -440,9 +441,12 @@ void lp_products()
          std::to_string(runs) + " instances, " + std::to_string(bad) + " mismatches");
 }
 
-// Host overhead of the drop-in per call: pg::propagate (side-table lookup, BoundsState
-// marshalling, C-ABI) against bp_propagate on the same device problem with the same host bounds; the
-// difference must stay <= 50 us per call, on a 10k x 10k and a 300k x 300k instance (heavy rows).
+// Host overhead of the drop-in per call: what pulse::gpu::propagate adds to the
+// C-ABI call bp_propagate on the same device problem and host bounds -- the side-table lookup (key
+// sample + match) and the marshalling (none: it works in place on the BoundsState). Measured
+// directly (the lookup, 10^4 calls) and end to end as the median of paired per-call differences
+// (pg::propagate vs bp_propagate alternating, which cancels the GPU's own run-to-run variation);
+// both must stay <= 50 us, on a 10k x 10k and a 300k x 300k instance (heavy rows).
 void host_overhead()
 {
   bool ok = true;
@@ -450,31 +454,52 @@ void host_overhead()
   for (const auto& [n, heavy] : {std::pair<int, int>{10000, 0}, std::pair<int, int>{300000, 8}}) {
     const ProblemDef p = mixed_instance(77 + n, n, n, heavy, 40000);
     bp_problem* h      = pg::detail::handle(p);
-    const int reps     = n > 100000 ? 20 : 200;
+    const int reps     = n > 100000 ? 21 : 101;
     BoundsState warm(p);
     pg::propagate(p, warm);  // upload + warm-up
     auto now = [] { return std::chrono::steady_clock::now(); };
-    double t_abi = 0.0, t_pg = 0.0;
+    auto us  = [](auto a, auto b) { return 1e6 * std::chrono::duration<double>(b - a).count(); };
+    const auto l0 = now();
+    for (int r = 0; r < 10000; ++r) pg::detail::handle(p);
+    const double lookup_us = us(l0, now()) / 10000;
     const bp_limits l = pg::detail::limits(PropagationLimits{});
+    std::vector<double> diff;
+    double t_abi = 0.0, t_pg = 0.0;
     for (int r = 0; r < reps; ++r) {
       std::vector<double> raw = BoundsState(p).raw();
-      int32_t inf             = 0;
-      bp_result res{};
-      const auto t0 = now();
-      pg::detail::check(bp_propagate(h, raw.data(), &inf, &l, &res));
-      const auto t1 = now();
       BoundsState b(p);
-      const auto t2 = now();
-      pg::propagate(p, b);
-      const auto t3 = now();
-      t_abi += std::chrono::duration<double>(t1 - t0).count();
-      t_pg += std::chrono::duration<double>(t3 - t2).count();
+      int32_t inf = 0;
+      bp_result res{};
+      double da, dp;
+      if (r % 2 == 0) {
+        auto t0 = now();
+        pg::detail::check(bp_propagate(h, raw.data(), &inf, &l, &res));
+        auto t1 = now();
+        pg::propagate(p, b);
+        auto t2 = now();
+        da = us(t0, t1);
+        dp = us(t1, t2);
+      } else {
+        auto t0 = now();
+        pg::propagate(p, b);
+        auto t1 = now();
+        pg::detail::check(bp_propagate(h, raw.data(), &inf, &l, &res));
+        auto t2 = now();
+        dp = us(t0, t1);
+        da = us(t1, t2);
+      }
+      t_abi += da;
+      t_pg += dp;
+      diff.push_back(dp - da);
     }
-    const double over_us = 1e6 * (t_pg - t_abi) / reps;
-    ok = ok && over_us <= 50.0;
-    char buf[160];
-    std::snprintf(buf, sizeof(buf), "%s%dx%d: bp_propagate %.1f us, pulse::gpu::propagate %.1f us, overhead %.1f us",
-                  detail.empty() ? "" : "; ", n, n, 1e6 * t_abi / reps, 1e6 * t_pg / reps, over_us);
+    std::sort(diff.begin(), diff.end());
+    const double med = diff[diff.size() / 2];
+    ok = ok && lookup_us <= 50.0 && med <= 50.0;
+    char buf[240];
+    std::snprintf(buf, sizeof(buf),
+                  "%s%dx%d: side-table lookup %.2f us; bp_propagate %.1f us, pulse::gpu::propagate %.1f us, "
+                  "median paired difference %.1f us",
+                  detail.empty() ? "" : "; ", n, n, lookup_us, t_abi / reps, t_pg / reps, med);
     detail += buf;
   }
   report("drop-in host overhead per propagate <= 50 us", ok, detail);
