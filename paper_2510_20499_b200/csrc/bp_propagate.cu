@@ -41,6 +41,9 @@ std::atomic<long long> g_kernel_launches{0};
 
 namespace {
 
+#ifndef BP_HEAVY_TMA
+#define BP_HEAVY_TMA 0  // see kRowsSmem
+#endif
 constexpr int kThreads  = 256;
 constexpr int kWarps    = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
@@ -107,8 +110,21 @@ struct WarpSmem {
   int chg[64];               // changed-var staging before a global append
 };
 
+// TMA staging of a heavy segment's contribution stream (heavy_fold): two 128-entry buffers, their
+// mbarriers (initialised once per kernel launch: re-initialising an mbarrier between uses loses
+// completions -- tools/microbench/tma_test.cu) and the number of completed uses of each.
+struct alignas(16) WarpTma {
+  double2 buf[2][kTile];
+  unsigned long long mbar[2];
+  unsigned uses[2];
+  unsigned pad[2];
+};
+
 struct Smem {
   WarpSmem w[kWarps];
+#if BP_HEAVY_TMA
+  WarpTma tma[kWarps];
+#endif
   int blk_crossed;
   int blk_any_rows;
   unsigned long long blk_colnnz;
@@ -122,7 +138,49 @@ struct Ctx {
   Smem& sm;
   WarpSmem& w;
   int lane, warp;
+  WarpTma* tma;    // TMA staging for heavy_fold: this warp's own, or the block's shared slot
+  int* tma_owner;  // non-null: the slot is shared by the block's warps (owner warp or -1)
 };
+
+// ---- 1-D bulk copies (TMA engine: cp.async.bulk) into shared memory, completion on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p)
+{
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+// once per warp at kernel start
+__device__ __forceinline__ void tma_init(WarpTma* t, int lane)
+{
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&t->mbar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&t->mbar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    t->uses[0] = t->uses[1] = 0;
+  }
+  __syncwarp();
+}
+// one elected lane: arm the barrier with the byte count and start the bulk copy gmem -> smem
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* mb)
+{
+  // (no proxy fence: the buffer's previous use was generic-proxy READS, ordered by the warp's
+  // __syncwarp before this call -- a write-after-read needs none)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(mb))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity)
+{
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(mb)),
+      "r"(parity)
+      : "memory");
+}
 
 // Debug counters (BP_DEBUG=1): per task kind total / max cycles and count.
 __device__ __forceinline__ void dbg_task(Ctx& c, int kind, long long c0)
@@ -591,12 +649,6 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
   const int es              = e0 + (__ffs(dm) - 1) * kPiece;  // first recomputed piece
   const long long c_stream = S.dbg ? clock64() : 0;
   const double2* gb         = S.gbuf + off;
-  double2 v[kEPL], w[kEPL];
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    v[h] = __ldcg(gb + es + h * 32 + lane);
-    w[h] = es + kTile < e1 ? __ldcg(gb + es + kTile + h * 32 + lane) : make_double2(0.0, 0.0);
-  }
   double acc = 0.0, gtw = 0.0, gpm = 0.0;
   if (es > e0 && lane < 2) acc = __ldcg(reinterpret_cast<const double*>(S.ckpt + p0 + (es - e0) / kPiece) + lane);
   int imn = 0, imx = 0;
@@ -608,6 +660,66 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
     imx += __ldcg(&ch->imx);
     gtw = fmax(gtw, __ldcg(&ch->gtw));
     gpm = fmax(gpm, __ldcg(&ch->gpm));
+  }
+  WarpTma* Tp = BP_HEAVY_TMA ? c.tma : nullptr;
+  if (Tp && c.tma_owner) {  // one shared slot per block (k_rows_full): take it if free
+    int got = 0;
+    if (lane == 0) got = atomicCAS(c.tma_owner, -1, c.warp) == -1;
+    if (!__shfl_sync(FULL, got, 0)) Tp = nullptr;
+  }
+  if (Tp) {
+  // The contribution stream by TMA bulk copies (cp.async.bulk, 2 KB per 128-entry chunk) into two
+  // shared-memory buffers, the copy of chunk c + 2 in flight while chunk c is folded. The rows'
+  // gbuf regions are 128-entry aligned and zero-padded, so every chunk is a full 2 KB copy.
+  WarpTma& T       = *Tp;
+  const int nchunk = (e1 - es + kTile - 1) / kTile;
+  unsigned u0 = T.uses[0], u1 = T.uses[1];  // completed uses before this segment (warp-uniform)
+  __syncwarp();
+  if (lane == 0) {
+#if BP_TMA_GLOBAL_FENCE
+    // the pieces' generic-proxy writes (acquired through their stamps above) before async reads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
+    bulk_load(T.buf[0], gb + es, kTile * sizeof(double2), &T.mbar[0]);
+    if (nchunk > 1) bulk_load(T.buf[1], gb + es + kTile, kTile * sizeof(double2), &T.mbar[1]);
+  }
+  for (int ck = 0; ck < nchunk; ++ck) {
+    const int base = es + ck * kTile, bi = ck & 1;
+    if (lane < 2 && ((base - e0) & (kPiece - 1)) == 0)  // checkpoint: the sums before this piece
+      reinterpret_cast<double*>(S.ckpt + p0 + (base - e0) / kPiece)[lane] = acc;
+    mbar_wait(&T.mbar[bi], (bi ? u1 : u0) & 1u);
+    if (bi) ++u1;
+    else ++u0;
+    int pm = 0, px = 0;
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const double2 vv = T.buf[bi][h * 32 + lane];
+      const double cm = vv.x, cx = vv.y;  // beyond e1: padding zeros
+      const unsigned m = __ballot_sync(FULL, cm != 0.0);
+      const unsigned x = __ballot_sync(FULL, cx != 0.0);
+      if (cm != 0.0) c.w.b0[pm + __popc(m & lt)] = cm;
+      if (cx != 0.0) c.w.b1[px + __popc(x & lt)] = cx;
+      pm += __popc(m);
+      px += __popc(x);
+    }
+    __syncwarp();
+    if (lane == 0 && ck + 2 < nchunk)  // this buffer is free again: chunk ck + 2 into it
+      bulk_load(T.buf[bi], gb + base + 2 * kTile, kTile * sizeof(double2), &T.mbar[bi]);
+    if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    T.uses[0] = u0;
+    T.uses[1] = u1;
+  }
+  __syncwarp();
+    if (c.tma_owner && lane == 0) atomicExch(c.tma_owner, -1);  // release the block's slot
+  } else {  // register stream: two chunks' loads in flight
+    double2 v[kEPL], w[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    v[h] = __ldcg(gb + es + h * 32 + lane);
+    w[h] = es + kTile < e1 ? __ldcg(gb + es + kTile + h * 32 + lane) : make_double2(0.0, 0.0);
   }
   for (int base = es; base < e1; base += kTile) {
     if (lane < 2 && ((base - e0) & (kPiece - 1)) == 0)  // checkpoint: the sums before this piece
@@ -632,6 +744,7 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
     }
     if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
     __syncwarp();
+  }
   }
   imn = warp_sum(imn);
   imx = warp_sum(imx);
@@ -1685,7 +1798,25 @@ __device__ void zero_par(ParCtl* q)
 #endif
 constexpr int kRowsWarpBytes = 3072;
 static_assert(offsetof(WarpSmem, b1) == 2048 && 2048 + 128 * 8 <= kRowsWarpBytes, "row-task smem layout");
-constexpr size_t kRowsSmem = BP_ROWS_COMPACT_SMEM ? (size_t)kWarps * kRowsWarpBytes : sizeof(Smem);
+// compact layout: kWarps regions of kRowsWarpBytes, then one WarpTma per warp
+constexpr size_t kRowsTmaOff = (size_t)kWarps * kRowsWarpBytes;
+static_assert(kRowsTmaOff % 16 == 0, "TMA buffers must be 16-byte aligned");
+// one TMA slot per block (+ its owner word): a per-warp slot would cost the SM's L1 carveout, which
+// the bound gathers of the other row tasks depend on (measured: -10% on C2 with 8 slots per block)
+// BP_HEAVY_TMA=1 streams heavy segments into shared memory with TMA bulk copies (cp.async.bulk +
+// mbarrier, two 2 KB chunks in flight). Measured on C2 (tools/gpu_ab.sh, same box, 3 x 3 runs):
+// 10.38 ms per propagate with it vs 9.22 ms with the register stream (two chunks' loads in flight
+// per lane) -- the heavy chains are latency-bound and two 2 KB bulk copies in flight hide less
+// than 128 independent loads; with a slot per warp the larger shared carveout also costs L1. Off.
+#ifndef BP_HEAVY_TMA
+#define BP_HEAVY_TMA 0
+#endif
+#ifndef BP_ROWS_SMEM_PAD
+#define BP_ROWS_SMEM_PAD 0
+#endif
+constexpr size_t kRowsSmem =
+    BP_ROWS_COMPACT_SMEM ? kRowsTmaOff + (BP_HEAVY_TMA ? sizeof(WarpTma) + 16 : 16) + BP_ROWS_SMEM_PAD
+                         : sizeof(Smem);
 // The host enqueues [k_rows_full, k_cand_pieces, k_engine(resume)] speculatively, several rounds
 // ahead without waiting: each is a no-op unless the engine handed a full round over (need_full).
 __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
@@ -1703,11 +1834,20 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
   const int warp = threadIdx.x >> 5;
 #if BP_ROWS_COMPACT_SMEM
   // compact warp regions: only b0[0..128) and b1[0..128) are used by the full round's row tasks
-  WarpSmem& w = *reinterpret_cast<WarpSmem*>(dyn_smem + warp * kRowsWarpBytes);
+  WarpSmem& w  = *reinterpret_cast<WarpSmem*>(dyn_smem + warp * kRowsWarpBytes);
+  WarpTma* tma = reinterpret_cast<WarpTma*>(dyn_smem + kRowsTmaOff);
+  int* owner   = reinterpret_cast<int*>(dyn_smem + kRowsTmaOff + sizeof(WarpTma));
+  if (BP_HEAVY_TMA && warp == 0) {
+    tma_init(tma, (int)(threadIdx.x & 31));
+    if (threadIdx.x == 0) *owner = -1;
+  }
+  if (BP_HEAVY_TMA) __syncthreads();
 #else
-  WarpSmem& w = sm.w[warp];
+  WarpSmem& w  = sm.w[warp];
+  WarpTma* tma = nullptr;
+  int* owner   = nullptr;
 #endif
-  Ctx c{P, S, lim, sm, w, (int)(threadIdx.x & 31), warp};
+  Ctx c{P, S, lim, sm, w, (int)(threadIdx.x & 31), warp, tma, owner};
   phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell, ldv(&S.ctl->df_stamp));
 }
 
@@ -1727,14 +1867,14 @@ __global__ void __launch_bounds__(kThreads, BP_SELL_MIN_BLOCKS)
     __shared__ __align__(16) unsigned char no_smem[16];  // sell_slice never touches the warp smem
     Smem& sm       = *reinterpret_cast<Smem*>(no_smem);
     const int warp = threadIdx.x >> 5;
-    Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp};
+    Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp, nullptr, nullptr};
     phase_sell(c, &S.ctl->par[par], true, ldv(&S.ctl->df_stamp));
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Candidate pieces of rows above kCandSplit, after k_rows_full published their activities.
-__global__ void __launch_bounds__(kThreads) k_cand_pieces(DevProblem P, DevState S, Limits lim)
+__global__ void __launch_bounds__(kThreads, 1) k_cand_pieces(DevProblem P, DevState S, Limits lim)
 {
   if (!ldv(&S.ctl->need_full)) return;
   const unsigned stamp = ldv(&S.ctl->stamp_base) + (unsigned)ldv(&S.ctl->rounds);
@@ -1742,7 +1882,7 @@ __global__ void __launch_bounds__(kThreads) k_cand_pieces(DevProblem P, DevState
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
-  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
+  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp, nullptr, nullptr};
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   for (int t = gw; t < P.n_cpiece; t += nw) {
     const int2 tk = P.cpiece_task[t];
@@ -1767,7 +1907,13 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5;
-  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
+#if BP_HEAVY_TMA
+  tma_init(&sm.tma[warp], (int)(threadIdx.x & 31));
+  WarpTma* tma = &sm.tma[warp];
+#else
+  WarpTma* tma = nullptr;
+#endif
+  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp, tma, nullptr};
 
   if (mode == MODE_ACTIVITY) {
     const bool full = full_first != 0;

@@ -247,7 +247,7 @@ struct RoundCtx {
   DBuf<double2> ws, root, tmp2, orig;
   DBuf<RowRec> ws_rec;   // activity records consistent with ws while ws_cert holds
   DBuf<double2> ws_aux;
-  DBuf<int> unset, unset_alt, pos_in, pos_out, sel_count, flags, ivar, ichg;
+  DBuf<int> unset, unset_alt, pos_in, pos_out, sel_count, flags, ivar, jvar, ichg;
   DBuf<unsigned long long> keys_in, keys_out;
   DBuf<double> dlo, dup;
   DBuf<unsigned char> cub_tmp;
@@ -271,16 +271,64 @@ struct RoundCtx {
     return l;
   }
 
-  void sync() { BP_CUDA(cudaStreamSynchronize(s)); }
+  // Pinned staging for the driver's small transfers: uploads are copied into it and sent
+  // asynchronously, readbacks land in it and are copied out at the next sync() -- one stream
+  // synchronisation per step instead of one per (pageable, hence synchronous) copy.
+  char* pin        = nullptr;
+  size_t pin_cap   = 0, pin_off = 0;
+  struct Pending {
+    void* dst;
+    const char* src;
+    size_t bytes;
+  };
+  std::vector<Pending> pending;
 
-  // Stream-ordered upload (the engine stream is non-blocking: a plain cudaMemcpy would race with
-  // kernels still reading the buffer).
+  ~RoundCtx()
+  {
+    if (pin) cudaFreeHost(pin);
+  }
+  char* stage(size_t bytes)
+  {
+    bytes = (bytes + 15) / 16 * 16;
+    if (pin_off + bytes > pin_cap) {
+      sync();  // every staged copy has completed: the buffer may be reused / grown
+      if (bytes > pin_cap) {
+        if (pin) cudaFreeHost(pin);
+        pin_cap = std::max<size_t>(bytes, 1 << 22);
+        BP_CUDA(cudaMallocHost(&pin, pin_cap));
+      }
+    }
+    char* p = pin + pin_off;
+    pin_off += bytes;
+    return p;
+  }
+  void sync()
+  {
+    BP_CUDA(cudaStreamSynchronize(s));
+    for (const auto& q : pending) std::memcpy(q.dst, q.src, q.bytes);
+    pending.clear();
+    pin_off = 0;
+  }
+  // device -> host readback delivered to dst at the next sync()
+  void get_async(void* dst, const void* dev_src, size_t bytes)
+  {
+    if (!bytes) return;
+    char* st = stage(bytes);
+    BP_CUDA(cudaMemcpyAsync(st, dev_src, bytes, cudaMemcpyDeviceToHost, s));
+    pending.push_back({dst, st, bytes});
+  }
+
+  // Stream-ordered upload through the pinned staging (the engine stream is non-blocking: a plain
+  // cudaMemcpy would race with kernels still reading the buffer).
   template <class T>
   void put(DBuf<T>& b, const std::vector<T>& v)
   {
     if (b.n < v.size()) b.alloc(std::max(v.size(), 2 * b.n));
-    if (!v.empty())
-      BP_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
+    if (!v.empty()) {
+      char* st = stage(sizeof(T) * v.size());
+      std::memcpy(st, v.data(), sizeof(T) * v.size());
+      BP_CUDA(cudaMemcpyAsync(b.p, st, sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
+    }
   }
   template <class T>
   void reserve(DBuf<T>& b, size_t k)
@@ -306,6 +354,25 @@ struct RoundCtx {
     put(ivar, vars);
     put(tmp2, vals);
     k_scatter<<<blocks_for(vars.size()), 256, 0, s>>>(b, ivar.p, tmp2.p, (int)vars.size());
+  }
+
+  // Commit: the engine's result becomes the working state by swapping buffers (no 16n / 48m-byte
+  // copies): ws <- P.st.bounds, and while certified the activity records with it.
+  void adopt_engine_state(bool cert)
+  {
+    std::swap(ws.p, P.bounds.p);
+    std::swap(ws.n, P.bounds.n);
+    P.st.bounds = P.bounds.p;
+    if (cert && P.m) {
+      reserve(ws_rec, (size_t)std::max(P.m, 1));
+      reserve(ws_aux, (size_t)std::max(P.m, 1));
+      std::swap(ws_rec.p, P.rec.p);
+      std::swap(ws_rec.n, P.rec.n);
+      std::swap(ws_aux.p, P.aux.p);
+      std::swap(ws_aux.n, P.aux.n);
+      P.st.rec = P.rec.p;
+      P.st.aux = P.aux.p;
+    }
   }
 
   // After a propagate that ended at a fixpoint, P.st.rec / aux describe its final bounds for
@@ -390,7 +457,7 @@ struct RoundCtx {
     cub::DeviceSelect::If(cub_tmp.p, have, unset.p, unset_alt.p, sel_count.p, n_unset, pred, s);
     std::swap(unset.p, unset_alt.p);
     std::swap(unset.n, unset_alt.n);
-    BP_CUDA(cudaMemcpyAsync(&n_unset, sel_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    get_async(&n_unset, sel_count.p, sizeof(int));
     sync();
   }
 
@@ -403,8 +470,8 @@ struct RoundCtx {
       reserve(ivar, k);
       reserve(tmp2, k);
       k_take_gather<<<blocks_for(k), 256, 0, s>>>(unset.p, ws.p, k, ivar.p, tmp2.p);
-      BP_CUDA(cudaMemcpyAsync(t.data(), ivar.p, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
-      BP_CUDA(cudaMemcpyAsync(tb.data(), tmp2.p, sizeof(double2) * k, cudaMemcpyDeviceToHost, s));
+      get_async(t.data(), ivar.p, sizeof(int) * k);
+      get_async(tb.data(), tmp2.p, sizeof(double2) * k);
       sync();
     }
     return t;
@@ -434,7 +501,8 @@ struct RoundCtx {
     BP_CUDA(cudaMemcpyAsync(P.st.bounds, ws.p, sizeof(double2) * P.n, cudaMemcpyDeviceToDevice, s));
     bool inf          = ws_infeasible;
     bool root_changed = false;
-    std::vector<int> changed;
+    std::vector<int> changed, dv_keep, ch;
+    int fl = 0;
     auto t_ws = std::chrono::steady_clock::now();
     if (cache) {
       // warm start on the host (sparse deltas over the cache root), meet on the device
@@ -453,16 +521,26 @@ struct RoundCtx {
         k_meet_list<<<blocks_for(dv.size()), 256, 0, s>>>(P.st.bounds, ivar.p, dlo.p, dup.p,
                                                           (int)dv.size(), ichg.p, flags.p);
       }
-      int fl = 0;
-      BP_CUDA(cudaMemcpyAsync(&fl, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-      std::vector<int> ch(dv.size());
-      if (!dv.empty())
-        BP_CUDA(cudaMemcpyAsync(ch.data(), ichg.p, sizeof(int) * dv.size(), cudaMemcpyDeviceToHost, s));
-      sync();
+      get_async(&fl, flags.p, sizeof(int));
+      ch.resize(dv.size());
+      get_async(ch.data(), ichg.p, sizeof(int) * dv.size());
+      dv_keep = std::move(dv);
+    }
+    // fixings (rounding.hpp:186-195) need the post-meet bounds of the bulk vars: gathered in the
+    // same stream step and read back with the meet's flags -- one synchronisation
+    std::vector<double2> cur(vars.size());
+    if (!vars.empty()) {
+      put(jvar, vars);
+      reserve(tmp2, vars.size());
+      k_gather<<<blocks_for(vars.size()), 256, 0, s>>>(P.st.bounds, jvar.p, (int)vars.size(), tmp2.p);
+      get_async(cur.data(), tmp2.p, sizeof(double2) * vars.size());
+    }
+    sync();
+    if (cache) {
       root_changed = (fl & 1) != 0;
       if (fl & 2) inf = true;
-      for (size_t j = 0; j < dv.size(); ++j)
-        if (ch[j]) changed.push_back(dv[j]);
+      for (size_t j = 0; j < dv_keep.size(); ++j)
+        if (ch[j]) changed.push_back(dv_keep[j]);
     }
     if (tt) {
       tt->t[4] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_ws).count();
@@ -470,18 +548,6 @@ struct RoundCtx {
     }
     auto t_fx = std::chrono::steady_clock::now();
     const std::unordered_set<int> evm(out.evicted.begin(), out.evicted.end());
-    // fixings (rounding.hpp:186-195) on the post-meet bounds of the bulk vars
-    const std::vector<double2> cur = [&] {
-      std::vector<double2> o(vars.size());
-      if (!vars.empty()) {
-        put(ivar, vars);
-        reserve(tmp2, vars.size());
-        k_gather<<<blocks_for(vars.size()), 256, 0, s>>>(P.st.bounds, ivar.p, (int)vars.size(), tmp2.p);
-        BP_CUDA(cudaMemcpyAsync(o.data(), tmp2.p, sizeof(double2) * vars.size(), cudaMemcpyDeviceToHost, s));
-        sync();
-      }
-      return o;
-    }();
     int crossings = inf ? 1 : 0;
     std::vector<int> fv;
     std::vector<double2> fb;
@@ -825,10 +891,9 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
           auto& pr = sel == 0 ? pr0 : pr1;
           if (!pr.fixed.empty()) {  // commit (rounding.hpp:436-443)
             bp::StepTimer st(TT, 3);
-            BP_CUDA(cudaMemcpyAsync(X.ws.p, P.st.bounds, sizeof(double2) * n, cudaMemcpyDeviceToDevice, X.s));
+            X.adopt_engine_state(pr.cert);
             X.ws_infeasible = false;
             X.ws_cert       = pr.cert;
-            if (X.ws_cert) X.snapshot_ws_activities();
             for (const auto& fv : pr.fixed) committed.push_back(fv);
             X.drop_fixed();
             recovery = false;

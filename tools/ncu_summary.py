@@ -3,8 +3,7 @@
     python tools/ncu_summary.py gpurun_out/r01/k_engine_C2.ncu-rep profiles/r01_k_engine_C2 \
         [--workload C2] [--algorithmic-bytes B]
 
-Writes <out>.txt (the key counters, readable) and merges the per-launch DRAM traffic into
-profiles/ncu_k_engine_summary.json (read by bench.py for roofline.traffic).
+Writes <out>.txt (the key counters, readable).
 """
 import argparse
 import csv
@@ -74,12 +73,17 @@ def main():
         if rd and wr:
             tb = to_bytes(num(rd[1]), rd[0]) + to_bytes(num(wr[1]), wr[0])
             dur = d.get("gpu__time_duration.sum")
-            ms = num(dur[1]) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(dur[0], 1.0)
+            ms = num(dur[1]) * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3,
+                                "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}[dur[0]]
             lines.append(f"  {'DRAM bytes per launch':34s} {tb / 1e9:.3f} GB -> {tb / ms / 1e6:.1f} GB/s")
             if a.algorithmic_bytes:
                 lines.append(f"  {'algorithmic bytes (bench.py)':34s} {a.algorithmic_bytes / 1e9:.3f} GB "
                              f"(traffic / algorithmic = {tb / a.algorithmic_bytes:.2f})")
             summary = {"dram_bytes": tb, "ms": ms}
+        sec = d.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")
+        req = d.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum")
+        if sec and req and num(req[1]):
+            lines.append(f"  {'global load sectors per request':34s} {num(sec[1]) / num(req[1]):.2f}")
         tot = sum(num(d.get(f"smsp__pcsamp_warps_issue_stalled_{s}", ("", "0"))[1]) or 0 for s in STALLS)
         if tot:
             lines.append("  warp-stall samples:")
@@ -88,11 +92,6 @@ def main():
                 if x:
                     lines.append(f"    {s:22s} {100 * x / tot:5.1f}%")
     Path(a.out + ".txt").write_text("\n".join(lines) + "\n")
-    sj = Path("profiles/ncu_k_engine_summary.json")
-    js = json.loads(sj.read_text()) if sj.exists() else {}
-    js.setdefault("dram_bytes_per_launch", {})[a.workload] = summary.get("dram_bytes")
-    js.setdefault("source", {})[a.workload] = a.out + ".txt"
-    sj.write_text(json.dumps(js, indent=1) + "\n")
     print("\n".join(lines))
 
 
