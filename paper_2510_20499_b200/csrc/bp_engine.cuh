@@ -104,6 +104,7 @@ struct DevState {
   double2* ckpt;          // per heavy-row piece: (min, max) running sums of its segment before it
   unsigned* task_stamp;   // per SELL slice / medium-row group: stamp of the dirty-filtered round
   int n_task;             // SELL slices + medium-row groups
+  unsigned char* row_flag;  // per light row: low byte of the dirty-filtered round's mark
   int* df_slice;          // dirty lists (phase_df_lists)
   int* df_group;
   int* df_piece;
@@ -148,6 +149,7 @@ struct Problem {
   DBuf<int> col_mark;
   DBuf<unsigned> task_stamp;
   DBuf<int> df_lists;
+  DBuf<unsigned char> row_flag;
   int n_task = 0;
   DBuf<int2> piece_task, fold_task, cpiece_task;
   DBuf<int> scol, sc_ptr, sc_row, sc_tile;

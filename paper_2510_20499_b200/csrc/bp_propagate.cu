@@ -764,14 +764,15 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
 // non-zero contributions into its own shared-memory slice, and its lanes 0/1 run the row's
 // sequential min/max sums -- the four rows' chains advance in the same instructions. Then the
 // candidates of the non-quiet rows.
-__device__ void group_fold(Ctx& c, int t0, int nt, bool cand)
+__device__ void group_fold(Ctx& c, int t0, int nt, bool cand, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   const int lane = c.lane, g = lane >> 3, gl = lane & 7;
   const unsigned gmask = 0xFFu << (8 * g);
   const int k          = g < nt ? __ldg(&P.fold_task[t0 + g].x) : -1;
-  const bool act       = k >= 0;
+  // dirty-filtered round: clean rows of the group stay idle (see sell_slice)
+  const bool act = k >= 0 && (ds == 0 || __ldcg(S.row_flag + k) == (unsigned char)ds);
   int rs = 0, L = 0;
   if (act) {
     rs = __ldg(P.row_start + k);
@@ -910,13 +911,14 @@ __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp, unsigned d
 #endif
 constexpr int kSellUnroll = BP_SELL_UNROLL;  // entries per lane in flight
 
-__device__ void sell_slice(Ctx& c, int sl, bool cand)
+__device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  // (dirty-filtered rounds select whole slices: recomputing a clean row is exact and republishes
-  // candidates its variables' persistent slots already hold)
-  const int k = __ldg(P.srow + 32 * sl + c.lane);
+  // dirty-filtered round: the slice is dirty; its clean rows (byte flag != the round's mark; a stale
+  // byte matching by wrap-around only recomputes a clean row, which is exact) are idle lanes
+  int k = __ldg(P.srow + 32 * sl + c.lane);
+  if (ds != 0 && k >= 0 && __ldcg(S.row_flag + k) != (unsigned char)ds) k = -1;
   const int b0 = __ldg(P.sr_tile + sl), b1 = __ldg(P.sr_tile + sl + 1);
   const int Lm = (b1 - b0) >> 5;
   const int* ciq   = P.sr_ci + b0 + c.lane;
@@ -1067,7 +1069,7 @@ __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
   if (ds != 0) {  // dirty-filtered round: the engine's list of dirty slices, 4 per fetch
     const int nd = ldv(&S.ctl->df_cnt[0]);
     for (Prefetch it_t(c, &pc->cur_a, 4, nd, true); it_t.t < nd; it_t.advance())
-      for (int q = it_t.t; q < min(nd, it_t.t + 4); ++q) sell_slice(c, __ldcg(S.df_slice + q), cand);
+      for (int q = it_t.t; q < min(nd, it_t.t + 4); ++q) sell_slice(c, __ldcg(S.df_slice + q), cand, ds);
     return;
   }
   for (Prefetch it_t(c, &pc->cur_s, 1, nsl, true); it_t.t < nsl; it_t.advance()) {
@@ -1121,7 +1123,7 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       const int nd = ldv(&S.ctl->df_cnt[1]);
       for (Prefetch it_t(c, &pc->cur_g, 1, nd, true); it_t.t < nd; it_t.advance()) {
         const int t0 = 4 * __ldcg(S.df_group + it_t.t);
-        group_fold(c, nfh + t0, min(4, nf - nfh - t0), cand);
+        group_fold(c, nfh + t0, min(4, nf - nfh - t0), cand, ds);
       }
     }
     if (sell_here) phase_sell(c, pc, cand, ds);
@@ -1681,7 +1683,8 @@ __device__ __forceinline__ void mark_entry(const DevProblem& P, const DevState& 
 {
   const int mk = __ldg(P.col_mark + e);
   if (mk >= 0) {
-    S.task_stamp[mk] = stamp;  // SELL slice / medium-row group
+    S.task_stamp[mk] = stamp;  // SELL slice / medium-row group, and the row inside it
+    S.row_flag[__ldg(P.col_row + e)] = (unsigned char)stamp;
   } else {                     // heavy row: its piece, and the row for its segment folds
     S.piece_dirty[-mk - 2] = stamp;
     S.row_stamp[__ldg(P.col_row + e)] = stamp;
@@ -2492,6 +2495,9 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.pstamp    = P.pstamp.p;
   S.piece_dirty = P.piece_dirty.p;
   S.task_stamp  = P.task_stamp.p;
+  P.row_flag.alloc(mm);
+  BP_CUDA(cudaMemset(P.row_flag.p, 0, mm));
+  S.row_flag = P.row_flag.p;
   S.n_task      = P.n_task;
   P.df_lists.alloc((size_t)std::max(P.n_task + P.n_piece, 1));
   S.df_slice = P.df_lists.p;
@@ -2595,8 +2601,9 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   static const int split_env = getenv("BP_SPLIT_SELL") ? atoi(getenv("BP_SPLIT_SELL")) : 0;
   const int split_sell       = split_env && P.n_srtile > 0 ? 1 : 0;
   // dirty-filtered rounds when the changed vars' columns hold at most BP_DF_MARK_PCT % of the nnz:
-  // beyond that nearly every row task is dirty and the marks cost more than they save (C2)
-  static const int mark_pct = getenv("BP_DF_MARK_PCT") ? atoi(getenv("BP_DF_MARK_PCT")) : 3;
+  // beyond that the marks and lists cost more than the rows they spare (C2, tools/gpu_ab.sh:
+  // 1 % 8.72, 2 % 8.77, 3 % 8.83, 5 % 8.94, 8 % 9.06, 15 % 9.24 ms per propagate)
+  static const int mark_pct = getenv("BP_DF_MARK_PCT") ? atoi(getenv("BP_DF_MARK_PCT")) : 1;
   unsigned long long mark_max = (unsigned long long)(P.nnz * mark_pct / 100);
   void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume, &mark_max};
   BP_CUDA(cudaEventRecord(P.ev0, s));
