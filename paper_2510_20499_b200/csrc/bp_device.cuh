@@ -323,10 +323,11 @@ struct DevProblem {
   const uint8_t* sr_own;    // unused
   const int* sr_tile;       // n_srtile + 1 slice offsets
   // Heavy rows (nnz > kHeavyFold): pieces of kPiece entries compute their contributions in
-  // parallel into gbuf (+ per-128-chunk aggregates in chunk_info), then one warp per
-  // 16384-entry segment streams gbuf and runs the reference's sequential sums: the sequential
-  // chain is the only serial part of a full round, so it is fed from a pure stream.
-  const int* long_off;      // per row: 128-aligned offset of its entries in gbuf, -1 otherwise
+  // parallel and compact the non-zero ones into the min / max contribution streams (+ per-128-
+  // chunk aggregates), then one warp per 16384-entry segment streams them and runs the
+  // reference's sequential sums: the chain is the only serial part of a round, so it is fed
+  // from dense streams.
+  const int* long_off;      // per row: 128-aligned offset of its entries in the streams, -1 otherwise
   const int* hpiece;        // per heavy row: index of its first piece in piece_task
   int n_piece;
   const int2* piece_task;   // (row, piece) of heavy rows, longest rows first

@@ -89,7 +89,11 @@ struct DevState {
   double2* bounds;
   RowRec* rec;
   double2* aux;
-  double2* gbuf;      // gathered bounds of long rows' entries (DevProblem::long_off)
+  // heavy rows' contribution streams (DevProblem::long_off): per piece, its non-zero min / max
+  // contributions compacted in entry order at off + first entry of the piece; counts in pcnt
+  double* gmin;
+  double* gmax;
+  int2* pcnt;
   CandSlot* slot;     // fused full round: per-var candidate slots
   // Candidate-slot state, kept across calls (outside Ctl, which callers zero per call): 0 = all
   // empty, 1 = valid for the current bounds (left by a full or dirty-filtered round's finalize:
@@ -98,8 +102,8 @@ struct DevState {
   int* slot_state;
   unsigned* ready;    // per row: stamp of the round whose activity is published
   unsigned char* rquiet;  // per row: 1 if no entry can publish a candidate (set before `ready`)
-  ChunkInfo* cinfo;       // heavy rows: per 128-entry chunk of gbuf
-  unsigned* pstamp;       // per heavy-row piece: stamp of the round whose contributions are in gbuf
+  ChunkInfo* cinfo;       // heavy rows: per 128-entry chunk of the row
+  unsigned* pstamp;       // per heavy-row piece: stamp of the round whose contributions are in gmin/gmax
   unsigned* piece_dirty;  // per heavy-row piece: stamp of the dirty-filtered round that recomputes it
   double2* ckpt;          // per heavy-row piece: (min, max) running sums of its segment before it
   unsigned* task_stamp;   // per SELL slice / medium-row group: stamp of the dirty-filtered round
@@ -166,7 +170,8 @@ struct Problem {
   DBuf<double2> bounds;
   DBuf<RowRec> rec;
   DBuf<double2> aux;
-  DBuf<double2> gbuf;
+  DBuf<double2> gbuf;  // storage of gmin / gmax (n_long_entries doubles each)
+  DBuf<int2> pcnt;
   DBuf<CandSlot> slot;
   DBuf<int> slot_state;
   DBuf<unsigned> ready;

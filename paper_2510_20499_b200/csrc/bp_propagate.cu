@@ -41,9 +41,6 @@ std::atomic<long long> g_kernel_launches{0};
 
 namespace {
 
-#ifndef BP_HEAVY_TMA
-#define BP_HEAVY_TMA 0  // see kRowsSmem
-#endif
 constexpr int kThreads  = 256;
 constexpr int kWarps    = kThreads / 32;
 constexpr unsigned FULL = 0xffffffffu;
@@ -110,21 +107,8 @@ struct WarpSmem {
   int chg[64];               // changed-var staging before a global append
 };
 
-// TMA staging of a heavy segment's contribution stream (heavy_fold): two 128-entry buffers, their
-// mbarriers (initialised once per kernel launch: re-initialising an mbarrier between uses loses
-// completions -- tools/microbench/tma_test.cu) and the number of completed uses of each.
-struct alignas(16) WarpTma {
-  double2 buf[2][kTile];
-  unsigned long long mbar[2];
-  unsigned uses[2];
-  unsigned pad[2];
-};
-
 struct Smem {
   WarpSmem w[kWarps];
-#if BP_HEAVY_TMA
-  WarpTma tma[kWarps];
-#endif
   int blk_crossed;
   int blk_any_rows;
   unsigned long long blk_colnnz;
@@ -138,54 +122,19 @@ struct Ctx {
   Smem& sm;
   WarpSmem& w;
   int lane, warp;
-  WarpTma* tma;    // TMA staging for heavy_fold: this warp's own, or the block's shared slot
-  int* tma_owner;  // non-null: the slot is shared by the block's warps (owner warp or -1)
 };
 
-// ---- 1-D bulk copies (TMA engine: cp.async.bulk) into shared memory, completion on an mbarrier
-__device__ __forceinline__ unsigned smem_u32(const void* p)
-{
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-// once per warp at kernel start
-__device__ __forceinline__ void tma_init(WarpTma* t, int lane)
-{
-  if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&t->mbar[0])) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&t->mbar[1])) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    t->uses[0] = t->uses[1] = 0;
-  }
-  __syncwarp();
-}
-// one elected lane: arm the barrier with the byte count and start the bulk copy gmem -> smem
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* mb)
-{
-  // (no proxy fence: the buffer's previous use was generic-proxy READS, ordered by the warp's
-  // __syncwarp before this call -- a write-after-read needs none)
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(mb))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity)
-{
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(mb)),
-      "r"(parity)
-      : "memory");
-}
-
 // Debug counters (BP_DEBUG=1): per task kind total / max cycles and count.
+// Task / gate statistics (BP_DEBUG=1) only exist in builds with -DBP_DBG_STATS=1: compiled into the
+// unrolled row loops they cost code size (instruction-cache misses) even when disabled at run time.
+#ifndef BP_DBG_STATS
+#define BP_DBG_STATS 0
+#endif
+#define DBG_ON(S) (BP_DBG_STATS && (S).dbg)
+
 __device__ __forceinline__ void dbg_task(Ctx& c, int kind, long long c0)
 {
-  if (c.S.dbg && c.lane == 0) {
+  if (DBG_ON(c.S) && c.lane == 0) {
     const unsigned long long d = (unsigned long long)(clock64() - c0);
     atomicAdd(c.S.dbg + 3 * kind, d);
     atomicMax(c.S.dbg + 3 * kind + 1, d);
@@ -244,14 +193,19 @@ struct Prefetch {
     if (stat) {
       t = lim <= 0 ? 0x3FFFFFFF : (blockIdx.x * kWarps + c.warp) * step;
     } else {
-      t = warp_fetch(c, cur, step);
+      t = 0x3FFFFFFF;
+      if (c.lane == 0) t = claim();
+      t = __shfl_sync(FULL, t, 0);
       issue();
     }
   }
+  // an exhausted cursor is only read: with short lists most of the grid's warps would otherwise
+  // queue atomics on one address for nothing (a value >= lim is a claim past the end either way)
+  __device__ __forceinline__ int claim() { return ldv(cur) < lim ? atomicAdd(cur, step) : lim; }
   __device__ __forceinline__ void issue()
   {
     nx = 0x3FFFFFFF;
-    if (c.lane == 0 && t < lim) nx = atomicAdd(cur, step);
+    if (c.lane == 0 && t < lim) nx = claim();
   }
   __device__ __forceinline__ void advance()
   {
@@ -307,6 +261,25 @@ __device__ __forceinline__ void publish(CandSlot* s, double cl, double cu, doubl
   }
 }
 
+#ifndef BP_EMIT_NOINLINE
+#define BP_EMIT_NOINLINE 0
+#endif
+// The candidates of one non-quiet entry (cand_explicit + publish). Inlined: an out-of-line copy
+// (BP_EMIT_NOINLINE=1) shrinks k_rows_full's code by a fifth but costs C2 5% (call overhead and
+// register saves around the call in the row loops; tools/gpu_ab.sh).
+#if BP_EMIT_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void emit_cand(CandSlot* slot, int ci, double a, double lo, double up, double mnf, int nmn,
+               double mxf, int nmx, double g, double h, int k)
+{
+  double cl, cu;
+  cand_explicit(lo, up, ci < 0, a, mnf, nmn, mxf, nmx, g, h, cl, cu);
+  publish(slot + (ci & ~kIntBit), cl, cu, lo, up, k);
+}
+
 // Dirty filter of a full round's row tasks: ds = 0 (true full round) or the stamp the previous
 // round's finalize wrote into row_stamp for the rows of its changed vars.
 __device__ __forceinline__ bool row_live(const DevState& S, int k, unsigned ds)
@@ -356,9 +329,7 @@ __device__ void long_candidates(Ctx& c, int k, int e0, int e1, double mnf, int n
       double tw, pm;
       entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pm);
       if (entry_quiet(tw, pm, mnf, nmn, mxf, nmx, g, hh)) continue;
-      double cl, cu;
-      cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], mnf, nmn, mxf, nmx, g, hh, cl, cu);
-      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
+      emit_cand(S.slot, ci[h], a[h], bd[h].x, bd[h].y, mnf, nmn, mxf, nmx, g, hh, k);
     }
   }
 }
@@ -551,8 +522,12 @@ __device__ void long_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp)
   fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
 }
 
-// F2a (heavy rows): contributions of piece p (kPiece entries) of row k into gbuf, with the
-// per-128-chunk aggregates; the piece is published with this round's stamp.
+// F2a (heavy rows): contributions of piece p (kPiece entries) of row k, with the per-128-chunk
+// aggregates. The non-zero min / max contributions are compacted in entry order into the piece's
+// slots of the two contribution streams (gmin / gmax at off + e0, counts in pcnt[p]): the segment
+// fold then runs its chains over dense streams (the compaction off its critical path; see
+// tools/microbench/mb_fold.cu: 139 -> 81 us per 16384-entry segment). The piece is published with
+// this round's stamp.
 __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
 {
   const DevProblem& P = c.P;
@@ -563,6 +538,10 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
   const int k = tk.x, rs = __ldg(P.row_start + k), L = __ldg(P.row_start + k + 1) - rs;
   const int off = __ldg(P.long_off + k);
   const int e0 = tk.y * kPiece, e1 = min(L, e0 + kPiece);
+  double* gmn = S.gmin + off + e0;
+  double* gmx = S.gmax + off + e0;
+  const unsigned lt = lanemask_lt();
+  int pm = 0, px = 0;
   for (int j0 = e0; j0 < e1; j0 += kTile) {
     int ci[kEPL];
     double a[kEPL];
@@ -590,7 +569,13 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
         gtw = fmax(gtw, tw);
         gpm = fmax(gpm, pw);
       }
-      S.gbuf[off + j0 + h * 32 + c.lane] = make_double2(cm, cx);  // padding slots get 0.0
+      // zero contributions are skipped: exact, the running sums are never -0.0
+      const unsigned m = __ballot_sync(FULL, cm != 0.0);
+      const unsigned x = __ballot_sync(FULL, cx != 0.0);
+      if (cm != 0.0) gmn[pm + __popc(m & lt)] = cm;
+      if (cx != 0.0) gmx[px + __popc(x & lt)] = cx;
+      pm += __popc(m);
+      px += __popc(x);
     }
     imn = warp_sum(imn);
     imx = warp_sum(imx);
@@ -606,14 +591,18 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
   }
   __syncwarp();
   if (c.lane == 0) {
+    S.pcnt[pi] = make_int2(pm, px);
     __threadfence();
     atomicExch(S.pstamp + pi, stamp);
   }
 }
 
-// F2b (heavy rows): one 16384-entry segment. Waits for the segment's pieces, then streams their
-// contributions from gbuf (two chunks in flight) while lanes 0/1 run the sequential sums over
-// the order-preserving compaction of the non-zero contributions.
+// F2b (heavy rows): one 16384-entry segment. Waits for the segment's pieces, then runs the
+// reference's sequential min / max sums (lanes 0 / 1) over the pieces' compacted contribution
+// streams in chunks of kFoldVals values: every lane stages chunk t + 1 into shared memory (the
+// other buffer) and has chunk t + 2's loads in flight while the chains fold chunk t.
+constexpr int kFoldVals = 96;  // 4 buffers fill the 3 KB row-task staging region (kRowsWarpBytes)
+static_assert(kFoldVals % 32 == 0 && 4 * kFoldVals * 8 <= 3072, "fold staging buffers");
 __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
@@ -646,13 +635,11 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
     while (ldv(S.pstamp + p0 + lane) != stamp) __nanosleep(100);
   __syncwarp();
   __threadfence();
-  const int es              = e0 + (__ffs(dm) - 1) * kPiece;  // first recomputed piece
-  const long long c_stream = S.dbg ? clock64() : 0;
-  const double2* gb         = S.gbuf + off;
+  const int pf             = __ffs(dm) - 1;  // first recomputed piece
+  const long long c_stream = DBG_ON(S) ? clock64() : 0;
   double acc = 0.0, gtw = 0.0, gpm = 0.0;
-  if (es > e0 && lane < 2) acc = __ldcg(reinterpret_cast<const double*>(S.ckpt + p0 + (es - e0) / kPiece) + lane);
+  if (pf > 0 && lane < 2) acc = __ldcg(reinterpret_cast<const double*>(S.ckpt + p0 + pf) + lane);
   int imn = 0, imx = 0;
-  const unsigned lt = lanemask_lt();
   // chunk aggregates of the segment: lanes read them strided (off the fold's critical path)
   for (int q = (off + e0) / kTile + lane; q < (off + e1 + kTile - 1) / kTile; q += 32) {
     const ChunkInfo* ch = S.cinfo + q;
@@ -661,90 +648,59 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
     gtw = fmax(gtw, __ldcg(&ch->gtw));
     gpm = fmax(gpm, __ldcg(&ch->gpm));
   }
-  WarpTma* Tp = BP_HEAVY_TMA ? c.tma : nullptr;
-  if (Tp && c.tma_owner) {  // one shared slot per block (k_rows_full): take it if free
-    int got = 0;
-    if (lane == 0) got = atomicCAS(c.tma_owner, -1, c.warp) == -1;
-    if (!__shfl_sync(FULL, got, 0)) Tp = nullptr;
-  }
-  if (Tp) {
-  // The contribution stream by TMA bulk copies (cp.async.bulk, 2 KB per 128-entry chunk) into two
-  // shared-memory buffers, the copy of chunk c + 2 in flight while chunk c is folded. The rows'
-  // gbuf regions are 128-entry aligned and zero-padded, so every chunk is a full 2 KB copy.
-  WarpTma& T       = *Tp;
-  const int nchunk = (e1 - es + kTile - 1) / kTile;
-  unsigned u0 = T.uses[0], u1 = T.uses[1];  // completed uses before this segment (warp-uniform)
+  // the chunk list from piece pf on (kFoldVals values per chunk and stream): lane q holds piece q's
+  // counts and its chunks' inclusive prefix (at least one chunk per piece, possibly empty: its
+  // checkpoint is written when it starts)
+  const int2 cnt = lane < np ? __ldcg(S.pcnt + p0 + lane) : make_int2(0, 0);
+  const int nck  = lane >= pf && lane < np ? max(1, (max(cnt.x, cnt.y) + kFoldVals - 1) / kFoldVals) : 0;
+  const int incl = warp_incl_scan(nck, lane);
+  const int T    = __shfl_sync(FULL, incl, 31);
+  const double* gmn = S.gmin + off + e0;
+  const double* gmx = S.gmax + off + e0;
+  // chunk t -> piece q, chunk cc of the piece, and this chunk's value counts (warp-uniform)
+  auto locate = [&](int t, int& q, int& cc, int& nm, int& nx) {
+    q  = __popc(__ballot_sync(FULL, incl <= t));
+    cc = t - (__shfl_sync(FULL, incl, q) - __shfl_sync(FULL, nck, q));
+    nm = min(kFoldVals, max(0, __shfl_sync(FULL, cnt.x, q) - cc * kFoldVals));
+    nx = min(kFoldVals, max(0, __shfl_sync(FULL, cnt.y, q) - cc * kFoldVals));
+  };
+  constexpr int V = kFoldVals / 32;
+  double rm[V], rx[V];
+  auto fetch = [&](int t) {  // chunk t's values into registers (zeros past the counts / the list)
+    int q = 0, cc = 0, nm = 0, nx = 0;
+    if (t < T) locate(t, q, cc, nm, nx);
+    const int base = q * kPiece + cc * kFoldVals;
+#pragma unroll
+    for (int h = 0; h < V; ++h) {
+      const int j = h * 32 + lane;
+      rm[h]       = j < nm ? __ldcg(gmn + base + j) : 0.0;
+      rx[h]       = j < nx ? __ldcg(gmx + base + j) : 0.0;
+    }
+  };
+  // two buffers per stream in the warp's staging region (b0 / b1 are contiguous)
+  double* buf = c.w.b0;
+  auto stage = [&](int bi) {
+#pragma unroll
+    for (int h = 0; h < V; ++h) {
+      buf[bi * kFoldVals + h * 32 + lane]                 = rm[h];
+      buf[(2 + bi) * kFoldVals + h * 32 + lane]           = rx[h];
+    }
+  };
+  fetch(0);
+  stage(0);
+  fetch(1);
   __syncwarp();
-  if (lane == 0) {
-#if BP_TMA_GLOBAL_FENCE
-    // the pieces' generic-proxy writes (acquired through their stamps above) before async reads
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-#endif
-    bulk_load(T.buf[0], gb + es, kTile * sizeof(double2), &T.mbar[0]);
-    if (nchunk > 1) bulk_load(T.buf[1], gb + es + kTile, kTile * sizeof(double2), &T.mbar[1]);
-  }
-  for (int ck = 0; ck < nchunk; ++ck) {
-    const int base = es + ck * kTile, bi = ck & 1;
-    if (lane < 2 && ((base - e0) & (kPiece - 1)) == 0)  // checkpoint: the sums before this piece
-      reinterpret_cast<double*>(S.ckpt + p0 + (base - e0) / kPiece)[lane] = acc;
-    mbar_wait(&T.mbar[bi], (bi ? u1 : u0) & 1u);
-    if (bi) ++u1;
-    else ++u0;
-    int pm = 0, px = 0;
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      const double2 vv = T.buf[bi][h * 32 + lane];
-      const double cm = vv.x, cx = vv.y;  // beyond e1: padding zeros
-      const unsigned m = __ballot_sync(FULL, cm != 0.0);
-      const unsigned x = __ballot_sync(FULL, cx != 0.0);
-      if (cm != 0.0) c.w.b0[pm + __popc(m & lt)] = cm;
-      if (cx != 0.0) c.w.b1[px + __popc(x & lt)] = cx;
-      pm += __popc(m);
-      px += __popc(x);
+  for (int t = 0; t < T; ++t) {
+    const int bi = t & 1;
+    stage(bi ^ 1);  // chunk t + 1 (its buffers were last read in iteration t - 1)
+    int q, cc, nm, nx;
+    locate(t, q, cc, nm, nx);
+    fetch(t + 2);
+    if (lane < 2) {
+      if (cc == 0) reinterpret_cast<double*>(S.ckpt + p0 + q)[lane] = acc;  // the sums before piece q
+      acc = fold_seq(buf + (2 * lane + bi) * kFoldVals, lane ? nx : nm, acc);
     }
     __syncwarp();
-    if (lane == 0 && ck + 2 < nchunk)  // this buffer is free again: chunk ck + 2 into it
-      bulk_load(T.buf[bi], gb + base + 2 * kTile, kTile * sizeof(double2), &T.mbar[bi]);
-    if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
-    __syncwarp();
-  }
-  if (lane == 0) {
-    T.uses[0] = u0;
-    T.uses[1] = u1;
-  }
-  __syncwarp();
-    if (c.tma_owner && lane == 0) atomicExch(c.tma_owner, -1);  // release the block's slot
-  } else {  // register stream: two chunks' loads in flight
-    double2 v[kEPL], w[kEPL];
-#pragma unroll
-  for (int h = 0; h < kEPL; ++h) {
-    v[h] = __ldcg(gb + es + h * 32 + lane);
-    w[h] = es + kTile < e1 ? __ldcg(gb + es + kTile + h * 32 + lane) : make_double2(0.0, 0.0);
-  }
-  for (int base = es; base < e1; base += kTile) {
-    if (lane < 2 && ((base - e0) & (kPiece - 1)) == 0)  // checkpoint: the sums before this piece
-      reinterpret_cast<double*>(S.ckpt + p0 + (base - e0) / kPiece)[lane] = acc;
-    int pm = 0, px = 0;
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      const double cm = v[h].x, cx = v[h].y;  // beyond e1: padding zeros
-      const unsigned m = __ballot_sync(FULL, cm != 0.0);
-      const unsigned x = __ballot_sync(FULL, cx != 0.0);
-      if (cm != 0.0) c.w.b0[pm + __popc(m & lt)] = cm;
-      if (cx != 0.0) c.w.b1[px + __popc(x & lt)] = cx;
-      pm += __popc(m);
-      px += __popc(x);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      v[h]         = w[h];
-      const int e2 = base + 2 * kTile + h * 32 + lane;
-      w[h]         = base + 2 * kTile < e1 ? __ldcg(gb + e2) : make_double2(0.0, 0.0);
-    }
-    if (lane < 2) acc = fold_seq(lane ? c.w.b1 : c.w.b0, lane ? px : pm, acc);
-    __syncwarp();
-  }
   }
   imn = warp_sum(imn);
   imx = warp_sum(imx);
@@ -870,9 +826,7 @@ __device__ void group_fold(Ctx& c, int t0, int nt, bool cand, unsigned ds = 0)
       double tw, pw;
       entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pw);
       if (entry_quiet(tw, pw, smn, imn, smx, imx, cb.y, cb.x)) continue;
-      double cl, cu;
-      cand_explicit(bd[h].x, bd[h].y, ci[h] < 0, a[h], smn, imn, smx, imx, cb.y, cb.x, cl, cu);
-      publish(S.slot + (ci[h] & ~kIntBit), cl, cu, bd[h].x, bd[h].y, k);
+      emit_cand(S.slot, ci[h], a[h], bd[h].x, bd[h].y, smn, imn, smx, imx, cb.y, cb.x, k);
     }
   }
 }
@@ -910,7 +864,6 @@ __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp, unsigned d
 #define BP_SELL_UNROLL 4
 #endif
 constexpr int kSellUnroll = BP_SELL_UNROLL;  // entries per lane in flight
-
 __device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
@@ -968,7 +921,7 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
   }
   if (!cand) return;
   const bool quiet = k < 0 || (kRowGate && entry_quiet(gtw, gpm, smn, imn, smx, imx, cb.y, cb.x));
-  if (S.dbg) {  // gate statistics (BP_DEBUG=1)
+  if (DBG_ON(S)) {  // gate statistics (BP_DEBUG=1, built with -DBP_DBG_STATS=1)
     const unsigned nr = __popc(__ballot_sync(FULL, k >= 0)), nq = __popc(__ballot_sync(FULL, !quiet));
     if (c.lane == 0) {
       atomicAdd(S.dbg + 16, (unsigned long long)nr);
@@ -992,12 +945,10 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
       if (ci[u] == -1) continue;
       double tw, pw;
       entry_reach(a[u], bd[u].x, bd[u].y, ci[u] < 0, tw, pw);
-      if (S.dbg) atomicAdd(S.dbg + 18, 1ull);
+      if (DBG_ON(S)) atomicAdd(S.dbg + 18, 1ull);
       if (entry_quiet(tw, pw, smn, imn, smx, imx, cb.y, cb.x)) continue;
-      if (S.dbg) atomicAdd(S.dbg + 19, 1ull);
-      double cl, cu;
-      cand_explicit(bd[u].x, bd[u].y, ci[u] < 0, a[u], smn, imn, smx, imx, cb.y, cb.x, cl, cu);
-      publish(S.slot + (ci[u] & ~kIntBit), cl, cu, bd[u].x, bd[u].y, k);
+      if (DBG_ON(S)) atomicAdd(S.dbg + 19, 1ull);
+      emit_cand(S.slot, ci[u], a[u], bd[u].x, bd[u].y, smn, imn, smx, imx, cb.y, cb.x, k);
     }
   }
 }
@@ -1073,12 +1024,12 @@ __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
     return;
   }
   for (Prefetch it_t(c, &pc->cur_s, 1, nsl, true); it_t.t < nsl; it_t.advance()) {
-    const long long c0 = S.dbg ? clock64() : 0;
+    const long long c0 = DBG_ON(S) ? clock64() : 0;
     sell_slice(c, it_t.t, cand);
     dbg_task(c, 1, c0);
   }
   for (Prefetch it_t(c, &pc->cur_a, 4, ns - nsl, true); nsl + it_t.t < ns; it_t.advance()) {
-    const long long c0 = S.dbg ? clock64() : 0;
+    const long long c0 = DBG_ON(S) ? clock64() : 0;
     for (int q = nsl + it_t.t; q < min(ns, nsl + it_t.t + 4); ++q) sell_slice(c, q, cand);
     dbg_task(c, 1, c0);
   }
@@ -1108,14 +1059,14 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     }
     const int nfh = P.n_fold_heavy;
     for (Prefetch it_t(c, &pc->cur_b, 1, nfh); it_t.t < nfh; it_t.advance()) {
-      const long long c0 = S.dbg ? clock64() : 0;
+      const long long c0 = DBG_ON(S) ? clock64() : 0;
       const int2 tk      = folds[it_t.t];
       if (row_live(S, tk.x, ds)) heavy_fold(c, tk.x, tk.y, cand, stamp, ds);
       dbg_task(c, 0, c0);
     }
     if (ds == 0) {
       for (Prefetch it_t(c, &pc->cur_g, 4, nf - nfh, true); nfh + it_t.t < nf; it_t.advance()) {
-        const long long c0 = S.dbg ? clock64() : 0;
+        const long long c0 = DBG_ON(S) ? clock64() : 0;
         group_fold(c, nfh + it_t.t, min(4, nf - nfh - it_t.t), cand);
         dbg_task(c, 4, c0);
       }
@@ -1129,7 +1080,7 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     if (sell_here) phase_sell(c, pc, cand, ds);
     const int nc = cand && pieces_here ? P.n_cpiece : 0;
     for (Prefetch it_t(c, &pc->cur_c, 1, nc); it_t.t < nc; it_t.advance()) {
-      const long long c0 = S.dbg ? clock64() : 0;
+      const long long c0 = DBG_ON(S) ? clock64() : 0;
       const int2 tk      = P.cpiece_task[it_t.t];
       long_cand_piece(c, tk.x, tk.y, stamp, ds);
       dbg_task(c, 2, c0);
@@ -1679,16 +1630,31 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
 // Dirty marks for a dirty-filtered full round: row_stamp[k] = stamp for every row of a variable
 // that changed this round (the reference's dirty_rows, propagation.hpp:474-476). Changed vars with
 // short columns go 32 per warp (flattened 128-entry windows); longer columns by their chunk tasks.
-__device__ __forceinline__ void mark_entry(const DevProblem& P, const DevState& S, int e, unsigned stamp)
+__device__ __forceinline__ void mark_entry(const DevState& S, int mk, int row, unsigned stamp)
 {
-  const int mk = __ldg(P.col_mark + e);
   if (mk >= 0) {
     S.task_stamp[mk] = stamp;  // SELL slice / medium-row group, and the row inside it
-    S.row_flag[__ldg(P.col_row + e)] = (unsigned char)stamp;
+    S.row_flag[row]  = (unsigned char)stamp;
   } else {                     // heavy row: its piece, and the row for its segment folds
     S.piece_dirty[-mk - 2] = stamp;
-    S.row_stamp[__ldg(P.col_row + e)] = stamp;
+    S.row_stamp[row]       = stamp;
   }
+}
+
+// Marks the entries [e0, e1) (at most kTile) of a column, 32 lanes x kEPL loads in flight.
+__device__ __forceinline__ void mark_window(const DevProblem& P, const DevState& S, int e0, int e1,
+                                            int lane, unsigned stamp)
+{
+  int mk[kEPL], rw[kEPL];
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h) {
+    const int e = e0 + h * 32 + lane;
+    mk[h]       = e < e1 ? __ldg(P.col_mark + e) : 0;
+    rw[h]       = e < e1 ? __ldg(P.col_row + e) : -1;
+  }
+#pragma unroll
+  for (int h = 0; h < kEPL; ++h)
+    if (rw[h] >= 0) mark_entry(S, mk[h], rw[h], stamp);
 }
 
 // Dirty marks for a dirty-filtered full round: every row task (SELL slice, group of four medium rows,
@@ -1701,22 +1667,18 @@ __device__ void phase_mark_rows(Ctx& c, ParCtl* pc, unsigned stamp)
   const DevState& S   = c.S;
   const int nch       = ldv(&pc->n_changed);
   const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
-  for (int j = gw * 32 + c.lane; j < nch; j += nw * 32) {
+  // a warp per changed var (a lane walking its column serially costs a load latency per entry)
+  for (int j = gw; j < nch; j += nw) {
     const int i  = S.changed[j];
     const int cs = __ldg(P.col_start + i), ce = __ldg(P.col_start + i + 1);
-    if (ce - cs > kTile) continue;
-    for (int e = cs; e < ce; ++e) mark_entry(P, S, e, stamp);
+    if (ce - cs <= kTile) mark_window(P, S, cs, ce, c.lane, stamp);
   }
   const int ntask = ldv(&pc->n_ctask);
   for (int t = gw; t < ntask; t += nw) {
     const int2 tk = S.ctask[t];
     const int ce  = __ldg(P.col_start + tk.x + 1);
-    const int e0  = __ldg(P.col_start + tk.x) + tk.y * kTile, e1 = min(ce, e0 + kTile);
-#pragma unroll
-    for (int h = 0; h < kEPL; ++h) {
-      const int e = e0 + h * 32 + c.lane;
-      if (e < e1) mark_entry(P, S, e, stamp);
-    }
+    const int e0  = __ldg(P.col_start + tk.x) + tk.y * kTile;
+    mark_window(P, S, e0, min(ce, e0 + kTile), c.lane, stamp);
   }
 }
 
@@ -1792,34 +1754,24 @@ __device__ void zero_par(ParCtl* q)
 #ifndef BP_F2_MIN_BLOCKS
 #define BP_F2_MIN_BLOCKS 2
 #endif
-// Shared memory of k_rows_full: its row tasks stage at most 128 values per chain (heavy folds)
-// or 4 x 32 (grouped medium rows) in b0 / b1, so each warp gets a 3 KB region (b0 at 0, b1 at
-// 2 KB) instead of a full WarpSmem: 24 KB per block, which lets the SM keep the larger L1 split
-// (the bound gathers are L1 hits as often as the L1 is large).
+// Shared memory of k_rows_full: its row tasks stage 4 x kFoldVals values (heavy folds) or 4 x 32
+// (grouped medium rows) in b0 / b1, so each warp gets a 3 KB region (b0 at 0, b1 at 2 KB) instead
+// of a full WarpSmem: 24 KB per block, which lets the SM keep the larger L1 split (the bound
+// gathers are L1 hits as often as the L1 is large).
+// (TMA bulk copies of the heavy contribution streams were measured in round 2 -- 12% slower on C2:
+// two chunks in flight per warp hide less latency than 128 independent register loads, and more
+// buffers cost the L1 carveout; removed. profiles/README.md.)
 #ifndef BP_ROWS_COMPACT_SMEM
 #define BP_ROWS_COMPACT_SMEM 1
 #endif
 constexpr int kRowsWarpBytes = 3072;
 static_assert(offsetof(WarpSmem, b1) == 2048 && 2048 + 128 * 8 <= kRowsWarpBytes, "row-task smem layout");
-// compact layout: kWarps regions of kRowsWarpBytes, then one WarpTma per warp
-constexpr size_t kRowsTmaOff = (size_t)kWarps * kRowsWarpBytes;
-static_assert(kRowsTmaOff % 16 == 0, "TMA buffers must be 16-byte aligned");
-// one TMA slot per block (+ its owner word): a per-warp slot would cost the SM's L1 carveout, which
-// the bound gathers of the other row tasks depend on (measured: -10% on C2 with 8 slots per block)
-// BP_HEAVY_TMA=1 streams heavy segments into shared memory with TMA bulk copies (cp.async.bulk +
-// mbarrier, two 2 KB chunks in flight). Measured on C2 (tools/gpu_ab.sh, same box, 3 x 3 runs):
-// 10.38 ms per propagate with it vs 9.22 ms with the register stream (two chunks' loads in flight
-// per lane) -- the heavy chains are latency-bound and two 2 KB bulk copies in flight hide less
-// than 128 independent loads; with a slot per warp the larger shared carveout also costs L1. Off.
-#ifndef BP_HEAVY_TMA
-#define BP_HEAVY_TMA 0
-#endif
+static_assert(4 * kFoldVals * 8 <= kRowsWarpBytes, "heavy-fold staging buffers");
 #ifndef BP_ROWS_SMEM_PAD
 #define BP_ROWS_SMEM_PAD 0
 #endif
 constexpr size_t kRowsSmem =
-    BP_ROWS_COMPACT_SMEM ? kRowsTmaOff + (BP_HEAVY_TMA ? sizeof(WarpTma) + 16 : 16) + BP_ROWS_SMEM_PAD
-                         : sizeof(Smem);
+    BP_ROWS_COMPACT_SMEM ? (size_t)kWarps * kRowsWarpBytes + 16 + BP_ROWS_SMEM_PAD : sizeof(Smem);
 // The host enqueues [k_rows_full, k_cand_pieces, k_engine(resume)] speculatively, several rounds
 // ahead without waiting: each is a no-op unless the engine handed a full round over (need_full).
 __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
@@ -1836,21 +1788,12 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
 #if BP_ROWS_COMPACT_SMEM
-  // compact warp regions: only b0[0..128) and b1[0..128) are used by the full round's row tasks
-  WarpSmem& w  = *reinterpret_cast<WarpSmem*>(dyn_smem + warp * kRowsWarpBytes);
-  WarpTma* tma = reinterpret_cast<WarpTma*>(dyn_smem + kRowsTmaOff);
-  int* owner   = reinterpret_cast<int*>(dyn_smem + kRowsTmaOff + sizeof(WarpTma));
-  if (BP_HEAVY_TMA && warp == 0) {
-    tma_init(tma, (int)(threadIdx.x & 31));
-    if (threadIdx.x == 0) *owner = -1;
-  }
-  if (BP_HEAVY_TMA) __syncthreads();
+  // compact warp regions: only the first 3 KB of a WarpSmem are used by the full round's row tasks
+  WarpSmem& w = *reinterpret_cast<WarpSmem*>(dyn_smem + warp * kRowsWarpBytes);
 #else
-  WarpSmem& w  = sm.w[warp];
-  WarpTma* tma = nullptr;
-  int* owner   = nullptr;
+  WarpSmem& w = sm.w[warp];
 #endif
-  Ctx c{P, S, lim, sm, w, (int)(threadIdx.x & 31), warp, tma, owner};
+  Ctx c{P, S, lim, sm, w, (int)(threadIdx.x & 31), warp};
   phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell, ldv(&S.ctl->df_stamp));
 }
 
@@ -1870,7 +1813,7 @@ __global__ void __launch_bounds__(kThreads, BP_SELL_MIN_BLOCKS)
     __shared__ __align__(16) unsigned char no_smem[16];  // sell_slice never touches the warp smem
     Smem& sm       = *reinterpret_cast<Smem*>(no_smem);
     const int warp = threadIdx.x >> 5;
-    Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp, nullptr, nullptr};
+    Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp};
     phase_sell(c, &S.ctl->par[par], true, ldv(&S.ctl->df_stamp));
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1885,7 +1828,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cand_pieces(DevProblem P, DevSt
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
-  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp, nullptr, nullptr};
+  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   for (int t = gw; t < P.n_cpiece; t += nw) {
     const int2 tk = P.cpiece_task[t];
@@ -1910,13 +1853,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5;
-#if BP_HEAVY_TMA
-  tma_init(&sm.tma[warp], (int)(threadIdx.x & 31));
-  WarpTma* tma = &sm.tma[warp];
-#else
-  WarpTma* tma = nullptr;
-#endif
-  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp, tma, nullptr};
+  Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
 
   if (mode == MODE_ACTIVITY) {
     const bool full = full_first != 0;
@@ -2067,10 +2004,11 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
         if (lead) S.ctl->df_cnt[0] = S.ctl->df_cnt[1] = S.ctl->df_cnt[2] = 0;
         phase_mark_rows(c, pc, stamp);
         grid.sync();  // marks (and the zeroed counts) visible grid-wide
+        if (st && lead) st[8] = (long long)(globaltimer() - t0);  // (expansion columns: unused here)
         phase_df_lists(c, stamp);
         df_next = stamp;
         if (!ext_f2 || st) grid.sync();  // in-engine row phase: lists complete first
-        if (st && lead) st[11] = (long long)(globaltimer() - t0);
+        if (st && lead) st[9] = st[11] = (long long)(globaltimer() - t0);
       }
       full = true;
     };
@@ -2440,6 +2378,7 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.rec.alloc(mm);
   P.aux.alloc(mm);
   P.gbuf.alloc((size_t)std::max(P.n_long_entries, 1ll));
+  P.pcnt.alloc((size_t)std::max(P.n_piece, 1));
   P.cinfo.alloc((size_t)std::max(P.n_long_entries / kTile, 1ll));
   P.pstamp.alloc((size_t)std::max(P.n_piece, 1));
   P.piece_dirty.alloc((size_t)std::max(P.n_piece, 1));
@@ -2484,7 +2423,9 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.bounds    = P.bounds.p;
   S.rec       = P.rec.p;
   S.aux       = P.aux.p;
-  S.gbuf      = P.gbuf.p;
+  S.gmin      = reinterpret_cast<double*>(P.gbuf.p);
+  S.gmax      = S.gmin + std::max(P.n_long_entries, 1ll);
+  S.pcnt      = P.pcnt.p;
   S.slot      = P.slot.p;
   P.slot_state.alloc(1);
   BP_CUDA(cudaMemset(P.slot_state.p, 0, sizeof(int)));  // the slots start empty

@@ -257,6 +257,12 @@ struct RoundCtx {
   bool ws_cert       = false;
   long long bp_calls = 0;
   double dev_ms      = 0.0;
+  // BP_ROUND_STATS=1 (with BP_ROUND_PROFILE): per-round work and phase times of every engine call,
+  // aggregated by round index (device stats rows, see kStatCols)
+  bool stats_on = getenv("BP_ROUND_STATS") != nullptr;
+  DBuf<long long> d_stats;
+  std::vector<double> st_sum = std::vector<double>(17 * 10, 0.0);
+  std::vector<long long> st_rounds = std::vector<long long>(66, 0);
 
   RoundCtx(Problem& P_, const bp_problem_host& H_) : P(P_), H(H_), s(P_.stream) {}
 
@@ -401,7 +407,32 @@ struct RoundCtx {
       stage_changed(P, changed.data(), (int)changed.size(), s);
       flags = ENGINE_START_FRONTIER;
     }
-    const RunResult r = run_engine(P, MODE_PROPAGATE, true, limits(), s, flags);
+    long long* stp = nullptr;
+    if (stats_on) {
+      reserve(d_stats, 64 * kStatCols);
+      BP_CUDA(cudaMemsetAsync(d_stats.p, 0, sizeof(long long) * 64 * kStatCols, s));
+      stp = d_stats.p;
+    }
+    const RunResult r = run_engine(P, MODE_PROPAGATE, true, limits(), s, flags, stp);
+    if (stats_on) {
+      std::vector<long long> h(64 * kStatCols);
+      BP_CUDA(cudaMemcpy(h.data(), d_stats.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost));
+      st_rounds[std::min(r.rounds, 65)]++;
+      long long prev = 0;
+      for (int q = 0; q < std::min(r.rounds, 64); ++q) {
+        const long long* row = h.data() + q * kStatCols;
+        const int b = std::min(q, 16);
+        double* o = st_sum.data() + b * 10;
+        // calls reaching this round, full rounds, |R|, A, |V|, B, then us: gather, activity,
+        // tightening, expansion (rows + vars)
+        o[0] += 1; o[1] += row[0]; o[2] += row[1]; o[3] += row[2]; o[4] += row[3]; o[5] += row[4];
+        o[6] += (row[10] - prev) * 1e-3;
+        o[7] += (row[6] - row[10]) * 1e-3;
+        o[8] += (row[7] - row[6]) * 1e-3;
+        o[9] += (row[9] - row[7]) * 1e-3;
+        prev = row[9];
+      }
+    }
     bp_calls++;
     dev_ms += P.last_kernel_ms;
     return r;
@@ -1015,6 +1046,19 @@ int round_impl(bp_problem* p, const double* start_values, const bp_cache* cache,
         fprintf(stderr, "[bp round] %-18s n=%lld total=%.3f s avg=%.1f us\n", nm[q], TT.n[q], TT.t[q],
                 TT.n[q] ? 1e6 * TT.t[q] / TT.n[q] : 0.0);
       fprintf(stderr, "[bp round] engine device %.3f s over %lld calls\n", X.dev_ms * 1e-3, X.bp_calls);
+      if (X.stats_on) {
+        fprintf(stderr, "[bp round] engine rounds per call:");
+        for (int q = 0; q < 66; ++q)
+          if (X.st_rounds[q]) fprintf(stderr, " %d:%lld", q, X.st_rounds[q]);
+        fprintf(stderr, "\n[bp round]  rnd  calls  full%%      |R|          A      |V|          B   gath_us    act_us  tight_us    exp_us (means per call reaching the round)\n");
+        for (int q = 0; q < 17; ++q) {
+          const double* o = X.st_sum.data() + q * 10;
+          if (o[0] == 0) continue;
+          fprintf(stderr, "[bp round] %3d%s %7.0f %5.1f %9.0f %10.0f %8.0f %10.0f %9.1f %9.1f %9.1f %9.1f\n", q + 1,
+                  q == 16 ? "+" : " ", o[0], 100 * o[1] / o[0], o[2] / o[0], o[3] / o[0], o[4] / o[0],
+                  o[5] / o[0], o[6] / o[0], o[7] / o[0], o[8] / o[0], o[9] / o[0]);
+        }
+      }
     }
     o.completed       = X.n_unset == 0;
     o.bounds_feasible = o.completed && !o.rounding_infeasible && !X.ws_infeasible;
