@@ -377,6 +377,15 @@ constexpr int kPackNnz   = BP_PACK_NNZ;   // full rounds: rows up to this length
 static_assert(kPackNnz == kShortNnz, "BP_PACK_NNZ must equal kShortNnz (the validated configuration)");
 constexpr int kPackTile  = BP_PACK_TILE;  // packed row tiles: <= 32 rows and <= this many entries
 
+// Per heavy-row piece: round-to-nearest sums and absolute sums of its min / max contributions
+// (any order), its reach maxima and infinite-contributor counts -- the inputs of the row-level
+// quietness certificate that lets a full round skip a heavy row's sequential chains (heavy_fold).
+struct PieceAgg {
+  double smin, amin, smax, amax;
+  double gtw, gpm;
+  int imn, imx;
+};
+
 struct SegPart {
   double min, max;
   double tmax, pmax;  // row-level candidate gating: max |a|(w + 1), max |a|max(|lo|,|up|)

@@ -79,7 +79,7 @@ struct Ctl {
   // recomputed and publish candidates, the candidate slots of unchanged vars persisting.
   unsigned df_stamp;
   int df_cnt[3];  // dirty lists of a dirty-filtered round: slices, medium-row groups, heavy pieces
-  int pad1;
+  int stale;      // some heavy row's activity record is stale (certified quiet, chain skipped)
   unsigned long long t0;      // globaltimer at the start of the propagate (time limit, stats)
   int pad[2];
 };
@@ -94,6 +94,8 @@ struct DevState {
   double* gmin;
   double* gmax;
   int2* pcnt;
+  PieceAgg* pagg;   // per piece: the quietness-certificate aggregates
+  unsigned* sfold;  // per heavy segment (at its first piece): stamp of its last exact fold
   CandSlot* slot;     // fused full round: per-var candidate slots
   // Candidate-slot state, kept across calls (outside Ctl, which callers zero per call): 0 = all
   // empty, 1 = valid for the current bounds (left by a full or dirty-filtered round's finalize:
@@ -172,6 +174,8 @@ struct Problem {
   DBuf<double2> aux;
   DBuf<double2> gbuf;  // storage of gmin / gmax (n_long_entries doubles each)
   DBuf<int2> pcnt;
+  DBuf<PieceAgg> pagg;
+  DBuf<unsigned> sfold;
   DBuf<CandSlot> slot;
   DBuf<int> slot_state;
   DBuf<unsigned> ready;

@@ -542,6 +542,7 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
   double* gmx = S.gmax + off + e0;
   const unsigned lt = lanemask_lt();
   int pm = 0, px = 0;
+  PieceAgg ag{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};  // this lane's part of the piece aggregates
   for (int j0 = e0; j0 < e1; j0 += kTile) {
     int ci[kEPL];
     double a[kEPL];
@@ -569,6 +570,10 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
         gtw = fmax(gtw, tw);
         gpm = fmax(gpm, pw);
       }
+      ag.smin = __dadd_rn(ag.smin, cm);
+      ag.amin = __dadd_rn(ag.amin, fabs(cm));
+      ag.smax = __dadd_rn(ag.smax, cx);
+      ag.amax = __dadd_rn(ag.amax, fabs(cx));
       // zero contributions are skipped: exact, the running sums are never -0.0
       const unsigned m = __ballot_sync(FULL, cm != 0.0);
       const unsigned x = __ballot_sync(FULL, cx != 0.0);
@@ -588,9 +593,21 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
       ChunkInfo ci_{gtw, gpm, imn, imx};
       S.cinfo[(off + j0) / kTile] = ci_;
     }
+    ag.gtw = fmax(ag.gtw, gtw);  // (warp-uniform after the reductions above)
+    ag.gpm = fmax(ag.gpm, gpm);
+    ag.imn += imn;
+    ag.imx += imx;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    ag.smin = __dadd_rn(ag.smin, __shfl_xor_sync(FULL, ag.smin, o));
+    ag.amin = __dadd_rn(ag.amin, __shfl_xor_sync(FULL, ag.amin, o));
+    ag.smax = __dadd_rn(ag.smax, __shfl_xor_sync(FULL, ag.smax, o));
+    ag.amax = __dadd_rn(ag.amax, __shfl_xor_sync(FULL, ag.amax, o));
   }
   __syncwarp();
   if (c.lane == 0) {
+    S.pagg[pi] = ag;
     S.pcnt[pi] = make_int2(pm, px);
     __threadfence();
     atomicExch(S.pstamp + pi, stamp);
@@ -603,7 +620,89 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
 // other buffer) and has chunk t + 2's loads in flight while the chains fold chunk t.
 constexpr int kFoldVals = 96;  // 4 buffers fill the 3 KB row-task staging region (kRowsWarpBytes)
 static_assert(kFoldVals % 32 == 0 && 4 * kFoldVals * 8 <= 3072, "fold staging buffers");
-__device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, unsigned ds = 0)
+// Fold modes: exact (frontier rounds, activity calls), lazy (full / dirty-filtered rounds: a row
+// certified quiet skips its chains and keeps a stale record), refresh (stale rows only, chains
+// from the first piece changed since their segment's last exact fold).
+enum { kFoldExact = 0, kFoldLazy = 1, kFoldRefresh = 2 };
+
+// Quietness certificate of a heavy row without its sequential sums: from the pieces'
+// any-order sums S and absolute sums A of the min / max contributions, the reference's segmented
+// sequential sum lies within eps*A of S (both err by at most L u sum|x|; eps = 8 (L + 1024) u also
+// covers the bound's own rounding), so the row-level gate (entry_quiet with the row's reach
+// maxima) evaluated in directed rounding over that interval proves that no entry of the row can
+// publish a candidate -- exactly what the gate with the exact activity would prove, or more.
+// Waits for this round's recomputed pieces of the row. Infinite contributors: only counts of 0
+// (side usable with finite parts) or >= 2 (side unusable) are certified.
+__device__ bool heavy_row_quiet(Ctx& c, int k, int L, unsigned stamp, unsigned ds)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int lane = c.lane;
+  const int hp = __ldg(P.hpiece + k), npr = (L + kPiece - 1) / kPiece;
+  for (int q = lane; q < npr; q += 32)
+    if (ds == 0 || __ldcg(S.piece_dirty + hp + q) == ds)
+      while (ldv(S.pstamp + hp + q) != stamp) __nanosleep(100);
+  __syncwarp();
+  __threadfence();
+  double sm = 0.0, am = 0.0, sx = 0.0, ax = 0.0, gtw = 0.0, gpm = 0.0;
+  int imn = 0, imx = 0;
+  for (int q = lane; q < npr; q += 32) {
+    const PieceAgg* a = S.pagg + hp + q;
+    sm = __dadd_rn(sm, __ldcg(&a->smin));
+    am = __dadd_rn(am, __ldcg(&a->amin));
+    sx = __dadd_rn(sx, __ldcg(&a->smax));
+    ax = __dadd_rn(ax, __ldcg(&a->amax));
+    gtw = fmax(gtw, __ldcg(&a->gtw));
+    gpm = fmax(gpm, __ldcg(&a->gpm));
+    imn += __ldcg(&a->imn);
+    imx += __ldcg(&a->imx);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sm  = __dadd_rn(sm, __shfl_xor_sync(FULL, sm, o));
+    am  = __dadd_rn(am, __shfl_xor_sync(FULL, am, o));
+    sx  = __dadd_rn(sx, __shfl_xor_sync(FULL, sx, o));
+    ax  = __dadd_rn(ax, __shfl_xor_sync(FULL, ax, o));
+    gtw = fmax(gtw, __shfl_xor_sync(FULL, gtw, o));
+    gpm = fmax(gpm, __shfl_xor_sync(FULL, gpm, o));
+    imn += __shfl_xor_sync(FULL, imn, o);
+    imx += __shfl_xor_sync(FULL, imx, o);
+  }
+  const double2 cb  = __ldg(&P.cons[k]);
+  const double g = cb.y, h = cb.x;
+  const double eps  = (double)(L + 1024) * 0x1p-50;
+  const double rtw  = __dmul_ru(gtw, 1.0 + 1e-12);
+  bool qg = !isfinite(g) || imn >= 2;
+  if (!qg && imn == 0) {  // side g: slack g - act_min over act_min in [lo, hi]
+    const double e  = __dmul_ru(eps, am);
+    const double hi = __dadd_ru(sm, e), lo = __dsub_rd(sm, e);
+    const double mg = __dmul_ru(1e-12, __dadd_ru(__dadd_ru(fabs(g), fmax(fabs(lo), fabs(hi))), gpm));
+    qg = __dsub_rd(g, hi) >= __dadd_ru(__dadd_ru(rtw, mg), 1e-300);
+  }
+  bool qh = !isfinite(h) || imx >= 2;
+  if (!qh && imx == 0) {  // side h: slack act_max - h
+    const double e  = __dmul_ru(eps, ax);
+    const double hi = __dadd_ru(sx, e), lo = __dsub_rd(sx, e);
+    const double mg = __dmul_ru(1e-12, __dadd_ru(__dadd_ru(fabs(h), fmax(fabs(lo), fabs(hi))), gpm));
+    qh = __dsub_rd(lo, h) >= __dadd_ru(__dadd_ru(rtw, mg), 1e-300);
+  }
+  return qg && qh;
+}
+
+// True when a piece of row k changed after its segment's last exact fold (stale record).
+__device__ bool heavy_row_stale(Ctx& c, int k, int L)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int hp = __ldg(P.hpiece + k), npr = (L + kPiece - 1) / kPiece;
+  constexpr int kSegPieces = kSumSegment / kPiece;
+  bool st = false;
+  for (int q = c.lane; q < npr; q += 32)
+    st = st || ldv(S.pstamp + hp + q) > ldv(S.sfold + hp + q / kSegPieces * kSegPieces);
+  return __any_sync(FULL, st);
+}
+
+__device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, unsigned ds, int mode)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
@@ -612,15 +711,40 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
   const int off = __ldg(P.long_off + k);
   const int e0 = seg * kSumSegment, e1 = min(L, e0 + kSumSegment);
   const int p0 = __ldg(P.hpiece + k) + e0 / kPiece, np = (e1 - e0 + kPiece - 1) / kPiece;
-  // dirty-filtered round: the segment's sum is replayed from the checkpoint of its first recomputed
-  // piece (the prefix before it is unchanged); a segment without one keeps its partial
-  const bool mine = lane < np && (ds == 0 || __ldcg(S.piece_dirty + p0 + lane) == ds);
-  const unsigned dm = __ballot_sync(FULL, mine);
+  if (mode == kFoldRefresh) {
+    if (!heavy_row_stale(c, k, L)) return;
+  } else if (mode == kFoldLazy && cand && heavy_row_quiet(c, k, L, stamp, ds)) {
+    // every segment's warp reaches the same verdict: no chain, no record, no candidates; the
+    // record is refreshed before anything reads it (phase_refresh)
+    if (seg == 0 && lane == 0) {
+      if (L > kCandSplit) {
+        S.rquiet[k] = 1;
+        __threadfence();
+        atomicExch(S.ready + k, stamp);
+      }
+      S.ctl->stale = 1;
+    }
+    return;
+  }
+  if (mode != kFoldRefresh) {
+    // this round's recomputed pieces of the segment (dirty-filtered round: the marked ones)
+    const bool mine = lane < np && (ds == 0 || __ldcg(S.piece_dirty + p0 + lane) == ds);
+    if (mine)
+      while (ldv(S.pstamp + p0 + lane) != stamp) __nanosleep(100);
+    __syncwarp();
+    __threadfence();
+  }
+  // the sum is replayed from the checkpoint of the first piece that changed after the segment's
+  // last exact fold (the prefix before it is unchanged); a segment without one keeps its partial
+  const unsigned fs = ldv(S.sfold + p0);
+  unsigned dm = __ballot_sync(FULL, lane < np && ldv(S.pstamp + p0 + lane) > fs);
+  const int sb = __ldg(P.seg_base + k);
+  if (dm == 0 && sb < 0) dm = 1u;  // (single-segment rows always have a changed piece when folded)
   if (dm == 0) {
     double smn = 0.0, smx = 0.0, gtw = 0.0, gpm = 0.0;
     int imn = 0, imx = 0;
     if (lane == 0) {
-      const SegPart* sq = S.seg_part + __ldg(P.seg_base + k) + seg;
+      const SegPart* sq = S.seg_part + sb + seg;
       smn = __ldcg(&sq->min);
       smx = __ldcg(&sq->max);
       imn = __ldcg(&sq->nmin);
@@ -631,11 +755,7 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
     fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
     return;
   }
-  if (mine)
-    while (ldv(S.pstamp + p0 + lane) != stamp) __nanosleep(100);
-  __syncwarp();
-  __threadfence();
-  const int pf             = __ffs(dm) - 1;  // first recomputed piece
+  const int pf             = __ffs(dm) - 1;  // first changed piece
   const long long c_stream = DBG_ON(S) ? clock64() : 0;
   double acc = 0.0, gtw = 0.0, gpm = 0.0;
   if (pf > 0 && lane < 2) acc = __ldcg(reinterpret_cast<const double*>(S.ckpt + p0 + pf) + lane);
@@ -711,6 +831,7 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
   }
   const double smn = __shfl_sync(FULL, acc, 0);
   const double smx = __shfl_sync(FULL, acc, 1);
+  if (lane == 0) S.sfold[p0] = stamp;  // the segment's partial and checkpoints are exact as of now
   dbg_task(c, 3, c_stream);  // streaming part of a heavy segment (after its pieces are ready)
   fold_finish(c, k, L, seg, smn, smx, imn, imx, gtw, gpm, cand, stamp);
 }
@@ -1061,7 +1182,7 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     for (Prefetch it_t(c, &pc->cur_b, 1, nfh); it_t.t < nfh; it_t.advance()) {
       const long long c0 = DBG_ON(S) ? clock64() : 0;
       const int2 tk      = folds[it_t.t];
-      if (row_live(S, tk.x, ds)) heavy_fold(c, tk.x, tk.y, cand, stamp, ds);
+      if (row_live(S, tk.x, ds)) heavy_fold(c, tk.x, tk.y, cand, stamp, ds, kFoldLazy);
       dbg_task(c, 0, c0);
     }
     if (ds == 0) {
@@ -1092,12 +1213,26 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       heavy_piece(c, S.dpiece[par][it_t.t].x, stamp);
     for (Prefetch it_t(c, &pc->cur_b, 1, nf); it_t.t < nf; it_t.advance()) {
       const int2 tk = folds[it_t.t];
-      if (__ldg(P.long_off + tk.x) >= 0) heavy_fold(c, tk.x, tk.y, false, stamp);
+      if (__ldg(P.long_off + tk.x) >= 0) heavy_fold(c, tk.x, tk.y, false, stamp, 0, kFoldExact);
       else long_fold(c, tk.x, tk.y, false, stamp);
     }
     const int n = ldv(&pc->n_drow_s);
     for (Prefetch it_t(c, &pc->cur_c, 32, n); it_t.t < n; it_t.advance())
       short_list_tile(c, S.drow_s[par], it_t.t, n);
+  }
+}
+
+// Exact records for the heavy rows a lazy full round left stale (certified quiet, chains skipped):
+// every segment of such a row replays its sum from the first piece changed since its last exact
+// fold (the pieces' streams are current). Run before anything reads the records: a frontier
+// round's tightening, and the end of the call.
+__device__ void phase_refresh(Ctx& c, unsigned stamp)
+{
+  const DevProblem& P = c.P;
+  const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
+  for (int t = gw; t < P.n_fold_heavy; t += nw) {
+    const int2 tk = P.fold_task[t];
+    heavy_fold(c, tk.x, tk.y, false, stamp, 0, kFoldRefresh);
   }
 }
 
@@ -1939,6 +2074,15 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
       }
     }
     df_next = 0;
+    if (!fr) {  // a frontier round reads records it does not recompute: no stale heavy row
+      const bool rf = ldv(&S.ctl->stale) != 0;
+      if (rf) {
+        grid.sync();  // every block has read the flag
+        if (lead) S.ctl->stale = 0;
+        phase_refresh(c, stamp);
+        grid.sync();
+      }
+    }
     if (resumed) {
       resumed = false;  // this round's F2 (fused rows + candidates) ran in k_rows_full
     } else if (fr && ext_f2) {
@@ -2037,6 +2181,15 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     full = dense_thr != ~0ull && ldv(&qc->roww) + ldv(&qc->colw) > 2 * dense_thr;
     if (full) go_full();
   }
+  }
+  {  // the call leaves exact records: refresh the heavy rows a lazy round left stale
+    const bool rf = ldv(&S.ctl->stale) != 0;
+    if (rf) {
+      grid.sync();
+      if (lead) S.ctl->stale = 0;
+      phase_refresh(c, stamp_base + (unsigned)rounds);
+      grid.sync();
+    }
   }
   if (lead) {
     if (status == BP_STATUS_UNSET) status = any_change ? BP_STATUS_TIGHTENED : BP_STATUS_UNCHANGED;
@@ -2379,6 +2532,9 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   P.aux.alloc(mm);
   P.gbuf.alloc((size_t)std::max(P.n_long_entries, 1ll));
   P.pcnt.alloc((size_t)std::max(P.n_piece, 1));
+  P.pagg.alloc((size_t)std::max(P.n_piece, 1));
+  P.sfold.alloc((size_t)std::max(P.n_piece, 1));
+  BP_CUDA(cudaMemset(P.sfold.p, 0, sizeof(unsigned) * P.sfold.n));
   P.cinfo.alloc((size_t)std::max(P.n_long_entries / kTile, 1ll));
   P.pstamp.alloc((size_t)std::max(P.n_piece, 1));
   P.piece_dirty.alloc((size_t)std::max(P.n_piece, 1));
@@ -2426,6 +2582,8 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.gmin      = reinterpret_cast<double*>(P.gbuf.p);
   S.gmax      = S.gmin + std::max(P.n_long_entries, 1ll);
   S.pcnt      = P.pcnt.p;
+  S.pagg      = P.pagg.p;
+  S.sfold     = P.sfold.p;
   S.slot      = P.slot.p;
   P.slot_state.alloc(1);
   BP_CUDA(cudaMemset(P.slot_state.p, 0, sizeof(int)));  // the slots start empty
@@ -2518,6 +2676,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
     BP_CUDA(cudaMemsetAsync(P.var_stamp.p, 0, sizeof(unsigned) * P.var_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.ready.p, 0, sizeof(unsigned) * P.ready.n, s));
     BP_CUDA(cudaMemsetAsync(P.pstamp.p, 0, sizeof(unsigned) * P.pstamp.n, s));
+    BP_CUDA(cudaMemsetAsync(P.sfold.p, 0, sizeof(unsigned) * P.sfold.n, s));
     BP_CUDA(cudaMemsetAsync(P.piece_dirty.p, 0, sizeof(unsigned) * P.piece_dirty.n, s));
     BP_CUDA(cudaMemsetAsync(P.task_stamp.p, 0, sizeof(unsigned) * P.task_stamp.n, s));
     P.stamp_base = 1;
