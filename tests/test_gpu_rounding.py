@@ -251,3 +251,88 @@ def test_c4_scaled_full_cache_vs_reference(oracle_built):
     assert g.completed and rf["completed"]
     isint = p.is_integer.astype(bool)
     assert np.array_equal(g.values[isint], rv[isint])
+
+
+def _tight_heavy_instance(seed=11, n=80_000):
+    """Heavy rows (two 16384-segments each) that are knapsacks over binaries, next to loose heavy
+    rows: in each knapsack a chain of 12 binaries (c0 >= 1, c_{i+1} >= c_i, weight 30) rises one
+    per round, so the knapsack's slack shrinks round by round from 400 to 40 -- certified quiet
+    (chains skipped, record stale) while the slack exceeds its reach, exact once it does not, then
+    fixing its heavy binaries to 0. Frontier calls and probing then read the records the lazy
+    rounds left behind."""
+    from paper_2510_20499_b200.problem import problem_from_csr
+    rng = np.random.default_rng(seed)
+    nb, ni = int(0.6 * n), int(0.2 * n)
+    lo = np.zeros(n)
+    up = np.concatenate([np.ones(nb), np.full(ni, 10.0), rng.uniform(1.0, 50.0, n - nb - ni)])
+    isint = np.concatenate([np.ones(nb + ni, np.uint8), np.zeros(n - nb - ni, np.uint8)])
+    rows, cl, cu = [], [], []
+    for q in range(2):  # over disjoint halves of the binaries
+        c = np.sort(q * (nb // 2) + rng.choice(nb // 2, size=20_000, replace=False))
+        w = rng.integers(1, 100, size=c.size).astype(np.float64)
+        chain = np.sort(rng.choice(c.size, size=12, replace=False))
+        w[chain] = 30.0
+        rows.append((c, w))
+        cl.append(-math.inf)
+        cu.append(400.0)
+        cv = c[chain]
+        rows.append((cv[:1], np.ones(1)))
+        cl.append(1.0)
+        cu.append(math.inf)
+        for i in range(11):
+            rows.append((np.sort(cv[i:i + 2]), np.where(cv[i:i + 2] == cv[i + 1], 1.0, -1.0)[np.argsort(cv[i:i + 2])]))
+            cl.append(0.0)
+            cu.append(math.inf)
+    for _ in range(2):  # loose heavy rows, fractional coefficients
+        c = np.sort(rng.choice(n, size=40_000, replace=False))
+        rows.append((c, rng.uniform(0.1, 5.0, size=c.size) * rng.choice([-1.0, 1.0], size=c.size)))
+        cl.append(-1e7)
+        cu.append(1e7)
+    for _ in range(12000):  # short mixed rows
+        L = int(rng.integers(2, 9))
+        c = np.sort(rng.choice(n, size=L, replace=False))
+        a = np.where(c < nb + ni, rng.integers(1, 6, size=L), rng.uniform(0.5, 3.0, size=L)) * rng.choice([-1.0, 1.0], size=L)
+        rows.append((c, a.astype(np.float64)))
+        cl.append(-math.inf)
+        cu.append(float(np.sum(np.maximum(a, 0.0) * up[c]) * 0.6))
+    row_start = np.concatenate([[0], np.cumsum([r[0].size for r in rows])]).astype(np.int32)
+    cols = np.concatenate([r[0] for r in rows]).astype(np.int32)
+    vals = np.concatenate([r[1] for r in rows])
+    p = problem_from_csr(n, len(rows), row_start, cols, vals, lo, up, isint, np.array(cl), np.array(cu),
+                         name="tight-heavy")
+    start = lo + rng.random(n) * (up - lo)
+    return p, start
+
+
+def test_lazy_heavy_rows_vs_reference(oracle_built):
+    """Propagate (incremental and every-round-full), probing from the resulting certified root and
+    fix-and-propagate with that cache, all against the reference, on _tight_heavy_instance."""
+    from oracle.bind import Ref, RefCache, RefProblem, cache_mismatches, ref_propagate, ref_propagation_round
+    if not Ref.available():
+        pytest.skip("reference library missing")
+    from paper_2510_20499_b200 import BoundsState, PropagationLimits, propagate
+    p, start = _tight_heavy_instance()
+    assert (np.diff(p.row_start) > 16384).sum() == 4
+    rp = RefProblem.from_def(p)
+    for inc in (True, False):
+        ob, oinf, ost, orr, ocr = ref_propagate(rp, p.root_bounds(), lim=PropagationLimits(incremental=inc))
+        b = BoundsState(p)
+        r = propagate(p, b, PropagationLimits(incremental=inc))
+        assert (b.infeasible(), int(r.status), r.rounds, r.crossed_vars) == (oinf, ost, orr, ocr)
+        assert r.rounds >= 3
+        assert np.array_equal(b.raw().view(np.uint64), ob.view(np.uint64)), inc
+    b = BoundsState(p)
+    propagate(p, b)
+    q = synth.with_bounds(p, b.raw())
+    rq = RefProblem.from_def(q)
+    gcache = build_cache(q, 1e9)
+    free = [v for v in range(q.n_vars) if q.var_lower[v] != q.var_upper[v] and q.is_integer[v]]
+    sample = np.random.default_rng(3).choice(free, size=48, replace=False)
+    checked, bad = cache_mismatches(gcache, RefCache.probe_into(rq, q.n_vars, q.root_bounds(), sample), sample)
+    assert checked == 48 and bad == []
+    rcache = RefCache.from_gpu(rq, gcache)
+    rv, rf = ref_propagation_round(rq, q.n_vars, start, rcache, 7)
+    g = propagation_round(q, start, gcache, 7)
+    assert {k: int(getattr(g, k)) for k in FLAGS} == {k: rf[k] for k in FLAGS}
+    isint = q.is_integer.astype(bool)
+    assert np.array_equal(g.values[isint], rv[isint])
