@@ -543,18 +543,25 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
   const unsigned lt = lanemask_lt();
   int pm = 0, px = 0;
   PieceAgg ag{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0, 0};  // this lane's part of the piece aggregates
-  for (int j0 = e0; j0 < e1; j0 += kTile) {
-    int ci[kEPL];
-    double a[kEPL];
-    double2 bd[kEPL];
+  // software pipeline over the piece's chunks: chunk j+1's bound gathers and chunk j+2's index /
+  // value loads are in flight while chunk j is evaluated
+  int ci[kEPL], ci2[kEPL];
+  double a[kEPL], a2[kEPL];
+  double2 bd[kEPL];
+  auto load = [&](int j0, int (&ci_)[kEPL], double (&a_)[kEPL]) {
 #pragma unroll
     for (int h = 0; h < kEPL; ++h) {
       const int e = j0 + h * 32 + c.lane;
-      ci[h]       = e < e1 ? __ldg(P.row_ci + rs + e) : -1;
-      a[h]        = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
+      ci_[h]      = e < e1 ? __ldg(P.row_ci + rs + e) : -1;
+      a_[h]       = e < e1 ? __ldg(P.row_val + rs + e) : 0.0;
     }
+  };
+  load(e0, ci, a);
+  load(e0 + kTile, ci2, a2);
 #pragma unroll
-    for (int h = 0; h < kEPL; ++h) bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+  for (int h = 0; h < kEPL; ++h) bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+  for (int j0 = e0; j0 < e1; j0 += kTile) {
+    double cmv[kEPL], cxv[kEPL];
     int imn = 0, imx = 0;
     double gtw = 0.0, gpm = 0.0;
 #pragma unroll
@@ -570,6 +577,20 @@ __device__ void heavy_piece(Ctx& c, int pi, unsigned stamp)
         gtw = fmax(gtw, tw);
         gpm = fmax(gpm, pw);
       }
+      cmv[h] = cm;
+      cxv[h] = cx;
+    }
+    // next chunk: its gathers (indices loaded one chunk ago) and the loads of the one after
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      ci[h] = ci2[h];
+      a[h]  = a2[h];
+      bd[h] = ci[h] != -1 ? S.bounds[ci[h] & ~kIntBit] : make_double2(0.0, 0.0);
+    }
+    load(j0 + 2 * kTile, ci2, a2);
+#pragma unroll
+    for (int h = 0; h < kEPL; ++h) {
+      const double cm = cmv[h], cx = cxv[h];
       ag.smin = __dadd_rn(ag.smin, cm);
       ag.amin = __dadd_rn(ag.amin, fabs(cm));
       ag.smax = __dadd_rn(ag.smax, cx);
