@@ -1959,7 +1959,7 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
 // exiting, every block waits for k_rows_full to complete (griddepcontrol.wait), so this grid's
 // completion -- which the following launches are stream-ordered on -- implies that one's.
 #ifndef BP_SELL_MIN_BLOCKS
-#define BP_SELL_MIN_BLOCKS 4
+#define BP_SELL_MIN_BLOCKS 3  // 80 registers, 48 B spills (4: 64 registers, 216 B spills, slower)
 #endif
 __global__ void __launch_bounds__(kThreads, BP_SELL_MIN_BLOCKS)
     k_rows_sell(DevProblem P, DevState S, Limits lim)
@@ -2674,6 +2674,8 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   BP_CUDA(cudaFuncSetAttribute(k_cand_pieces, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)sizeof(Smem)));
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_rows_full, kThreads, kRowsSmem));
+  static const int f2_per_sm = getenv("BP_F2_PER_SM") ? atoi(getenv("BP_F2_PER_SM")) : 0;
+  if (f2_per_sm > 0) per_sm2 = std::min(per_sm2, f2_per_sm);
   P.f2_blocks = dev_sms * std::max(per_sm2, 1);
   int per_sm3   = 0;
   BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_rows_sell, kThreads, 0));
@@ -2717,9 +2719,11 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   static const long long ext_min = getenv("BP_EXT_MIN_NNZ") ? atoll(getenv("BP_EXT_MIN_NNZ")) : 2000000;
   int ext        = (mode == MODE_PROPAGATE && !no_ext && P.nnz >= ext_min) ? 1 : 0;
   int resume     = 0;
-  // BP_SPLIT_SELL=1: SELL slices in k_rows_sell at their own (higher) occupancy. Measured slower on
-  // C2 (9.45 -> 11.0 ms: more warps in flight only lengthen each gather), so off.
-  static const int split_env = getenv("BP_SPLIT_SELL") ? atoi(getenv("BP_SPLIT_SELL")) : 0;
+  // SELL slices in k_rows_sell at their own occupancy (24 warps / SM at 80 registers, vs 16 in
+  // k_rows_full), a programmatic dependent of k_rows_full. Round 1 measured it slower (9.45 -> 11.0
+  // ms, 64 registers with spills, next to the heavy chains); with lazy heavy rows and 3 blocks / SM
+  // it is 1-3% faster on C2 (tools/gpu_ab.sh: 6.98 -> 6.76, 6.93 -> 6.86 ms). BP_SPLIT_SELL=0: off.
+  static const int split_env = getenv("BP_SPLIT_SELL") ? atoi(getenv("BP_SPLIT_SELL")) : 1;
   const int split_sell       = split_env && P.n_srtile > 0 ? 1 : 0;
   // dirty-filtered rounds when the changed vars' columns hold at most BP_DF_MARK_PCT % of the nnz:
   // beyond that the marks and lists cost more than the rows they spare (C2, tools/gpu_ab.sh:
