@@ -20,6 +20,13 @@ if what in ("all", "prop"):
     q = synth.c2(n=120_000, m=120_000, cap=30_000, n_heavy=4)  # > 2M nnz: external row phase
     r = propagate(q, BoundsState(q))
     print("C2-120k propagate", r, q.nnz())
+    # lazy heavy rows: certified-quiet rounds, exact rounds, refresh before frontier rounds
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tests"))
+    from paper_2510_20499_b200 import PropagationLimits  # noqa: E402
+    from test_gpu_rounding import _tight_heavy_instance  # noqa: E402
+    t, _ = _tight_heavy_instance()
+    for inc in (True, False):
+        print("tight-heavy propagate", propagate(t, BoundsState(t), PropagationLimits(incremental=inc)))
 if what in ("all", "probe"):
     p0, _ = synth.c4(n=6000, m=6000, n_long=4, long_len=2500)
     b = BoundsState(p0)
