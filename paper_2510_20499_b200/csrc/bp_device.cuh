@@ -317,6 +317,7 @@ struct DevProblem {
   // has 32 rows srow[32 s + i] (-1 padding) and entries sr_ci / sr_val[sr_tile[s] + 32 j + i].
   int n_srow, n_srtile, n_srow_long;  // n_srow_long: leading slices with rows > kShortNnz
   const int* srow;          // slice lane -> row id
+  const int* sell_pos;      // row -> 32 * slice + lane for rows in SELL slices (-1 otherwise)
   const int* sr_ptr;        // unused
   const int* sr_ci;         // column | integrality << 31, -1 = padding
   const double* sr_val;

@@ -78,8 +78,10 @@ struct Ctl {
   // otherwise only rows with row_stamp == df_stamp (rows of the vars changed last round) are
   // recomputed and publish candidates, the candidate slots of unchanged vars persisting.
   unsigned df_stamp;
-  int df_cnt[3];  // dirty lists of a dirty-filtered round: slices, medium-row groups, heavy pieces
+  int df_cnt[4];  // dirty lists of a dirty-filtered round: slices, medium-row groups, heavy pieces,
+                  // and the dirty rows of SELL slices
   int stale;      // some heavy row's activity record is stale (certified quiet, chain skipped)
+  int pad1;
   unsigned long long t0;      // globaltimer at the start of the propagate (time limit, stats)
   int pad[2];
 };
@@ -114,6 +116,9 @@ struct DevState {
   int* df_slice;          // dirty lists (phase_df_lists)
   int* df_group;
   int* df_piece;
+  int* df_rows;           // dirty rows of SELL slices (appended by the marking, deduplicated by sell_stamp)
+  unsigned* sell_stamp;   // per row: stamp of the marking that listed it (its own array: the frontier
+                          // expansion stamps row_stamp with the same round stamp)
   SegPart* seg_part;
   int* seg_done;
   unsigned* row_stamp;
@@ -155,6 +160,9 @@ struct Problem {
   DBuf<int> col_mark;
   DBuf<unsigned> task_stamp;
   DBuf<int> df_lists;
+  DBuf<int> df_rows;
+  DBuf<unsigned> sell_stamp;
+  DBuf<int> sell_pos;
   DBuf<unsigned char> row_flag;
   int n_task = 0;
   DBuf<int2> piece_task, fold_task, cpiece_task;

@@ -1006,22 +1006,16 @@ __device__ void long_cand_piece(Ctx& c, int k, int p, unsigned stamp, unsigned d
 #define BP_SELL_UNROLL 4
 #endif
 constexpr int kSellUnroll = BP_SELL_UNROLL;  // entries per lane in flight
-__device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
+// The thread-per-row SELL evaluation of row k (-1: idle lane) whose entries are at ciq / aq + 32 j
+// for j < Lm (padding entries are -1), the loop running Lw >= Lm steps (warp-uniform).
+__device__ __forceinline__ void sell_core(Ctx& c, int k, const int* ciq, const double* aq, int Lm, int Lw, bool cand)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
-  // dirty-filtered round: the slice is dirty; its clean rows (byte flag != the round's mark; a stale
-  // byte matching by wrap-around only recomputes a clean row, which is exact) are idle lanes
-  int k = __ldg(P.srow + 32 * sl + c.lane);
-  if (ds != 0 && k >= 0 && __ldcg(S.row_flag + k) != (unsigned char)ds) k = -1;
-  const int b0 = __ldg(P.sr_tile + sl), b1 = __ldg(P.sr_tile + sl + 1);
-  const int Lm = (b1 - b0) >> 5;
-  const int* ciq   = P.sr_ci + b0 + c.lane;
-  const double* aq = P.sr_val + b0 + c.lane;
   double smn = 0.0, smx = 0.0, gtw = 0.0, gpm = 0.0;
   int imn = 0, imx = 0;
   constexpr int U = kSellUnroll;
-  for (int j = 0; j < Lm; j += U) {
+  for (int j = 0; j < Lw; j += U) {
     int ci[U];
     double a[U];
     double2 bd[U];
@@ -1071,7 +1065,7 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
     }
   }
   if (__all_sync(FULL, quiet)) return;
-  for (int j = 0; j < Lm; j += U) {
+  for (int j = 0; j < Lw; j += U) {
     int ci[U];
     double a[U];
     double2 bd[U];
@@ -1093,6 +1087,41 @@ __device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
       emit_cand(S.slot, ci[u], a[u], bd[u].x, bd[u].y, smn, imn, smx, imx, cb.y, cb.x, k);
     }
   }
+}
+
+__device__ void sell_slice(Ctx& c, int sl, bool cand, unsigned ds = 0)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  // dirty-filtered round: the slice is dirty; its clean rows (byte flag != the round's mark; a stale
+  // byte matching by wrap-around only recomputes a clean row, which is exact) are idle lanes
+  int k = __ldg(P.srow + 32 * sl + c.lane);
+  if (ds != 0 && k >= 0 && __ldcg(S.row_flag + k) != (unsigned char)ds) k = -1;
+  const int b0 = __ldg(P.sr_tile + sl), b1 = __ldg(P.sr_tile + sl + 1);
+  const int Lm = (b1 - b0) >> 5;
+  sell_core(c, k, P.sr_ci + b0 + c.lane, P.sr_val + b0 + c.lane, Lm, Lm, cand);
+}
+
+// Dirty-filtered round with few dirty short rows: 32 listed rows per warp, each lane reading its
+// row where it lies in its SELL slice (sell_pos) -- no idle lanes, at the price of uncoalesced
+// index / value loads.
+__device__ void sell_rows(Ctx& c, int base, int n, bool cand)
+{
+  const DevProblem& P = c.P;
+  const DevState& S   = c.S;
+  const int i = base + c.lane;
+  int k = -1, b = 0, Lm = 0;
+  if (i < n) {
+    k             = __ldcg(S.df_rows + i);
+    const int pos = __ldg(P.sell_pos + k);
+    const int b0 = __ldg(P.sr_tile + (pos >> 5)), b1 = __ldg(P.sr_tile + (pos >> 5) + 1);
+    Lm            = (b1 - b0) >> 5;
+    b             = b0 + (pos & 31);
+  }
+  int Lw = Lm;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) Lw = max(Lw, __shfl_xor_sync(FULL, Lw, o));
+  sell_core(c, k, P.sr_ci + b, P.sr_val + b, Lm, Lw, cand);
 }
 
 // Listed short rows (frontier rounds): flattened 128-entry windows, each lane folds its row.
@@ -1152,6 +1181,11 @@ __device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
   if (k >= 0) write_rec(P, c.S, k, smn, smx, imn, imx);
 }
 
+#ifndef BP_SELL_ROWS_PER_SLICE
+#define BP_SELL_ROWS_PER_SLICE 16
+#endif
+constexpr int kSellRowsPerSlice = BP_SELL_ROWS_PER_SLICE;  // listed rows below this many per dirty slice
+
 // SELL slices of a full round, longest first: slices of rows > 32 entries one per fetch, the rest
 // four per fetch (one cursor shared by the whole grid is the contended resource).
 __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
@@ -1159,8 +1193,14 @@ __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   const int ns = P.n_srtile, nsl = P.n_srow_long;
-  if (ds != 0) {  // dirty-filtered round: the engine's list of dirty slices, 4 per fetch
-    const int nd = ldv(&S.ctl->df_cnt[0]);
+  if (ds != 0) {  // dirty-filtered round
+    const int nr = ldv(&S.ctl->df_cnt[3]), nd = ldv(&S.ctl->df_cnt[0]);
+    if (nr <= kSellRowsPerSlice * nd) {  // few dirty rows per dirty slice: the listed rows, 32 per warp
+      const int nt = (nr + 31) / 32;
+      for (Prefetch it_t(c, &pc->cur_a, 1, nt, true); it_t.t < nt; it_t.advance()) sell_rows(c, 32 * it_t.t, nr, cand);
+      return;
+    }
+    // else the engine's list of dirty slices, 4 per fetch (clean lanes idle)
     for (Prefetch it_t(c, &pc->cur_a, 4, nd, true); it_t.t < nd; it_t.advance())
       for (int q = it_t.t; q < min(nd, it_t.t + 4); ++q) sell_slice(c, __ldcg(S.df_slice + q), cand, ds);
     return;
@@ -1797,7 +1837,9 @@ __device__ __forceinline__ void mark_entry(const DevState& S, int mk, int row, u
   }
 }
 
-// Marks the entries [e0, e1) (at most kTile) of a column, 32 lanes x kEPL loads in flight.
+// Marks the entries [e0, e1) (at most kTile) of a column, 32 lanes x kEPL loads in flight; rows of
+// SELL slices are also appended, once per round (sell_stamp), to the dirty-row list (one atomic per
+// warp and step).
 __device__ __forceinline__ void mark_window(const DevProblem& P, const DevState& S, int e0, int e1,
                                             int lane, unsigned stamp)
 {
@@ -1809,8 +1851,17 @@ __device__ __forceinline__ void mark_window(const DevProblem& P, const DevState&
     rw[h]       = e < e1 ? __ldg(P.col_row + e) : -1;
   }
 #pragma unroll
-  for (int h = 0; h < kEPL; ++h)
+  for (int h = 0; h < kEPL; ++h) {
     if (rw[h] >= 0) mark_entry(S, mk[h], rw[h], stamp);
+    const bool fresh = rw[h] >= 0 && mk[h] >= 0 && mk[h] < P.n_srtile && atomicExch(S.sell_stamp + rw[h], stamp) != stamp;
+    const unsigned b = __ballot_sync(FULL, fresh);
+    if (b) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&S.ctl->df_cnt[3], __popc(b));
+      base = __shfl_sync(FULL, base, 0);
+      if (fresh) S.df_rows[base + __popc(b & lanemask_lt())] = rw[h];
+    }
+  }
 }
 
 // Dirty marks for a dirty-filtered full round: every row task (SELL slice, group of four medium rows,
@@ -2125,6 +2176,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     if (st && lead) st[6] = (long long)(globaltimer() - t0);
     if (lead) {
       zero_par(qc);  // safe: every block has finished reading the previous round's counters
+      S.ctl->df_cnt[3] = 0;  // the dirty-row list of the marks below (this round's rows ran)
       if (timed && (double)(globaltimer() - t0) * 1e-9 >= lim.time_limit) pc->stop = 1;
     }
     if (fr) phase_finalize(c, pc);
@@ -2246,6 +2298,7 @@ DevProblem Problem::dev() const
   d.n_srtile    = n_srtile;
   d.n_srow_long = n_srow_long;
   d.srow        = srow.p;
+  d.sell_pos    = sell_pos.p;
   d.sr_ptr      = sr_ptr.p;
   d.sr_ci       = sr_ci.p;
   d.sr_val      = sr_val.p;
@@ -2413,6 +2466,10 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
     while (P.n_srow_long < nsl && sbase[P.n_srow_long + 1] - sbase[P.n_srow_long] > 32 * kShortNnz)
       ++P.n_srow_long;
     P.srow.upload(srow);
+    std::vector<int> spos(std::max(m, 1), -1);
+    for (size_t q = 0; q < srow.size(); ++q)
+      if (srow[q] >= 0) spos[srow[q]] = (int)q;
+    P.sell_pos.upload(spos);
     srow_h = srow;
     P.sr_ci.upload(sci);
     P.sr_val.upload(sval);
@@ -2623,6 +2680,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.df_slice = P.df_lists.p;
   S.df_group = P.df_lists.p + P.n_srtile;
   S.df_piece = P.df_lists.p + P.n_task;
+  P.df_rows.alloc((size_t)std::max(m, 1));
+  S.df_rows = P.df_rows.p;
+  P.sell_stamp.alloc((size_t)std::max(m, 1));
+  BP_CUDA(cudaMemset(P.sell_stamp.p, 0, sizeof(unsigned) * P.sell_stamp.n));
+  S.sell_stamp = P.sell_stamp.p;
   S.ckpt      = P.ckpt.p;
   S.seg_part  = P.seg_part.p;
   S.seg_done  = P.seg_done.p;
@@ -2696,6 +2758,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   // stamps: one value per round, never reused until wrap-around (then the stamp arrays reset)
   if (P.stamp_base > 0xF0000000u - (unsigned)std::max(lim.max_rounds, 1) - 2) {
     BP_CUDA(cudaMemsetAsync(P.row_stamp.p, 0, sizeof(unsigned) * P.row_stamp.n, s));
+    BP_CUDA(cudaMemsetAsync(P.sell_stamp.p, 0, sizeof(unsigned) * P.sell_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.var_stamp.p, 0, sizeof(unsigned) * P.var_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.ready.p, 0, sizeof(unsigned) * P.ready.n, s));
     BP_CUDA(cudaMemsetAsync(P.pstamp.p, 0, sizeof(unsigned) * P.pstamp.n, s));
