@@ -81,7 +81,7 @@ struct Ctl {
   int df_cnt[4];  // dirty lists of a dirty-filtered round: slices, medium-row groups, heavy pieces,
                   // and the dirty rows of SELL slices
   int stale;      // some heavy row's activity record is stale (certified quiet, chain skipped)
-  int pad1;
+  int n_touch;    // variables whose slot a dirty-filtered round's rows published into (touched)
   unsigned long long t0;      // globaltimer at the start of the propagate (time limit, stats)
   int pad[2];
 };
@@ -119,6 +119,8 @@ struct DevState {
   int* df_rows;           // dirty rows of SELL slices (appended by the marking, deduplicated by sell_stamp)
   unsigned* sell_stamp;   // per row: stamp of the marking that listed it (its own array: the frontier
                           // expansion stamps row_stamp with the same round stamp)
+  unsigned* vtouch;       // per var: dirty-filtered round stamp of its first publish (touched list)
+  int* touched;           // the touched variables of the running dirty-filtered round
   SegPart* seg_part;
   int* seg_done;
   unsigned* row_stamp;
@@ -162,6 +164,8 @@ struct Problem {
   DBuf<int> df_lists;
   DBuf<int> df_rows;
   DBuf<unsigned> sell_stamp;
+  DBuf<unsigned> vtouch;
+  DBuf<int> touched;
   DBuf<int> sell_pos;
   DBuf<unsigned char> row_flag;
   int n_task = 0;

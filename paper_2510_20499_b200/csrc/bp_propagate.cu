@@ -122,6 +122,7 @@ struct Ctx {
   Smem& sm;
   WarpSmem& w;
   int lane, warp;
+  unsigned touch = 0;  // dirty-filtered round stamp: publishes list their variables (finalize)
 };
 
 // Debug counters (BP_DEBUG=1): per task kind total / max cycles and count.
@@ -248,7 +249,7 @@ __device__ __forceinline__ void publish_zero(unsigned* z, int k, bool neg)
 
 // Publishes the candidates of one (row k, variable) entry that strictly improve the round-start
 // bounds (lo, up) into the variable's slot.
-__device__ __forceinline__ void publish(CandSlot* s, double cl, double cu, double lo, double up,
+__device__ __forceinline__ bool publish(CandSlot* s, double cl, double cu, double lo, double up,
                                        int k)
 {
   if (cu < up) {
@@ -259,6 +260,7 @@ __device__ __forceinline__ void publish(CandSlot* s, double cl, double cu, doubl
     atomicMax(&s->lo_key, okey(cl == 0.0 ? 0.0 : cl));
     if (cl == 0.0) publish_zero(&s->lo_zero, k, signbit(cl));
   }
+  return cu < up || lo < cl;
 }
 
 #ifndef BP_EMIT_NOINLINE
@@ -272,12 +274,16 @@ __device__ __noinline__
 #else
 __device__ __forceinline__
 #endif
-void emit_cand(CandSlot* slot, int ci, double a, double lo, double up, double mnf, int nmn,
-               double mxf, int nmx, double g, double h, int k)
+void emit_cand(const DevState& S, unsigned touch, int ci, double a, double lo, double up, double mnf,
+               int nmn, double mxf, int nmx, double g, double h, int k)
 {
   double cl, cu;
   cand_explicit(lo, up, ci < 0, a, mnf, nmn, mxf, nmx, g, h, cl, cu);
-  publish(slot + (ci & ~kIntBit), cl, cu, lo, up, k);
+  const int v = ci & ~kIntBit;
+  // a dirty-filtered round lists the variables it publishes to: only their slots can have changed,
+  // so its finalize visits them alone (the others' slots and bounds are those of the last finalize)
+  if (publish(S.slot + v, cl, cu, lo, up, k) && touch && atomicExch(S.vtouch + v, touch) != touch)
+    S.touched[atomicAdd(&S.ctl->n_touch, 1)] = v;
 }
 
 // Dirty filter of a full round's row tasks: ds = 0 (true full round) or the stamp the previous
@@ -329,7 +335,7 @@ __device__ void long_candidates(Ctx& c, int k, int e0, int e1, double mnf, int n
       double tw, pm;
       entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pm);
       if (entry_quiet(tw, pm, mnf, nmn, mxf, nmx, g, hh)) continue;
-      emit_cand(S.slot, ci[h], a[h], bd[h].x, bd[h].y, mnf, nmn, mxf, nmx, g, hh, k);
+      emit_cand(S, c.touch, ci[h], a[h], bd[h].x, bd[h].y, mnf, nmn, mxf, nmx, g, hh, k);
     }
   }
 }
@@ -968,7 +974,7 @@ __device__ void group_fold(Ctx& c, int t0, int nt, bool cand, unsigned ds = 0)
       double tw, pw;
       entry_reach(a[h], bd[h].x, bd[h].y, ci[h] < 0, tw, pw);
       if (entry_quiet(tw, pw, smn, imn, smx, imx, cb.y, cb.x)) continue;
-      emit_cand(S.slot, ci[h], a[h], bd[h].x, bd[h].y, smn, imn, smx, imx, cb.y, cb.x, k);
+      emit_cand(S, c.touch, ci[h], a[h], bd[h].x, bd[h].y, smn, imn, smx, imx, cb.y, cb.x, k);
     }
   }
 }
@@ -1084,7 +1090,7 @@ __device__ __forceinline__ void sell_core(Ctx& c, int k, const int* ciq, const d
       if (DBG_ON(S)) atomicAdd(S.dbg + 18, 1ull);
       if (entry_quiet(tw, pw, smn, imn, smx, imx, cb.y, cb.x)) continue;
       if (DBG_ON(S)) atomicAdd(S.dbg + 19, 1ull);
-      emit_cand(S.slot, ci[u], a[u], bd[u].x, bd[u].y, smn, imn, smx, imx, cb.y, cb.x, k);
+      emit_cand(S, c.touch, ci[u], a[u], bd[u].x, bd[u].y, smn, imn, smx, imx, cb.y, cb.x, k);
     }
   }
 }
@@ -1389,15 +1395,17 @@ __device__ void tally_flush_block(Ctx& c, ParCtl* pc, Tally& t)
 }
 
 // F4: per variable, the fold result from its candidate slot, then the reference's rules.
-__device__ void phase_finalize(Ctx& c, ParCtl* pc)
+__device__ void phase_finalize(Ctx& c, ParCtl* pc, const int* list = nullptr, int nlist = 0)
 {
   const DevProblem& P = c.P;
   const DevState& S   = c.S;
   Tally t{0, 0, 0ull, 0ull, 0ull, 0};
-  // uniform per-variable work: a static grid-stride sweep (no shared work cursor)
+  // uniform per-variable work: a static grid-stride sweep (no shared work cursor) over every
+  // variable, or over the listed (touched) ones of a dirty-filtered round
   const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
-  for (int q = 32 * gw; q < P.n; q += 32 * nw) {
-    const int i = q + c.lane;
+  const int N  = list ? nlist : P.n;
+  for (int q = 32 * gw; q < N; q += 32 * nw) {
+    const int i = list ? (q + c.lane < nlist ? __ldcg(list + q + c.lane) : P.n) : q + c.lane;
     int res     = 0;
     if (i < P.n) {
       CandSlot* s                 = S.slot + i;
@@ -1826,15 +1834,17 @@ __device__ void phase_expand_vars(Ctx& c, ParCtl* pc, ParCtl* qc, int qpar, unsi
 // Dirty marks for a dirty-filtered full round: row_stamp[k] = stamp for every row of a variable
 // that changed this round (the reference's dirty_rows, propagation.hpp:474-476). Changed vars with
 // short columns go 32 per warp (flattened 128-entry windows); longer columns by their chunk tasks.
-__device__ __forceinline__ void mark_entry(const DevState& S, int mk, int row, unsigned stamp)
+// Appends id to dirty list q (0 slices, 1 groups, 2 pieces, 3 rows of SELL slices) for the lanes
+// with `fresh`: one atomic per warp.
+__device__ __forceinline__ void df_append(const DevState& S, int q, bool fresh, int id, int lane)
 {
-  if (mk >= 0) {
-    S.task_stamp[mk] = stamp;  // SELL slice / medium-row group, and the row inside it
-    S.row_flag[row]  = (unsigned char)stamp;
-  } else {                     // heavy row: its piece, and the row for its segment folds
-    S.piece_dirty[-mk - 2] = stamp;
-    S.row_stamp[row]       = stamp;
-  }
+  const unsigned b = __ballot_sync(FULL, fresh);
+  if (!b) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(&S.ctl->df_cnt[q], __popc(b));
+  base = __shfl_sync(FULL, base, 0);
+  int* list = q == 0 ? S.df_slice : q == 1 ? S.df_group : q == 2 ? S.df_piece : S.df_rows;
+  if (fresh) list[base + __popc(b & lanemask_lt())] = id;
 }
 
 // Marks the entries [e0, e1) (at most kTile) of a column, 32 lanes x kEPL loads in flight; rows of
@@ -1852,15 +1862,20 @@ __device__ __forceinline__ void mark_window(const DevProblem& P, const DevState&
   }
 #pragma unroll
   for (int h = 0; h < kEPL; ++h) {
-    if (rw[h] >= 0) mark_entry(S, mk[h], rw[h], stamp);
-    const bool fresh = rw[h] >= 0 && mk[h] >= 0 && mk[h] < P.n_srtile && atomicExch(S.sell_stamp + rw[h], stamp) != stamp;
-    const unsigned b = __ballot_sync(FULL, fresh);
-    if (b) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&S.ctl->df_cnt[3], __popc(b));
-      base = __shfl_sync(FULL, base, 0);
-      if (fresh) S.df_rows[base + __popc(b & lanemask_lt())] = rw[h];
+    const bool on = rw[h] >= 0, light = on && mk[h] >= 0, sell = light && mk[h] < P.n_srtile;
+    // the task (SELL slice / medium-row group / heavy-row piece) and the row: listed once per round
+    bool task_new = false;
+    if (light) {
+      task_new = atomicExch(S.task_stamp + mk[h], stamp) != stamp;
+      S.row_flag[rw[h]] = (unsigned char)stamp;
+    } else if (on) {
+      task_new = atomicExch(S.piece_dirty + (-mk[h] - 2), stamp) != stamp;
+      S.row_stamp[rw[h]] = stamp;  // heavy row: its segment folds run (row_live)
     }
+    df_append(S, 0, task_new && sell, mk[h], lane);
+    df_append(S, 1, task_new && light && !sell, mk[h] - P.n_srtile, lane);
+    df_append(S, 2, task_new && !light, -mk[h] - 2, lane);
+    df_append(S, 3, sell && atomicExch(S.sell_stamp + rw[h], stamp) != stamp, rw[h], lane);
   }
 }
 
@@ -1886,51 +1901,6 @@ __device__ void phase_mark_rows(Ctx& c, ParCtl* pc, unsigned stamp)
     const int ce  = __ldg(P.col_start + tk.x + 1);
     const int e0  = __ldg(P.col_start + tk.x) + tk.y * kTile;
     mark_window(P, S, e0, min(ce, e0 + kTile), c.lane, stamp);
-  }
-}
-
-// Compacts the task stamps of this round's marks into the dirty lists the next (dirty-filtered)
-// round's row phase fetches from: SELL slices, medium-row groups, heavy-row pieces.
-__device__ void phase_df_lists(Ctx& c, unsigned stamp)
-{
-  const DevProblem& P = c.P;
-  const DevState& S   = c.S;
-  const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
-  const int n_all = S.n_task + P.n_piece;
-  // contiguous spans of >= 8 x 32 tasks per warp: one list append (atomic) per warp and kind
-  const int span = max(256, ((n_all + nw - 1) / nw + 31) / 32 * 32);
-  const int t_lo = gw * span, t_hi = min(n_all, t_lo + span);
-  if (t_lo >= t_hi) return;
-  int cnt[3] = {0, 0, 0};
-  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {  // pass 1: counts
-    const int t = t0 + c.lane;
-    const unsigned* st = t < S.n_task ? S.task_stamp + t : S.piece_dirty + (t - S.n_task);
-    const bool d       = t < t_hi && __ldcg(st) == stamp;
-    const int kind     = t < P.n_srtile ? 0 : t < S.n_task ? 1 : 2;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) cnt[q] += __popc(__ballot_sync(FULL, d && kind == q));
-  }
-  int base[3];
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    base[q] = 0;
-    if (c.lane == 0 && cnt[q]) base[q] = atomicAdd(&S.ctl->df_cnt[q], cnt[q]);
-    base[q] = __shfl_sync(FULL, base[q], 0);
-  }
-  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {  // pass 2: ids (the stamps are L2 hits now)
-    const int t = t0 + c.lane;
-    const unsigned* st = t < S.n_task ? S.task_stamp + t : S.piece_dirty + (t - S.n_task);
-    const bool d       = t < t_hi && __ldcg(st) == stamp;
-    const int kind     = t < P.n_srtile ? 0 : t < S.n_task ? 1 : 2;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const unsigned m = __ballot_sync(FULL, d && kind == q);
-      if (d && kind == q) {
-        const int id = q == 0 ? t : q == 1 ? t - P.n_srtile : t - S.n_task;
-        (q == 0 ? S.df_slice : q == 1 ? S.df_group : S.df_piece)[base[q] + __popc(m & lanemask_lt())] = id;
-      }
-      base[q] += __popc(m);
-    }
   }
 }
 
@@ -2001,7 +1971,8 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
   WarpSmem& w = sm.w[warp];
 #endif
   Ctx c{P, S, lim, sm, w, (int)(threadIdx.x & 31), warp};
-  phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell, ldv(&S.ctl->df_stamp));
+  c.touch = ldv(&S.ctl->df_stamp);
+  phase_rows(c, &S.ctl->par[par], par, true, true, stamp, false, !split_sell, c.touch);
 }
 
 // The SELL slices of a full round (short rows, thread per row) at this kernel's own occupancy:
@@ -2021,7 +1992,8 @@ __global__ void __launch_bounds__(kThreads, BP_SELL_MIN_BLOCKS)
     Smem& sm       = *reinterpret_cast<Smem*>(no_smem);
     const int warp = threadIdx.x >> 5;
     Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp};
-    phase_sell(c, &S.ctl->par[par], true, ldv(&S.ctl->df_stamp));
+    c.touch = ldv(&S.ctl->df_stamp);
+    phase_sell(c, &S.ctl->par[par], true, c.touch);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -2036,6 +2008,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cand_pieces(DevProblem P, DevSt
   Smem& sm       = *reinterpret_cast<Smem*>(dyn_smem);
   const int warp = threadIdx.x >> 5;
   Ctx c{P, S, lim, sm, sm.w[warp], (int)(threadIdx.x & 31), warp};
+  c.touch = ds;
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   for (int t = gw; t < P.n_cpiece; t += nw) {
     const int2 tk = P.cpiece_task[t];
@@ -2146,6 +2119,8 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
       }
     }
     df_next = 0;
+    // the dirty-filter stamp of this round's row phase (handed to k_rows_full before a resume)
+    const unsigned rds = resumed ? ldv(&S.ctl->df_stamp) : ds;
     if (!fr) {  // a frontier round reads records it does not recompute: no stale heavy row
       const bool rf = ldv(&S.ctl->stale) != 0;
       if (rf) {
@@ -2170,18 +2145,23 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
       return;
     } else {
       if (st && lead) st[10] = (long long)(globaltimer() - t0);
+      c.touch = fr ? ds : 0u;
       phase_rows(c, pc, ppar, fr, fr, stamp, true, true, ds);
+      c.touch = 0;
       grid.sync();
     }
     if (st && lead) st[6] = (long long)(globaltimer() - t0);
     if (lead) {
       zero_par(qc);  // safe: every block has finished reading the previous round's counters
-      S.ctl->df_cnt[3] = 0;  // the dirty-row list of the marks below (this round's rows ran)
+      // the dirty lists the marks below append to (this round's row phase has consumed them)
+      S.ctl->df_cnt[0] = S.ctl->df_cnt[1] = S.ctl->df_cnt[2] = S.ctl->df_cnt[3] = 0;
       if (timed && (double)(globaltimer() - t0) * 1e-9 >= lim.time_limit) pc->stop = 1;
     }
-    if (fr) phase_finalize(c, pc);
+    if (fr && rds != 0) phase_finalize(c, pc, S.touched, ldv(&S.ctl->n_touch));
+    else if (fr) phase_finalize(c, pc);
     else phase_tighten(c, pc, ppar, false);
     grid.sync();
+    if (lead) S.ctl->n_touch = 0;  // (read by every block before the barrier above)
     slot_state   = fr ? 1 : (slot_state == 0 ? 0 : 2);  // a frontier round leaves the slots stale
     const int cr = ldv(&pc->n_crossed);
     const int nc = ldv(&pc->n_changed);
@@ -2218,14 +2198,10 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     // (complete even when a frontier expansion below stopped early) and filter by them
     auto go_full = [&]() {
       if (slot_state == 1 && ldv(&pc->colnnz) <= mark_max) {
-        if (lead) S.ctl->df_cnt[0] = S.ctl->df_cnt[1] = S.ctl->df_cnt[2] = 0;
-        phase_mark_rows(c, pc, stamp);
-        grid.sync();  // marks (and the zeroed counts) visible grid-wide
-        if (st && lead) st[8] = (long long)(globaltimer() - t0);  // (expansion columns: unused here)
-        phase_df_lists(c, stamp);
+        phase_mark_rows(c, pc, stamp);  // marks + dirty lists (appended)
+        grid.sync();                    // complete before the row phase reads them
+        if (st && lead) st[8] = st[9] = st[11] = (long long)(globaltimer() - t0);
         df_next = stamp;
-        if (!ext_f2 || st) grid.sync();  // in-engine row phase: lists complete first
-        if (st && lead) st[9] = st[11] = (long long)(globaltimer() - t0);
       }
       full = true;
     };
@@ -2682,6 +2658,11 @@ void problem_build(Problem& P, int n, int m, const int* row_start, const int* ro
   S.df_piece = P.df_lists.p + P.n_task;
   P.df_rows.alloc((size_t)std::max(m, 1));
   S.df_rows = P.df_rows.p;
+  P.vtouch.alloc((size_t)std::max(n, 1));
+  BP_CUDA(cudaMemset(P.vtouch.p, 0, sizeof(unsigned) * P.vtouch.n));
+  S.vtouch = P.vtouch.p;
+  P.touched.alloc((size_t)std::max(n, 1));
+  S.touched = P.touched.p;
   P.sell_stamp.alloc((size_t)std::max(m, 1));
   BP_CUDA(cudaMemset(P.sell_stamp.p, 0, sizeof(unsigned) * P.sell_stamp.n));
   S.sell_stamp = P.sell_stamp.p;
@@ -2759,6 +2740,7 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   if (P.stamp_base > 0xF0000000u - (unsigned)std::max(lim.max_rounds, 1) - 2) {
     BP_CUDA(cudaMemsetAsync(P.row_stamp.p, 0, sizeof(unsigned) * P.row_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.sell_stamp.p, 0, sizeof(unsigned) * P.sell_stamp.n, s));
+    BP_CUDA(cudaMemsetAsync(P.vtouch.p, 0, sizeof(unsigned) * P.vtouch.n, s));
     BP_CUDA(cudaMemsetAsync(P.var_stamp.p, 0, sizeof(unsigned) * P.var_stamp.n, s));
     BP_CUDA(cudaMemsetAsync(P.ready.p, 0, sizeof(unsigned) * P.ready.n, s));
     BP_CUDA(cudaMemsetAsync(P.pstamp.p, 0, sizeof(unsigned) * P.pstamp.n, s));
