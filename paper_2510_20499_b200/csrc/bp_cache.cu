@@ -201,43 +201,48 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
   std::vector<int>& tslot = W.tslot;
   std::vector<double>& tlo = W.tlo;
   std::vector<double>& tup = W.tup;
-  tv.clear();
-  tslot.clear();
-  tlo.clear();
-  tup.clear();
-  tv.reserve(2 * vars.size());
-  tslot.reserve(2 * vars.size());
-  tlo.reserve(2 * vars.size());
-  tup.reserve(2 * vars.size());
-  C.e_var.reserve(vars.size());
-  C.e_kind.reserve(vars.size());
-  C.e_feas.reserve(2 * vars.size());
-  C.e_force.reserve(2 * vars.size());
-  C.e_branch.reserve(4 * vars.size());
+  // (sized up front and filled by index: this loop runs over every candidate on the host)
+  const size_t nv = vars.size();
+  tv.resize(2 * nv);
+  tslot.resize(2 * nv);
+  tlo.resize(2 * nv);
+  tup.resize(2 * nv);
+  C.e_var.resize(nv);
+  C.e_kind.assign(nv, 0);
+  C.e_feas.assign(2 * nv, 1);
+  C.e_force.assign(2 * nv, 0);
+  C.e_branch.assign(4 * nv, 0.0);
+  int ne_ = 0;
+  size_t nt = 0;
   for (int v : vars) {
     if (v < 0 || v >= n) throw std::out_of_range("probe var out of range");
     int e = C.entry_of[v];
     if (e < 0) {
-      e            = (int)C.e_var.size();
+      e             = ne_++;
       C.entry_of[v] = e;
-      C.e_var.push_back(v);
-      C.e_kind.push_back(0);
-      C.e_feas.insert(C.e_feas.end(), {1, 1});
-      C.e_force.insert(C.e_force.end(), {0, 0});
-      C.e_branch.insert(C.e_branch.end(), {0.0, 0.0, 0.0, 0.0});
+      C.e_var[e]    = v;
     }
     double sp[4];
     const int kind = branch_spec(root[2 * v], root[2 * v + 1], sp);
     if (!kind) continue;  // default entry: no spec (probing.hpp:231)
     C.e_kind[e] = kind - 1;
     for (int q = 0; q < 4; ++q) C.e_branch[4 * e + q] = sp[q];
-    for (int side = 0; side < 2; ++side) {
-      tv.push_back(v);
-      tlo.push_back(sp[2 * side]);
-      tup.push_back(sp[2 * side + 1]);
-      tslot.push_back(2 * e + side);
+    for (int side = 0; side < 2; ++side, ++nt) {
+      tv[nt]    = v;
+      tlo[nt]   = sp[2 * side];
+      tup[nt]   = sp[2 * side + 1];
+      tslot[nt] = 2 * e + side;
     }
   }
+  tv.resize(nt);
+  tslot.resize(nt);
+  tlo.resize(nt);
+  tup.resize(nt);
+  C.e_var.resize(ne_);
+  C.e_kind.resize(ne_);
+  C.e_feas.resize(2 * (size_t)ne_);
+  C.e_force.resize(2 * (size_t)ne_);
+  C.e_branch.resize(4 * (size_t)ne_);
   static const bool prof = getenv("BP_PROBE_PROFILE") != nullptr;
   const double t_tasks = elapsed();
   const int ne = (int)C.e_var.size();

@@ -1986,16 +1986,27 @@ __global__ void __launch_bounds__(kThreads, BP_F2_MIN_BLOCKS)
 __global__ void __launch_bounds__(kThreads, BP_SELL_MIN_BLOCKS)
     k_rows_sell(DevProblem P, DevState S, Limits lim)
 {
-  if (ldv(&S.ctl->need_full)) {
+  const bool on = ldv(&S.ctl->need_full) != 0;
+  __shared__ __align__(16) unsigned char no_smem[16];  // sell_slice never touches the warp smem
+  Smem& sm       = *reinterpret_cast<Smem*>(no_smem);
+  const int warp = threadIdx.x >> 5;
+  Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp};
+  if (on) {
     const int par = ldv(&S.ctl->rounds) & 1;
-    __shared__ __align__(16) unsigned char no_smem[16];  // sell_slice never touches the warp smem
-    Smem& sm       = *reinterpret_cast<Smem*>(no_smem);
-    const int warp = threadIdx.x >> 5;
-    Ctx c{P, S, lim, sm, sm.w[0], (int)(threadIdx.x & 31), warp};
-    c.touch = ldv(&S.ctl->df_stamp);
+    c.touch       = ldv(&S.ctl->df_stamp);
     phase_sell(c, &S.ctl->par[par], true, c.touch);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // k_rows_full is complete: the candidate pieces of rows above kCandSplit (their activities are
+  // published), here instead of in a launch of their own
+  if (on) {
+    const unsigned stamp = ldv(&S.ctl->stamp_base) + (unsigned)ldv(&S.ctl->rounds);
+    const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+    for (int t = gw; t < P.n_cpiece; t += nw) {
+      const int2 tk = P.cpiece_task[t];
+      long_cand_piece(c, tk.x, tk.y, stamp, c.touch);
+    }
+  }
 }
 
 // Candidate pieces of rows above kCandSplit, after k_rows_full published their activities.
@@ -2800,12 +2811,12 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
         BP_CUDA(cudaLaunchKernelEx(&cfg, k_rows_sell, d, st, l));
         ++g_kernel_launches;
       }
-      if (P.n_cpiece)
+      if (P.n_cpiece && !split_sell)  // (with split SELL they run at the end of k_rows_sell)
         k_cand_pieces<<<std::min(P.f2_blocks, (P.n_cpiece + kWarps - 1) / kWarps), kThreads,
                         sizeof(Smem), s>>>(d, st, l);
       BP_CUDA(cudaGetLastError());
       BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
-      g_kernel_launches += P.n_cpiece ? 3 : 2;
+      g_kernel_launches += P.n_cpiece && !split_sell ? 3 : 2;
     }
     int h = 0;
     BP_CUDA(cudaMemcpyAsync(&h, &P.st.ctl->need_full, sizeof(int), cudaMemcpyDeviceToHost, s));
