@@ -1192,6 +1192,23 @@ __device__ void short_list_tile(Ctx& c, const int* ids, int base, int n)
 #endif
 constexpr int kSellRowsPerSlice = BP_SELL_ROWS_PER_SLICE;  // listed rows below this many per dirty slice
 
+#ifndef BP_PIECE_STEP
+#define BP_PIECE_STEP 1
+#endif
+#ifndef BP_GROUP_STEP
+#define BP_GROUP_STEP 1
+#endif
+// heavy pieces / groups of four medium rows per cursor claim in full rounds (measured on C2: 4
+// pieces 5.67 -> 5.80 ms, 4 groups -> 6.95 ms: the medium rows balance only at one group a claim)
+constexpr int kPieceStep = BP_PIECE_STEP;
+constexpr int kGroupStep = BP_GROUP_STEP;
+// SELL slices (k_rows_sell) statically assigned: 6.31 -> 5.55 ms on C2 against one shared cursor
+// (every claim an atomic on one address, 7k claims per round)
+#ifndef BP_STATIC_SELL
+#define BP_STATIC_SELL 1
+#endif
+constexpr bool kStaticSell = BP_STATIC_SELL != 0;
+
 // SELL slices of a full round, longest first: slices of rows > 32 entries one per fetch, the rest
 // four per fetch (one cursor shared by the whole grid is the contended resource).
 __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
@@ -1201,14 +1218,20 @@ __device__ void phase_sell(Ctx& c, ParCtl* pc, bool cand, unsigned ds = 0)
   const int ns = P.n_srtile, nsl = P.n_srow_long;
   if (ds != 0) {  // dirty-filtered round
     const int nr = ldv(&S.ctl->df_cnt[3]), nd = ldv(&S.ctl->df_cnt[0]);
+    const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
     if (nr <= kSellRowsPerSlice * nd) {  // few dirty rows per dirty slice: the listed rows, 32 per warp
-      const int nt = (nr + 31) / 32;
-      for (Prefetch it_t(c, &pc->cur_a, 1, nt, true); it_t.t < nt; it_t.advance()) sell_rows(c, 32 * it_t.t, nr, cand);
+      for (int t = 32 * gw; t < nr; t += 32 * nw) sell_rows(c, t, nr, cand);
       return;
     }
-    // else the engine's list of dirty slices, 4 per fetch (clean lanes idle)
-    for (Prefetch it_t(c, &pc->cur_a, 4, nd, true); it_t.t < nd; it_t.advance())
-      for (int q = it_t.t; q < min(nd, it_t.t + 4); ++q) sell_slice(c, __ldcg(S.df_slice + q), cand, ds);
+    // else the engine's list of dirty slices (clean lanes idle)
+    for (int q = gw; q < nd; q += nw) sell_slice(c, __ldcg(S.df_slice + q), cand, ds);
+    return;
+  }
+  if (kStaticSell) {
+    // slices are independent (no task waits on another): a static grid-stride assignment, no
+    // shared cursor; the slices are sorted by length, so every warp gets one of each length class
+    const int gw = blockIdx.x * kWarps + c.warp, nw = gridDim.x * kWarps;
+    for (int q = gw; q < ns; q += nw) sell_slice(c, q, cand);
     return;
   }
   for (Prefetch it_t(c, &pc->cur_s, 1, nsl, true); it_t.t < nsl; it_t.advance()) {
@@ -1240,7 +1263,8 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     // heavy rows' contribution pieces first: the segment folds that wait for them are fetched
     // only after every piece has been fetched by a running warp (no deadlock)
     if (ds == 0) {
-      for (Prefetch it_t(c, &pc->cur_p, 1, P.n_piece); it_t.t < P.n_piece; it_t.advance()) heavy_piece(c, it_t.t, stamp);
+      for (Prefetch it_t(c, &pc->cur_p, kPieceStep, P.n_piece); it_t.t < P.n_piece; it_t.advance())
+        for (int q = it_t.t; q < min(P.n_piece, it_t.t + kPieceStep); ++q) heavy_piece(c, q, stamp);
     } else {  // dirty-filtered round: the engine's list of dirty pieces
       const int nd = ldv(&S.ctl->df_cnt[2]);
       for (Prefetch it_t(c, &pc->cur_p, 1, nd); it_t.t < nd; it_t.advance()) heavy_piece(c, __ldcg(S.df_piece + it_t.t), stamp);
@@ -1253,9 +1277,10 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       dbg_task(c, 0, c0);
     }
     if (ds == 0) {
-      for (Prefetch it_t(c, &pc->cur_g, 4, nf - nfh, true); nfh + it_t.t < nf; it_t.advance()) {
+      for (Prefetch it_t(c, &pc->cur_g, 4 * kGroupStep, nf - nfh, true); nfh + it_t.t < nf; it_t.advance()) {
         const long long c0 = DBG_ON(S) ? clock64() : 0;
-        group_fold(c, nfh + it_t.t, min(4, nf - nfh - it_t.t), cand);
+        for (int q = it_t.t; q < min(nf - nfh, it_t.t + 4 * kGroupStep); q += 4)
+          group_fold(c, nfh + q, min(4, nf - nfh - q), cand);
         dbg_task(c, 4, c0);
       }
     } else {  // dirty-filtered round: the engine's list of dirty groups of four medium rows
