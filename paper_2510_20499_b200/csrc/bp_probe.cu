@@ -31,6 +31,9 @@ constexpr unsigned FULL  = 0xffffffffu;
 #define PB_WARPS_V 4
 #endif
 constexpr int PB_WARPS   = PB_WARPS_V;  // warps per block
+#ifndef PB_CLAIM
+#define PB_CLAIM 1  // C3 kernel: 1 -> 25.17 ms, 4 -> 25.69, 16 -> 26.37 (claims are not the bound)
+#endif
 constexpr int PB_BCAP    = 128;   // bounds overlay slots (power of 2)
 constexpr int PB_ACAP    = 128;   // activity overlay slots (power of 2)
 #ifndef PB_RCAP_V
@@ -559,11 +562,13 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PCtx c{P, R, lim, sm.w[warp], lane};
   unsigned long long wk[5] = {0, 0, 0, 0, 0};  // warp-uniform work counters
-  for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(B.cursor, 1);
-    t = __shfl_sync(FULL, t, 0);
-    if (t >= B.n_task) break;
+  for (;;) {  // PB_CLAIM branches per claim of the shared cursor
+    int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(B.cursor, PB_CLAIM);
+    t0 = __shfl_sync(FULL, t0, 0);
+    if (t0 >= B.n_task) break;
+    const int t1 = min(t0 + PB_CLAIM, B.n_task);
+    for (int t = t0; t < t1; ++t) {
     const int v      = B.var[t];
     unsigned long long bw[5] = {0, 0, 0, 0, 0};
     const int status = probe_branch(c, v, B.lo[t], B.up[t], bw);
@@ -614,6 +619,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 1)
       }
     }
     __syncwarp();
+    }
   }
   if (lane == 0 && B.work)
     for (int q = 0; q < 5; ++q)
