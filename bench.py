@@ -753,9 +753,13 @@ def main():
     if rank == 0:
         peak, peak_kind = peaks()
         achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
-        # DRAM traffic needs a profiler pass (ncu): not measured inside this run; the committed
-        # capture of the same code is profiles/r02/ 
+        # DRAM traffic needs a profiler pass (ncu), not run inside the timed bench: the committed
+        # per-launch dram__bytes_read/write sum of one propagate of the same code
+        # (tools/gpu_profiles.sh -> tools/ncu_traffic.py -> profiles/r02/ncu_traffic_summary.json)
         traffic = None
+        tj = ROOT / "profiles" / "r02" / "ncu_traffic_summary.json"
+        if tj.exists():
+            traffic = json.loads(tj.read_text()).get("dram_bytes_per_launch", {}).get(args.workload)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             res = cpu_reference_propagate(p, reps=1)

@@ -4,11 +4,13 @@ O=gpurun_out/prof; mkdir -p $O
 N="ncu --clock-control none"
 # C2 propagate: per-launch time + DRAM bytes
 timeout 900 $N --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv --log-file $O/launches_C2.csv python tools/ncu_target.py --workload C2 --reps 1 > /dev/null 2>&1
-# k_rows_full: an early (round 2, all rows) and a late (round 22, dirty-filtered) launch; k_engine round 5; k_cand_pieces
+# k_rows_full and k_rows_sell: an early (round 2, all rows) and a late (round 20, dirty-filtered)
+# launch; k_engine in a dirty-filtered round (12: finalize over the touched vars + marks)
 timeout 900 $N --set full --import-source on -k regex:k_rows_full -s 1 -c 1 -o $O/k_rows_full_C2_r2 python tools/ncu_target.py --workload C2 --reps 1 > $O/n1.log 2>&1
-timeout 900 $N --set full --import-source on -k regex:k_rows_full -s 21 -c 1 -o $O/k_rows_full_C2_r22 python tools/ncu_target.py --workload C2 --reps 1 > $O/n2.log 2>&1
-timeout 900 $N --set full --import-source on -k regex:k_engine -s 4 -c 1 -o $O/k_engine_C2_r5 python tools/ncu_target.py --workload C2 --reps 1 > $O/n3.log 2>&1
-timeout 900 $N --set full --import-source on -k regex:k_cand_pieces -s 1 -c 1 -o $O/k_cand_pieces_C2 python tools/ncu_target.py --workload C2 --reps 1 > $O/n4.log 2>&1
+timeout 900 $N --set full --import-source on -k regex:k_rows_full -s 19 -c 1 -o $O/k_rows_full_C2_r20 python tools/ncu_target.py --workload C2 --reps 1 > $O/n2.log 2>&1
+timeout 900 $N --set full --import-source on -k regex:k_rows_sell -s 1 -c 1 -o $O/k_rows_sell_C2_r2 python tools/ncu_target.py --workload C2 --reps 1 > $O/n3.log 2>&1
+timeout 900 $N --set full --import-source on -k regex:k_rows_sell -s 19 -c 1 -o $O/k_rows_sell_C2_r20 python tools/ncu_target.py --workload C2 --reps 1 > $O/n4.log 2>&1
+timeout 900 $N --set full --import-source on -k regex:k_engine -s 11 -c 1 -o $O/k_engine_C2_r12 python tools/ncu_target.py --workload C2 --reps 1 > $O/n8.log 2>&1
 # probing: the warp kernel on C3, the block kernel on a scaled C4
 timeout 900 $N --set full --import-source on -k regex:k_probe -c 1 -o $O/k_probe_C3 python tools/ncu_probe_target.py > $O/n5.log 2>&1
 timeout 1200 $N --set full --import-source on -k regex:k_probe_block -c 1 -o $O/k_probe_block_C4s python tools/ncu_c4probe_target.py > $O/n6.log 2>&1

@@ -1,6 +1,6 @@
 """Sums per-launch DRAM traffic and time of one propagate's launch sequence from an ncu CSV
 (--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum) and records it in
-profiles/ncu_k_engine_summary.json as the roofline `traffic` of that workload (bench.py).
+profiles/r02/ncu_traffic_summary.json as the roofline `traffic` of that workload (bench.py).
 
     python tools/ncu_traffic.py launches.csv --workload C2 [--skip-warmup-launches K]
 """
@@ -25,7 +25,7 @@ names = {}
 for r in rows:
     per[int(r[0])][r[12]] = float(r[14].replace(",", "")) * SCALE.get(r[13], 1.0)
     names[int(r[0])] = r[4].split("(")[0].split("::")[-1]
-eng = [i for i in sorted(per) if names[i] in ("k_engine", "k_rows_full", "k_cand_pieces")]
+eng = [i for i in sorted(per) if names[i] in ("k_engine", "k_rows_full", "k_rows_sell", "k_cand_pieces")]
 tot_b = sum(per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0) for i in eng)
 tot_t = sum(per[i].get("gpu__time_duration.sum", 0) for i in eng)
 by = defaultdict(lambda: [0, 0.0, 0.0])
@@ -38,7 +38,7 @@ print(f"{len(eng)} engine launches in {a.reps} propagate(s): {tot_t * 1e3 / a.re
 for k, (n, t, b) in sorted(by.items()):
     print(f"  {k:14s} n={n:4d} time={t * 1e3 / a.reps:8.3f} ms  dram={b / 1e9 / a.reps:7.3f} GB  "
           f"share={t / tot_t:5.1%}")
-sj = Path(__file__).resolve().parents[1] / "profiles" / "ncu_k_engine_summary.json"
+sj = Path(__file__).resolve().parents[1] / "profiles" / "r02" / "ncu_traffic_summary.json"
 js = json.loads(sj.read_text()) if sj.exists() else {}
 js.setdefault("dram_bytes_per_launch", {})[a.workload] = tot_b / a.reps
 js.setdefault("source", {})[a.workload] = f"{a.csv} (sum over the propagate's engine launches)"
