@@ -1204,6 +1204,11 @@ constexpr int kPieceStep = BP_PIECE_STEP;
 constexpr int kGroupStep = BP_GROUP_STEP;
 // SELL slices (k_rows_sell) statically assigned: 6.31 -> 5.55 ms on C2 against one shared cursor
 // (every claim an atomic on one address, 7k claims per round)
+#ifndef BP_MULTI_CURSORS
+#define BP_MULTI_CURSORS 8
+#endif
+constexpr int kMultiCursors = BP_MULTI_CURSORS;  // medium-row group cursors in full rounds (1: one)
+static_assert(kMultiCursors <= kMaxMultiCursors, "Ctl::mcur holds kMaxMultiCursors per parity");
 #ifndef BP_STATIC_SELL
 #define BP_STATIC_SELL 1
 #endif
@@ -1276,7 +1281,26 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       if (row_live(S, tk.x, ds)) heavy_fold(c, tk.x, tk.y, cand, stamp, ds, kFoldLazy);
       dbg_task(c, 0, c0);
     }
-    if (ds == 0) {
+    if (ds == 0 && kMultiCursors > 1) {
+      // groups claimed one at a time (balance) from kMultiCursors interleaved sub-ranges, each with
+      // its own cursor on its own line: a warp starts on sub-range (warp mod K) and moves on when
+      // it is exhausted -- K times fewer atomics queue on any one address
+      const int ng = (nf - nfh + 3) / 4;
+      int* mc      = S.ctl->mcur + par * kMultiCursors * 32;
+      int k        = (blockIdx.x * kWarps + c.warp) % kMultiCursors;
+      for (int tried = 0; tried < kMultiCursors;) {
+        int g = 0;
+        if (c.lane == 0) g = atomicAdd(mc + 32 * k, 1);
+        const int item = k + kMultiCursors * __shfl_sync(FULL, g, 0);
+        if (item >= ng) {
+          k = (k + 1) % kMultiCursors;
+          ++tried;
+          continue;
+        }
+        tried = 0;
+        group_fold(c, nfh + 4 * item, min(4, nf - nfh - 4 * item), cand);
+      }
+    } else if (ds == 0) {
       for (Prefetch it_t(c, &pc->cur_g, 4 * kGroupStep, nf - nfh, true); nfh + it_t.t < nf; it_t.advance()) {
         const long long c0 = DBG_ON(S) ? clock64() : 0;
         for (int q = it_t.t; q < min(nf - nfh, it_t.t + 4 * kGroupStep); q += 4)
@@ -2189,6 +2213,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     if (st && lead) st[6] = (long long)(globaltimer() - t0);
     if (lead) {
       zero_par(qc);  // safe: every block has finished reading the previous round's counters
+      for (int j = 0; j < kMultiCursors; ++j) S.ctl->mcur[(qpar * kMultiCursors + j) * 32] = 0;
       // the dirty lists the marks below append to (this round's row phase has consumed them)
       S.ctl->df_cnt[0] = S.ctl->df_cnt[1] = S.ctl->df_cnt[2] = S.ctl->df_cnt[3] = 0;
       if (timed && (double)(globaltimer() - t0) * 1e-9 >= lim.time_limit) pc->stop = 1;

@@ -16,4 +16,14 @@ timeout 900 $N --set full --import-source on -k regex:k_probe -c 1 -o $O/k_probe
 timeout 1200 $N --set full --import-source on -k regex:k_probe_block -c 1 -o $O/k_probe_block_C4s python tools/ncu_c4probe_target.py > $O/n6.log 2>&1
 # PDHG products
 timeout 900 $N --set full --import-source on -k regex:spmv -c 2 -o $O/lp_spmv_C2 python tools/ncu_lp_target.py > $O/n7.log 2>&1
+# summaries on the box (the reports together exceed gpurun's 64 MiB copy-back): ncu_summary.py text
+# + the per-source-line stall table of each capture; the reports themselves are removed
+for r in $O/*.ncu-rep; do
+  b=$(basename $r .ncu-rep)
+  python tools/ncu_summary.py $r $O/ncu_$b > /dev/null 2>&1
+  ncu -i $r --page source --print-source cuda,sass --csv > $O/src.csv 2>/dev/null && python tools/ncu_lines.py $O/src.csv 40 > $O/lines_$b.txt 2>&1
+  rm -f $O/src.csv
+done
+python tools/ncu_traffic.py $O/launches_C2.csv --workload C2 > $O/traffic_C2.txt 2>&1
+rm -f $O/*.ncu-rep
 echo done > $O/DONE
