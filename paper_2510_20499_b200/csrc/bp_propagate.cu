@@ -868,6 +868,11 @@ __device__ void heavy_fold(Ctx& c, int k, int seg, bool cand, unsigned stamp, un
 // non-zero contributions into its own shared-memory slice, and its lanes 0/1 run the row's
 // sequential min/max sums -- the four rows' chains advance in the same instructions. Then the
 // candidates of the non-quiet rows.
+#ifndef BP_WARP_ROW_MIN
+#define BP_WARP_ROW_MIN 256  // C2: off 5.61, 128 5.60, 256 5.60, 512 5.60 ms (late rounds 63-130 -> 57-65 us)
+#endif
+constexpr int kWarpRowMin = BP_WARP_ROW_MIN;  // medium rows above: a warp per row (group_fold)
+
 __device__ void group_fold(Ctx& c, int t0, int nt, bool cand, unsigned ds = 0)
 {
   const DevProblem& P = c.P;
@@ -885,6 +890,16 @@ __device__ void group_fold(Ctx& c, int t0, int nt, bool cand, unsigned ds = 0)
   int Lmax = L;
 #pragma unroll
   for (int o = 16; o; o >>= 1) Lmax = max(Lmax, __shfl_xor_sync(FULL, Lmax, o));
+  if (Lmax > kWarpRowMin) {
+    // long medium rows (the group's rows have similar lengths): one after another with the whole
+    // warp (128-entry chunks, two in flight) -- 4x fewer dependent load steps per row than 8 lanes
+    const unsigned am = __ballot_sync(FULL, act && gl == 0);
+    for (int q = 0; q < 4; ++q) {
+      const int kq = __shfl_sync(FULL, k, 8 * q);
+      if ((am >> (8 * q)) & 1u) long_fold(c, kq, 0, cand, 0u);
+    }
+    return;
+  }
   double* gb0 = c.w.b0 + 32 * g;  // group slices of the staging buffers (<= 32 per chunk)
   double* gb1 = c.w.b1 + 32 * g;
   int ci[4], cn[4];
@@ -2079,7 +2094,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cand_pieces(DevProblem P, DevSt
 __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     k_engine(DevProblem P, DevState S, Limits lim, int mode, int full_first, unsigned stamp_base,
              unsigned long long dense_thr, long long* stats, int ext_f2, int resume,
-             unsigned long long mark_max)
+             unsigned long long mark_max, int df_local)
 {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Smem& sm            = *reinterpret_cast<Smem*>(dyn_smem);
@@ -2192,8 +2207,13 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     }
     if (resumed) {
       resumed = false;  // this round's F2 (fused rows + candidates) ran in k_rows_full
-    } else if (fr && ext_f2) {
+    } else if (fr && ext_f2 &&
+               !(ds != 0 && ldv(&S.ctl->df_cnt[1]) + ldv(&S.ctl->df_cnt[2]) +
+                                    min(ldv(&S.ctl->df_cnt[0]), (ldv(&S.ctl->df_cnt[3]) + 31) / 32) <=
+                                df_local)) {
       // hand the full round's row phase to k_rows_full; the host relaunches us with resume=1
+      // (a dirty-filtered round with at most df_local row tasks runs here: its launches and the
+      // relaunch would cost more than the occupancy they buy)
       if (lead) {
         if (st) st[10] = (long long)(globaltimer() - t0);
         S.ctl->rounds     = rounds;
@@ -2836,7 +2856,11 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   // 1 % 8.72, 2 % 8.77, 3 % 8.83, 5 % 8.94, 8 % 9.06, 15 % 9.24 ms per propagate)
   static const int mark_pct = getenv("BP_DF_MARK_PCT") ? atoi(getenv("BP_DF_MARK_PCT")) : 1;
   unsigned long long mark_max = (unsigned long long)(P.nnz * mark_pct / 100);
-  void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume, &mark_max};
+  // dirty-filtered rounds with at most this many row tasks run inside the engine (BP_DF_LOCAL;
+  // C2: 0 -> 5.63, 1000 -> 5.74, 3000 -> 5.57, 10000 -> 5.60 ms)
+  static const int df_local_env = getenv("BP_DF_LOCAL") ? atoi(getenv("BP_DF_LOCAL")) : 3000;
+  int df_local = df_local_env;
+  void* args[]   = {&d, &st, &l, &md, &ff, &sb, &dense_thr, &stp, &ext, &resume, &mark_max, &df_local};
   BP_CUDA(cudaEventRecord(P.ev0, s));
   BP_CUDA(cudaLaunchCooperativeKernel((void*)k_engine, P.grid_blocks, kThreads, args, sizeof(Smem), s));
   ++g_kernel_launches;
