@@ -59,16 +59,19 @@ def build_cache_sharded(p, vars_, root=None, device=None, group=None):
     rank 0 (None on other ranks) and this rank's local device time (ms)."""
     import torch.distributed as dist
 
-    from .probing import ProbingCache, probe_variables
-    from .propagation import BoundsState
+    from .probing import probe_variables
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     local = probe_variables(p, root, shard(vars_, rank, world))
-    slices = gather_packed(local.pack(), device=device, group=group)
+    if world == 1:  # nothing to gather: the local cache is the cache
+        return local, local.probe_ms
+    # rank 0 keeps its own slice in place and merges the others' into it (entries are per
+    # variable, so the merge order does not change the cache)
+    slices = gather_packed(local.pack() if rank != 0 else np.zeros(0, np.uint8), device=device, group=group)
     if rank != 0:
         return None, local.probe_ms
-    merged = ProbingCache.empty(root if root is not None else BoundsState(p))
-    for s in slices:
-        merged.merge_packed(s)
-    return merged, local.probe_ms
+    for s in slices[1:]:
+        if s.size:
+            local.merge_packed(s)
+    return local, local.probe_ms
