@@ -347,9 +347,6 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
       BP_CUDA(cudaMemcpyAsync(cn, dcnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
       // the batch's deltas in task order (device scan + pack), appended to the flat host pool
       const long long hbase = (long long)hp_var.size();
-      hp_var.resize(hbase + used);
-      hp_lo.resize(hbase + used);
-      hp_up.resize(hbase + used);
       int* hqv    = nullptr;
       double* hql = nullptr;
       double* hqu = nullptr;
@@ -374,10 +371,10 @@ HostCache probe_vars(Problem& P, const std::vector<double>& root, const std::vec
         BP_CUDA(cudaMemcpyAsync(hqu, qup.p, sizeof(double) * used, cudaMemcpyDeviceToHost, s));
       }
       BP_CUDA(cudaStreamSynchronize(s));
-      if (used) {
-        std::memcpy(hp_var.data() + hbase, hqv, sizeof(int) * used);
-        std::memcpy(hp_lo.data() + hbase, hql, sizeof(double) * used);
-        std::memcpy(hp_up.data() + hbase, hqu, sizeof(double) * used);
+      if (used) {  // appended from the pinned staging (one copy, no zero-fill of a resize)
+        hp_var.insert(hp_var.end(), hqv, hqv + used);
+        hp_lo.insert(hp_lo.end(), hql, hql + used);
+        hp_up.insert(hp_up.end(), hqu, hqu + used);
       }
       const double tb3 = elapsed();
       if (prof)
