@@ -2853,9 +2853,10 @@ RunResult run_engine(Problem& P, Mode mode, bool full, const Limits& lim, cudaSt
   const int split_sell       = split_env && P.n_srtile > 0 ? 1 : 0;
   // dirty-filtered rounds when the changed vars' columns hold at most BP_DF_MARK_PCT % of the nnz:
   // beyond that the marks and lists cost more than the rows they spare (C2, tools/gpu_ab.sh:
-  // 1 % 8.72, 2 % 8.77, 3 % 8.83, 5 % 8.94, 8 % 9.06, 15 % 9.24 ms per propagate)
-  static const int mark_pct = getenv("BP_DF_MARK_PCT") ? atoi(getenv("BP_DF_MARK_PCT")) : 1;
-  unsigned long long mark_max = (unsigned long long)(P.nnz * mark_pct / 100);
+  // 1 % 8.72, 2 % 8.77, 3 % 8.83, 5 % 8.94, 8 % 9.06, 15 % 9.24 ms per propagate; at the end of the
+  // round: 0.5 % 5.52, 0.75 % 5.62, 1 % 5.53, 1.5 % 5.55, 2 % 5.57, 3 % 5.68)
+  static const double mark_pct = getenv("BP_DF_MARK_PCT") ? atof(getenv("BP_DF_MARK_PCT")) : 1.0;
+  unsigned long long mark_max = (unsigned long long)((double)P.nnz * mark_pct / 100.0);
   // dirty-filtered rounds with at most this many row tasks run inside the engine (BP_DF_LOCAL;
   // C2: 0 -> 5.63, 1000 -> 5.74, 3000 -> 5.57, 10000 -> 5.60 ms)
   static const int df_local_env = getenv("BP_DF_LOCAL") ? atoi(getenv("BP_DF_LOCAL")) : 3000;
