@@ -86,10 +86,9 @@ struct Ctl {
   int n_touch;    // variables whose slot a dirty-filtered round's rows published into (touched)
   unsigned long long t0;      // globaltimer at the start of the propagate (time limit, stats)
   int pad[2];
-  // full rounds: per parity, kMaxMultiCursors work cursors for the medium-row groups and for the
-  // heavy-row pieces, each on its own 128-byte line (zeroed with the rest of Ctl per call, the next
-  // parity's per round)
-  alignas(128) int mcur[2 * 2 * kMaxMultiCursors * 32];  // [parity][kind: groups, pieces][cursor]
+  // full rounds: per parity, kMaxMultiCursors work cursors for the medium-row groups, each on its
+  // own 128-byte line (zeroed with the rest of Ctl per call, the next parity's per round)
+  alignas(128) int mcur[2 * kMaxMultiCursors * 32];
 };
 
 // Mutable per-problem workspace (one propagate at a time per problem; calls serialized).

@@ -1224,28 +1224,6 @@ constexpr int kGroupStep = BP_GROUP_STEP;
 #endif
 constexpr int kMultiCursors = BP_MULTI_CURSORS;  // medium-row group cursors in full rounds (1: one)
 static_assert(kMultiCursors <= kMaxMultiCursors, "Ctl::mcur holds kMaxMultiCursors per parity");
-
-// Items [0, n) claimed one at a time from kMultiCursors interleaved sub-ranges (item mod K), each
-// with its own cursor on its own 128-byte line: a warp starts on sub-range (warp mod K) and moves on
-// when it is exhausted -- K times fewer atomics queue on any one address than on one cursor, and
-// the call returns only after every sub-range was seen exhausted (all items claimed).
-template <class F>
-__device__ __forceinline__ void multi_claim(Ctx& c, int* mc, int n, F&& f)
-{
-  int k = (blockIdx.x * kWarps + c.warp) % kMultiCursors;
-  for (int tried = 0; tried < kMultiCursors;) {
-    int g = 0;
-    if (c.lane == 0) g = atomicAdd(mc + 32 * k, 1);
-    const int item = k + kMultiCursors * __shfl_sync(FULL, g, 0);
-    if (item >= n) {
-      k = (k + 1) % kMultiCursors;
-      ++tried;
-      continue;
-    }
-    tried = 0;
-    f(item);
-  }
-}
 #ifndef BP_STATIC_SELL
 #define BP_STATIC_SELL 1
 #endif
@@ -1304,8 +1282,8 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
     // above kCandSplit (they wait for their row's fold, all of which have been fetched by then)
     // heavy rows' contribution pieces first: the segment folds that wait for them are fetched
     // only after every piece has been fetched by a running warp (no deadlock)
-    if (ds == 0) {  // (pieces from interleaved multi_claim sub-ranges: 5.50 -> 6.01 ms on C2 -- a
-                    // row's pieces then finish scattered in time and its folds wait longer)
+    if (ds == 0) {  // (pieces from 8 interleaved cursors like the groups below: 5.50 -> 6.01 ms on C2
+                    // -- a row's pieces then finish scattered in time and its folds wait longer)
       for (Prefetch it_t(c, &pc->cur_p, kPieceStep, P.n_piece); it_t.t < P.n_piece; it_t.advance())
         for (int q = it_t.t; q < min(P.n_piece, it_t.t + kPieceStep); ++q) heavy_piece(c, q, stamp);
     } else {  // dirty-filtered round: the engine's list of dirty pieces
@@ -1320,9 +1298,24 @@ __device__ void phase_rows(Ctx& c, ParCtl* pc, int par, bool full, bool cand, un
       dbg_task(c, 0, c0);
     }
     if (ds == 0 && kMultiCursors > 1) {
+      // groups claimed one at a time (balance) from kMultiCursors interleaved sub-ranges, each with
+      // its own cursor on its own line: a warp starts on sub-range (warp mod K) and moves on when
+      // it is exhausted -- K times fewer atomics queue on any one address
       const int ng = (nf - nfh + 3) / 4;
-      multi_claim(c, S.ctl->mcur + (2 * par) * kMultiCursors * 32, ng,
-                  [&](int g) { group_fold(c, nfh + 4 * g, min(4, nf - nfh - 4 * g), cand); });
+      int* mc      = S.ctl->mcur + par * kMultiCursors * 32;
+      int k        = (blockIdx.x * kWarps + c.warp) % kMultiCursors;
+      for (int tried = 0; tried < kMultiCursors;) {
+        int g = 0;
+        if (c.lane == 0) g = atomicAdd(mc + 32 * k, 1);
+        const int item = k + kMultiCursors * __shfl_sync(FULL, g, 0);
+        if (item >= ng) {
+          k = (k + 1) % kMultiCursors;
+          ++tried;
+          continue;
+        }
+        tried = 0;
+        group_fold(c, nfh + 4 * item, min(4, nf - nfh - 4 * item), cand);
+      }
     } else if (ds == 0) {
       for (Prefetch it_t(c, &pc->cur_g, 4 * kGroupStep, nf - nfh, true); nfh + it_t.t < nf; it_t.advance()) {
         const long long c0 = DBG_ON(S) ? clock64() : 0;
@@ -2241,7 +2234,7 @@ __global__ void __launch_bounds__(kThreads, BP_MIN_BLOCKS)
     if (st && lead) st[6] = (long long)(globaltimer() - t0);
     if (lead) {
       zero_par(qc);  // safe: every block has finished reading the previous round's counters
-      for (int j = 0; j < 2 * kMultiCursors; ++j) S.ctl->mcur[(2 * qpar * kMultiCursors + j) * 32] = 0;
+      for (int j = 0; j < kMultiCursors; ++j) S.ctl->mcur[(qpar * kMultiCursors + j) * 32] = 0;
       // the dirty lists the marks below append to (this round's row phase has consumed them)
       S.ctl->df_cnt[0] = S.ctl->df_cnt[1] = S.ctl->df_cnt[2] = S.ctl->df_cnt[3] = 0;
       if (timed && (double)(globaltimer() - t0) * 1e-9 >= lim.time_limit) pc->stop = 1;
